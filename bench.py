@@ -1,0 +1,420 @@
+"""Benchmark: decoded B-spline samples/s of the 1024^2 ray-cast (BASELINE config 3).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step renders one 1024^2 frame of the config-3 model (1024^3-equivalent
+synthetic turbulence: 1025^3 lattice, 4 LODs, 4,680 micro-blocks of 65^3
+samples, degree 3, NCP 40..65) from orbit_trajectory(100, radius=2.0)
+pose (W + k) % 100, sd = 1e-3, ML transfer function, gradient shading.
+`value` = decoded samples / s with every block resident in HBM (device
+time, CUDA events on the render stream, L2 flushed between steps, max over
+ranks); `e2e` = the same metric through the public runtime API (ModelCache
+of 200 blocks + linear prefetch fed from pinned host memory, frame read
+back to the host), i.e. BASELINE config 4.  N > 1: one process per GPU
+(torchrun), each rank renders interleaved 8-row bands, NCCL gather of
+the RGBA8 tiles to rank 0 inside the timed step.
+
+--impl reference times the reference algorithm on the host CPU: the
+float64 C restatement in oracle/ (the reference itself is pure Python and
+is not on the GPU box), all host threads, on a row band of the same frames.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "decoded samples/s (1024^2 ray-cast, config 3)"
+UNIT = "samples/s"
+FLOP_PER_SAMPLE_P3 = 384  # 2*(2q^3+3q^2+4q), q=4: separable value+gradient contraction
+WORKLOAD = {"workload": "config3: 1024^3-equiv synthetic turbulence, 4 LODs, 4680 blocks (micro 65, degree 3, "
+                        "ncp 40-65), 1024x1024 ray-cast, sd 1e-3, ML TF + gradient shading, "
+                        "orbit_trajectory(100, r=2.0)",
+            "frame": [1024, 1024], "sample_distance": 1e-3, "blocks": 4680,
+            "l2": "flushed between steps (512 MiB write outside the per-step events)"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--size", type=int, default=1024)
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-rows", type=int, default=24, help="rows of the frame in the CPU sample")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ data
+def build_model(pinned: bool):
+    from paper_2409_00184_b200 import synth
+
+    alloc = None
+    if pinned:
+        import torch
+
+        def alloc(n):
+            t = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+            alloc.keep = t
+            return t.numpy()
+
+    t0 = time.time()
+    man, blobs = synth.turbulence_store(alloc=alloc)
+    return man, blobs, time.time() - t0
+
+
+def measure_fma_peak(dev):
+    """FP32 FMA peak of this GPU: a dependent-chain-free FFMA kernel in libafam."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2409_00184_b200 import _lib
+
+    out = torch.empty(148 * 8 * 256, dtype=torch.float32, device=dev)
+    s = torch.cuda.current_stream(dev)
+    flops = C.c_double()
+    best = 0.0
+    for _ in range(4):
+        ms = C.c_float()
+        _lib.check(_lib.lib().afam_bench_fma(C.c_void_p(out.data_ptr()), 4096, C.byref(ms), C.byref(flops),
+                                             C.c_void_p(s.cuda_stream)))
+        best = max(best, flops.value / (ms.value * 1e-3))
+    return best / 1e12
+
+
+# ------------------------------------------------------------------ ours
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2409_00184_b200 import render, runtime
+    from paper_2409_00184_b200.device import DeviceStore
+    from paper_2409_00184_b200.partition import BlockAddress
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    man, blobs, gen_s = build_model(pinned=not args.no_e2e)
+    povs = runtime.orbit_trajectory(100, radius=2.0)
+    S = args.size
+    params = render.RenderParams(width=S, height=S, sample_distance=1e-3)
+    tf = render.TransferFunction.ml_preset()
+
+    # -- every block resident in HBM (the `value` measurement)
+    t0 = time.time()
+    ds = DeviceStore(len(blobs) + 1, 65, device=local_rank)
+    resident_all = {a: ds.load_mfa(b, man.entries[a].ncp, man.entries[a].extent, a.lod) for a, b in blobs.items()}
+    torch.cuda.synchronize(dev)
+    upload_s = time.time() - t0
+    nfp64 = sum(ds.info(b.slot)["fp64"] for b in list(resident_all.values())[:: max(1, len(resident_all) // 256)])
+
+    band = 8
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    frame_out = torch.empty((render._lib.lib().afam_frame_rows(S, band, world, rank), S, 4), dtype=torch.uint8,
+                            device=dev)
+    gather_bufs = None
+    if world > 1 and rank == 0:
+        gather_bufs = [torch.empty((render._lib.lib().afam_frame_rows(S, band, world, r), S, 4), dtype=torch.uint8,
+                                   device=dev) for r in range(world)]
+
+    def step(k):
+        pov = povs[k % len(povs)]
+        vis = render.select_visible(pov, man, params.aspect)
+        blocks = {a: resident_all[a] for a in vis}
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        _, info, _ = render.render_part(pov, blocks, tf, params, band_rows=band, nparts=world, part=rank,
+                                        device=local_rank, out=frame_out)
+        ev1.record(stream)
+        ev2 = torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.gather(frame_out, gather_bufs if rank == 0 else None, dst=0)
+        ev2.record(stream)
+        return ev0, ev1, ev2, info, len(vis)
+
+    for k in range(args.warmup):
+        step(k)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    times, ktimes, samples, fp64s, nvis = [], [], 0, 0, []
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        wall0 = time.perf_counter()
+        for k in range(args.steps):
+            flush.zero_()  # evict the previous frame's blocks from L2 (outside the events)
+            ev0, ev1, ev2, info, nv = step(args.warmup + k)
+            torch.cuda.synchronize(dev)
+            ktimes.append(ev0.elapsed_time(ev1))
+            times.append(ev0.elapsed_time(ev2))
+            samples += info["samples"]
+            fp64s += info["fp64_samples"]
+            nvis.append(nv)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        wall = time.perf_counter() - wall0
+    step_ms = float(np.mean(times))
+    kern_ms = float(np.mean(ktimes))
+    tot = torch.tensor([samples, fp64s], dtype=torch.float64, device=dev)
+    tmax = torch.tensor([sum(times), sum(ktimes), wall], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    total_samples, total_fp64 = float(tot[0]), float(tot[1])
+    t_steps, t_kern, t_wall = float(tmax[0]) / 1e3, float(tmax[1]) / 1e3, float(tmax[2])
+    value = total_samples / t_steps
+
+    # -- roofline of the dominant kernel (render_kernel)
+    fma_peak = measure_fma_peak(dev)
+    achieved = (samples * FLOP_PER_SAMPLE_P3) / (sum(ktimes) / 1e3) / 1e12
+    traffic = None
+    prof = ROOT / "profiles" / "render_kernel_traffic.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "fp32", "achieved": achieved, "peak": fma_peak, "unit": "TFLOP/s",
+                "frac": achieved / fma_peak if fma_peak else None, "traffic": traffic,
+                "kernel": "render_kernel (K2)",
+                "note": "algorithmic FLOP = 384/sample (separable p=3 value+gradient contraction, basis "
+                        "evaluation not credited) x samples / render-call event time; peak = FFMA "
+                        "microbenchmark on this GPU (MEASURED_PEAKS.json has no FP32 figure)"}
+
+    result = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+              "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+              "scaling": "strong", "vs_baseline": None, "dtype": "f32 (f64 geometry; f64 decode on "
+                                                                 "ill-conditioned blocks)",
+              "data": "synthetic (seeded turbulence, fitted like the reference encoder)",
+              "config": dict(WORKLOAD, parallelism=f"image bands x{world}", frame_ms=step_ms,
+                             kernel_ms=kern_ms, visible_blocks_mean=float(np.mean(nvis)),
+                             fp64_sample_frac=total_fp64 / max(1.0, total_samples), gen_s=round(gen_s, 1),
+                             upload_s=round(upload_s, 2), fp64_slot_sample=int(nfp64)),
+              "roofline": roofline, "clocks": clk.summary(), "gpu_launches": 3 * args.steps,
+              "wall_s_timed_region": t_wall}
+
+    # -- e2e through the public runtime API: ModelCache(200) + linear prefetch, pinned host source
+    if not args.no_e2e:
+        result["e2e"] = run_e2e(args, man, blobs, povs, tf, params, rank, world, local_rank)
+    del resident_all, ds
+    return result, man, blobs
+
+
+def run_e2e(args, man, blobs, povs, tf, params, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2409_00184_b200 import render, runtime
+    from paper_2409_00184_b200.device import DeviceStore
+
+    cap = 200
+    ds = DeviceStore(cap + 1, 65, device=local_rank)
+    loader = runtime.make_loader(None, man, ds, source=lambda a: blobs[a])
+    cache = runtime.ModelCache(cap, loader)
+    band = 8
+    S = params.width
+
+    def draw(pov, resident, tf_, params_):
+        out, info, _ = render.render_part(pov, resident, tf_, params_, band_rows=band, nparts=world, part=rank,
+                                          device=local_rank)
+        draw.samples += info["samples"]
+        if world > 1:
+            bufs = [torch.empty((render._lib.lib().afam_frame_rows(S, band, world, r), S, 4), dtype=torch.uint8,
+                                device=out.device) for r in range(world)] if rank == 0 else None
+            dist.gather(out, bufs, dst=0)
+            if rank == 0:
+                out = torch.cat(bufs)
+        host = out.cpu().numpy()  # D2H of the frame (the step's result)
+        draw.d2h += host.nbytes
+        return host
+
+    draw.samples, draw.d2h = 0, 0
+    nwarm = args.warmup
+    nsteps = args.e2e_steps or args.steps
+    runtime.replay(povs[:nwarm], man, cache, tf, params, prefetch="linear", keep_frames=False, render_fn=draw)
+    c0 = cache.counters()
+    draw.samples, draw.d2h = 0, 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    timings, _, agg = runtime.replay(povs[nwarm:nwarm + nsteps], man, cache, tf, params, prefetch="linear",
+                                     keep_frames=False, render_fn=draw)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    el = time.perf_counter() - t0
+    c1 = cache.counters()
+    tot = torch.tensor([draw.samples, el], dtype=torch.float64, device=torch.device("cuda", local_rank))
+    if world > 1:
+        s = tot.clone()
+        dist.all_reduce(s, op=dist.ReduceOp.SUM)
+        m = tot.clone()
+        dist.all_reduce(m, op=dist.ReduceOp.MAX)
+        tot = torch.stack([s[0], m[1]])
+    h2d = (c1["bytes_loaded"] - c0["bytes_loaded"]) / nsteps
+    return {"value": float(tot[0]) / float(tot[1]), "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": draw.d2h / nsteps, "steps": nsteps,
+            "api": "runtime.replay(ModelCache(200), prefetch='linear') -> render_part -> Frame bytes on host",
+            "mean_caching_ms": agg["mean_caching_ms"], "mean_rendering_ms": agg["mean_rendering_ms"],
+            "mean_latency_ms": agg["mean_latency_ms"], "miss_rate": agg["miss_rate"],
+            "prefetch_models_loaded": agg["prefetch_models_loaded"]}
+
+
+# ------------------------------------------------------------------ CPU
+def cpu_sample(man, blobs, povs, tf, params, rows, frame_index):
+    """Time the oracle (float64 C restatement of render.py:398-466) on a row band."""
+    from oracle import oracle
+
+    from paper_2409_00184_b200 import model, render
+
+    pov = povs[frame_index % len(povs)]
+    vis = render.select_visible(pov, man, params.aspect)
+    host = {a: model.deserialize(bytes(blobs[a]), man.entries[a].ncp, man.entries[a].extent, a.lod) for a in vis}
+    H = params.height
+    r0 = (H - rows) // 2
+    threads = oracle.max_threads()
+    t0 = time.perf_counter()
+    _, info = oracle.render(pov, host, tf, params, rows=(r0, r0 + rows), nthreads=threads)
+    el = time.perf_counter() - t0
+    return info["samples"], el, threads, f"rows {r0}..{r0 + rows} of orbit frame {frame_index % len(povs)}"
+
+
+def run_reference(args):
+    from paper_2409_00184_b200 import render, runtime
+
+    man, blobs, _ = build_model(pinned=False)
+    povs = runtime.orbit_trajectory(100, radius=2.0)
+    S = args.size
+    params = render.RenderParams(width=S, height=S, sample_distance=1e-3)
+    tf = render.TransferFunction.ml_preset()
+    for k in range(min(args.warmup, 1)):
+        cpu_sample(man, blobs, povs, tf, params, 2, k)
+    tot_s, tot_t, times = 0, 0.0, []
+    threads, desc = 1, ""
+    rows = args.cpu_rows
+    for k in range(args.steps):
+        s, t, threads, desc = cpu_sample(man, blobs, povs, tf, params, rows, args.warmup + k)
+        tot_s += s
+        tot_t += t
+        times.append(t)
+    value = tot_s / tot_t
+    import platform
+
+    return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (same model as --impl ours)",
+            "config": dict(WORKLOAD, l2="n/a (CPU)"), "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": f"{rows}-row band per step of the 1024^2 frames ({desc}); oracle/ C "
+                                       f"float64 restatement, OpenMP x{threads}, host {platform.processor()}"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        print(json.dumps(run_reference(args)), flush=True)
+        return
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.init_process_group("nccl")
+    res, man, blobs = run_ours(args, rank, world, local_rank)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from paper_2409_00184_b200 import render, runtime
+
+        povs = runtime.orbit_trajectory(100, radius=2.0)
+        params = render.RenderParams(width=args.size, height=args.size, sample_distance=1e-3)
+        s, t, threads, desc = cpu_sample(man, blobs, povs, render.TransferFunction.ml_preset(), params,
+                                         args.cpu_rows, args.warmup)
+        res["cpu_baseline"] = {"value": s / t, "unit": UNIT, "cores": threads, "kind": "port",
+                               "sample": f"{desc}: {s} samples in {t:.1f} s (oracle/ C float64, OpenMP x{threads})"}
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,194 @@
+/*
+ * afam.h -- C ABI of the B200-native Adaptive-FAM decode-and-render path.
+ *
+ * One shared library (libafam.so, sm_100a) exports everything below.  All
+ * functions are extern "C", take plain pointers and sizes, return an int
+ * status (AFAM_OK == 0) and record a thread-local message readable with
+ * afam_last_error().  Every device operation takes a cudaStream_t (passed
+ * as void*) and is asynchronous on it unless stated.
+ *
+ * Each entry point replaces one reference interface of the Python package
+ * splinecast (paths relative to /root/reference/pkg/src/splinecast/):
+ *
+ *   afam_store_put_mfa    store.load_model + model.deserialize   store.py:43-47, model.py:121-148
+ *   afam_store_put        MicroModel(...) construction            model.py:27-54
+ *   afam_store_evict      ModelCache._evict_one (device side)     runtime.py:104-110
+ *   afam_eval_points      MicroModel.values_at / gradients_at,    model.py:64-87,
+ *                         bspline.evaluate_points[_with_gradient] bspline.py:206-229
+ *   afam_decode_grid      MicroModel.decode_grid,                 model.py:89-93,
+ *                         bspline.decode_tensor_product           bspline.py:162-172
+ *   afam_select_visible   render.select_visible                   render.py:281-320
+ *   afam_render           render.render                           render.py:398-466
+ *
+ * Status -> Python exception (reference errors.py:12-25):
+ *   1 MissingBlockError, 2 FormatError, 3 CapacityError, 4 ValueError,
+ *   5 RuntimeError (CUDA failure).
+ */
+#ifndef AFAM_H_
+#define AFAM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AFAM_OK 0
+#define AFAM_E_MISSING_BLOCK 1
+#define AFAM_E_FORMAT 2
+#define AFAM_E_CAPACITY 3
+#define AFAM_E_VALUE 4
+#define AFAM_E_CUDA 5
+
+#define AFAM_MAX_DEGREE 3     /* degrees 1..3 are evaluated on device */
+#define AFAM_MAX_TF_POINTS 32
+
+/* Per-slot flags (afam_store_info). */
+#define AFAM_SLOT_VALID 1u
+#define AFAM_SLOT_FP64 2u     /* ill-conditioned: evaluated in float64 */
+
+const char *afam_last_error(void);
+int afam_version(void);
+int afam_device_count(void);
+
+/* ------------------------------------------------------------------ store */
+typedef struct afam_store afam_store;
+
+/*
+ * A device store of `slots` micro-model slots on `device`.  Every slot can
+ * hold a model with ncp <= max_ncp and degree <= AFAM_MAX_DEGREE.
+ * fp64_ctrl_limit: a slot whose max |control point| exceeds it is flagged
+ * AFAM_SLOT_FP64 and decoded in float64 (ill-conditioned
+ * endpoint-pinned fits); <= 0 selects the default (4.0).
+ */
+int afam_store_create(afam_store **out, int device, int32_t slots, int32_t max_ncp,
+                      double fp64_ctrl_limit);
+int afam_store_destroy(afam_store *s);
+int afam_store_slots(const afam_store *s, int32_t *slots, int32_t *max_ncp);
+
+/*
+ * Upload one .mfa file image (FORMAT.md:16-70) into `slot`: the raw bytes
+ * are copied H2D as-is (pinned host memory makes it truly async) and a
+ * device kernel realigns the knots/control points and builds the per-span
+ * basis tables.  ncp and extent[6] = {lo_x,hi_x,lo_y,hi_y,lo_z,hi_z} come
+ * from the manifest (FORMAT.md:63-70).  Returns AFAM_E_FORMAT for a length
+ * or degree-byte mismatch (model.py:123-133).
+ */
+int afam_store_put_mfa(afam_store *s, int32_t slot, const uint8_t *bytes, uint64_t nbytes, int32_t ncp,
+                       const double extent[6], void *stream);
+
+/* Upload an already-decoded model: knots (3, ncp+degree+1) float32 full
+ * clamped vectors, ctrl ncp^3 float32 x-fastest. */
+int afam_store_put(afam_store *s, int32_t slot, int32_t degree, int32_t ncp, const float *knots,
+                   const float *ctrl, const double extent[6], void *stream);
+
+int afam_store_evict(afam_store *s, int32_t slot);
+
+/* Synchronous query (waits for the slot's upload). */
+int afam_store_info(afam_store *s, int32_t slot, int32_t *ncp, int32_t *degree, uint32_t *flags,
+                    float *max_abs_ctrl);
+
+/* Device -> host copy of a slot's control points (x-fastest, ncp^3) and
+ * knots (3*(ncp+degree+1)); synchronous.  For parity tests. */
+int afam_store_read(afam_store *s, int32_t slot, float *ctrl, float *knots);
+
+/* ------------------------------------------------------------ K1: points */
+#define AFAM_EVAL_PARAM 1u    /* pts are extent-local parameters u, not world points */
+
+/*
+ * Value (and optionally gradient) of the model in slot slots[i] (or
+ * `slot` for all points when slots == NULL) at pts[i] (n x 3 float64,
+ * device memory).  World points follow MicroModel.values_at/gradients_at
+ * (u = clip((p-lo)/(hi-lo), 0, 1), gradient divided by the extent span);
+ * with AFAM_EVAL_PARAM the points are parameters (bspline.evaluate_points).
+ * val (n) / grad (n x 3) are float32 device buffers; grad may be NULL.
+ */
+int afam_eval_points(afam_store *s, const int32_t *slots, int32_t slot, const double *pts, int64_t n,
+                     float *val, float *grad, uint32_t flags, void *stream);
+
+/* --------------------------------------------------------- K3: grid decode */
+/*
+ * Decode blocks slots[0..nblk) on the uniform m^3 lattice (params
+ * linspace(0,1,m), fresh float64 clamped knots, bspline.py:109-125).
+ * out: nblk * m^3 float32 device buffer, block-major, x fastest within a
+ * block.  slots is a host array.
+ */
+int afam_decode_grid(afam_store *s, const int32_t *slots, int32_t nblk, int32_t m, float *out,
+                     void *stream);
+
+/* ------------------------------------------------------------ visibility */
+typedef struct afam_manifest afam_manifest;
+
+/* Level tables: bpa[l] blocks per axis and extents[l] (bpa^3 * 6 float64,
+ * index ((i*bpa+j)*bpa+k)*6) for lod = l+1.  A block missing from the
+ * manifest has NaN extents and is never emitted. */
+int afam_manifest_create(afam_manifest **out, int32_t levels, const int32_t *bpa,
+                         const double *const *extents);
+int afam_manifest_destroy(afam_manifest *m);
+
+/*
+ * render.select_visible: pos, and the PointOfView.basis() triad f, r, u
+ * (render.py:68-73), tan_y = tan(radians(fov_y)/2).  ranges may be NULL
+ * (0.8-wide default bands).  Writes sorted (lod,i,j,k) quadruples; returns
+ * AFAM_E_CAPACITY if more than cap blocks are visible.
+ */
+int afam_select_visible(const afam_manifest *m, const double pos[3], const double f[3], const double r[3],
+                        const double u[3], double tan_y, double aspect, double near_, const double *ranges,
+                        int32_t nranges, int32_t *out, int32_t cap, int32_t *count);
+
+/* --------------------------------------------------------------- K2: render */
+typedef struct {
+    double origin[3], f[3], r[3], u[3]; /* PointOfView position + basis() */
+    double tan_x, tan_y;                /* render.py:330-331 */
+    int32_t width, height;              /* full frame */
+    /* Rows rendered by this call: bands of band_rows rows, band b handled
+     * iff b % nparts == part.  Output rows are packed in band order. */
+    int32_t band_rows, nparts, part;
+    double sample_distance, power, o_max, near_;     /* RenderParams */
+    double ambient, diffuse, specular, shininess;
+    /* TransferFunction (render.py:93-124) */
+    int32_t ncolor, nopacity;
+    double domain_lo, domain_hi;
+    double color[AFAM_MAX_TF_POINTS][4];  /* scalar, r, g, b */
+    double opacity[AFAM_MAX_TF_POINTS][2];/* scalar, alpha */
+    uint32_t flags;                       /* AFAM_RENDER_* */
+} afam_frame;
+
+#define AFAM_RENDER_DEBUG 1u   /* write per-ray sample counts + owner hashes */
+
+typedef struct {
+    uint64_t samples;      /* decoded samples (value+gradient evaluations) */
+    int64_t missing_key;   /* (step << 32) | ray of the first sample in an uncovered finest cell, or -1 */
+    uint64_t fp64_samples; /* samples decoded on the float64 path */
+    uint64_t pad;
+} afam_render_stats;
+
+/*
+ * render.render for the resident blocks slots[0..nblocks) given in sorted
+ * BlockAddress order (host array; the finest-cell owner grid of
+ * render.py:357-375 is built from their extents).  rgba: device uint8
+ * buffer of (rows rendered) x width x 4.  stats: device afam_render_stats
+ * (zeroed by this call).  Debug (flags & AFAM_RENDER_DEBUG): nsamp[ray]
+ * int32 and ohash[ray] uint64 (FNV-1a over owner indices) device buffers.
+ */
+int afam_render(afam_store *s, const afam_frame *frame, const int32_t *slots, int32_t nblocks, uint8_t *rgba,
+                afam_render_stats *stats, int32_t *nsamp, uint64_t *ohash, void *stream);
+
+/* Rows of the full frame rendered by (band_rows, nparts, part). */
+int32_t afam_frame_rows(int32_t height, int32_t band_rows, int32_t nparts, int32_t part);
+
+/* Finest-cell owner grid of render.py:357-375 for the given slots (host). */
+int afam_owner_grid(afam_store *s, const int32_t *slots, int32_t nblocks, int32_t *cells, int32_t *grid,
+                    int32_t cap);
+
+/* ------------------------------------------------------------ tooling */
+/* FP32 FMA throughput probe (the K2 roofline denominator; MEASURED_PEAKS.json
+ * has no FP32 figure): independent FFMA chains on every SM; writes the
+ * elapsed ms and the FLOPs executed.  out: device float[148*8*256]. */
+int afam_bench_fma(float *out, int32_t iters, float *ms, double *flops, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AFAM_H_ */

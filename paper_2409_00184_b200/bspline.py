@@ -1,0 +1,120 @@
+"""B-spline decode entry points of the reference's bspline module, on B200.
+
+Drop-in for reference bspline.py:162-229 (evaluate_points,
+evaluate_points_with_gradient, decode_tensor_product): the arithmetic runs
+in libafam's K1 (point decode) and K3 (grid decode) kernels.  Results are
+float32 on device (float64 for ill-conditioned grids, see include/afam.h
+AFAM_SLOT_FP64) and returned as float64 arrays, within the 1e-5 x range
+gate of BASELINE.json's north_star.  Knot vectors travel as float32 (the
+.mfa storage type, FORMAT.md:22-30).
+
+The least-squares fit (bspline.py:109-159) is encoder-side and out of
+scope; clamped_knots is kept because callers build default knots with it.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from types import SimpleNamespace
+
+import numpy as np
+
+from . import _lib
+from .device import as_device_blocks, stream_handle
+
+__all__ = ["clamped_knots", "evaluate_points", "evaluate_points_with_gradient", "decode_tensor_product",
+           "eval_device", "decode_slots"]
+
+
+def clamped_knots(ncp: int, degree: int) -> np.ndarray:
+    """Full clamped uniform knot vector on [0, 1], length ncp+degree+1."""
+    if degree < 1:
+        raise ValueError(f"degree must be >= 1, got {degree}")
+    if ncp < degree + 1:
+        raise ValueError(f"ncp must be >= degree+1 ({degree + 1}), got {ncp}")
+    nspan = ncp - degree
+    inner = np.arange(1, nspan, dtype=np.float64) / nspan
+    return np.r_[np.zeros(degree + 1), inner, np.ones(degree + 1)]
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def eval_device(store, slots, points, gradient: bool = True, param: bool = False):
+    """K1 on resident slots: `slots` is one slot id or an int array (n,).
+    Returns values (n,) [and gradients (n, 3)] as float64 numpy arrays."""
+    torch = _torch()
+    pts = np.ascontiguousarray(np.atleast_2d(np.asarray(points, dtype=np.float64)))
+    if pts.shape[-1] != 3:
+        raise ValueError(f"points must have shape (n, 3), got {pts.shape}")
+    n = pts.shape[0]
+    dev = torch.device("cuda", store.device)
+    d_pts = torch.from_numpy(pts).to(dev, non_blocking=False)
+    d_val = torch.empty(n, dtype=torch.float32, device=dev)
+    d_grad = torch.empty((n, 3), dtype=torch.float32, device=dev) if gradient else None
+    one_slot, d_slots = 0, None
+    if np.ndim(slots) == 0:
+        one_slot = int(slots)
+    else:
+        d_slots = torch.from_numpy(np.ascontiguousarray(slots, dtype=np.int32)).to(dev)
+    flags = _lib.AFAM_EVAL_PARAM if param else 0
+    with torch.cuda.device(dev):
+        _lib.check(_lib.lib().afam_eval_points(
+            store.handle, None if d_slots is None else C.c_void_p(d_slots.data_ptr()), one_slot,
+            C.c_void_p(d_pts.data_ptr()), n, C.c_void_p(d_val.data_ptr()),
+            None if d_grad is None else C.c_void_p(d_grad.data_ptr()), flags, C.c_void_p(stream_handle(None, dev))))
+        val = d_val.cpu().numpy().astype(np.float64)
+        if not gradient:
+            return val
+        return val, d_grad.cpu().numpy().astype(np.float64)
+
+
+def decode_slots(store, slots, m: int) -> np.ndarray:
+    """K3 on resident slots -> (nblk, m, m, m) float64 array indexed [b, i, j, k]."""
+    torch = _torch()
+    slots = np.ascontiguousarray(slots, dtype=np.int32)
+    dev = torch.device("cuda", store.device)
+    out = torch.empty((len(slots), m, m, m), dtype=torch.float32, device=dev)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.lib().afam_decode_grid(store.handle, slots.ctypes.data_as(C.c_void_p), len(slots), int(m),
+                                               C.c_void_p(out.data_ptr()), C.c_void_p(stream_handle(None, dev))))
+        host = out.cpu().numpy()
+    # device layout is x fastest within a block: [b][k][j][i]
+    return np.ascontiguousarray(host.transpose(0, 3, 2, 1)).astype(np.float64)
+
+
+def _as_model(coeff, degree, knots):
+    c = np.asarray(coeff)
+    ncp = c.shape[0]
+    if c.ndim != 3 or c.shape[1] != ncp or c.shape[2] != ncp:
+        raise ValueError("coefficient grid must be cubic (isotropic ncp)")
+    if knots is None:
+        kv = np.repeat(clamped_knots(ncp, degree)[None, :], 3, axis=0)
+    else:
+        kv = np.stack([np.asarray(k, dtype=np.float64) for k in knots])
+    return SimpleNamespace(control=c, knots=kv.astype(np.float32), degree=int(degree),
+                           extent=np.array([[0.0, 1.0]] * 3), lod=1)
+
+
+def evaluate_points(coeff, degree: int, u, knots=None) -> np.ndarray:
+    """Spline values at parameters u (n, 3) (reference bspline.py:206-214)."""
+    store, (slot,) = as_device_blocks([_as_model(coeff, degree, knots)])
+    return eval_device(store, slot, u, gradient=False, param=True)
+
+
+def evaluate_points_with_gradient(coeff, degree: int, u, knots=None):
+    """Values and parameter-space gradients (reference bspline.py:217-229)."""
+    store, (slot,) = as_device_blocks([_as_model(coeff, degree, knots)])
+    return eval_device(store, slot, u, gradient=True, param=True)
+
+
+def decode_tensor_product(coeff, degree: int, dims) -> np.ndarray:
+    """Decode onto the uniform dims lattice (reference bspline.py:162-172)."""
+    d = tuple(int(v) for v in dims)
+    if d[0] != d[1] or d[1] != d[2]:
+        raise ValueError(f"decode dims must be cubic on the device path, got {d}")
+    store, (slot,) = as_device_blocks([_as_model(coeff, degree, None)])
+    return decode_slots(store, [slot], d[0])[0]

@@ -1,0 +1,229 @@
+// Device-side B-spline evaluation shared by K1 (points) and K2 (ray march).
+//
+// Restates, in registers, reference bspline.py:41-95 (span search and the
+// Cox-de Boor value/derivative recurrences) and bspline.py:175-229 (gather
+// of the (p+1)^3 control points and the tensor-product contraction), using
+// the per-span tables built by the store (afam_internal.h: tab_stride) so
+// the hot path has no divisions.
+#pragma once
+
+#include "afam_internal.h"
+
+namespace afam {
+
+template <typename T>
+__device__ __forceinline__ T clamp01(T v) {
+    return v < T(0) ? T(0) : (v > T(1) ? T(1) : v);
+}
+
+// searchsorted(knots, u, 'right') - 1 clipped to [deg, ncp-1]
+// (bspline.py:41-47): start from the uniform-knot guess and walk to the
+// exact span using the stored knots, so any (non-uniform) knot vector works.
+template <typename T>
+__device__ __forceinline__ int find_span(const float *__restrict__ kv, int ncp, int deg, int nspan, T u) {
+    int s = deg + min(max((int)(u * (T)nspan), 0), nspan - 1);
+    while (s > deg && u < (T)__ldg(kv + s)) --s;
+    while (s < ncp - 1 && u >= (T)__ldg(kv + s + 1)) ++s;
+    return s;
+}
+
+// Register copy of one table entry; only the first tab_stride(P) values are used.
+template <typename T>
+using Tab = T[kTabStrideMax];
+
+template <int P>
+__device__ __forceinline__ void load_entry(const float *__restrict__ p, Tab<float> &t) {
+    const float4 *q = reinterpret_cast<const float4 *>(p);
+#pragma unroll
+    for (int i = 0; i < tab_stride(P) / 4; i++) {
+        float4 v = __ldg(q + i);
+        t[4 * i] = v.x; t[4 * i + 1] = v.y; t[4 * i + 2] = v.z; t[4 * i + 3] = v.w;
+    }
+}
+
+template <int P>
+__device__ __forceinline__ void load_entry(const double *__restrict__ p, Tab<double> &t) {
+    const double2 *q = reinterpret_cast<const double2 *>(p);
+#pragma unroll
+    for (int i = 0; i < tab_stride(P) / 2; i++) {
+        double2 v = __ldg(q + i);
+        t[2 * i] = v.x; t[2 * i + 1] = v.y;
+    }
+}
+
+// Cox-de Boor (bspline.py:50-70) and degree-reduction derivatives
+// (bspline.py:73-95) from one table entry: window W = t[s-p+1 .. s+p],
+// inv[j][r] = 1/(t[s+r+1] - t[s+1-j+r]).
+template <int P, typename T>
+__device__ __forceinline__ void basis_eval(const Tab<T> &t, T u, T (&N)[P + 1], T (&D)[P + 1]) {
+    const T *W = t;
+    const T *inv = t + 2 * P;
+    T left[P + 1], right[P + 1], L[P];
+    N[0] = T(1);
+    int o = 0;
+#pragma unroll
+    for (int j = 1; j <= P; j++) {
+        left[j] = u - W[P - j];
+        right[j] = W[P - 1 + j] - u;
+        T saved = T(0);
+#pragma unroll
+        for (int r = 0; r < j; r++) {
+            T tmp = N[r] * inv[o + r];
+            N[r] = saved + right[r + 1] * tmp;
+            saved = left[j - r] * tmp;
+        }
+        N[j] = saved;
+        o += j;
+        if (j == P - 1) {
+#pragma unroll
+            for (int k = 0; k < P; k++) L[k] = N[k];
+        }
+    }
+    if (P == 1) L[0] = T(1);
+    const T *invP = inv + P * (P - 1) / 2;
+#pragma unroll
+    for (int j = 0; j <= P; j++) {
+        T term = T(0);
+        if (j > 0) term = L[j - 1] * invP[j - 1];
+        if (j < P) term = term - L[j] * invP[j];
+        D[j] = T(P) * term;
+    }
+}
+
+template <int P, typename T>
+__device__ __forceinline__ void basis_vals_only(const Tab<T> &t, T u, T (&N)[P + 1]) {
+    const T *W = t;
+    const T *inv = t + 2 * P;
+    T left[P + 1], right[P + 1];
+    N[0] = T(1);
+    int o = 0;
+#pragma unroll
+    for (int j = 1; j <= P; j++) {
+        left[j] = u - W[P - j];
+        right[j] = W[P - 1 + j] - u;
+        T saved = T(0);
+#pragma unroll
+        for (int r = 0; r < j; r++) {
+            T tmp = N[r] * inv[o + r];
+            N[r] = saved + right[r + 1] * tmp;
+            saved = left[j - r] * tmp;
+        }
+        N[j] = saved;
+        o += j;
+    }
+}
+
+// Separable contraction of the (P+1)^3 control points c[(cz*Q+by)*Q+ax]
+// (bspline.py:214, :224-228): x first, then y, then z.  2q^3+3q^2+4q FMAs.
+template <int P, typename T, typename CT>
+__device__ __forceinline__ void contract_grad(const CT (&c)[64], const T (&Nx)[P + 1],
+                                              const T (&Dx)[P + 1], const T (&Ny)[P + 1], const T (&Dy)[P + 1],
+                                              const T (&Nz)[P + 1], const T (&Dz)[P + 1], T &v, T g[3]) {
+    constexpr int Q = P + 1;
+    T ry[Q], rdxy[Q], rdy[Q];
+#pragma unroll
+    for (int cz = 0; cz < Q; cz++) {
+        T ay = T(0), adxy = T(0), ady = T(0);
+#pragma unroll
+        for (int by = 0; by < Q; by++) {
+            T rx = T(0), rdx = T(0);
+#pragma unroll
+            for (int ax = 0; ax < Q; ax++) {
+                T cv = (T)c[(cz * Q + by) * Q + ax];
+                rx = fma(Nx[ax], cv, rx);
+                rdx = fma(Dx[ax], cv, rdx);
+            }
+            ay = fma(Ny[by], rx, ay);
+            adxy = fma(Ny[by], rdx, adxy);
+            ady = fma(Dy[by], rx, ady);
+        }
+        ry[cz] = ay; rdxy[cz] = adxy; rdy[cz] = ady;
+    }
+    T vv = T(0), gx = T(0), gy = T(0), gz = T(0);
+#pragma unroll
+    for (int cz = 0; cz < Q; cz++) {
+        vv = fma(Nz[cz], ry[cz], vv);
+        gx = fma(Nz[cz], rdxy[cz], gx);
+        gy = fma(Nz[cz], rdy[cz], gy);
+        gz = fma(Dz[cz], ry[cz], gz);
+    }
+    v = vv; g[0] = gx; g[1] = gy; g[2] = gz;
+}
+
+template <int P, typename T, typename CT>
+__device__ __forceinline__ T contract_val(const CT (&c)[64], const T (&Nx)[P + 1],
+                                          const T (&Ny)[P + 1], const T (&Nz)[P + 1]) {
+    constexpr int Q = P + 1;
+    T vv = T(0);
+#pragma unroll
+    for (int cz = 0; cz < Q; cz++) {
+        T ay = T(0);
+#pragma unroll
+        for (int by = 0; by < Q; by++) {
+            T rx = T(0);
+#pragma unroll
+            for (int ax = 0; ax < Q; ax++) rx = fma(Nx[ax], (T)c[(cz * Q + by) * Q + ax], rx);
+            ay = fma(Ny[by], rx, ay);
+        }
+        vv = fma(Nz[cz], ay, vv);
+    }
+    return vv;
+}
+
+// Gather the (P+1)^3 control points at corner (x0,y0,z0) (bspline.py:175-181).
+template <int P>
+__device__ __forceinline__ void gather(const float *__restrict__ ctrl, int ncp, int pitch, int x0, int y0, int z0,
+                                       float (&c)[64]) {
+    constexpr int Q = P + 1;
+#pragma unroll
+    for (int cz = 0; cz < Q; cz++)
+#pragma unroll
+        for (int by = 0; by < Q; by++) {
+            const float *row = ctrl + ((size_t)(z0 + cz) * ncp + (y0 + by)) * pitch + x0;
+#pragma unroll
+            for (int ax = 0; ax < Q; ax++) c[(cz * Q + by) * Q + ax] = __ldg(row + ax);
+        }
+}
+
+// One full evaluation (no caching): parameters u in [0,1]^3 -> value and
+// parameter-space gradient (bspline.py:217-229).
+template <int P, typename T, bool GRAD>
+__device__ __forceinline__ T eval_uncached(const BlockDesc &d, const T (&u)[3], T g[3]) {
+    Tab<T> te[3];
+    int s[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        s[a] = find_span<T>(d.knots + a * d.nk, d.ncp, P, d.nspan, u[a]);
+        const size_t off = ((size_t)a * d.nspan + (s[a] - P)) * tab_stride(P);
+        if constexpr (sizeof(T) == 4) load_entry<P>(d.tab32 + off, te[a]);
+        else load_entry<P>(d.tab64 + off, te[a]);
+    }
+    float c[64];
+    gather<P>(d.ctrl, d.ncp, d.pitch, s[0] - P, s[1] - P, s[2] - P, c);
+    if constexpr (GRAD) {
+        T Nx[P + 1], Dx[P + 1], Ny[P + 1], Dy[P + 1], Nz[P + 1], Dz[P + 1];
+        basis_eval<P, T>(te[0], u[0], Nx, Dx);
+        basis_eval<P, T>(te[1], u[1], Ny, Dy);
+        basis_eval<P, T>(te[2], u[2], Nz, Dz);
+        T v;
+        contract_grad<P, T, float>(c, Nx, Dx, Ny, Dy, Nz, Dz, v, g);
+        return v;
+    } else {
+        T Nx[P + 1], Ny[P + 1], Nz[P + 1];
+        basis_vals_only<P, T>(te[0], u[0], Nx);
+        basis_vals_only<P, T>(te[1], u[1], Ny);
+        basis_vals_only<P, T>(te[2], u[2], Nz);
+        return contract_val<P, T, float>(c, Nx, Ny, Nz);
+    }
+}
+
+__device__ __forceinline__ BlockDesc load_desc(const BlockDesc *__restrict__ p) {
+    BlockDesc d;
+    const int4 *src = reinterpret_cast<const int4 *>(p);
+    int4 *dst = reinterpret_cast<int4 *>(&d);
+#pragma unroll
+    for (int i = 0; i < (int)(sizeof(BlockDesc) / 16); i++) dst[i] = __ldg(src + i);
+    return d;
+}
+
+}  // namespace afam

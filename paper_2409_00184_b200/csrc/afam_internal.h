@@ -1,0 +1,109 @@
+// Internal definitions shared by the libafam translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/afam.h"
+
+namespace afam {
+
+// Per-span basis table entry (built by the K4 unpack kernel, read by K1/K2).
+// For degree p and span s the entry holds
+//   W[k]   = t[s-p+1+k],                     k = 0 .. 2p-1   (knot window)
+//   inv    = 1/(t[s+r+1] - t[s+1-j+r])       j = 1..p, r = 0..j-1 (row-major)
+// i.e. every Cox-de Boor denominator of bspline.py:62-68 and the two
+// derivative denominators of bspline.py:91-93 (the j = p row), so basis
+// values and derivatives need no division on the hot path.
+__host__ __device__ constexpr int tab_stride(int p) {
+    return ((2 * p + p * (p + 1) / 2) + 3) / 4 * 4;  // p=1:4 p=2:8 p=3:12
+}
+constexpr int kTabStrideMax = 12;  // tab_stride(AFAM_MAX_DEGREE)
+
+// Device-resident descriptor of one slot (one micro-model).
+struct alignas(16) BlockDesc {
+    const float *ctrl;    // ncp x ncp rows of `pitch` floats: ctrl[(iz*ncp+iy)*pitch+ix]
+    const float *tab32;   // [3][nspan][tab_stride(deg)] float
+    const double *tab64;  // [3][nspan][tab_stride(deg)] double
+    const float *knots;   // [3][nk] float (full clamped vectors)
+    double lo[3];         // extent low corner
+    double span[3];       // hi - lo
+    double inv_span[3];   // 1 / (hi - lo)
+    int32_t ncp, deg, pitch, nk;
+    int32_t nspan;        // ncp - deg
+    uint32_t flags;       // AFAM_SLOT_*
+    float max_abs;
+    int32_t pad;
+};
+
+// Host mirror of a slot.
+struct SlotHost {
+    bool valid = false;
+    int32_t ncp = 0, deg = 0;
+    double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+    cudaEvent_t ready = nullptr;  // recorded after the upload kernels
+};
+
+struct DecodeOp {  // banded collocation matrix of bspline.py:98-125 for (ncp, deg, m)
+    float *b32 = nullptr;   // [m][4]
+    double *b64 = nullptr;  // [m][4]
+    int32_t *col0 = nullptr;// [m] first nonzero column (span - deg)
+};
+
+}  // namespace afam
+
+struct afam_store {
+    int device = 0;
+    int32_t nslots = 0, max_ncp = 0;
+    double fp64_limit = 4.0;
+    size_t raw_bytes = 0, ctrl_floats = 0, knot_floats = 0, tab_elems = 0, slot_bytes = 0;
+    char *arena = nullptr;               // nslots * slot_bytes device bytes
+    afam::BlockDesc *d_desc = nullptr;   // nslots descriptors (device)
+    float *d_maxabs = nullptr;           // nslots (device)
+    std::vector<afam::SlotHost> host;
+    std::mutex mu;
+    std::map<std::tuple<int, int, int>, afam::DecodeOp> ops;
+
+    char *slot_base(int32_t slot) const { return arena + (size_t)slot * slot_bytes; }
+    uint8_t *raw_ptr(int32_t slot) const { return (uint8_t *)slot_base(slot); }
+    float *ctrl_ptr(int32_t slot) const { return (float *)(slot_base(slot) + raw_off()); }
+    float *knot_ptr(int32_t slot) const { return (float *)(slot_base(slot) + knot_off()); }
+    float *tab32_ptr(int32_t slot) const { return (float *)(slot_base(slot) + tab32_off()); }
+    double *tab64_ptr(int32_t slot) const { return (double *)(slot_base(slot) + tab64_off()); }
+    static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
+    size_t raw_off() const { return align256(raw_bytes); }
+    size_t knot_off() const { return raw_off() + align256(ctrl_floats * 4); }
+    size_t tab32_off() const { return knot_off() + align256(knot_floats * 4); }
+    size_t tab64_off() const { return tab32_off() + align256(tab_elems * 4); }
+};
+
+struct afam_manifest {
+    int32_t levels = 0;
+    std::vector<int32_t> bpa;
+    std::vector<std::vector<double>> extents;  // per level, bpa^3*6
+};
+
+namespace afam {
+void set_error(const char *fmt, ...);
+int cuda_fail(cudaError_t e, const char *what);
+}  // namespace afam
+
+#define AFAM_CUDA(call)                                                         \
+    do {                                                                        \
+        cudaError_t e_ = (call);                                                \
+        if (e_ != cudaSuccess) return afam::cuda_fail(e_, #call);               \
+    } while (0)
+
+#define AFAM_CHECK(cond, code, ...)                                             \
+    do {                                                                        \
+        if (!(cond)) {                                                          \
+            afam::set_error(__VA_ARGS__);                                       \
+            return code;                                                        \
+        }                                                                       \
+    } while (0)

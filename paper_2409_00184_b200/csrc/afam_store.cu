@@ -1,0 +1,316 @@
+// Device store of micro-models (K4): slot arena, .mfa ingest, per-span tables.
+//
+// Replaces the read side of store.load_model / model.deserialize
+// (reference store.py:43-47, model.py:121-148) with an HBM-resident slot
+// arena.  The .mfa payload is misaligned (knots at byte 1, control points
+// at byte 1+12(ncp+d), FORMAT.md:24-30), so the raw file image is copied
+// H2D verbatim and realigned on device by unpack_ctrl_kernel /
+// build_tables_kernel; no host-side repacking.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "afam_internal.h"
+
+namespace afam {
+
+static thread_local std::string g_err;
+
+void set_error(const char *fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+}
+
+int cuda_fail(cudaError_t e, const char *what) {
+    set_error("CUDA error %s (%s) in %s", cudaGetErrorName(e), cudaGetErrorString(e), what);
+    return AFAM_E_CUDA;
+}
+
+static __device__ __forceinline__ float load_le_f32(const uint8_t *p) {
+    uint32_t v = (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
+    return __uint_as_float(v);
+}
+
+// One thread per padded control point: gather the little-endian float32 at
+// byte offset src_off + 4*(ix + ncp*(iy + ncp*iz)) (x fastest, FORMAT.md:57-61)
+// into the row-pitched layout ctrl[(iz*ncp + iy)*pitch + ix]; padding is 0.
+// Also reduces max |c| into *maxabs (float bits are ordered for c >= 0).
+__global__ void unpack_ctrl_kernel(const uint8_t *__restrict__ raw, uint64_t src_off, int ncp, int pitch,
+                                   float *__restrict__ ctrl, unsigned int *maxabs) {
+    const int64_t total = (int64_t)ncp * ncp * pitch;
+    float m = 0.f;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int ix = (int)(i % pitch);
+        int64_t row = i / pitch;  // iz*ncp + iy
+        float v = 0.f;
+        if (ix < ncp) {
+            v = load_le_f32(raw + src_off + 4 * ((uint64_t)row * ncp + ix));
+            m = fmaxf(m, fabsf(v));
+        }
+        ctrl[i] = v;
+    }
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(maxabs, __float_as_uint(m));
+}
+
+// Knots + per-span basis tables + the slot descriptor.  knot_off: byte
+// offset of the knots; has_t0 = 0 for .mfa images (t0 = 0 implicit,
+// FORMAT.md:44-55), 1 for full vectors.
+__global__ void build_tables_kernel(const uint8_t *__restrict__ raw, uint64_t knot_off, int has_t0, int ncp,
+                                    int deg, float *__restrict__ knots, float *__restrict__ tab32,
+                                    double *__restrict__ tab64, BlockDesc *desc, BlockDesc proto,
+                                    const unsigned int *maxabs, float fp64_limit) {
+    const int nk = ncp + deg + 1;
+    const int nspan = ncp - deg;
+    const int ts = tab_stride(deg);
+    auto knot = [&](int a, int k) -> float {
+        if (has_t0) return load_le_f32(raw + knot_off + 4 * (uint64_t)(a * nk + k));
+        if (k == 0) return 0.f;
+        return load_le_f32(raw + knot_off + 4 * (uint64_t)(a * (nk - 1) + (k - 1)));
+    };
+    for (int i = threadIdx.x; i < 3 * nk; i += blockDim.x) knots[i] = knot(i / nk, i % nk);
+    for (int i = threadIdx.x; i < 3 * nspan; i += blockDim.x) {
+        const int a = i / nspan, s = deg + i % nspan;
+        double W[2 * AFAM_MAX_DEGREE];
+        for (int k = 0; k < 2 * deg; k++) {
+            int idx = s - deg + 1 + k;
+            W[k] = (idx >= 0 && idx < nk) ? (double)knot(a, idx) : 0.0;
+        }
+        float *e32 = tab32 + (size_t)i * ts;
+        double *e64 = tab64 + (size_t)i * ts;
+        for (int k = 0; k < 2 * deg; k++) { e32[k] = (float)W[k]; e64[k] = W[k]; }
+        int o = 2 * deg;
+        for (int j = 1; j <= deg; j++)
+            for (int r = 0; r < j; r++, o++) {
+                // t[s+r+1] - t[s+1-j+r] = W[deg+r] - W[deg-j+r]
+                double den = W[deg + r] - W[deg - j + r];
+                double inv = den != 0.0 ? 1.0 / den : 0.0;
+                e32[o] = (float)inv;
+                e64[o] = inv;
+            }
+        for (; o < ts; o++) { e32[o] = 0.f; e64[o] = 0.0; }
+    }
+    if (threadIdx.x == 0) {
+        BlockDesc d = proto;
+        d.max_abs = __uint_as_float(*maxabs);
+        d.flags = AFAM_SLOT_VALID | (d.max_abs > fp64_limit ? AFAM_SLOT_FP64 : 0u);
+        *desc = d;
+    }
+}
+
+}  // namespace afam
+
+using namespace afam;
+
+extern "C" {
+
+const char *afam_last_error(void) { return g_err.c_str(); }
+int afam_version(void) { return 1; }
+
+int afam_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+static size_t serialized_size(int64_t ncp, int64_t deg) { return 1 + (size_t)((ncp + deg) * 3 + ncp * ncp * ncp) * 4; }
+static int pitch_for(int ncp) { return (ncp + 3) & ~3; }
+
+int afam_store_create(afam_store **out, int device, int32_t slots, int32_t max_ncp, double fp64_ctrl_limit) {
+    AFAM_CHECK(out, AFAM_E_VALUE, "afam_store_create: out is NULL");
+    AFAM_CHECK(slots >= 1, AFAM_E_VALUE, "cache capacity must be at least 1 slot");
+    AFAM_CHECK(max_ncp >= 2 && max_ncp <= 1024, AFAM_E_VALUE, "max_ncp %d out of range", max_ncp);
+    AFAM_CUDA(cudaSetDevice(device));
+    afam_store *s = new afam_store();
+    s->device = device;
+    s->nslots = slots;
+    s->max_ncp = max_ncp;
+    s->fp64_limit = fp64_ctrl_limit > 0 ? fp64_ctrl_limit : 4.0;
+    const size_t P = (size_t)pitch_for(max_ncp);
+    // raw staging must also hold a decoded (full-knot) upload: 3*(ncp+4) + ncp^3 floats
+    s->raw_bytes = std::max(serialized_size(max_ncp, AFAM_MAX_DEGREE),
+                            (size_t)(3 * (max_ncp + AFAM_MAX_DEGREE + 1) + (size_t)max_ncp * max_ncp * max_ncp) * 4 + 64);
+    s->ctrl_floats = P * max_ncp * max_ncp;
+    s->knot_floats = 3 * (size_t)(max_ncp + AFAM_MAX_DEGREE + 1);
+    s->tab_elems = 3 * (size_t)max_ncp * kTabStrideMax;
+    s->slot_bytes = s->tab64_off() + afam_store::align256(s->tab_elems * 8);
+    cudaError_t e = cudaMalloc(&s->arena, s->slot_bytes * (size_t)slots);
+    if (e != cudaSuccess) {
+        delete s;
+        if (e == cudaErrorMemoryAllocation) {
+            set_error("device store of %d slots x %zu bytes does not fit in device memory", slots,
+                      (size_t)0);
+            return AFAM_E_CAPACITY;
+        }
+        return cuda_fail(e, "cudaMalloc(arena)");
+    }
+    AFAM_CUDA(cudaMalloc(&s->d_desc, sizeof(BlockDesc) * slots));
+    AFAM_CUDA(cudaMemset(s->d_desc, 0, sizeof(BlockDesc) * slots));
+    AFAM_CUDA(cudaMalloc(&s->d_maxabs, sizeof(float) * slots));
+    s->host.resize(slots);
+    for (auto &h : s->host) AFAM_CUDA(cudaEventCreateWithFlags(&h.ready, cudaEventDisableTiming));
+    *out = s;
+    return AFAM_OK;
+}
+
+int afam_store_destroy(afam_store *s) {
+    if (!s) return AFAM_OK;
+    cudaSetDevice(s->device);
+    cudaDeviceSynchronize();
+    for (auto &h : s->host)
+        if (h.ready) cudaEventDestroy(h.ready);
+    for (auto &kv : s->ops) {
+        cudaFree(kv.second.b32);
+        cudaFree(kv.second.b64);
+        cudaFree(kv.second.col0);
+    }
+    cudaFree(s->arena);
+    cudaFree(s->d_desc);
+    cudaFree(s->d_maxabs);
+    delete s;
+    return AFAM_OK;
+}
+
+int afam_store_slots(const afam_store *s, int32_t *slots, int32_t *max_ncp) {
+    AFAM_CHECK(s, AFAM_E_VALUE, "store is NULL");
+    if (slots) *slots = s->nslots;
+    if (max_ncp) *max_ncp = s->max_ncp;
+    return AFAM_OK;
+}
+
+// Shared tail of both put paths: raw region already holds the bytes (queued on stream).
+static int launch_unpack(afam_store *s, int32_t slot, int deg, int ncp, uint64_t knot_off, int has_t0,
+                         uint64_t ctrl_off, const double extent[6], cudaStream_t st) {
+    BlockDesc proto{};
+    proto.ctrl = s->ctrl_ptr(slot);
+    proto.tab32 = s->tab32_ptr(slot);
+    proto.tab64 = s->tab64_ptr(slot);
+    proto.knots = s->knot_ptr(slot);
+    for (int a = 0; a < 3; a++) {
+        proto.lo[a] = extent[2 * a];
+        proto.span[a] = extent[2 * a + 1] - extent[2 * a];
+        proto.inv_span[a] = 1.0 / proto.span[a];
+    }
+    proto.ncp = ncp;
+    proto.deg = deg;
+    proto.pitch = pitch_for(ncp);
+    proto.nk = ncp + deg + 1;
+    proto.nspan = ncp - deg;
+    AFAM_CUDA(cudaMemsetAsync(s->d_maxabs + slot, 0, sizeof(float), st));
+    const int64_t total = (int64_t)ncp * ncp * proto.pitch;
+    int grid = (int)std::min<int64_t>((total + 255) / 256, 1184);
+    unpack_ctrl_kernel<<<grid, 256, 0, st>>>(s->raw_ptr(slot), ctrl_off, ncp, proto.pitch, s->ctrl_ptr(slot),
+                                             (unsigned int *)(s->d_maxabs + slot));
+    build_tables_kernel<<<1, 256, 0, st>>>(s->raw_ptr(slot), knot_off, has_t0, ncp, deg, s->knot_ptr(slot),
+                                           s->tab32_ptr(slot), s->tab64_ptr(slot), s->d_desc + slot, proto,
+                                           (const unsigned int *)(s->d_maxabs + slot), (float)s->fp64_limit);
+    AFAM_CUDA(cudaGetLastError());
+    SlotHost &h = s->host[slot];
+    h.valid = true;
+    h.ncp = ncp;
+    h.deg = deg;
+    for (int a = 0; a < 3; a++) { h.lo[a] = extent[2 * a]; h.hi[a] = extent[2 * a + 1]; }
+    AFAM_CUDA(cudaEventRecord(h.ready, st));
+    return AFAM_OK;
+}
+
+static int check_put(afam_store *s, int32_t slot, int deg, int ncp, const double *extent) {
+    AFAM_CHECK(s, AFAM_E_VALUE, "store is NULL");
+    AFAM_CHECK(slot >= 0 && slot < s->nslots, AFAM_E_VALUE, "slot %d outside [0, %d)", slot, s->nslots);
+    AFAM_CHECK(ncp <= s->max_ncp, AFAM_E_CAPACITY, "ncp %d exceeds the store's max_ncp %d", ncp, s->max_ncp);
+    AFAM_CHECK(deg >= 1 && deg <= AFAM_MAX_DEGREE, AFAM_E_VALUE,
+               "degree %d is not supported by the device path (1..%d)", deg, AFAM_MAX_DEGREE);
+    AFAM_CHECK(extent, AFAM_E_VALUE, "extent is NULL");
+    for (int a = 0; a < 3; a++)
+        AFAM_CHECK(extent[2 * a + 1] > extent[2 * a], AFAM_E_VALUE, "degenerate extent");
+    return AFAM_OK;
+}
+
+int afam_store_put_mfa(afam_store *s, int32_t slot, const uint8_t *bytes, uint64_t nbytes, int32_t ncp,
+                       const double extent[6], void *stream) {
+    AFAM_CHECK(bytes && nbytes >= 1, AFAM_E_FORMAT, "empty micro-model byte string");
+    const int deg = bytes[0];
+    // model.py:123-133
+    AFAM_CHECK(deg < ncp, AFAM_E_FORMAT, "degree byte %d >= ncp %d", deg, ncp);
+    const size_t expected = serialized_size(ncp, deg);
+    AFAM_CHECK(nbytes == expected, AFAM_E_FORMAT,
+               "micro-model length mismatch: expected %zu bytes for ncp=%d, degree=%d, found %llu", expected,
+               ncp, deg, (unsigned long long)nbytes);
+    int rc = check_put(s, slot, deg, ncp, extent);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    std::lock_guard<std::mutex> lk(s->mu);
+    AFAM_CUDA(cudaSetDevice(s->device));
+    // the previous upload into this slot (possibly on another stream) must be done
+    AFAM_CUDA(cudaStreamWaitEvent(st, s->host[slot].ready, 0));
+    AFAM_CUDA(cudaMemcpyAsync(s->raw_ptr(slot), bytes, nbytes, cudaMemcpyHostToDevice, st));
+    return launch_unpack(s, slot, deg, ncp, 1, 0, 1 + 12ull * (ncp + deg), extent, st);
+}
+
+int afam_store_put(afam_store *s, int32_t slot, int32_t degree, int32_t ncp, const float *knots,
+                   const float *ctrl, const double extent[6], void *stream) {
+    int rc = check_put(s, slot, degree, ncp, extent);
+    if (rc) return rc;
+    AFAM_CHECK(knots && ctrl, AFAM_E_VALUE, "knots/ctrl is NULL");
+    cudaStream_t st = (cudaStream_t)stream;
+    std::lock_guard<std::mutex> lk(s->mu);
+    AFAM_CUDA(cudaSetDevice(s->device));
+    const size_t kb = sizeof(float) * 3 * (size_t)(ncp + degree + 1);
+    const size_t cb = sizeof(float) * (size_t)ncp * ncp * ncp;
+    const uint64_t koff = 0, coff = (kb + 15) & ~(size_t)15;
+    AFAM_CUDA(cudaStreamWaitEvent(st, s->host[slot].ready, 0));
+    AFAM_CUDA(cudaMemcpyAsync(s->raw_ptr(slot) + koff, knots, kb, cudaMemcpyHostToDevice, st));
+    AFAM_CUDA(cudaMemcpyAsync(s->raw_ptr(slot) + coff, ctrl, cb, cudaMemcpyHostToDevice, st));
+    return launch_unpack(s, slot, degree, ncp, koff, 1, coff, extent, st);
+}
+
+int afam_store_evict(afam_store *s, int32_t slot) {
+    AFAM_CHECK(s, AFAM_E_VALUE, "store is NULL");
+    AFAM_CHECK(slot >= 0 && slot < s->nslots, AFAM_E_VALUE, "slot %d outside [0, %d)", slot, s->nslots);
+    std::lock_guard<std::mutex> lk(s->mu);
+    s->host[slot].valid = false;
+    return AFAM_OK;
+}
+
+int afam_store_info(afam_store *s, int32_t slot, int32_t *ncp, int32_t *degree, uint32_t *flags,
+                    float *max_abs_ctrl) {
+    AFAM_CHECK(s, AFAM_E_VALUE, "store is NULL");
+    AFAM_CHECK(slot >= 0 && slot < s->nslots, AFAM_E_VALUE, "slot %d outside [0, %d)", slot, s->nslots);
+    AFAM_CUDA(cudaSetDevice(s->device));
+    SlotHost &h = s->host[slot];
+    AFAM_CHECK(h.valid, AFAM_E_VALUE, "slot %d is empty", slot);
+    AFAM_CUDA(cudaEventSynchronize(h.ready));
+    BlockDesc d;
+    AFAM_CUDA(cudaMemcpy(&d, s->d_desc + slot, sizeof(d), cudaMemcpyDeviceToHost));
+    if (ncp) *ncp = d.ncp;
+    if (degree) *degree = d.deg;
+    if (flags) *flags = d.flags;
+    if (max_abs_ctrl) *max_abs_ctrl = d.max_abs;
+    return AFAM_OK;
+}
+
+int afam_store_read(afam_store *s, int32_t slot, float *ctrl, float *knots) {
+    AFAM_CHECK(s, AFAM_E_VALUE, "store is NULL");
+    AFAM_CHECK(slot >= 0 && slot < s->nslots, AFAM_E_VALUE, "slot %d outside [0, %d)", slot, s->nslots);
+    SlotHost &h = s->host[slot];
+    AFAM_CHECK(h.valid, AFAM_E_VALUE, "slot %d is empty", slot);
+    AFAM_CUDA(cudaSetDevice(s->device));
+    AFAM_CUDA(cudaEventSynchronize(h.ready));
+    const int ncp = h.ncp, P = pitch_for(ncp);
+    if (ctrl) {
+        // strip the row padding: rows of ncp floats at pitch P
+        AFAM_CUDA(cudaMemcpy2D(ctrl, sizeof(float) * ncp, s->ctrl_ptr(slot), sizeof(float) * P,
+                               sizeof(float) * ncp, (size_t)ncp * ncp, cudaMemcpyDeviceToHost));
+    }
+    if (knots)
+        AFAM_CUDA(cudaMemcpy(knots, s->knot_ptr(slot), sizeof(float) * 3 * (ncp + h.deg + 1),
+                             cudaMemcpyDeviceToHost));
+    return AFAM_OK;
+}
+
+}  // extern "C"

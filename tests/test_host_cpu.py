@@ -1,0 +1,184 @@
+"""CPU tests of the product's host side: the C-ABI library loads and exports
+every symbol include/afam.h declares, native visibility is bit-exact with
+the reference (golden), and the format / manifest / synthesis helpers
+behave like the reference.  No device compute here."""
+
+import json
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from helpers import golden_store, npz, pov_ns, vis_for
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2409_00184_b200 import _lib
+
+    hdr = (ROOT / "include" / "afam.h").read_text()
+    declared = set(re.findall(r"\b(afam_[a-z0-9_]+)\s*\(", hdr))
+    bound = {name for name, _, _ in _lib.SIGNATURES}
+    assert declared == bound, declared ^ bound
+    lib = _lib.lib()
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert lib.afam_version() == 1
+
+
+def test_struct_layouts_match_header():
+    """ctypes mirrors of afam_frame / afam_render_stats have the C sizes."""
+    import ctypes as C
+
+    from paper_2409_00184_b200 import _lib
+
+    assert C.sizeof(_lib.AfamRenderStats) == 32
+    # 12 + 2 doubles, 5 ints (+pad), 8 doubles, 2 ints, 2 doubles, 32*4 + 32*2 doubles, flags (+pad)
+    expect = 14 * 8 + 5 * 4 + 4 + 8 * 8 + 2 * 4 + 2 * 8 + 32 * 4 * 8 + 32 * 2 * 8 + 8
+    assert C.sizeof(_lib.AfamFrame) == expect
+
+
+def test_no_device_raises_loudly():
+    from paper_2409_00184_b200 import _lib
+
+    if _lib.lib().afam_device_count() > 0:
+        pytest.skip("a CUDA device is present")
+    with pytest.raises(RuntimeError, match="no CUDA device"):
+        _lib.require_device()
+
+
+def test_frame_rows_partition():
+    from paper_2409_00184_b200 import _lib
+
+    lib = _lib.lib()
+    for H in (1, 7, 64, 1000, 1024):
+        for br in (1, 8, 16):
+            for n in (1, 2, 3, 8):
+                assert sum(lib.afam_frame_rows(H, br, n, p) for p in range(n)) == H
+
+
+@pytest.mark.parametrize("name", ["smooth33", "ml65_p3", "config3", "config2"])
+def test_native_select_visible_bit_exact(name):
+    from paper_2409_00184_b200 import partition, render
+
+    z = npz("visible.npz")
+    man = partition.LODManifest.from_json(json.loads(bytes(z[f"{name}_manifest"]).decode()))
+    table, rtable = z[f"{name}_vis"], z[f"{name}_vis_ranges"]
+    bad = 0
+    for pi, row in enumerate(z["povs"]):
+        pov = pov_ns(row)  # the reference's stored (already normalized) camera
+        for col in (2, 3):
+            got = [(a.lod, *a.ijk) for a in render.select_visible(pov, man, aspect=col / 2.0)]
+            bad += got != vis_for(table, pi, col)
+        if pi < 40:
+            for ri, ranges in enumerate([(1e-9, 2e-9, 3e-9), (1e9, 2e9, 3e9), (0.5, 1.0, 1.7)]):
+                got = [(a.lod, *a.ijk) for a in render.select_visible(pov, man, 1.0, ranges=ranges[: man.levels - 1])]
+                bad += got != vis_for(rtable, pi, ri)
+    assert bad == 0
+
+
+def test_lod_for_distance_frozen():
+    from paper_2409_00184_b200 import render
+
+    z = npz("visible.npz")
+    for d, l4, l2 in zip(z["lod_d"], z["lod_l4"], z["lod_l2"]):
+        assert render.lod_for_distance(float(d), 4) == l4
+        assert render.lod_for_distance(float(d), 2) == l2
+    with pytest.raises(ValueError):
+        render.lod_for_distance(-0.1, 4)
+
+
+def test_mfa_codec_round_trip_golden():
+    from paper_2409_00184_b200 import model
+
+    man, models, raw = golden_store("ml65_p3")
+    for a, data in raw.items():
+        m = model.deserialize(data, man.entries[a].ncp, man.entries[a].extent, a.lod)
+        np.testing.assert_array_equal(m.control, models[a].control)
+        np.testing.assert_array_equal(m.knots, models[a].knots)
+        assert model.serialize(m) == data
+        assert m.nbytes == len(data) == model.serialized_size(m.ncp, m.degree)
+
+
+def test_mfa_format_errors():
+    from paper_2409_00184_b200 import model
+    from paper_2409_00184_b200.errors import FormatError
+
+    man, models, raw = golden_store("smooth33")
+    a, data = next(iter(raw.items()))
+    ncp = man.entries[a].ncp
+    with pytest.raises(FormatError, match="length mismatch"):
+        model.deserialize(data[:-1], ncp, man.entries[a].extent, a.lod)
+    with pytest.raises(FormatError, match="degree byte"):
+        model.deserialize(bytes([ncp]) + data[1:], ncp, man.entries[a].extent, a.lod)
+    with pytest.raises(FormatError, match="empty"):
+        model.deserialize(b"", ncp, man.entries[a].extent, a.lod)
+    assert model.serialized_size(3, 2) == 169 and model.serialized_size(4, 2) == 329  # FORMAT.md:38-40
+
+
+def test_manifest_json_round_trip(tmp_path):
+    from paper_2409_00184_b200 import partition
+
+    z = npz("store_smooth33.npz")
+    obj = json.loads(bytes(z["manifest"]).decode())
+    man = partition.LODManifest.from_json(obj)
+    man.save(tmp_path)
+    back = partition.LODManifest.load(tmp_path)
+    assert back.to_json() == man.to_json()
+    assert json.loads(json.dumps(man.to_json())) == obj
+
+
+def test_skeleton_matches_reference_extents():
+    from paper_2409_00184_b200 import partition
+
+    z = npz("visible.npz")
+    obj = json.loads(bytes(z["config3_manifest"]).decode())
+    ref = partition.LODManifest.from_json(obj)
+    sk = partition.skeleton(4, 2, 65)
+    assert set(sk.entries) == set(ref.entries) and len(sk.entries) == 4680
+    for a, e in ref.entries.items():
+        np.testing.assert_array_equal(sk.entries[a].extent, e.extent)
+
+
+def test_fit_operator_reproduces_polynomials():
+    from paper_2409_00184_b200 import synth
+
+    for m, ncp, d in [(9, 7, 3), (17, 12, 2), (65, 40, 3)]:
+        P = synth.fit_operator(m, ncp, d)
+        x = np.linspace(0, 1, m)
+        assert np.allclose(P @ np.ones(m), 1.0, atol=1e-12)
+        c = P @ (0.3 + 0.7 * x)  # the clamped B-spline space contains linear functions
+        assert c[0] == pytest.approx(0.3) and c[-1] == pytest.approx(1.0)
+
+
+def test_fit_operator_matches_reference_fit():
+    """Synthetic stores are fitted like the reference encoder (golden d-cases)."""
+    from paper_2409_00184_b200 import synth
+
+    z = npz("bspline.npz")
+    for j, (ncp, degree, m) in enumerate(z["dcases"]):
+        ncp, degree, m = int(ncp), int(degree), int(m)
+        x = np.linspace(0.0, 7.0, m)
+        X, Y, Zc = np.meshgrid(x, x, x, indexing="ij")
+        s = synth.ml_value(X, Y, Zc).astype(np.float32).astype(np.float64)
+        P = synth.fit_operator(m, ncp, degree)
+        c = np.einsum("ai,ijk->ajk", P, s)
+        c = np.einsum("bj,ajk->abk", P, c)
+        c = np.einsum("ck,abk->abc", P, c)
+        ref = z[f"d{j}_control"]
+        tol = 1e-5 * max(1.0, np.abs(ref).max())
+        assert np.abs(c.astype(np.float32) - ref).max() <= tol
+
+
+def test_ncp_rule_and_pack():
+    from paper_2409_00184_b200 import model, synth
+    from paper_2409_00184_b200.partition import BlockAddress
+
+    ns = [synth.ncp_for(BlockAddress(1, (i, j, 0))) for i in range(16) for j in range(16)]
+    assert min(ns) >= 40 and max(ns) <= 65 and len(set(ns)) > 10
+    c = np.random.default_rng(0).normal(size=(6, 6, 6)).astype(np.float32)
+    blob = synth.pack_mfa(2, c)
+    m = model.deserialize(blob, 6, [[-1, 1]] * 3, 1)
+    np.testing.assert_array_equal(m.control, c)
