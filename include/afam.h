@@ -95,6 +95,7 @@ int afam_store_read(afam_store *s, int32_t slot, float *ctrl, float *knots);
 
 /* ------------------------------------------------------------ K1: points */
 #define AFAM_EVAL_PARAM 1u    /* pts are extent-local parameters u, not world points */
+#define AFAM_EVAL_OUT_F64 2u  /* val/grad are float64 buffers (default float32) */
 
 /*
  * Value (and optionally gradient) of the model in slot slots[i] (or
@@ -102,10 +103,11 @@ int afam_store_read(afam_store *s, int32_t slot, float *ctrl, float *knots);
  * device memory).  World points follow MicroModel.values_at/gradients_at
  * (u = clip((p-lo)/(hi-lo), 0, 1), gradient divided by the extent span);
  * with AFAM_EVAL_PARAM the points are parameters (bspline.evaluate_points).
- * val (n) / grad (n x 3) are float32 device buffers; grad may be NULL.
+ * val (n) / grad (n x 3) are device buffers of float32 (or float64 with
+ * AFAM_EVAL_OUT_F64); grad may be NULL.
  */
 int afam_eval_points(afam_store *s, const int32_t *slots, int32_t slot, const double *pts, int64_t n,
-                     float *val, float *grad, uint32_t flags, void *stream);
+                     void *val, void *grad, uint32_t flags, void *stream);
 
 /* --------------------------------------------------------- K3: grid decode */
 /*

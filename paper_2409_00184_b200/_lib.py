@@ -26,6 +26,7 @@ AFAM_MAX_TF_POINTS = 32
 AFAM_SLOT_VALID = 1
 AFAM_SLOT_FP64 = 2
 AFAM_EVAL_PARAM = 1
+AFAM_EVAL_OUT_F64 = 2
 AFAM_RENDER_DEBUG = 1
 
 _lib = None

@@ -43,24 +43,26 @@ def _torch():
     return torch
 
 
-def eval_device(store, slots, points, gradient: bool = True, param: bool = False):
+def eval_device(store, slots, points, gradient: bool = True, param: bool = False, out_f64: bool = True):
     """K1 on resident slots: `slots` is one slot id or an int array (n,).
-    Returns values (n,) [and gradients (n, 3)] as float64 numpy arrays."""
+    Returns values (n,) [and gradients (n, 3)] as float64 numpy arrays
+    (device output float64 unless out_f64=False)."""
     torch = _torch()
     pts = np.ascontiguousarray(np.atleast_2d(np.asarray(points, dtype=np.float64)))
     if pts.shape[-1] != 3:
         raise ValueError(f"points must have shape (n, 3), got {pts.shape}")
     n = pts.shape[0]
     dev = torch.device("cuda", store.device)
+    odt = torch.float64 if out_f64 else torch.float32
     d_pts = torch.from_numpy(pts).to(dev, non_blocking=False)
-    d_val = torch.empty(n, dtype=torch.float32, device=dev)
-    d_grad = torch.empty((n, 3), dtype=torch.float32, device=dev) if gradient else None
+    d_val = torch.empty(n, dtype=odt, device=dev)
+    d_grad = torch.empty((n, 3), dtype=odt, device=dev) if gradient else None
     one_slot, d_slots = 0, None
     if np.ndim(slots) == 0:
         one_slot = int(slots)
     else:
         d_slots = torch.from_numpy(np.ascontiguousarray(slots, dtype=np.int32)).to(dev)
-    flags = _lib.AFAM_EVAL_PARAM if param else 0
+    flags = (_lib.AFAM_EVAL_PARAM if param else 0) | (_lib.AFAM_EVAL_OUT_F64 if out_f64 else 0)
     with torch.cuda.device(dev):
         _lib.check(_lib.lib().afam_eval_points(
             store.handle, None if d_slots is None else C.c_void_p(d_slots.data_ptr()), one_slot,
@@ -95,8 +97,19 @@ def _as_model(coeff, degree, knots):
         kv = np.repeat(clamped_knots(ncp, degree)[None, :], 3, axis=0)
     else:
         kv = np.stack([np.asarray(k, dtype=np.float64) for k in knots])
-    return SimpleNamespace(control=c, knots=kv.astype(np.float32), degree=int(degree),
-                           extent=np.array([[0.0, 1.0]] * 3), lod=1)
+    return _GridModel(c, kv.astype(np.float32), int(degree))
+
+
+class _GridModel:
+    """A bare coefficient grid posing as a model on the unit extent (weak-referenceable,
+    so the scratch store can tell a recycled id() from the same object)."""
+
+    __slots__ = ("control", "knots", "degree", "extent", "lod", "__weakref__")
+
+    def __init__(self, control, knots, degree):
+        self.control, self.knots, self.degree = control, knots, degree
+        self.extent = np.array([[0.0, 1.0]] * 3)
+        self.lod = 1
 
 
 def evaluate_points(coeff, degree: int, u, knots=None) -> np.ndarray:

@@ -19,11 +19,13 @@ __device__ __forceinline__ T clamp01(T v) {
 // searchsorted(knots, u, 'right') - 1 clipped to [deg, ncp-1]
 // (bspline.py:41-47): start from the uniform-knot guess and walk to the
 // exact span using the stored knots, so any (non-uniform) knot vector works.
-template <typename T>
-__device__ __forceinline__ int find_span(const float *__restrict__ kv, int ncp, int deg, int nspan, T u) {
-    int s = deg + min(max((int)(u * (T)nspan), 0), nspan - 1);
-    while (s > deg && u < (T)__ldg(kv + s)) --s;
-    while (s < ncp - 1 && u >= (T)__ldg(kv + s + 1)) ++s;
+// The comparison is float64 against the float32 knots upcast, exactly as
+// the reference compares its float64 parameters (bspline.py:193-195), so
+// the span (and the one-sided derivative at a knot) matches bit-for-bit.
+__device__ __forceinline__ int find_span(const float *__restrict__ kv, int ncp, int deg, int nspan, double u) {
+    int s = deg + min(max((int)(u * (double)nspan), 0), nspan - 1);
+    while (s > deg && u < (double)__ldg(kv + s)) --s;
+    while (s < ncp - 1 && u >= (double)__ldg(kv + s + 1)) ++s;
     return s;
 }
 
@@ -51,11 +53,19 @@ __device__ __forceinline__ void load_entry(const double *__restrict__ p, Tab<dou
     }
 }
 
-// Cox-de Boor (bspline.py:50-70) and degree-reduction derivatives
+// Cox-de Boor (bspline.py:50-70) and the degree-reduction derivative
 // (bspline.py:73-95) from one table entry: window W = t[s-p+1 .. s+p],
 // inv[j][r] = 1/(t[s+r+1] - t[s+1-j+r]).
+//
+// The derivative is returned in difference form: with L the degree p-1
+// bases, sum_j c_j N'_j = sum_{k<p} E[k] (c_{k+1} - c_k) where
+// E[k] = p * L[k] / (t[s+k+1] - t[s+k+1-p]) -- the same identity as the
+// reference's N'_j, regrouped so a locally constant patch has an exactly
+// zero gradient (the reference's float64 gradient there is ~1e-17, below
+// its 1e-12 "lit" threshold in _shade, render.py:386; a float32
+// sum_j c_j N'_j would leave ~1e-8 noise and light flat regions).
 template <int P, typename T>
-__device__ __forceinline__ void basis_eval(const Tab<T> &t, T u, T (&N)[P + 1], T (&D)[P + 1]) {
+__device__ __forceinline__ void basis_eval(const Tab<T> &t, T u, T (&N)[P + 1], T (&E)[P]) {
     const T *W = t;
     const T *inv = t + 2 * P;
     T left[P + 1], right[P + 1], L[P];
@@ -82,12 +92,7 @@ __device__ __forceinline__ void basis_eval(const Tab<T> &t, T u, T (&N)[P + 1], 
     if (P == 1) L[0] = T(1);
     const T *invP = inv + P * (P - 1) / 2;
 #pragma unroll
-    for (int j = 0; j <= P; j++) {
-        T term = T(0);
-        if (j > 0) term = L[j - 1] * invP[j - 1];
-        if (j < P) term = term - L[j] * invP[j];
-        D[j] = T(P) * term;
-    }
+    for (int k = 0; k < P; k++) E[k] = T(P) * L[k] * invP[k];
 }
 
 template <int P, typename T>
@@ -114,29 +119,39 @@ __device__ __forceinline__ void basis_vals_only(const Tab<T> &t, T u, T (&N)[P +
 }
 
 // Separable contraction of the (P+1)^3 control points c[(cz*Q+by)*Q+ax]
-// (bspline.py:214, :224-228): x first, then y, then z.  2q^3+3q^2+4q FMAs.
+// (bspline.py:214, :224-228): x first, then y, then z.  Value uses the
+// N weights; each gradient component applies the difference weights E of
+// basis_eval to forward differences along its own axis.
 template <int P, typename T, typename CT>
-__device__ __forceinline__ void contract_grad(const CT (&c)[64], const T (&Nx)[P + 1],
-                                              const T (&Dx)[P + 1], const T (&Ny)[P + 1], const T (&Dy)[P + 1],
-                                              const T (&Nz)[P + 1], const T (&Dz)[P + 1], T &v, T g[3]) {
+__device__ __forceinline__ void contract_grad(const CT (&c)[64], const T (&Nx)[P + 1], const T (&Ex)[P],
+                                              const T (&Ny)[P + 1], const T (&Ey)[P], const T (&Nz)[P + 1],
+                                              const T (&Ez)[P], T &v, T g[3]) {
     constexpr int Q = P + 1;
     T ry[Q], rdxy[Q], rdy[Q];
 #pragma unroll
     for (int cz = 0; cz < Q; cz++) {
+        T rx[Q], rdx[Q];
+#pragma unroll
+        for (int by = 0; by < Q; by++) {
+            T cv[Q];
+#pragma unroll
+            for (int ax = 0; ax < Q; ax++) cv[ax] = (T)c[(cz * Q + by) * Q + ax];
+            T acc = T(0), dacc = T(0);
+#pragma unroll
+            for (int ax = 0; ax < Q; ax++) acc = fma(Nx[ax], cv[ax], acc);
+#pragma unroll
+            for (int k = 0; k < P; k++) dacc = fma(Ex[k], cv[k + 1] - cv[k], dacc);
+            rx[by] = acc;
+            rdx[by] = dacc;
+        }
         T ay = T(0), adxy = T(0), ady = T(0);
 #pragma unroll
         for (int by = 0; by < Q; by++) {
-            T rx = T(0), rdx = T(0);
-#pragma unroll
-            for (int ax = 0; ax < Q; ax++) {
-                T cv = (T)c[(cz * Q + by) * Q + ax];
-                rx = fma(Nx[ax], cv, rx);
-                rdx = fma(Dx[ax], cv, rdx);
-            }
-            ay = fma(Ny[by], rx, ay);
-            adxy = fma(Ny[by], rdx, adxy);
-            ady = fma(Dy[by], rx, ady);
+            ay = fma(Ny[by], rx[by], ay);
+            adxy = fma(Ny[by], rdx[by], adxy);
         }
+#pragma unroll
+        for (int k = 0; k < P; k++) ady = fma(Ey[k], rx[k + 1] - rx[k], ady);
         ry[cz] = ay; rdxy[cz] = adxy; rdy[cz] = ady;
     }
     T vv = T(0), gx = T(0), gy = T(0), gz = T(0);
@@ -145,8 +160,9 @@ __device__ __forceinline__ void contract_grad(const CT (&c)[64], const T (&Nx)[P
         vv = fma(Nz[cz], ry[cz], vv);
         gx = fma(Nz[cz], rdxy[cz], gx);
         gy = fma(Nz[cz], rdy[cz], gy);
-        gz = fma(Dz[cz], ry[cz], gz);
     }
+#pragma unroll
+    for (int k = 0; k < P; k++) gz = fma(Ez[k], ry[k + 1] - ry[k], gz);
     v = vv; g[0] = gx; g[1] = gy; g[2] = gz;
 }
 
@@ -188,12 +204,14 @@ __device__ __forceinline__ void gather(const float *__restrict__ ctrl, int ncp, 
 // One full evaluation (no caching): parameters u in [0,1]^3 -> value and
 // parameter-space gradient (bspline.py:217-229).
 template <int P, typename T, bool GRAD>
-__device__ __forceinline__ T eval_uncached(const BlockDesc &d, const T (&u)[3], T g[3]) {
+__device__ __forceinline__ T eval_uncached(const BlockDesc &d, const double (&u64)[3], T g[3]) {
     Tab<T> te[3];
     int s[3];
+    T u[3];
 #pragma unroll
     for (int a = 0; a < 3; a++) {
-        s[a] = find_span<T>(d.knots + a * d.nk, d.ncp, P, d.nspan, u[a]);
+        u[a] = (T)u64[a];
+        s[a] = find_span(d.knots + a * d.nk, d.ncp, P, d.nspan, u64[a]);
         const size_t off = ((size_t)a * d.nspan + (s[a] - P)) * tab_stride(P);
         if constexpr (sizeof(T) == 4) load_entry<P>(d.tab32 + off, te[a]);
         else load_entry<P>(d.tab64 + off, te[a]);
@@ -201,7 +219,7 @@ __device__ __forceinline__ T eval_uncached(const BlockDesc &d, const T (&u)[3], 
     float c[64];
     gather<P>(d.ctrl, d.ncp, d.pitch, s[0] - P, s[1] - P, s[2] - P, c);
     if constexpr (GRAD) {
-        T Nx[P + 1], Dx[P + 1], Ny[P + 1], Dy[P + 1], Nz[P + 1], Dz[P + 1];
+        T Nx[P + 1], Dx[P], Ny[P + 1], Dy[P], Nz[P + 1], Dz[P];
         basis_eval<P, T>(te[0], u[0], Nx, Dx);
         basis_eval<P, T>(te[1], u[1], Ny, Dy);
         basis_eval<P, T>(te[2], u[2], Nz, Dz);

@@ -45,6 +45,7 @@ struct alignas(16) BlockDesc {
 // Host mirror of a slot.
 struct SlotHost {
     bool valid = false;
+    bool pending = false;  // upload possibly still in flight (ready not yet observed)
     int32_t ncp = 0, deg = 0;
     double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     cudaEvent_t ready = nullptr;  // recorded after the upload kernels

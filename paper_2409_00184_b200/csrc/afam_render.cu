@@ -90,9 +90,10 @@ __device__ __forceinline__ void decode_f32(const BlockDesc &d, MarchCache &mc, T
     bool span_changed = fresh;
 #pragma unroll
     for (int a = 0; a < 3; a++) {
-        // model.py:64-68 params_for: u = clip((p - lo)/span, 0, 1)
-        u[a] = (float)clamp01((pos[a] - d.lo[a]) * d.inv_span[a]);
-        s[a] = find_span<float>(d.knots + a * d.nk, d.ncp, P, d.nspan, u[a]);
+        // model.py:64-68 params_for: u = clip((p - lo)/span, 0, 1); span chosen in float64
+        const double u64 = clamp01((pos[a] - d.lo[a]) * d.inv_span[a]);
+        u[a] = (float)u64;
+        s[a] = find_span(d.knots + a * d.nk, d.ncp, P, d.nspan, u64);
         if (fresh || s[a] != mc.s[a]) {
             load_entry<P>(d.tab32 + ((size_t)a * d.nspan + (s[a] - P)) * tab_stride(P), te[a]);
             mc.s[a] = s[a];
@@ -100,7 +101,7 @@ __device__ __forceinline__ void decode_f32(const BlockDesc &d, MarchCache &mc, T
         }
     }
     if (span_changed) gather<P>(d.ctrl, d.ncp, d.pitch, s[0] - P, s[1] - P, s[2] - P, mc.c);
-    float Nx[P + 1], Dx[P + 1], Ny[P + 1], Dy[P + 1], Nz[P + 1], Dz[P + 1];
+    float Nx[P + 1], Dx[P], Ny[P + 1], Dy[P], Nz[P + 1], Dz[P];
     basis_eval<P, float>(te[0], u[0], Nx, Dx);
     basis_eval<P, float>(te[1], u[1], Ny, Dy);
     basis_eval<P, float>(te[2], u[2], Nz, Dz);
@@ -115,7 +116,7 @@ template <int P>
 __device__ __forceinline__ void decode_f64(const BlockDesc &d, const double (&pos)[3], float &v, float (&g)[3]) {
     double u[3], gg[3];
 #pragma unroll
-    for (int a = 0; a < 3; a++) u[a] = clamp01(__ddiv_rn(pos[a] - d.lo[a], d.span[a]));
+    for (int a = 0; a < 3; a++) u[a] = clamp01(__ddiv_rn(__dsub_rn(pos[a], d.lo[a]), d.span[a]));
     double vv = eval_uncached<P, double, true>(d, u, gg);
     v = (float)vv;
 #pragma unroll

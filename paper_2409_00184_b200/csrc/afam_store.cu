@@ -212,6 +212,7 @@ static int launch_unpack(afam_store *s, int32_t slot, int deg, int ncp, uint64_t
     AFAM_CUDA(cudaGetLastError());
     SlotHost &h = s->host[slot];
     h.valid = true;
+    h.pending = true;
     h.ncp = ncp;
     h.deg = deg;
     for (int a = 0; a < 3; a++) { h.lo[a] = extent[2 * a]; h.hi[a] = extent[2 * a + 1]; }

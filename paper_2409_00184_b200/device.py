@@ -201,7 +201,8 @@ class _ScratchStore:
         key = id(model)
         with self.lock:
             hit = self.lru.get(key)
-            if hit is not None and (hit[0] is None or hit[0]() is model):
+            # objects that cannot be weakly referenced are never reused: id() may be recycled
+            if hit is not None and hit[0] is not None and hit[0]() is model:
                 self.lru.move_to_end(key)
                 return hit[1]
             if hit is not None:

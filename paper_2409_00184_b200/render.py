@@ -311,11 +311,11 @@ def _missing_message(pov, params, cells, key) -> str:
     for a in range(3):
         inv = 1.0 / d[a] if d[a] != 0.0 else math.copysign(math.inf, d[a])
         ta, tb = (-1.0 - o[a]) * inv, (1.0 - o[a]) * inv
-        lo = np.fmin(ta, tb)
+        lo = float(np.fmin(ta, tb))
         te = max(te, -math.inf if math.isnan(lo) else lo)
     te = max(te, float(params.near))
     t = te + (step + 0.5) * float(params.sample_distance)
-    pos = [min(max(o[a] + t * d[a], -1.0), 1.0) for a in range(3)]
+    pos = [float(min(max(o[a] + t * d[a], -1.0), 1.0)) for a in range(3)]
     cell = tuple(min(max(int(((p + 1.0) / 2.0) * cells), 0), cells - 1) for p in pos)
     return (f"no resident block covers sample {pos} (finest cell {cell}); "
             "the resident set does not cover the visible region")
