@@ -29,18 +29,26 @@ constexpr int kTabStrideMax = 12;  // tab_stride(AFAM_MAX_DEGREE)
 // Device-resident descriptor of one slot (one micro-model).
 struct alignas(16) BlockDesc {
     const float *ctrl;    // ncp x ncp rows of `pitch` floats: ctrl[(iz*ncp+iy)*pitch+ix]
+    const float4 *ctrl4;  // x-quad layout: ctrl4[(iz*ncp+iy)*ncp+ix] = c[ix..ix+3][iy][iz] (0 past ncp-1)
     const float *tab32;   // [3][nspan][tab_stride(deg)] float
     const double *tab64;  // [3][nspan][tab_stride(deg)] double
     const float *knots;   // [3][nk] float (full clamped vectors)
     double lo[3];         // extent low corner
     double span[3];       // hi - lo
     double inv_span[3];   // 1 / (hi - lo)
+    float lo_f[3];        // lo as float32 (block extents are dyadic: exact)
+    float inv_span_f[3];  // 1/(hi-lo) as float32
     int32_t ncp, deg, pitch, nk;
     int32_t nspan;        // ncp - deg
-    uint32_t flags;       // AFAM_SLOT_*
+    uint32_t flags;       // AFAM_SLOT_* | kFlagUniform
     float max_abs;
-    int32_t pad;
+    int32_t pad[3];
 };
+
+// Internal desc flag: all three knot vectors are the clamped uniform ones
+// (stored knot k == float32((k-deg)/nspan)), so interior spans use the
+// closed-form uniform B-spline basis.
+constexpr uint32_t kFlagUniform = 0x100u;
 
 // Host mirror of a slot.
 struct SlotHost {
@@ -63,7 +71,7 @@ struct afam_store {
     int device = 0;
     int32_t nslots = 0, max_ncp = 0;
     double fp64_limit = 4.0;
-    size_t raw_bytes = 0, ctrl_floats = 0, knot_floats = 0, tab_elems = 0, slot_bytes = 0;
+    size_t raw_bytes = 0, ctrl_floats = 0, ctrl4_elems = 0, knot_floats = 0, tab_elems = 0, slot_bytes = 0;
     char *arena = nullptr;               // nslots * slot_bytes device bytes
     afam::BlockDesc *d_desc = nullptr;   // nslots descriptors (device)
     float *d_maxabs = nullptr;           // nslots (device)
@@ -74,12 +82,14 @@ struct afam_store {
     char *slot_base(int32_t slot) const { return arena + (size_t)slot * slot_bytes; }
     uint8_t *raw_ptr(int32_t slot) const { return (uint8_t *)slot_base(slot); }
     float *ctrl_ptr(int32_t slot) const { return (float *)(slot_base(slot) + raw_off()); }
+    float4 *ctrl4_ptr(int32_t slot) const { return (float4 *)(slot_base(slot) + ctrl4_off()); }
     float *knot_ptr(int32_t slot) const { return (float *)(slot_base(slot) + knot_off()); }
     float *tab32_ptr(int32_t slot) const { return (float *)(slot_base(slot) + tab32_off()); }
     double *tab64_ptr(int32_t slot) const { return (double *)(slot_base(slot) + tab64_off()); }
     static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
     size_t raw_off() const { return align256(raw_bytes); }
-    size_t knot_off() const { return raw_off() + align256(ctrl_floats * 4); }
+    size_t ctrl4_off() const { return raw_off() + align256(ctrl_floats * 4); }
+    size_t knot_off() const { return ctrl4_off() + align256(ctrl4_elems * 16); }
     size_t tab32_off() const { return knot_off() + align256(knot_floats * 4); }
     size_t tab64_off() const { return tab32_off() + align256(tab_elems * 4); }
 };

@@ -9,15 +9,19 @@
 // Numerics.  Block/LOD selection must match the reference bit-exactly, so
 // ray setup, the sample position t = t_enter + (k+0.5)*sd, pos = clip(o +
 // t*d) and the finest-cell index are float64 with the reference's op order
-// and no FMA contraction (__dadd_rn/__dmul_rn/...).  Decoding is float32
+// and no FMA contraction (__dadd_rn/__dmul_rn/...).  The knot span is also
+// chosen in float64 against the stored float32 knots.  Decoding is float32
 // (float64 for slots flagged AFAM_SLOT_FP64); TF, shading and compositing
 // are float32 (parity gate: PSNR >= 60 dB).
 //
 // Schedule.  One thread per ray; a warp is an 8x4 pixel tile and a CTA a
 // 16x8 tile, so a warp's samples almost always share the owner block
-// (SURVEY.md sec. 7 coherence measurement).  Along a ray the (p+1)^3
-// control points and the three per-axis span tables stay in registers and
-// are re-gathered only when the ray crosses into a new knot span or block.
+// (SURVEY.md sec. 7 coherence measurement).  Interior knot spans of
+// clamped-uniform models use the closed-form uniform B-spline basis (no
+// table, no division); the 2p boundary spans per axis read the per-span
+// table.  The (p+1)^3 control points of the current spans stay in
+// registers as (p+1)^2 float4 rows of the x-quad layout and are re-gathered
+// (one 16-byte load per row) only when a span or the owner block changes.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -39,10 +43,12 @@ struct RenderArgs {
     int32_t power_one;  // power == 1
     int32_t ncolor, nopac;
     float dom_lo, dom_hi;
-    float cx[AFAM_MAX_TF_POINTS], cv[3][AFAM_MAX_TF_POINTS], cs[3][AFAM_MAX_TF_POINTS];
-    float ox[AFAM_MAX_TF_POINTS], ov[AFAM_MAX_TF_POINTS], os[AFAM_MAX_TF_POINTS];
+    // TF tables, rows: 0 cx, 1-3 color values, 4-6 color slopes, 7 ox, 8 opacity, 9 opacity slope
+    float tf[10][AFAM_MAX_TF_POINTS];
     uint32_t flags;
 };
+
+constexpr int kTfRows = 10;
 
 // np.interp(v, xs, ys) (numpy compiled_base.c) for v already clipped to the
 // TF domain; slopes precomputed on the host in float64.
@@ -74,60 +80,231 @@ __device__ __forceinline__ int frame_row(const RenderArgs &A, int lr) {
     return (b * A.nparts + A.part) * A.band_rows + lr % A.band_rows;
 }
 
-// Per-thread decode state: cached block descriptor, span tables and the
-// (P+1)^3 control points of the current spans.
-struct MarchCache {
-    int32_t slot;
-    int32_t s[3];
-    float c[64];
+// Uniform B-spline basis on an interior span, local coordinate x in [0,1):
+// the Cox-de Boor values for equally spaced knots, and the difference-form
+// derivative weights E[k] = nspan * L[k] (L: degree p-1 basis), cf. basis_eval.
+template <int P>
+__device__ __forceinline__ void uniform_basis(float x, float ns, float (&N)[P + 1], float (&E)[P]) {
+    const float m = 1.f - x;
+    if (P == 1) {
+        N[0] = m;
+        N[1] = x;
+        E[0] = ns;
+    } else if (P == 2) {
+        const float x2 = x * x;
+        N[0] = 0.5f * m * m;
+        N[1] = fmaf(-1.f, x2, x) + 0.5f;
+        N[2] = 0.5f * x2;
+        E[0] = ns * m;
+        E[1] = ns * x;
+    } else {
+        const float x2 = x * x, x3 = x2 * x, m2 = m * m;
+        const float s6 = 1.f / 6.f;
+        N[0] = s6 * m2 * m;
+        N[1] = fmaf(0.5f, x3, fmaf(-1.f, x2, 2.f / 3.f));
+        N[2] = fmaf(-0.5f, x3, fmaf(0.5f, x2, fmaf(0.5f, x, s6)));
+        N[3] = s6 * x3;
+        const float hn = 0.5f * ns;
+        E[0] = hn * m2;
+        E[1] = ns * (fmaf(-1.f, x2, x) + 0.5f);
+        E[2] = hn * x2;
+    }
+}
+
+// The owner block's fields used per sample (kept in registers).
+struct BlockLite {
+    const float4 *ctrl4;
+    const float *tab32;
+    const float *knots;
+    double lo[3], inv_span[3];
+    float inv_span_f[3];
+    int32_t ncp, nspan, deg;
+    uint32_t flags;
 };
 
-template <int P>
-__device__ __forceinline__ void decode_f32(const BlockDesc &d, MarchCache &mc, Tab<float> (&te)[3],
-                                           const double (&pos)[3], float &v, float (&g)[3], bool fresh) {
-    float u[3];
-    int s[3];
-    bool span_changed = fresh;
+__device__ __forceinline__ void load_lite(const BlockDesc *__restrict__ p, BlockLite &b) {
+    b.ctrl4 = (const float4 *)__ldg((const unsigned long long *)&p->ctrl4);
+    b.tab32 = (const float *)__ldg((const unsigned long long *)&p->tab32);
+    b.knots = (const float *)__ldg((const unsigned long long *)&p->knots);
 #pragma unroll
     for (int a = 0; a < 3; a++) {
-        // model.py:64-68 params_for: u = clip((p - lo)/span, 0, 1); span chosen in float64
-        const double u64 = clamp01((pos[a] - d.lo[a]) * d.inv_span[a]);
-        u[a] = (float)u64;
-        s[a] = find_span(d.knots + a * d.nk, d.ncp, P, d.nspan, u64);
-        if (fresh || s[a] != mc.s[a]) {
-            load_entry<P>(d.tab32 + ((size_t)a * d.nspan + (s[a] - P)) * tab_stride(P), te[a]);
-            mc.s[a] = s[a];
-            span_changed = true;
-        }
+        b.lo[a] = __ldg(&p->lo[a]);
+        b.inv_span[a] = __ldg(&p->inv_span[a]);
+        b.inv_span_f[a] = __ldg(&p->inv_span_f[a]);
     }
-    if (span_changed) gather<P>(d.ctrl, d.ncp, d.pitch, s[0] - P, s[1] - P, s[2] - P, mc.c);
-    float Nx[P + 1], Dx[P], Ny[P + 1], Dy[P], Nz[P + 1], Dz[P];
-    basis_eval<P, float>(te[0], u[0], Nx, Dx);
-    basis_eval<P, float>(te[1], u[1], Ny, Dy);
-    basis_eval<P, float>(te[2], u[2], Nz, Dz);
-    float gg[3];
-    contract_grad<P, float, float>(mc.c, Nx, Dx, Ny, Dy, Nz, Dz, v, gg);
-    // model.py:79 gradient / span
-#pragma unroll
-    for (int a = 0; a < 3; a++) g[a] = gg[a] * (float)d.inv_span[a];
+    b.ncp = __ldg(&p->ncp);
+    b.nspan = __ldg(&p->nspan);
+    b.deg = __ldg(&p->deg);
+    b.flags = __ldg(&p->flags);
+}
+
+// Knot span + basis for one axis.  The span is the reference's
+// searchsorted(float32 knots, u64, 'right') - 1 (bspline.py:41-47): for
+// uniform models floor(u*nspan) except within 1e-4 of a knot, where the
+// stored knots decide.
+template <int P>
+__device__ __forceinline__ int axis_basis(const BlockLite &b, int a, double u64, float (&N)[P + 1], float (&E)[P]) {
+    const double tq = u64 * (double)b.nspan;
+    int k = min(max((int)tq, 0), b.nspan - 1);
+    const double fr = tq - (double)k;
+    const bool uni = b.flags & kFlagUniform;
+    int s = P + k;
+    if (!uni || fr < 1e-4 || fr > 1.0 - 1e-4) s = find_span(b.knots + a * (b.ncp + P + 1), b.ncp, P, b.nspan, u64);
+    if (uni && s >= 2 * P - 1 && s <= b.ncp - P) {
+        uniform_basis<P>((float)(tq - (double)(s - P)), (float)b.nspan, N, E);
+    } else {
+        Tab<float> t;
+        load_entry<P>(b.tab32 + ((size_t)a * b.nspan + (s - P)) * tab_stride(P), t);
+        basis_eval<P, float>(t, (float)u64, N, E);
+    }
+    return s;
 }
 
 template <int P>
-__device__ __forceinline__ void decode_f64(const BlockDesc &d, const double (&pos)[3], float &v, float (&g)[3]) {
-    double u[3], gg[3];
-#pragma unroll
-    for (int a = 0; a < 3; a++) u[a] = clamp01(__ddiv_rn(__dsub_rn(pos[a], d.lo[a]), d.span[a]));
-    double vv = eval_uncached<P, double, true>(d, u, gg);
-    v = (float)vv;
-#pragma unroll
-    for (int a = 0; a < 3; a++) g[a] = (float)(gg[a] / d.span[a]);
+__device__ __forceinline__ float q4(const float4 &v) {
+    return P == 0 ? v.x : (P == 1 ? v.y : (P == 2 ? v.z : v.w));
 }
 
-__global__ void __launch_bounds__(128) render_kernel(const BlockDesc *__restrict__ descs,
-                                                     const int16_t *__restrict__ grid,
-                                                     const int32_t *__restrict__ idx2slot, const RenderArgs A,
-                                                     uint8_t *__restrict__ rgba, afam_render_stats *stats,
-                                                     int32_t *__restrict__ nsamp, uint64_t *__restrict__ ohash) {
+template <int K>
+__device__ __forceinline__ float comp(const float4 &v) {
+    if constexpr (K == 0) return v.x;
+    else if constexpr (K == 1) return v.y;
+    else if constexpr (K == 2) return v.z;
+    else return v.w;
+}
+
+template <int P, int AX, typename T>
+__device__ __forceinline__ void row_contract(const float4 &r, const T (&Nx)[P + 1], const T (&Ex)[P], T &acc,
+                                             T &dacc) {
+    if constexpr (AX <= P) {
+        acc = fma(Nx[AX], (T)comp<AX>(r), acc);
+        if constexpr (AX < P) dacc = fma(Ex[AX], (T)comp<AX + 1>(r) - (T)comp<AX>(r), dacc);
+        row_contract<P, AX + 1, T>(r, Nx, Ex, acc, dacc);
+    }
+}
+
+// contract_grad (afam_eval.cuh) on x-quad rows c4[cz*Q+by].
+template <int P, typename T>
+__device__ __forceinline__ void contract_quad(const float4 (&c4)[16], const T (&Nx)[P + 1], const T (&Ex)[P],
+                                              const T (&Ny)[P + 1], const T (&Ey)[P], const T (&Nz)[P + 1],
+                                              const T (&Ez)[P], T &v, T (&g)[3]) {
+    constexpr int Q = P + 1;
+    T ry[Q], rdxy[Q], rdy[Q];
+#pragma unroll
+    for (int cz = 0; cz < Q; cz++) {
+        T rx[Q], rdx[Q];
+#pragma unroll
+        for (int by = 0; by < Q; by++) {
+            T acc = T(0), dacc = T(0);
+            row_contract<P, 0, T>(c4[cz * Q + by], Nx, Ex, acc, dacc);
+            rx[by] = acc;
+            rdx[by] = dacc;
+        }
+        T ay = T(0), adxy = T(0), ady = T(0);
+#pragma unroll
+        for (int by = 0; by < Q; by++) {
+            ay = fma(Ny[by], rx[by], ay);
+            adxy = fma(Ny[by], rdx[by], adxy);
+        }
+#pragma unroll
+        for (int k = 0; k < P; k++) ady = fma(Ey[k], rx[k + 1] - rx[k], ady);
+        ry[cz] = ay; rdxy[cz] = adxy; rdy[cz] = ady;
+    }
+    T vv = T(0), gx = T(0), gy = T(0), gz = T(0);
+#pragma unroll
+    for (int cz = 0; cz < Q; cz++) {
+        vv = fma(Nz[cz], ry[cz], vv);
+        gx = fma(Nz[cz], rdxy[cz], gx);
+        gy = fma(Nz[cz], rdy[cz], gy);
+    }
+#pragma unroll
+    for (int k = 0; k < P; k++) gz = fma(Ez[k], ry[k + 1] - ry[k], gz);
+    v = vv; g[0] = gx; g[1] = gy; g[2] = gz;
+}
+
+struct GatherCache {
+    int32_t slot, x0, y0, z0;
+    float4 c4[16];
+};
+
+// bspline.py:175-181 gather: (p+1)^2 rows of the x-quad layout, skipped
+// when the owner slot and the three spans are unchanged since the last sample.
+template <int P>
+__device__ __forceinline__ void gather_quad(const BlockLite &b, int32_t slot, GatherCache &G, int x0, int y0, int z0) {
+    constexpr int Q = P + 1;
+    if (slot != G.slot || x0 != G.x0 || y0 != G.y0 || z0 != G.z0) {
+        const float4 *base = b.ctrl4 + ((size_t)z0 * b.ncp + y0) * b.ncp + x0;
+#pragma unroll
+        for (int cz = 0; cz < Q; cz++)
+#pragma unroll
+            for (int by = 0; by < Q; by++) G.c4[cz * Q + by] = __ldg(base + ((size_t)cz * b.ncp + by) * b.ncp);
+        G.slot = slot;
+        G.x0 = x0;
+        G.y0 = y0;
+        G.z0 = z0;
+    }
+}
+
+template <int P>
+__device__ __forceinline__ void decode_f32(const BlockLite &b, int32_t slot, GatherCache &G, const double (&pos)[3],
+                                           float &v, float (&g)[3]) {
+    constexpr int Q = P + 1;
+    float Nx[Q], Ex[P], Ny[Q], Ey[P], Nz[Q], Ez[P];
+    // model.py:64-68 params_for: u = clip((p - lo)/span, 0, 1), float64
+    const int sx = axis_basis<P>(b, 0, clamp01((pos[0] - b.lo[0]) * b.inv_span[0]), Nx, Ex);
+    const int sy = axis_basis<P>(b, 1, clamp01((pos[1] - b.lo[1]) * b.inv_span[1]), Ny, Ey);
+    const int sz = axis_basis<P>(b, 2, clamp01((pos[2] - b.lo[2]) * b.inv_span[2]), Nz, Ez);
+    gather_quad<P>(b, slot, G, sx - P, sy - P, sz - P);
+    float gg[3];
+    contract_quad<P, float>(G.c4, Nx, Ex, Ny, Ey, Nz, Ez, v, gg);
+#pragma unroll
+    for (int a = 0; a < 3; a++) g[a] = gg[a] * b.inv_span_f[a];  // model.py:79 gradient / span
+}
+
+// Ill-conditioned slots: the same schedule with float64 parameters (the
+// reference's division), float64 basis from the float64 table and float64
+// accumulation; control points are float32 in the file, so the float4 rows
+// are shared with the float32 path.
+template <int P>
+__device__ __forceinline__ void decode_f64(const BlockLite &b, const BlockDesc *__restrict__ dp, int32_t slot,
+                                           GatherCache &G, const double (&pos)[3], float &v, float (&g)[3]) {
+    constexpr int Q = P + 1;
+    double N[3][Q], E[3][P], span[3];
+    int s[3];
+    const double *tab64 = (const double *)__ldg((const unsigned long long *)&dp->tab64);
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        span[a] = __ldg(&dp->span[a]);
+        const double u = clamp01(__ddiv_rn(__dsub_rn(pos[a], b.lo[a]), span[a]));
+        s[a] = find_span(b.knots + a * (b.ncp + P + 1), b.ncp, P, b.nspan, u);
+        Tab<double> t;
+        load_entry<P>(tab64 + ((size_t)a * b.nspan + (s[a] - P)) * tab_stride(P), t);
+        basis_eval<P, double>(t, u, N[a], E[a]);
+    }
+    gather_quad<P>(b, slot, G, s[0] - P, s[1] - P, s[2] - P);
+    double vv, gg[3];
+    contract_quad<P, double>(G.c4, N[0], E[0], N[1], E[1], N[2], E[2], vv, gg);
+    v = (float)vv;
+#pragma unroll
+    for (int a = 0; a < 3; a++) g[a] = (float)(gg[a] / span[a]);
+}
+
+template <bool DEBUG, bool SMEM_GRID, int MINB>
+__global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__restrict__ descs,
+                                                        const int16_t *__restrict__ grid,
+                                                        const int32_t *__restrict__ idx2slot, const RenderArgs A,
+                                                        uint8_t *__restrict__ rgba, afam_render_stats *stats,
+                                                        int32_t *__restrict__ nsamp, uint64_t *__restrict__ ohash) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    float(*tf)[AFAM_MAX_TF_POINTS] = reinterpret_cast<float(*)[AFAM_MAX_TF_POINTS]>(smem);
+    int16_t *sgrid = reinterpret_cast<int16_t *>(smem + sizeof(float) * kTfRows * AFAM_MAX_TF_POINTS);
+    for (int i = threadIdx.x; i < kTfRows * AFAM_MAX_TF_POINTS; i += blockDim.x)
+        tf[i / AFAM_MAX_TF_POINTS][i % AFAM_MAX_TF_POINTS] = A.tf[i / AFAM_MAX_TF_POINTS][i % AFAM_MAX_TF_POINTS];
+    if (SMEM_GRID)
+        for (int i = threadIdx.x; i < A.cells * A.cells * A.cells; i += blockDim.x) sgrid[i] = grid[i];
+    __syncthreads();
+    const int16_t *own_grid = SMEM_GRID ? sgrid : grid;
+
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int j = blockIdx.x * 16 + (warp & 1) * 8 + (lane & 7);
     const int lr = blockIdx.y * 8 + (warp >> 1) * 4 + (lane >> 3);
@@ -142,7 +319,8 @@ __global__ void __launch_bounds__(128) render_kernel(const BlockDesc *__restrict
     double d[3];
 #pragma unroll
     for (int a = 0; a < 3; a++) d[a] = __dadd_rn(__dadd_rn(A.f[a], __dmul_rn(px, A.r[a])), __dmul_rn(py, A.u[a]));
-    const double nrm = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])), __dmul_rn(d[2], d[2])));
+    const double nrm =
+        __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])), __dmul_rn(d[2], d[2])));
 #pragma unroll
     for (int a = 0; a < 3; a++) d[a] = __ddiv_rn(d[a], nrm);
     // _ray_box_span (render.py:340-354)
@@ -163,23 +341,25 @@ __global__ void __launch_bounds__(128) render_kernel(const BlockDesc *__restrict
 
     const float vdir[3] = {(float)d[0], (float)d[1], (float)d[2]};
     const double cellsd = (double)A.cells;
+    const float o_max = (float)A.o_max;
+    const bool o_max_exact = (double)o_max == A.o_max;
     float C0 = 0.f, C1 = 0.f, C2 = 0.f, Aacc = 0.f;
     uint32_t ns = 0, ns64 = 0;
     uint64_t h = 1469598103934665603ULL;
     int64_t miss = INT64_MAX;
 
-    MarchCache mc;
-    mc.slot = -1;
-    BlockDesc desc;
-    desc.deg = 0;
-    desc.flags = 0;
-    Tab<float> tabs[3];
+    int32_t cur_own = -1, cur_slot = -1;
+    BlockLite b;
+    b.deg = 0;
+    b.flags = 0;
+    GatherCache G;
+    G.slot = -1;
 
     if (active) {
         for (int64_t k = 0;; k++) {
             // render.py:422-423
             const double t = __dadd_rn(te, __dmul_rn((double)k + 0.5, A.sd));
-            if (!(t < tx && (double)Aacc <= A.o_max)) break;
+            if (!(t < tx && (o_max_exact ? Aacc <= o_max : (double)Aacc <= A.o_max))) break;
             // render.py:427-428, :378-379
             double pos[3];
             int cidx = 0;
@@ -193,48 +373,46 @@ __global__ void __launch_bounds__(128) render_kernel(const BlockDesc *__restrict
                 ci = min(max(ci, 0), A.cells - 1);
                 cidx = cidx * A.cells + ci;
             }
-            const int own = __ldg(grid + cidx);
+            const int own = own_grid[cidx];
             if (own < 0) {  // render.py:430-436
                 miss = ((int64_t)k << 32) | ray;
                 break;
             }
-            const int32_t slot = __ldg(idx2slot + own);
-            bool fresh = false;
-            if (slot != mc.slot) {
-                desc = load_desc(descs + slot);
-                mc.slot = slot;
-                fresh = true;
+            if (own != cur_own) {
+                cur_own = own;
+                cur_slot = __ldg(idx2slot + own);
+                load_lite(descs + cur_slot, b);
             }
             float v, g[3];
-            if (desc.flags & AFAM_SLOT_FP64) {
+            if (b.flags & AFAM_SLOT_FP64) {
                 ++ns64;
-                if (desc.deg == 3) decode_f64<3>(desc, pos, v, g);
-                else if (desc.deg == 2) decode_f64<2>(desc, pos, v, g);
-                else decode_f64<1>(desc, pos, v, g);
+                if (b.deg == 3) decode_f64<3>(b, descs + cur_slot, cur_slot, G, pos, v, g);
+                else if (b.deg == 2) decode_f64<2>(b, descs + cur_slot, cur_slot, G, pos, v, g);
+                else decode_f64<1>(b, descs + cur_slot, cur_slot, G, pos, v, g);
             } else {
-                if (desc.deg == 3) decode_f32<3>(desc, mc, tabs, pos, v, g, fresh);
-                else if (desc.deg == 2) decode_f32<2>(desc, mc, tabs, pos, v, g, fresh);
-                else decode_f32<1>(desc, mc, tabs, pos, v, g, fresh);
+                if (b.deg == 3) decode_f32<3>(b, cur_slot, G, pos, v, g);
+                else if (b.deg == 2) decode_f32<2>(b, cur_slot, G, pos, v, g);
+                else decode_f32<1>(b, cur_slot, G, pos, v, g);
             }
             ++ns;
-            if (A.flags & AFAM_RENDER_DEBUG) h = (h ^ (uint64_t)(uint32_t)own) * 1099511628211ULL;
+            if (DEBUG) h = (h ^ (uint64_t)(uint32_t)own) * 1099511628211ULL;
 
             // TransferFunction (render.py:117-124)
             const float vc = fminf(fmaxf(v, A.dom_lo), A.dom_hi);
-            const int jo = tf_segment(A.ox, A.nopac, vc);
-            const float atf = tf_lerp(A.ox, A.ov, A.os, A.nopac, jo, vc);
-            const int jc = tf_segment(A.cx, A.ncolor, vc);
+            const int jo = tf_segment(tf[7], A.nopac, vc);
+            const float atf = tf_lerp(tf[7], tf[8], tf[9], A.nopac, jo, vc);
+            const int jc = tf_segment(tf[0], A.ncolor, vc);
             float col[3];
 #pragma unroll
-            for (int c = 0; c < 3; c++) col[c] = tf_lerp(A.cx, A.cv[c], A.cs[c], A.ncolor, jc, vc);
+            for (int c = 0; c < 3; c++) col[c] = tf_lerp(tf[0], tf[1 + c], tf[4 + c], A.ncolor, jc, vc);
             // render.py:451 opacity correction
             const float as = A.power_one ? 1.f - (1.f - atf) : 1.f - __powf(1.f - atf, A.power);
             // _shade (render.py:383-395)
-            const float gn = sqrtf(fmaf(g[2], g[2], fmaf(g[1], g[1], g[0] * g[0])));
+            const float gn2 = fmaf(g[2], g[2], fmaf(g[1], g[1], g[0] * g[0]));
             float ndotl = 0.f;
-            if (gn > 1e-12f) {
-                const float ig = 1.f / gn;
-                ndotl = fabsf(-(g[0] * ig * vdir[0] + g[1] * ig * vdir[1] + g[2] * ig * vdir[2]));
+            if (gn2 > 1e-24f) {
+                const float ig = rsqrtf(gn2);
+                ndotl = fabsf(g[0] * vdir[0] + g[1] * vdir[1] + g[2] * vdir[2]) * ig;
             }
             const float dif = A.diffuse * ndotl;
             const float spec = A.specular * (A.shin_int >= 0 ? powi(ndotl, A.shin_int)
@@ -257,18 +435,18 @@ __global__ void __launch_bounds__(128) render_kernel(const BlockDesc *__restrict
         px4.w = (unsigned char)min(max(__float2int_rn(Aacc * 255.f), 0), 255);
         const int64_t local = (int64_t)lr * A.width + j;
         reinterpret_cast<uchar4 *>(rgba)[local] = px4;
-        if (A.flags & AFAM_RENDER_DEBUG) {
+        if (DEBUG) {
             nsamp[local] = (int32_t)ns;
             ohash[local] = h;
         }
     }
     // per-warp reductions of the counters
-    uint32_t wsum = __reduce_add_sync(0xffffffffu, ns);
-    uint32_t wsum64 = __reduce_add_sync(0xffffffffu, ns64);
+    const uint32_t wsum = __reduce_add_sync(0xffffffffu, ns);
+    const uint32_t wsum64 = __reduce_add_sync(0xffffffffu, ns64);
     int64_t wmiss = miss;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-        int64_t other = __shfl_xor_sync(0xffffffffu, wmiss, o);
+        const int64_t other = __shfl_xor_sync(0xffffffffu, wmiss, o);
         wmiss = other < wmiss ? other : wmiss;
     }
     if (lane == 0) {
@@ -295,8 +473,9 @@ static int build_owner_grid(afam_store *s, const int32_t *slots, int32_t nb, int
     std::vector<int> bpa(nb);
     cells = 1;
     for (int b = 0; b < nb; b++) {
+        AFAM_CHECK(slots[b] >= 0 && slots[b] < s->nslots && s->host[slots[b]].valid, AFAM_E_VALUE,
+                   "slot %d is empty", slots[b]);
         const SlotHost &h = s->host[slots[b]];
-        AFAM_CHECK(slots[b] >= 0 && slots[b] < s->nslots && h.valid, AFAM_E_VALUE, "slot %d is empty", slots[b]);
         const double w = h.hi[0] - h.lo[0];
         bpa[b] = (int)std::nearbyint(2.0 / w);  // int(round(2/width)), half-to-even
         if (b == 0 || bpa[b] > cells) cells = bpa[b];
@@ -314,6 +493,40 @@ static int build_owner_grid(afam_store *s, const int32_t *slots, int32_t nb, int
                     grid[((size_t)x * cells + y) * cells + z] = (int16_t)b;
     }
     return AFAM_OK;
+}
+
+constexpr int kSmemGridMaxCells = 24;  // 24^3 int16 = 27 KB
+
+// Resident CTAs per SM the kernel is compiled for (register budget
+// 65536/(128*MINB)); AFAM_RENDER_MINB=2|3 selects the variant (default 3).
+static int render_minb() {
+    static int v = [] {
+        const char *e = getenv("AFAM_RENDER_MINB");
+        return (e && atoi(e) == 2) ? 2 : 3;
+    }();
+    return v;
+}
+
+template <bool DEBUG, bool SMEM, int MINB>
+static void launch_render_v(dim3 g, size_t smem, cudaStream_t st, const BlockDesc *descs, const int16_t *grid,
+                            const int32_t *idx, const RenderArgs &A, uint8_t *rgba, afam_render_stats *stats,
+                            int32_t *nsamp, uint64_t *ohash) {
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(render_kernel<DEBUG, SMEM, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        configured = true;
+    }
+    render_kernel<DEBUG, SMEM, MINB><<<g, 128, smem, st>>>(descs, grid, idx, A, rgba, stats, nsamp, ohash);
+}
+
+template <bool DEBUG, bool SMEM>
+static void launch_render(dim3 g, size_t smem, cudaStream_t st, const BlockDesc *descs, const int16_t *grid,
+                          const int32_t *idx, const RenderArgs &A, uint8_t *rgba, afam_render_stats *stats,
+                          int32_t *nsamp, uint64_t *ohash) {
+    if (render_minb() == 2)
+        launch_render_v<DEBUG, SMEM, 2>(g, smem, st, descs, grid, idx, A, rgba, stats, nsamp, ohash);
+    else
+        launch_render_v<DEBUG, SMEM, 3>(g, smem, st, descs, grid, idx, A, rgba, stats, nsamp, ohash);
 }
 
 }  // namespace afam
@@ -357,7 +570,8 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
                    F->nopacity <= AFAM_MAX_TF_POINTS,
                AFAM_E_VALUE, "transfer function needs 1..%d control points", AFAM_MAX_TF_POINTS);
     AFAM_CHECK(nblocks >= 0 && nblocks < 32768, AFAM_E_VALUE, "too many resident blocks (%d)", nblocks);
-    AFAM_CHECK(!(F->flags & AFAM_RENDER_DEBUG) || (nsamp && ohash), AFAM_E_VALUE, "debug buffers missing");
+    const bool debug = F->flags & AFAM_RENDER_DEBUG;
+    AFAM_CHECK(!debug || (nsamp && ohash), AFAM_E_VALUE, "debug buffers missing");
     const int band_rows = F->band_rows > 0 ? F->band_rows : F->height;
     const int nparts = F->nparts > 0 ? F->nparts : 1;
     AFAM_CHECK(F->part >= 0 && F->part < nparts, AFAM_E_VALUE, "part %d outside [0, %d)", F->part, nparts);
@@ -396,20 +610,20 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
     A.dom_lo = (float)F->domain_lo;
     A.dom_hi = (float)F->domain_hi;
     for (int k = 0; k < F->ncolor; k++) {
-        A.cx[k] = (float)F->color[k][0];
+        A.tf[0][k] = (float)F->color[k][0];
         for (int c = 0; c < 3; c++) {
-            A.cv[c][k] = (float)F->color[k][1 + c];
-            A.cs[c][k] = k + 1 < F->ncolor ? (float)((F->color[k + 1][1 + c] - F->color[k][1 + c]) /
-                                                     (F->color[k + 1][0] - F->color[k][0]))
-                                           : 0.f;
+            A.tf[1 + c][k] = (float)F->color[k][1 + c];
+            A.tf[4 + c][k] = k + 1 < F->ncolor ? (float)((F->color[k + 1][1 + c] - F->color[k][1 + c]) /
+                                                         (F->color[k + 1][0] - F->color[k][0]))
+                                               : 0.f;
         }
     }
     for (int k = 0; k < F->nopacity; k++) {
-        A.ox[k] = (float)F->opacity[k][0];
-        A.ov[k] = (float)F->opacity[k][1];
-        A.os[k] = k + 1 < F->nopacity
-                      ? (float)((F->opacity[k + 1][1] - F->opacity[k][1]) / (F->opacity[k + 1][0] - F->opacity[k][0]))
-                      : 0.f;
+        A.tf[7][k] = (float)F->opacity[k][0];
+        A.tf[8][k] = (float)F->opacity[k][1];
+        A.tf[9][k] = k + 1 < F->nopacity ? (float)((F->opacity[k + 1][1] - F->opacity[k][1]) /
+                                                   (F->opacity[k + 1][0] - F->opacity[k][0]))
+                                         : 0.f;
     }
     A.flags = F->flags;
 
@@ -434,7 +648,15 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
     init_stats_kernel<<<1, 1, 0, st>>>(stats);
     if (A.rows > 0) {
         dim3 g((A.width + 15) / 16, (A.rows + 7) / 8);
-        render_kernel<<<g, 128, 0, st>>>(s->d_desc, d_grid, d_idx, A, rgba, stats, nsamp, ohash);
+        const bool sg = cells <= kSmemGridMaxCells;
+        const size_t smem = sizeof(float) * kTfRows * AFAM_MAX_TF_POINTS + (sg ? gbytes : 0);
+        if (debug) {
+            if (sg) launch_render<true, true>(g, smem, st, s->d_desc, d_grid, d_idx, A, rgba, stats, nsamp, ohash);
+            else launch_render<true, false>(g, smem, st, s->d_desc, d_grid, d_idx, A, rgba, stats, nsamp, ohash);
+        } else {
+            if (sg) launch_render<false, true>(g, smem, st, s->d_desc, d_grid, d_idx, A, rgba, stats, nsamp, ohash);
+            else launch_render<false, false>(g, smem, st, s->d_desc, d_grid, d_idx, A, rgba, stats, nsamp, ohash);
+        }
     }
     finish_stats_kernel<<<1, 1, 0, st>>>(stats);
     AFAM_CUDA(cudaGetLastError());

@@ -58,6 +58,22 @@ __global__ void unpack_ctrl_kernel(const uint8_t *__restrict__ raw, uint64_t src
     if ((threadIdx.x & 31) == 0) atomicMax(maxabs, __float_as_uint(m));
 }
 
+// x-quad layout for the ray march: one 16-byte load per (iy, iz) row of a
+// (p+1)^3 gather.  ctrl4[(iz*ncp+iy)*ncp+ix] = c[ix..ix+3][iy][iz], 0 past ncp-1.
+__global__ void unpack_quad_kernel(const uint8_t *__restrict__ raw, uint64_t src_off, int ncp,
+                                   float4 *__restrict__ ctrl4) {
+    const int64_t total = (int64_t)ncp * ncp * ncp;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int ix = (int)(i % ncp);
+        const uint8_t *row = raw + src_off + 4 * (uint64_t)(i - ix);
+        float v[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) v[k] = (ix + k < ncp) ? load_le_f32(row + 4 * (ix + k)) : 0.f;
+        ctrl4[i] = make_float4(v[0], v[1], v[2], v[3]);
+    }
+}
+
 // Knots + per-span basis tables + the slot descriptor.  knot_off: byte
 // offset of the knots; has_t0 = 0 for .mfa images (t0 = 0 implicit,
 // FORMAT.md:44-55), 1 for full vectors.
@@ -73,7 +89,17 @@ __global__ void build_tables_kernel(const uint8_t *__restrict__ raw, uint64_t kn
         if (k == 0) return 0.f;
         return load_le_f32(raw + knot_off + 4 * (uint64_t)(a * (nk - 1) + (k - 1)));
     };
-    for (int i = threadIdx.x; i < 3 * nk; i += blockDim.x) knots[i] = knot(i / nk, i % nk);
+    __shared__ int uniform;
+    if (threadIdx.x == 0) uniform = 1;
+    __syncthreads();
+    for (int i = threadIdx.x; i < 3 * nk; i += blockDim.x) {
+        const int k = i % nk;
+        const float t = knot(i / nk, k);
+        knots[i] = t;
+        // bspline.clamped_knots(ncp, deg).astype(float32) (bspline.py:29-38, model.py:98)
+        const float want = k <= deg ? 0.f : (k >= ncp ? 1.f : (float)((double)(k - deg) / (double)nspan));
+        if (__float_as_uint(t) != __float_as_uint(want)) atomicAnd(&uniform, 0);
+    }
     for (int i = threadIdx.x; i < 3 * nspan; i += blockDim.x) {
         const int a = i / nspan, s = deg + i % nspan;
         double W[2 * AFAM_MAX_DEGREE];
@@ -95,10 +121,11 @@ __global__ void build_tables_kernel(const uint8_t *__restrict__ raw, uint64_t kn
             }
         for (; o < ts; o++) { e32[o] = 0.f; e64[o] = 0.0; }
     }
+    __syncthreads();
     if (threadIdx.x == 0) {
         BlockDesc d = proto;
         d.max_abs = __uint_as_float(*maxabs);
-        d.flags = AFAM_SLOT_VALID | (d.max_abs > fp64_limit ? AFAM_SLOT_FP64 : 0u);
+        d.flags = AFAM_SLOT_VALID | (d.max_abs > fp64_limit ? AFAM_SLOT_FP64 : 0u) | (uniform ? kFlagUniform : 0u);
         *desc = d;
     }
 }
@@ -136,6 +163,7 @@ int afam_store_create(afam_store **out, int device, int32_t slots, int32_t max_n
     s->raw_bytes = std::max(serialized_size(max_ncp, AFAM_MAX_DEGREE),
                             (size_t)(3 * (max_ncp + AFAM_MAX_DEGREE + 1) + (size_t)max_ncp * max_ncp * max_ncp) * 4 + 64);
     s->ctrl_floats = P * max_ncp * max_ncp;
+    s->ctrl4_elems = (size_t)max_ncp * max_ncp * max_ncp;
     s->knot_floats = 3 * (size_t)(max_ncp + AFAM_MAX_DEGREE + 1);
     s->tab_elems = 3 * (size_t)max_ncp * kTabStrideMax;
     s->slot_bytes = s->tab64_off() + afam_store::align256(s->tab_elems * 8);
@@ -188,6 +216,7 @@ static int launch_unpack(afam_store *s, int32_t slot, int deg, int ncp, uint64_t
                          uint64_t ctrl_off, const double extent[6], cudaStream_t st) {
     BlockDesc proto{};
     proto.ctrl = s->ctrl_ptr(slot);
+    proto.ctrl4 = s->ctrl4_ptr(slot);
     proto.tab32 = s->tab32_ptr(slot);
     proto.tab64 = s->tab64_ptr(slot);
     proto.knots = s->knot_ptr(slot);
@@ -195,6 +224,8 @@ static int launch_unpack(afam_store *s, int32_t slot, int deg, int ncp, uint64_t
         proto.lo[a] = extent[2 * a];
         proto.span[a] = extent[2 * a + 1] - extent[2 * a];
         proto.inv_span[a] = 1.0 / proto.span[a];
+        proto.lo_f[a] = (float)proto.lo[a];
+        proto.inv_span_f[a] = (float)proto.inv_span[a];
     }
     proto.ncp = ncp;
     proto.deg = deg;
@@ -206,6 +237,9 @@ static int launch_unpack(afam_store *s, int32_t slot, int deg, int ncp, uint64_t
     int grid = (int)std::min<int64_t>((total + 255) / 256, 1184);
     unpack_ctrl_kernel<<<grid, 256, 0, st>>>(s->raw_ptr(slot), ctrl_off, ncp, proto.pitch, s->ctrl_ptr(slot),
                                              (unsigned int *)(s->d_maxabs + slot));
+    const int64_t total4 = (int64_t)ncp * ncp * ncp;
+    unpack_quad_kernel<<<(int)std::min<int64_t>((total4 + 255) / 256, 1184), 256, 0, st>>>(
+        s->raw_ptr(slot), ctrl_off, ncp, s->ctrl4_ptr(slot));
     build_tables_kernel<<<1, 256, 0, st>>>(s->raw_ptr(slot), knot_off, has_t0, ncp, deg, s->knot_ptr(slot),
                                            s->tab32_ptr(slot), s->tab64_ptr(slot), s->d_desc + slot, proto,
                                            (const unsigned int *)(s->d_maxabs + slot), (float)s->fp64_limit);
