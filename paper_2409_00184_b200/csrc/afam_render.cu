@@ -31,6 +31,18 @@
 
 namespace afam {
 
+constexpr int kTfMaxBp = 2 * AFAM_MAX_TF_POINTS;
+constexpr int kTfLut = 256;
+
+struct TfTable {
+    float4 val[kTfMaxBp];    // (r, g, b, alpha) at breakpoint j
+    float4 slope[kTfMaxBp];  // d/dv on [bp[j], bp[j+1]); 0 past the last breakpoint
+    float bp[kTfMaxBp];      // sorted union of color and opacity control scalars
+    int32_t nbp;
+    float lut_lo, lut_scale; // bucket = (v - lut_lo) * lut_scale over the TF domain
+    int8_t lut[kTfLut];      // last breakpoint <= bucket start (-1: none)
+};
+
 struct RenderArgs {
     double origin[3], f[3], r[3], u[3];
     double tan_x, tan_y;
@@ -39,39 +51,27 @@ struct RenderArgs {
     int32_t width, height, band_rows, nparts, part, rows;
     int32_t cells, nb;
     float power, ambient, diffuse, specular, shininess;
-    int32_t shin_int;   // shininess as a small non-negative integer, else -1
     int32_t power_one;  // power == 1
-    int32_t ncolor, nopac;
     float dom_lo, dom_hi;
-    // TF tables, rows: 0 cx, 1-3 color values, 4-6 color slopes, 7 ox, 8 opacity, 9 opacity slope
-    float tf[10][AFAM_MAX_TF_POINTS];
+    TfTable tf;
     uint32_t flags;
 };
 
-constexpr int kTfRows = 10;
-
-// np.interp(v, xs, ys) (numpy compiled_base.c) for v already clipped to the
-// TF domain; slopes precomputed on the host in float64.
-__device__ __forceinline__ int tf_segment(const float *xs, int n, float v) {
-    int j = 0;
-    for (int k = 1; k < n - 1; k++) j = (v >= xs[k]) ? k : j;
-    return j;
-}
-
-__device__ __forceinline__ float tf_lerp(const float *xs, const float *ys, const float *sl, int n, int j, float v) {
-    if (n == 1 || v < xs[0]) return ys[0];
-    if (v >= xs[n - 1]) return ys[n - 1];
-    return fmaf(sl[j], v - xs[j], ys[j]);
-}
-
-__device__ __forceinline__ float powi(float x, int e) {
-    float r = 1.f;
-    while (e) {
-        if (e & 1) r *= x;
-        x *= x;
-        e >>= 1;
-    }
-    return r;
+// TransferFunction.color_at / opacity_at (render.py:117-124): every
+// channel is np.interp over its own control points; on the sorted union of
+// all control scalars each channel is linear, so one segment search serves
+// r, g, b and alpha.  Values at the breakpoints are the float64 np.interp
+// values rounded to float32.
+__device__ __forceinline__ float4 tf_eval(const TfTable &T, float v) {
+    int bi = (int)((v - T.lut_lo) * T.lut_scale);
+    bi = min(max(bi, 0), kTfLut - 1);
+    int j = T.lut[bi];
+    while (j + 1 < T.nbp && v >= T.bp[j + 1]) ++j;
+    while (j >= 0 && v < T.bp[j]) --j;
+    if (j < 0) return T.val[0];
+    const float4 a = T.val[j], s = T.slope[j];
+    const float dx = v - T.bp[j];
+    return make_float4(fmaf(s.x, dx, a.x), fmaf(s.y, dx, a.y), fmaf(s.z, dx, a.z), fmaf(s.w, dx, a.w));
 }
 
 // Global frame row of local row lr for (band_rows, nparts, part).
@@ -116,8 +116,8 @@ struct BlockLite {
     const float4 *ctrl4;
     const float *tab32;
     const float *knots;
-    double lo[3], inv_span[3];
-    float inv_span_f[3];
+    double lo[3], scale[3];  // scale = nspan / (hi - lo): world offset -> span coordinate
+    float inv_span_f[3], nspan_f;
     int32_t ncp, nspan, deg;
     uint32_t flags;
 };
@@ -126,16 +126,17 @@ __device__ __forceinline__ void load_lite(const BlockDesc *__restrict__ p, Block
     b.ctrl4 = (const float4 *)__ldg((const unsigned long long *)&p->ctrl4);
     b.tab32 = (const float *)__ldg((const unsigned long long *)&p->tab32);
     b.knots = (const float *)__ldg((const unsigned long long *)&p->knots);
+    b.ncp = __ldg(&p->ncp);
+    b.nspan = __ldg(&p->nspan);
+    b.nspan_f = (float)b.nspan;
+    b.deg = __ldg(&p->deg);
+    b.flags = __ldg(&p->flags);
 #pragma unroll
     for (int a = 0; a < 3; a++) {
         b.lo[a] = __ldg(&p->lo[a]);
-        b.inv_span[a] = __ldg(&p->inv_span[a]);
+        b.scale[a] = __ldg(&p->inv_span[a]) * (double)b.nspan;
         b.inv_span_f[a] = __ldg(&p->inv_span_f[a]);
     }
-    b.ncp = __ldg(&p->ncp);
-    b.nspan = __ldg(&p->nspan);
-    b.deg = __ldg(&p->deg);
-    b.flags = __ldg(&p->flags);
 }
 
 // Knot span + basis for one axis.  The span is the reference's
@@ -143,15 +144,24 @@ __device__ __forceinline__ void load_lite(const BlockDesc *__restrict__ p, Block
 // uniform models floor(u*nspan) except within 1e-4 of a knot, where the
 // stored knots decide.
 template <int P>
-__device__ __forceinline__ int axis_basis(const BlockLite &b, int a, double u64, float (&N)[P + 1], float (&E)[P]) {
-    const double tq = u64 * (double)b.nspan;
-    int k = min(max((int)tq, 0), b.nspan - 1);
+__device__ __forceinline__ int axis_basis(const BlockLite &b, const BlockDesc *__restrict__ dp, int a, double p,
+                                          float (&N)[P + 1], float (&E)[P]) {
+    // fast path: interior span of a uniform model, not within 1e-4 spans of a knot
+    const double dpos = p - b.lo[a];
+    const double tq = fmin(fmax(dpos * b.scale[a], 0.0), (double)b.nspan);
+    const int k = min((int)tq, b.nspan - 1);
     const double fr = tq - (double)k;
-    const bool uni = b.flags & kFlagUniform;
     int s = P + k;
-    if (!uni || fr < 1e-4 || fr > 1.0 - 1e-4) s = find_span(b.knots + a * (b.ncp + P + 1), b.ncp, P, b.nspan, u64);
+    const bool uni = b.flags & kFlagUniform;
+    if (uni && fr >= 1e-4 && fr <= 1.0 - 1e-4 && s >= 2 * P - 1 && s <= b.ncp - P) {
+        uniform_basis<P>((float)fr, b.nspan_f, N, E);
+        return s;
+    }
+    // exact path: reference parameter (model.py:67) and span search against the stored knots
+    const double u64 = clamp01(dpos * __ldg(&dp->inv_span[a]));
+    s = find_span(b.knots + a * (b.ncp + P + 1), b.ncp, P, b.nspan, u64);
     if (uni && s >= 2 * P - 1 && s <= b.ncp - P) {
-        uniform_basis<P>((float)(tq - (double)(s - P)), (float)b.nspan, N, E);
+        uniform_basis<P>((float)(u64 * (double)b.nspan - (double)(s - P)), b.nspan_f, N, E);
     } else {
         Tab<float> t;
         load_entry<P>(b.tab32 + ((size_t)a * b.nspan + (s - P)) * tab_stride(P), t);
@@ -246,14 +256,15 @@ __device__ __forceinline__ void gather_quad(const BlockLite &b, int32_t slot, Ga
 }
 
 template <int P>
-__device__ __forceinline__ void decode_f32(const BlockLite &b, int32_t slot, GatherCache &G, const double (&pos)[3],
+__device__ __forceinline__ void decode_f32(const BlockLite &b, const BlockDesc *__restrict__ dp, int32_t slot,
+                                           GatherCache &G, const double (&pos)[3],
                                            float &v, float (&g)[3]) {
     constexpr int Q = P + 1;
     float Nx[Q], Ex[P], Ny[Q], Ey[P], Nz[Q], Ez[P];
     // model.py:64-68 params_for: u = clip((p - lo)/span, 0, 1), float64
-    const int sx = axis_basis<P>(b, 0, clamp01((pos[0] - b.lo[0]) * b.inv_span[0]), Nx, Ex);
-    const int sy = axis_basis<P>(b, 1, clamp01((pos[1] - b.lo[1]) * b.inv_span[1]), Ny, Ey);
-    const int sz = axis_basis<P>(b, 2, clamp01((pos[2] - b.lo[2]) * b.inv_span[2]), Nz, Ez);
+    const int sx = axis_basis<P>(b, dp, 0, pos[0], Nx, Ex);
+    const int sy = axis_basis<P>(b, dp, 1, pos[1], Ny, Ey);
+    const int sz = axis_basis<P>(b, dp, 2, pos[2], Nz, Ez);
     gather_quad<P>(b, slot, G, sx - P, sy - P, sz - P);
     float gg[3];
     contract_quad<P, float>(G.c4, Nx, Ex, Ny, Ey, Nz, Ez, v, gg);
@@ -296,10 +307,13 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
                                                         uint8_t *__restrict__ rgba, afam_render_stats *stats,
                                                         int32_t *__restrict__ nsamp, uint64_t *__restrict__ ohash) {
     extern __shared__ __align__(16) unsigned char smem[];
-    float(*tf)[AFAM_MAX_TF_POINTS] = reinterpret_cast<float(*)[AFAM_MAX_TF_POINTS]>(smem);
-    int16_t *sgrid = reinterpret_cast<int16_t *>(smem + sizeof(float) * kTfRows * AFAM_MAX_TF_POINTS);
-    for (int i = threadIdx.x; i < kTfRows * AFAM_MAX_TF_POINTS; i += blockDim.x)
-        tf[i / AFAM_MAX_TF_POINTS][i % AFAM_MAX_TF_POINTS] = A.tf[i / AFAM_MAX_TF_POINTS][i % AFAM_MAX_TF_POINTS];
+    TfTable &tf = *reinterpret_cast<TfTable *>(smem);
+    int16_t *sgrid = reinterpret_cast<int16_t *>(smem + sizeof(TfTable));
+    {
+        const int *src = reinterpret_cast<const int *>(&A.tf);
+        int *dst = reinterpret_cast<int *>(&tf);
+        for (int i = threadIdx.x; i < (int)(sizeof(TfTable) / 4); i += blockDim.x) dst[i] = src[i];
+    }
     if (SMEM_GRID)
         for (int i = threadIdx.x; i < A.cells * A.cells * A.cells; i += blockDim.x) sgrid[i] = grid[i];
     __syncthreads();
@@ -390,21 +404,17 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
                 else if (b.deg == 2) decode_f64<2>(b, descs + cur_slot, cur_slot, G, pos, v, g);
                 else decode_f64<1>(b, descs + cur_slot, cur_slot, G, pos, v, g);
             } else {
-                if (b.deg == 3) decode_f32<3>(b, cur_slot, G, pos, v, g);
-                else if (b.deg == 2) decode_f32<2>(b, cur_slot, G, pos, v, g);
-                else decode_f32<1>(b, cur_slot, G, pos, v, g);
+                if (b.deg == 3) decode_f32<3>(b, descs + cur_slot, cur_slot, G, pos, v, g);
+                else if (b.deg == 2) decode_f32<2>(b, descs + cur_slot, cur_slot, G, pos, v, g);
+                else decode_f32<1>(b, descs + cur_slot, cur_slot, G, pos, v, g);
             }
             ++ns;
             if (DEBUG) h = (h ^ (uint64_t)(uint32_t)own) * 1099511628211ULL;
 
             // TransferFunction (render.py:117-124)
-            const float vc = fminf(fmaxf(v, A.dom_lo), A.dom_hi);
-            const int jo = tf_segment(tf[7], A.nopac, vc);
-            const float atf = tf_lerp(tf[7], tf[8], tf[9], A.nopac, jo, vc);
-            const int jc = tf_segment(tf[0], A.ncolor, vc);
-            float col[3];
-#pragma unroll
-            for (int c = 0; c < 3; c++) col[c] = tf_lerp(tf[0], tf[1 + c], tf[4 + c], A.ncolor, jc, vc);
+            const float4 tfv = tf_eval(tf, fminf(fmaxf(v, A.dom_lo), A.dom_hi));
+            const float col[3] = {tfv.x, tfv.y, tfv.z};
+            const float atf = tfv.w;
             // render.py:451 opacity correction
             const float as = A.power_one ? 1.f - (1.f - atf) : 1.f - __powf(1.f - atf, A.power);
             // _shade (render.py:383-395)
@@ -415,8 +425,9 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
                 ndotl = fabsf(g[0] * vdir[0] + g[1] * vdir[1] + g[2] * vdir[2]) * ig;
             }
             const float dif = A.diffuse * ndotl;
-            const float spec = A.specular * (A.shin_int >= 0 ? powi(ndotl, A.shin_int)
-                                                             : (ndotl > 0.f ? __powf(ndotl, A.shininess) : 0.f));
+            // ndotl**shininess via exp2(shininess * log2(ndotl)) (MUFU.LG2 + MUFU.EX2)
+            const float spec = A.specular * (ndotl > 0.f ? exp2f(A.shininess * __log2f(ndotl))
+                                                         : (A.shininess == 0.f ? 1.f : 0.f));
             const float lit = A.ambient + dif;
             // render.py:453-455 front-to-back composite
             const float w = (1.f - Aacc) * as;
@@ -465,6 +476,51 @@ __global__ void init_stats_kernel(afam_render_stats *s) {
 
 __global__ void finish_stats_kernel(afam_render_stats *s) {
     if (s->missing_key == INT64_MAX) s->missing_key = -1;
+}
+
+// np.interp(x, xs, ys) (numpy compiled_base.c) in float64 on the host.
+static double host_interp(double x, const double (*pts)[4], const double (*opts)[2], int n, int col, bool color) {
+    auto X = [&](int k) { return color ? pts[k][0] : opts[k][0]; };
+    auto Y = [&](int k) { return color ? pts[k][col] : opts[k][1]; };
+    if (n == 1 || x <= X(0)) return Y(0);
+    if (x >= X(n - 1)) return Y(n - 1);
+    int j = 0;
+    while (j + 1 < n && X(j + 1) <= x) ++j;
+    if (X(j) == x) return Y(j);
+    const double slope = (Y(j + 1) - Y(j)) / (X(j + 1) - X(j));
+    return slope * (x - X(j)) + Y(j);
+}
+
+static void build_tf_table(const afam_frame *F, TfTable &T) {
+    std::vector<double> xs;
+    for (int k = 0; k < F->ncolor; k++) xs.push_back(F->color[k][0]);
+    for (int k = 0; k < F->nopacity; k++) xs.push_back(F->opacity[k][0]);
+    std::sort(xs.begin(), xs.end());
+    xs.erase(std::unique(xs.begin(), xs.end()), xs.end());
+    T.nbp = (int)xs.size();
+    auto eval = [&](double x, int c) {
+        return c < 3 ? host_interp(x, F->color, F->opacity, F->ncolor, 1 + c, true)
+                     : host_interp(x, F->color, F->opacity, F->nopacity, 1, false);
+    };
+    for (int j = 0; j < T.nbp; j++) {
+        T.bp[j] = (float)xs[j];
+        float v[4], s[4];
+        for (int c = 0; c < 4; c++) {
+            v[c] = (float)eval(xs[j], c);
+            s[c] = j + 1 < T.nbp ? (float)((eval(xs[j + 1], c) - eval(xs[j], c)) / (xs[j + 1] - xs[j])) : 0.f;
+        }
+        T.val[j] = make_float4(v[0], v[1], v[2], v[3]);
+        T.slope[j] = make_float4(s[0], s[1], s[2], s[3]);
+    }
+    const double lo = F->domain_lo, hi = F->domain_hi;
+    T.lut_lo = (float)lo;
+    T.lut_scale = (float)(kTfLut / (hi - lo));
+    for (int i = 0; i < kTfLut; i++) {
+        const double x = lo + (hi - lo) * i / kTfLut;
+        int j = -1;
+        while (j + 1 < T.nbp && xs[j + 1] <= x) ++j;
+        T.lut[i] = (int8_t)j;
+    }
 }
 
 // render.py:357-375 _BlockIndex over the given (sorted) slots.
@@ -603,28 +659,9 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
     A.diffuse = (float)F->diffuse;
     A.specular = (float)F->specular;
     A.shininess = (float)F->shininess;
-    A.shin_int = (F->shininess >= 0 && F->shininess <= 1024 && F->shininess == std::floor(F->shininess))
-                     ? (int)F->shininess : -1;
-    A.ncolor = F->ncolor;
-    A.nopac = F->nopacity;
     A.dom_lo = (float)F->domain_lo;
     A.dom_hi = (float)F->domain_hi;
-    for (int k = 0; k < F->ncolor; k++) {
-        A.tf[0][k] = (float)F->color[k][0];
-        for (int c = 0; c < 3; c++) {
-            A.tf[1 + c][k] = (float)F->color[k][1 + c];
-            A.tf[4 + c][k] = k + 1 < F->ncolor ? (float)((F->color[k + 1][1 + c] - F->color[k][1 + c]) /
-                                                         (F->color[k + 1][0] - F->color[k][0]))
-                                               : 0.f;
-        }
-    }
-    for (int k = 0; k < F->nopacity; k++) {
-        A.tf[7][k] = (float)F->opacity[k][0];
-        A.tf[8][k] = (float)F->opacity[k][1];
-        A.tf[9][k] = k + 1 < F->nopacity ? (float)((F->opacity[k + 1][1] - F->opacity[k][1]) /
-                                                   (F->opacity[k + 1][0] - F->opacity[k][0]))
-                                         : 0.f;
-    }
+    build_tf_table(F, A.tf);
     A.flags = F->flags;
 
     std::vector<int16_t> grid;
@@ -649,7 +686,7 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
     if (A.rows > 0) {
         dim3 g((A.width + 15) / 16, (A.rows + 7) / 8);
         const bool sg = cells <= kSmemGridMaxCells;
-        const size_t smem = sizeof(float) * kTfRows * AFAM_MAX_TF_POINTS + (sg ? gbytes : 0);
+        const size_t smem = sizeof(TfTable) + (sg ? gbytes : 0);
         if (debug) {
             if (sg) launch_render<true, true>(g, smem, st, s->d_desc, d_grid, d_idx, A, rgba, stats, nsamp, ohash);
             else launch_render<true, false>(g, smem, st, s->d_desc, d_grid, d_idx, A, rgba, stats, nsamp, ohash);
