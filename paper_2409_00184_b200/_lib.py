@@ -15,7 +15,7 @@ from pathlib import Path
 from .errors import CapacityError, FormatError, MissingBlockError
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libafam.so"
+LIB_PATH = Path(os.environ.get("AFAM_LIB", str(PKG / "libafam.so")))  # override: A/B kernel builds
 CSRC = PKG / "csrc"
 
 AFAM_OK = 0

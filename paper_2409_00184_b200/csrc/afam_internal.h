@@ -29,7 +29,7 @@ constexpr int kTabStrideMax = 12;  // tab_stride(AFAM_MAX_DEGREE)
 // Device-resident descriptor of one slot (one micro-model).
 struct alignas(16) BlockDesc {
     const float *ctrl;    // ncp x ncp rows of `pitch` floats: ctrl[(iz*ncp+iy)*pitch+ix]
-    const float4 *ctrl4;  // x-quad layout: ctrl4[(iz*ncp+iy)*ncp+ix] = c[ix..ix+3][iy][iz] (0 past ncp-1)
+    const float4 *ctrl4;  // x-quad layout: ctrl4[(iz*ncp+ix)*ncp+iy] = c[ix..ix+3][iy][iz] (0 past ncp-1)
     const float *tab32;   // [3][nspan][tab_stride(deg)] float
     const double *tab64;  // [3][nspan][tab_stride(deg)] double
     const float *knots;   // [3][nk] float (full clamped vectors)

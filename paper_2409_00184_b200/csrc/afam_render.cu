@@ -147,8 +147,10 @@ template <int P>
 __device__ __forceinline__ int axis_basis(const BlockLite &b, const BlockDesc *__restrict__ dp, int a, double p,
                                           float (&N)[P + 1], float (&E)[P]) {
     // fast path: interior span of a uniform model, not within 1e-4 spans of a knot
+    // no clamp needed here: a sample a hair outside [0, nspan] (rounding at a
+    // block face) lands within 1e-4 of an end knot and takes the exact path
     const double dpos = p - b.lo[a];
-    const double tq = fmin(fmax(dpos * b.scale[a], 0.0), (double)b.nspan);
+    const double tq = dpos * b.scale[a];
     const int k = min((int)tq, b.nspan - 1);
     const double fr = tq - (double)k;
     int s = P + k;
@@ -232,6 +234,14 @@ __device__ __forceinline__ void contract_quad(const float4 (&c4)[16], const T (&
     v = vv; g[0] = gx; g[1] = gy; g[2] = gz;
 }
 
+// Keep the gathered rows across samples (re-gather only on span/owner
+// change).  Off by default: at LOD-1 span widths a lane changes span on most
+// steps, so the cache mostly costs 64 registers of occupancy.
+#ifndef AFAM_GATHER_CACHE
+#define AFAM_GATHER_CACHE 0
+#endif
+constexpr bool kGatherCache = AFAM_GATHER_CACHE;
+
 struct GatherCache {
     int32_t slot, x0, y0, z0;
     float4 c4[16];
@@ -242,16 +252,21 @@ struct GatherCache {
 template <int P>
 __device__ __forceinline__ void gather_quad(const BlockLite &b, int32_t slot, GatherCache &G, int x0, int y0, int z0) {
     constexpr int Q = P + 1;
-    if (slot != G.slot || x0 != G.x0 || y0 != G.y0 || z0 != G.z0) {
-        const float4 *base = b.ctrl4 + ((size_t)z0 * b.ncp + y0) * b.ncp + x0;
+    if (!kGatherCache || slot != G.slot || x0 != G.x0 || y0 != G.y0 || z0 != G.z0) {
+        const float4 *base = b.ctrl4 + ((size_t)z0 * b.ncp + x0) * b.ncp + y0;
+        const size_t plane = (size_t)b.ncp * b.ncp;
 #pragma unroll
-        for (int cz = 0; cz < Q; cz++)
+        for (int cz = 0; cz < Q; cz++) {
+            const float4 *p = base + cz * plane;
 #pragma unroll
-            for (int by = 0; by < Q; by++) G.c4[cz * Q + by] = __ldg(base + ((size_t)cz * b.ncp + by) * b.ncp);
-        G.slot = slot;
-        G.x0 = x0;
-        G.y0 = y0;
-        G.z0 = z0;
+            for (int by = 0; by < Q; by++) G.c4[cz * Q + by] = __ldg(p + by);
+        }
+        if (kGatherCache) {
+            G.slot = slot;
+            G.x0 = x0;
+            G.y0 = y0;
+            G.z0 = z0;
+        }
     }
 }
 
@@ -380,7 +395,7 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
 #pragma unroll
             for (int a = 0; a < 3; a++) {
                 double p = __dadd_rn(A.origin[a], __dmul_rn(t, d[a]));
-                p = fmin(fmax(p, -1.0), 1.0);
+                p = p < -1.0 ? -1.0 : (p > 1.0 ? 1.0 : p);  // np.clip (p is never NaN here)
                 pos[a] = p;
                 const double sc = __dmul_rn(__dmul_rn(__dadd_rn(p, 1.0), 0.5), cellsd);
                 int ci = __double2int_rz(sc);
@@ -554,11 +569,13 @@ static int build_owner_grid(afam_store *s, const int32_t *slots, int32_t nb, int
 constexpr int kSmemGridMaxCells = 24;  // 24^3 int16 = 27 KB
 
 // Resident CTAs per SM the kernel is compiled for (register budget
-// 65536/(128*MINB)); AFAM_RENDER_MINB=2|3 selects the variant (default 3).
+// 65536/(128*MINB)); AFAM_RENDER_MINB=2|3|4 selects the variant (default 4:
+// 128 registers, 16 warps/SM, measured fastest on B200).
 static int render_minb() {
     static int v = [] {
         const char *e = getenv("AFAM_RENDER_MINB");
-        return (e && atoi(e) == 2) ? 2 : 3;
+        const int m = e ? atoi(e) : 0;
+        return (m == 2 || m == 3) ? m : 4;
     }();
     return v;
 }
@@ -581,6 +598,8 @@ static void launch_render(dim3 g, size_t smem, cudaStream_t st, const BlockDesc 
                           int32_t *nsamp, uint64_t *ohash) {
     if (render_minb() == 2)
         launch_render_v<DEBUG, SMEM, 2>(g, smem, st, descs, grid, idx, A, rgba, stats, nsamp, ohash);
+    else if (render_minb() == 4)
+        launch_render_v<DEBUG, SMEM, 4>(g, smem, st, descs, grid, idx, A, rgba, stats, nsamp, ohash);
     else
         launch_render_v<DEBUG, SMEM, 3>(g, smem, st, descs, grid, idx, A, rgba, stats, nsamp, ohash);
 }

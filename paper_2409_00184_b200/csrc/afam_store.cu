@@ -58,15 +58,18 @@ __global__ void unpack_ctrl_kernel(const uint8_t *__restrict__ raw, uint64_t src
     if ((threadIdx.x & 31) == 0) atomicMax(maxabs, __float_as_uint(m));
 }
 
-// x-quad layout for the ray march: one 16-byte load per (iy, iz) row of a
-// (p+1)^3 gather.  ctrl4[(iz*ncp+iy)*ncp+ix] = c[ix..ix+3][iy][iz], 0 past ncp-1.
+// x-quad layout for the ray march, y innermost: ctrl4[(iz*ncp+ix)*ncp+iy] =
+// c[ix..ix+3][iy][iz] (0 past ncp-1).  A (p+1)^3 gather is p+1 runs of p+1
+// consecutive 16-byte rows (one address per z plane).
 __global__ void unpack_quad_kernel(const uint8_t *__restrict__ raw, uint64_t src_off, int ncp,
                                    float4 *__restrict__ ctrl4) {
     const int64_t total = (int64_t)ncp * ncp * ncp;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const int ix = (int)(i % ncp);
-        const uint8_t *row = raw + src_off + 4 * (uint64_t)(i - ix);
+        const int iy = (int)(i % ncp);
+        const int ix = (int)((i / ncp) % ncp);
+        const int64_t iz = i / ((int64_t)ncp * ncp);
+        const uint8_t *row = raw + src_off + 4 * (uint64_t)((iz * ncp + iy) * ncp);  // x-fastest source row
         float v[4];
 #pragma unroll
         for (int k = 0; k < 4; k++) v[k] = (ix + k < ncp) ? load_le_f32(row + 4 * (ix + k)) : 0.f;
