@@ -50,7 +50,7 @@ WORKLOAD = {"workload": "config3: 1024^3-equiv synthetic turbulence, 4 LODs, 468
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--size", type=int, default=1024)
@@ -77,7 +77,7 @@ class ClockSampler:
             return self
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -205,14 +205,16 @@ def run_ours(args, rank, world, local_rank):
         ev2.record(stream)
         return ev0, ev1, ev2, info, len(vis)
 
-    for k in range(args.warmup):
-        step(k)
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
     times, ktimes, samples, fp64s, nvis = [], [], 0, 0, []
+    # the sampler starts before the warm-up: nvidia-smi's own start-up must not
+    # overlap the timed steps; its samples cover warm-up + timed region (all under load)
     with ClockSampler(local_rank) as clk:
+        time.sleep(1.0)
+        for k in range(args.warmup):
+            step(k)
         torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
         if world > 1:
             dist.barrier()
         wall0 = time.perf_counter()
