@@ -40,6 +40,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "decoded samples/s (1024^2 ray-cast, config 3)"
 UNIT = "samples/s"
 FLOP_PER_SAMPLE_P3 = 384  # 2*(2q^3+3q^2+4q), q=4: separable value+gradient contraction
+FLOP_VALUE_P3 = 168  # 2*(q^3+q^2+q): value only (transparent samples skip the gradient, see afam_render.cu)
 WORKLOAD = {"workload": "config3: 1024^3-equiv synthetic turbulence, 4 LODs, 4680 blocks (micro 65, degree 3, "
                         "ncp 40-65), 1024x1024 ray-cast, sd 1e-3, ML TF + gradient shading, "
                         "orbit_trajectory(100, r=2.0)",
@@ -185,27 +186,28 @@ def run_ours(args, rank, world, local_rank):
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     frame_out = torch.empty((render._lib.lib().afam_frame_rows(S, band, world, rank), S, 4), dtype=torch.uint8,
                             device=dev)
-    gather_bufs = None
-    if world > 1 and rank == 0:
-        gather_bufs = [torch.empty((render._lib.lib().afam_frame_rows(S, band, world, r), S, 4), dtype=torch.uint8,
-                                   device=dev) for r in range(world)]
+    from paper_2409_00184_b200 import tiles
 
     def step(k):
+        """One frame: render this rank's bands, gather them to rank 0.  Device
+        time = the render kernels (CUDA events recorded by afam_render on the
+        render stream around its launches) + the NCCL gather (events on the
+        same stream).  Host preparation is reported separately."""
         pov = povs[k % len(povs)]
         vis = render.select_visible(pov, man, params.aspect)
         blocks = {a: resident_all[a] for a in vis}
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0 = torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
         _, info, _ = render.render_part(pov, blocks, tf, params, band_rows=band, nparts=world, part=rank,
                                         device=local_rank, out=frame_out)
+        ev1, ev2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev1.record(stream)
-        ev2 = torch.cuda.Event(enable_timing=True)
-        if world > 1:
-            dist.gather(frame_out, gather_bufs if rank == 0 else None, dst=0)
+        if world > 1:  # NCCL gather of the RGBA8 bands to rank 0 + un-permute there
+            tiles.gather_bands(frame_out, S, band)
         ev2.record(stream)
         return ev0, ev1, ev2, info, len(vis)
 
-    times, ktimes, samples, fp64s, nvis = [], [], 0, 0, []
+    times, ktimes, envelope, samples, fp64s, shaded, nvis = [], [], [], 0, 0, 0, []
     # the sampler starts before the warm-up: nvidia-smi's own start-up must not
     # overlap the timed steps; its samples cover warm-up + timed region (all under load)
     with ClockSampler(local_rank) as clk:
@@ -222,10 +224,12 @@ def run_ours(args, rank, world, local_rank):
             flush.zero_()  # evict the previous frame's blocks from L2 (outside the events)
             ev0, ev1, ev2, info, nv = step(args.warmup + k)
             torch.cuda.synchronize(dev)
-            ktimes.append(ev0.elapsed_time(ev1))
-            times.append(ev0.elapsed_time(ev2))
+            ktimes.append(info["kernel_ms"])
+            times.append(info["kernel_ms"] + ev1.elapsed_time(ev2))
+            envelope.append(ev0.elapsed_time(ev1))
             samples += info["samples"]
             fp64s += info["fp64_samples"]
+            shaded += info["shaded_samples"]
             nvis.append(nv)
         torch.cuda.synchronize(dev)
         if world > 1:
@@ -244,7 +248,8 @@ def run_ours(args, rank, world, local_rank):
 
     # -- roofline of the dominant kernel (render_kernel)
     fma_peak = measure_fma_peak(dev)
-    achieved = (samples * FLOP_PER_SAMPLE_P3) / (sum(ktimes) / 1e3) / 1e12
+    flops = samples * FLOP_VALUE_P3 + shaded * (FLOP_PER_SAMPLE_P3 - FLOP_VALUE_P3)
+    achieved = flops / (sum(ktimes) / 1e3) / 1e12
     traffic = None
     prof = ROOT / "profiles" / "render_kernel_traffic.json"
     if prof.exists():
@@ -255,9 +260,11 @@ def run_ours(args, rank, world, local_rank):
     roofline = {"bound": "fp32", "achieved": achieved, "peak": fma_peak, "unit": "TFLOP/s",
                 "frac": achieved / fma_peak if fma_peak else None, "traffic": traffic,
                 "kernel": "render_kernel (K2)",
-                "note": "algorithmic FLOP = 384/sample (separable p=3 value+gradient contraction, basis "
-                        "evaluation not credited) x samples / render-call event time; peak = FFMA "
-                        "microbenchmark on this GPU (MEASURED_PEAKS.json has no FP32 figure)"}
+                "note": "algorithmic FLOP (separable p=3 contraction, basis evaluation not credited) = 168 per "
+                        "decoded sample (value) + 216 per shaded sample (gradient, TF opacity > 0), over the "
+                        "render kernels' device time (CUDA events on the render stream); peak = FFMA "
+                        "microbenchmark on this GPU (MEASURED_PEAKS.json has no FP32 figure)",
+                "shaded_frac": shaded / max(1, samples)}
 
     result = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
               "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
@@ -265,7 +272,8 @@ def run_ours(args, rank, world, local_rank):
                                                                  "ill-conditioned blocks)",
               "data": "synthetic (seeded turbulence, fitted like the reference encoder)",
               "config": dict(WORKLOAD, parallelism=f"image bands x{world}", frame_ms=step_ms,
-                             kernel_ms=kern_ms, visible_blocks_mean=float(np.mean(nvis)),
+                             kernel_ms=kern_ms, host_envelope_ms=float(np.mean(envelope)),
+                             visible_blocks_mean=float(np.mean(nvis)),
                              fp64_sample_frac=total_fp64 / max(1.0, total_samples), gen_s=round(gen_s, 1),
                              upload_s=round(upload_s, 2), fp64_slot_sample=int(nfp64)),
               "roofline": roofline, "clocks": clk.summary(), "gpu_launches": 3 * args.steps,
@@ -292,19 +300,16 @@ def run_e2e(args, man, blobs, povs, tf, params, rank, world, local_rank):
     band = 8
     S = params.width
 
+    from paper_2409_00184_b200 import tiles
+
     def draw(pov, resident, tf_, params_):
-        out, info, _ = render.render_part(pov, resident, tf_, params_, band_rows=band, nparts=world, part=rank,
-                                          device=local_rank)
-        draw.samples += info["samples"]
-        if world > 1:
-            bufs = [torch.empty((render._lib.lib().afam_frame_rows(S, band, world, r), S, 4), dtype=torch.uint8,
-                                device=out.device) for r in range(world)] if rank == 0 else None
-            dist.gather(out, bufs, dst=0)
-            if rank == 0:
-                out = torch.cat(bufs)
-        host = out.cpu().numpy()  # D2H of the frame (the step's result)
-        draw.d2h += host.nbytes
-        return host
+        # public API: tiles.render_tiles == render.render on one GPU; the
+        # Frame (host RGBA8) is the step's result read back to the host
+        frame = tiles.render_tiles(pov, resident, tf_, params_, band_rows=band)
+        draw.samples += tiles.render_tiles.last_stats["samples"]
+        if frame is not None:
+            draw.d2h += frame.rgba.nbytes
+        return frame
 
     draw.samples, draw.d2h = 0, 0
     nwarm = args.warmup

@@ -163,7 +163,7 @@ typedef struct {
     uint64_t samples;      /* decoded samples (value+gradient evaluations) */
     int64_t missing_key;   /* (step << 32) | ray of the first sample in an uncovered finest cell, or -1 */
     uint64_t fp64_samples; /* samples decoded on the float64 path */
-    uint64_t pad;
+    uint64_t shaded_samples; /* samples with TF opacity > 0 (gradient + shading evaluated) */
 } afam_render_stats;
 
 /*
@@ -176,6 +176,10 @@ typedef struct {
  */
 int afam_render(afam_store *s, const afam_frame *frame, const int32_t *slots, int32_t nblocks, uint8_t *rgba,
                 afam_render_stats *stats, int32_t *nsamp, uint64_t *ohash, void *stream);
+
+/* Device time (ms) of the kernels of the last afam_render on this store
+ * (CUDA events recorded on its stream around the launches); waits for them. */
+int afam_render_elapsed(afam_store *s, float *ms);
 
 /* Rows of the full frame rendered by (band_rows, nparts, part). */
 int32_t afam_frame_rows(int32_t height, int32_t band_rows, int32_t nparts, int32_t part);

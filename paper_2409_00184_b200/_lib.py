@@ -65,7 +65,7 @@ class AfamFrame(C.Structure):
 
 class AfamRenderStats(C.Structure):
     _fields_ = [("samples", C.c_uint64), ("missing_key", C.c_int64), ("fp64_samples", C.c_uint64),
-                ("pad", C.c_uint64)]
+                ("shaded_samples", C.c_uint64)]
 
 
 # (name, restype, argtypes) for every symbol declared in include/afam.h
@@ -94,6 +94,7 @@ SIGNATURES = [
                                       C.POINTER(C.c_int32)]),
     ("afam_render", C.c_int, [C.c_void_p, C.POINTER(AfamFrame), C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
                               C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("afam_render_elapsed", C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
     ("afam_frame_rows", C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
     ("afam_owner_grid", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.c_void_p,
                                   C.c_int32]),

@@ -76,6 +76,7 @@ struct afam_store {
     afam::BlockDesc *d_desc = nullptr;   // nslots descriptors (device)
     float *d_maxabs = nullptr;           // nslots (device)
     std::vector<afam::SlotHost> host;
+    cudaEvent_t ev_k0 = nullptr, ev_k1 = nullptr;  // bracket the last afam_render's kernels
     std::mutex mu;
     std::map<std::tuple<int, int, int>, afam::DecodeOp> ops;
 

@@ -270,10 +270,16 @@ __device__ __forceinline__ void gather_quad(const BlockLite &b, int32_t slot, Ga
     }
 }
 
+// Value first (separable x -> y -> z with the N weights, keeping the x and
+// y partial sums), then the transfer function; the gradient (difference
+// form, reusing the partial sums for d/dy and d/dz) only for samples the TF
+// makes non-transparent.  A sample with alpha_tf = 0 has a_s = 0 and adds
+// nothing to C or A (render.py:451-455), so skipping its gradient and
+// shading leaves the frame bit-identical.
 template <int P>
 __device__ __forceinline__ void decode_f32(const BlockLite &b, const BlockDesc *__restrict__ dp, int32_t slot,
-                                           GatherCache &G, const double (&pos)[3],
-                                           float &v, float (&g)[3]) {
+                                           GatherCache &G, const double (&pos)[3], const TfTable &tf, float dom_lo,
+                                           float dom_hi, float &v, float4 &tfv, float (&g)[3]) {
     constexpr int Q = P + 1;
     float Nx[Q], Ex[P], Ny[Q], Ey[P], Nz[Q], Ez[P];
     // model.py:64-68 params_for: u = clip((p - lo)/span, 0, 1), float64
@@ -281,10 +287,61 @@ __device__ __forceinline__ void decode_f32(const BlockLite &b, const BlockDesc *
     const int sy = axis_basis<P>(b, dp, 1, pos[1], Ny, Ey);
     const int sz = axis_basis<P>(b, dp, 2, pos[2], Nz, Ez);
     gather_quad<P>(b, slot, G, sx - P, sy - P, sz - P);
-    float gg[3];
-    contract_quad<P, float>(G.c4, Nx, Ex, Ny, Ey, Nz, Ez, v, gg);
+    // value pass; d/dy and d/dz come almost free from its partial sums
+    float ry[Q], gy = 0.f;
 #pragma unroll
-    for (int a = 0; a < 3; a++) g[a] = gg[a] * b.inv_span_f[a];  // model.py:79 gradient / span
+    for (int cz = 0; cz < Q; cz++) {
+        float rx[Q];
+        float ay = 0.f;
+#pragma unroll
+        for (int by = 0; by < Q; by++) {
+            const float4 &r = G.c4[cz * Q + by];
+            float acc = Nx[0] * comp<0>(r);
+            acc = fmaf(Nx[1], comp<1>(r), acc);
+            if constexpr (P >= 2) acc = fmaf(Nx[2], comp<2>(r), acc);
+            if constexpr (P >= 3) acc = fmaf(Nx[3], comp<3>(r), acc);
+            rx[by] = acc;
+            ay = fmaf(Ny[by], acc, ay);
+        }
+        float ady = 0.f;
+#pragma unroll
+        for (int k = 0; k < P; k++) ady = fmaf(Ey[k], rx[k + 1] - rx[k], ady);
+        gy = fmaf(Nz[cz], ady, gy);
+        ry[cz] = ay;
+    }
+    float vv = 0.f, gz = 0.f;
+#pragma unroll
+    for (int cz = 0; cz < Q; cz++) vv = fmaf(Nz[cz], ry[cz], vv);
+#pragma unroll
+    for (int k = 0; k < P; k++) gz = fmaf(Ez[k], ry[k + 1] - ry[k], gz);
+    v = vv;
+    tfv = tf_eval(tf, fminf(fmaxf(vv, dom_lo), dom_hi));  // TransferFunction (render.py:117-124)
+    if (!(tfv.w > 0.f)) {
+        g[0] = g[1] = g[2] = 0.f;
+        return;
+    }
+    // d/dx: differences along the x-quad rows, re-read from L1 so the rows
+    // need not stay in registers across the TF lookup
+    float gx = 0.f;
+    const float4 *base = b.ctrl4 + ((size_t)(sz - P) * b.ncp + (sx - P)) * b.ncp + (sy - P);
+    const size_t plane = (size_t)b.ncp * b.ncp;
+#pragma unroll
+    for (int cz = 0; cz < Q; cz++) {
+        float adxy = 0.f;
+#pragma unroll
+        for (int by = 0; by < Q; by++) {
+            const float4 r = kGatherCache ? G.c4[cz * Q + by] : __ldg(base + cz * plane + by);
+            float dacc = Ex[0] * (comp<1>(r) - comp<0>(r));
+            if constexpr (P >= 2) dacc = fmaf(Ex[1], comp<2>(r) - comp<1>(r), dacc);
+            if constexpr (P >= 3) dacc = fmaf(Ex[2], comp<3>(r) - comp<2>(r), dacc);
+            adxy = fmaf(Ny[by], dacc, adxy);
+        }
+        gx = fmaf(Nz[cz], adxy, gx);
+    }
+    // model.py:79 gradient / span
+    g[0] = gx * b.inv_span_f[0];
+    g[1] = gy * b.inv_span_f[1];
+    g[2] = gz * b.inv_span_f[2];
 }
 
 // Ill-conditioned slots: the same schedule with float64 parameters (the
@@ -373,7 +430,7 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
     const float o_max = (float)A.o_max;
     const bool o_max_exact = (double)o_max == A.o_max;
     float C0 = 0.f, C1 = 0.f, C2 = 0.f, Aacc = 0.f;
-    uint32_t ns = 0, ns64 = 0;
+    uint32_t ns = 0, ns64 = 0, nshade = 0;
     uint64_t h = 1469598103934665603ULL;
     int64_t miss = INT64_MAX;
 
@@ -413,23 +470,25 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
                 load_lite(descs + cur_slot, b);
             }
             float v, g[3];
+            float4 tfv;
             if (b.flags & AFAM_SLOT_FP64) {
                 ++ns64;
                 if (b.deg == 3) decode_f64<3>(b, descs + cur_slot, cur_slot, G, pos, v, g);
                 else if (b.deg == 2) decode_f64<2>(b, descs + cur_slot, cur_slot, G, pos, v, g);
                 else decode_f64<1>(b, descs + cur_slot, cur_slot, G, pos, v, g);
+                tfv = tf_eval(tf, fminf(fmaxf(v, A.dom_lo), A.dom_hi));
             } else {
-                if (b.deg == 3) decode_f32<3>(b, descs + cur_slot, cur_slot, G, pos, v, g);
-                else if (b.deg == 2) decode_f32<2>(b, descs + cur_slot, cur_slot, G, pos, v, g);
-                else decode_f32<1>(b, descs + cur_slot, cur_slot, G, pos, v, g);
+                if (b.deg == 3) decode_f32<3>(b, descs + cur_slot, cur_slot, G, pos, tf, A.dom_lo, A.dom_hi, v, tfv, g);
+                else if (b.deg == 2)
+                    decode_f32<2>(b, descs + cur_slot, cur_slot, G, pos, tf, A.dom_lo, A.dom_hi, v, tfv, g);
+                else decode_f32<1>(b, descs + cur_slot, cur_slot, G, pos, tf, A.dom_lo, A.dom_hi, v, tfv, g);
             }
             ++ns;
             if (DEBUG) h = (h ^ (uint64_t)(uint32_t)own) * 1099511628211ULL;
-
-            // TransferFunction (render.py:117-124)
-            const float4 tfv = tf_eval(tf, fminf(fmaxf(v, A.dom_lo), A.dom_hi));
-            const float col[3] = {tfv.x, tfv.y, tfv.z};
             const float atf = tfv.w;
+            if (!(atf > 0.f)) continue;  // a_s = 0: the sample changes neither C nor A
+            ++nshade;
+            const float col[3] = {tfv.x, tfv.y, tfv.z};
             // render.py:451 opacity correction
             const float as = A.power_one ? 1.f - (1.f - atf) : 1.f - __powf(1.f - atf, A.power);
             // _shade (render.py:383-395)
@@ -469,6 +528,7 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
     // per-warp reductions of the counters
     const uint32_t wsum = __reduce_add_sync(0xffffffffu, ns);
     const uint32_t wsum64 = __reduce_add_sync(0xffffffffu, ns64);
+    const uint32_t wshade = __reduce_add_sync(0xffffffffu, nshade);
     int64_t wmiss = miss;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -478,6 +538,7 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
     if (lane == 0) {
         if (wsum) atomicAdd((unsigned long long *)&stats->samples, (unsigned long long)wsum);
         if (wsum64) atomicAdd((unsigned long long *)&stats->fp64_samples, (unsigned long long)wsum64);
+        if (wshade) atomicAdd((unsigned long long *)&stats->shaded_samples, (unsigned long long)wshade);
         if (wmiss != INT64_MAX) atomicMin((long long *)&stats->missing_key, (long long)wmiss);
     }
 }
@@ -486,7 +547,7 @@ __global__ void init_stats_kernel(afam_render_stats *s) {
     s->samples = 0;
     s->fp64_samples = 0;
     s->missing_key = INT64_MAX;
-    s->pad = 0;
+    s->shaded_samples = 0;
 }
 
 __global__ void finish_stats_kernel(afam_render_stats *s) {
@@ -701,6 +762,7 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
     AFAM_CUDA(cudaMallocAsync(&d_idx, ibytes, st));
     AFAM_CUDA(cudaMemcpyAsync(d_grid, grid.data(), gbytes, cudaMemcpyHostToDevice, st));
     if (nblocks) AFAM_CUDA(cudaMemcpyAsync(d_idx, slots, (size_t)nblocks * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    AFAM_CUDA(cudaEventRecord(s->ev_k0, st));
     init_stats_kernel<<<1, 1, 0, st>>>(stats);
     if (A.rows > 0) {
         dim3 g((A.width + 15) / 16, (A.rows + 7) / 8);
@@ -715,8 +777,17 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
         }
     }
     finish_stats_kernel<<<1, 1, 0, st>>>(stats);
+    AFAM_CUDA(cudaEventRecord(s->ev_k1, st));
     AFAM_CUDA(cudaGetLastError());
     AFAM_CUDA(cudaFreeAsync(d_grid, st));
     AFAM_CUDA(cudaFreeAsync(d_idx, st));
+    return AFAM_OK;
+}
+
+extern "C" int afam_render_elapsed(afam_store *s, float *ms) {
+    AFAM_CHECK(s && ms, AFAM_E_VALUE, "NULL argument to afam_render_elapsed");
+    AFAM_CUDA(cudaSetDevice(s->device));
+    AFAM_CUDA(cudaEventSynchronize(s->ev_k1));
+    AFAM_CUDA(cudaEventElapsedTime(ms, s->ev_k0, s->ev_k1));
     return AFAM_OK;
 }

@@ -185,6 +185,8 @@ int afam_store_create(afam_store **out, int device, int32_t slots, int32_t max_n
     AFAM_CUDA(cudaMalloc(&s->d_maxabs, sizeof(float) * slots));
     s->host.resize(slots);
     for (auto &h : s->host) AFAM_CUDA(cudaEventCreateWithFlags(&h.ready, cudaEventDisableTiming));
+    AFAM_CUDA(cudaEventCreate(&s->ev_k0));
+    AFAM_CUDA(cudaEventCreate(&s->ev_k1));
     *out = s;
     return AFAM_OK;
 }
@@ -195,6 +197,8 @@ int afam_store_destroy(afam_store *s) {
     cudaDeviceSynchronize();
     for (auto &h : s->host)
         if (h.ready) cudaEventDestroy(h.ready);
+    if (s->ev_k0) cudaEventDestroy(s->ev_k0);
+    if (s->ev_k1) cudaEventDestroy(s->ev_k1);
     for (auto &kv : s->ops) {
         cudaFree(kv.second.b32);
         cudaFree(kv.second.b64);

@@ -322,10 +322,12 @@ def _missing_message(pov, params, cells, key) -> str:
 
 
 def render_part(pov, blocks: dict, tf, params, *, band_rows: int | None = None, nparts: int = 1, part: int = 0,
-                device: int | None = None, debug: bool = False, stream=None, out=None, raise_missing=True):
-    """Render this part's row bands on the GPU.  Returns (rgba device tensor
-    (rows, W, 4) uint8, stats host dict, debug tensors or None).  Rows are
-    the bands b with b % nparts == part, packed in band order."""
+                device: int | None = None, debug: bool = False, stream=None, out=None, raise_missing=True,
+                host_out: bool = False):
+    """Render this part's row bands on the GPU.  Returns (rgba tensor (rows,
+    W, 4) uint8 -- on the device, or in pinned host memory with host_out --,
+    stats host dict, debug tensors or None).  Rows are the bands b with
+    b % nparts == part, packed in band order."""
     import torch
 
     from .device import as_device_blocks, stream_handle
@@ -347,12 +349,25 @@ def render_part(pov, blocks: dict, tf, params, *, band_rows: int | None = None, 
         ohash = torch.empty((rows, W), dtype=torch.int64, device=dev)
     sl = np.ascontiguousarray(slots, dtype=np.int32)
     with torch.cuda.device(dev):
+        s_obj = stream if stream is not None else torch.cuda.current_stream(dev)
         _lib.check(_lib.lib().afam_render(
             store.handle, C.byref(fr), sl.ctypes.data_as(C.c_void_p), len(sl), C.c_void_p(out.data_ptr()),
             C.c_void_p(stats.data_ptr()), None if nsamp is None else C.c_void_p(nsamp.data_ptr()),
-            None if ohash is None else C.c_void_p(ohash.data_ptr()), C.c_void_p(stream_handle(stream, dev))))
-        st = stats.cpu().numpy()
-    info = {"samples": int(st[0]), "missing_key": int(st[1]), "fp64_samples": int(st[2])}
+            None if ohash is None else C.c_void_p(ohash.data_ptr()), C.c_void_p(int(s_obj.cuda_stream))))
+        # one synchronization: stats (and the frame, for host_out) into pinned host memory
+        with torch.cuda.stream(s_obj):
+            st_h = torch.empty(4, dtype=torch.int64, pin_memory=True)
+            st_h.copy_(stats, non_blocking=True)
+            if host_out:
+                h = torch.empty((rows, W, 4), dtype=torch.uint8, pin_memory=True)
+                h.copy_(out, non_blocking=True)
+                out = h
+        s_obj.synchronize()
+        st = st_h.numpy()
+    kms = C.c_float()
+    _lib.check(_lib.lib().afam_render_elapsed(store.handle, C.byref(kms)))
+    info = {"samples": int(st[0]), "missing_key": int(st[1]), "fp64_samples": int(st[2]),
+            "shaded_samples": int(st[3]), "kernel_ms": float(kms.value)}
     if raise_missing and info["missing_key"] >= 0:
         cells = C.c_int32()
         _lib.check(_lib.lib().afam_owner_grid(store.handle, sl.ctypes.data_as(C.c_void_p), len(sl), C.byref(cells),
@@ -364,8 +379,8 @@ def render_part(pov, blocks: dict, tf, params, *, band_rows: int | None = None, 
 
 def render(pov, blocks: dict, tf, params) -> Frame:
     """Front-to-back composite of the resident blocks (render.py:398-466) on the GPU."""
-    out, info, _ = render_part(pov, blocks, tf, params)
-    frame = Frame(width=int(params.width), height=int(params.height), rgba=out.cpu().numpy())
+    out, info, _ = render_part(pov, blocks, tf, params, host_out=True)
+    frame = Frame(width=int(params.width), height=int(params.height), rgba=out.numpy())
     render.last_stats = info
     return frame
 
