@@ -1,0 +1,192 @@
+"""Host-side semantics of the out-of-core runtime (reference runtime.py:57-225),
+checked on CPU with stand-in loaders: LRU order and counters against a
+textbook LRU, pinning, the load hook, capacity errors, prefetch preemption
+and fault tolerance, and the camera predictors."""
+
+import json
+import threading
+from collections import OrderedDict
+
+import numpy as np
+import pytest
+
+from helpers import npz
+
+
+class Blob:
+    def __init__(self, key, nbytes=100):
+        self.key, self.nbytes = key, nbytes
+
+
+def load_blob(key):
+    return Blob(key)
+
+
+class TextbookLRU:
+    def __init__(self, cap):
+        self.cap, self.d, self.hits, self.misses, self.evictions = cap, OrderedDict(), 0, 0, 0
+
+    def touch(self, k):
+        if k in self.d:
+            self.d.move_to_end(k)
+            self.hits += 1
+            return
+        self.misses += 1
+        if len(self.d) >= self.cap:
+            self.d.popitem(last=False)
+            self.evictions += 1
+        self.d[k] = 1
+
+
+@pytest.fixture(scope="module")
+def manifest():
+    from paper_2409_00184_b200 import partition
+
+    z = npz("store_smooth33.npz")
+    return partition.LODManifest.from_json(json.loads(bytes(z["manifest"]).decode()))
+
+
+def test_lru_matches_textbook_over_random_stream():
+    from paper_2409_00184_b200.runtime import ModelCache
+
+    rng = np.random.default_rng(3)
+    cache, ref = ModelCache(12, load_blob), TextbookLRU(12)
+    for _ in range(20000):
+        k = int(rng.integers(0, 40))
+        cache.fetch(k)
+        ref.touch(k)
+    assert cache.resident_addresses() == list(ref.d)
+    assert (cache.hits, cache.misses, cache.evictions) == (ref.hits, ref.misses, ref.evictions)
+
+
+def test_capacity_and_pinning():
+    from paper_2409_00184_b200.errors import CapacityError
+    from paper_2409_00184_b200.runtime import ModelCache
+
+    with pytest.raises(ValueError):
+        ModelCache(0, load_blob)
+    c = ModelCache(2, load_blob)
+    c.fetch("a"), c.fetch("b")
+    c.begin_frame({"a"})
+    c.fetch("c")  # the pinned "a" survives although it is the LRU entry
+    assert "a" in c and "b" not in c and "c" in c
+    c.begin_frame({"a", "c"})
+    with pytest.raises(CapacityError):
+        c.fetch("d")
+
+
+def test_evictions_release_device_slots():
+    from paper_2409_00184_b200.runtime import ModelCache
+
+    released = []
+    c = ModelCache(2, load_blob, on_evict=lambda b: released.append(b.key))
+    for k in "abcd":
+        c.fetch(k)
+    assert released == ["a", "b"]
+
+
+def test_counters_and_hook():
+    from paper_2409_00184_b200.runtime import ModelCache
+
+    ev = []
+    c = ModelCache(4, lambda k: Blob(k, 7), on_load=lambda a, s: ev.append((a, s)))
+    c.fetch("a"), c.fetch("b"), c.fetch("a"), c.fetch("x", record=False)
+    assert c.bytes_loaded == 21
+    assert (c.hits, c.misses) == (1, 2)  # the unrecorded prefetch fetch is not counted
+    assert ev == [("a", "frame"), ("b", "frame"), ("x", "prefetch")]
+
+
+def test_failed_load_leaves_cache_untouched():
+    from paper_2409_00184_b200.runtime import ModelCache
+
+    def bad(k):
+        raise OSError("io")
+
+    c = ModelCache(1, load_blob)
+    c.fetch("a")
+    c._loader = bad
+    with pytest.raises(OSError):
+        c.fetch("b")
+    assert c.resident_addresses() == ["a"] and c.evictions == 0
+
+
+def test_cache_frame_and_capacity_error(manifest):
+    from paper_2409_00184_b200.errors import CapacityError
+    from paper_2409_00184_b200.render import PointOfView, select_visible
+    from paper_2409_00184_b200.runtime import ModelCache, cache_frame
+
+    pov = PointOfView([0, 0, 5.0], [0, 0, -1], [0, 1, 0])
+    vis = select_visible(pov, manifest)
+    c = ModelCache(100, load_blob)
+    res = cache_frame(pov, manifest, c)
+    assert list(res) == vis and c.misses == len(vis) and c.hits == 0
+    cache_frame(pov, manifest, c)
+    assert c.hits == len(vis)
+    with pytest.raises(CapacityError, match="exceeds cache capacity"):
+        cache_frame(pov, manifest, ModelCache(len(vis) - 1, load_blob))
+
+
+def test_prefetch_preemption_and_faults(manifest):
+    from paper_2409_00184_b200.render import PointOfView, select_visible
+    from paper_2409_00184_b200.runtime import ModelCache, predict_static, prefetch_loop
+
+    pov = PointOfView([0, 0, 5.0], [0, 0, -1], [0, 1, 0])
+    vis = select_visible(pov, manifest)
+    done = threading.Event()
+    done.set()
+    assert prefetch_loop([pov], manifest, ModelCache(100, load_blob), done, predict_static) == 0
+    done = threading.Event()
+    c = ModelCache(100, load_blob, on_load=lambda a, s: done.set())  # render finishes mid-prefetch
+    assert prefetch_loop([pov], manifest, c, done, predict_static) == 1
+    calls = []
+
+    def flaky(k):
+        calls.append(k)
+        if len(calls) == 1:
+            raise OSError("transient")
+        return Blob(k)
+
+    c = ModelCache(100, flaky)
+    assert prefetch_loop([pov], manifest, c, threading.Event(), predict_static) == len(vis) - 1
+
+
+def test_prefetch_keeps_pinned_set(manifest):
+    from paper_2409_00184_b200.render import PointOfView, select_visible
+    from paper_2409_00184_b200.runtime import ModelCache, cache_frame, predict_static, prefetch_loop
+
+    pov = PointOfView([0, 0, 5.0], [0, 0, -1], [0, 1, 0])
+    c = ModelCache(len(select_visible(pov, manifest)), load_blob)
+    res = cache_frame(pov, manifest, c)
+    other = PointOfView([0.2, 0.2, 1.2], [0, 0, -1], [0, 1, 0], fov_y=70)
+    prefetch_loop([other], manifest, c, threading.Event(), predict_static)
+    assert set(res) <= set(c.resident_addresses())
+
+
+def test_predictors():
+    from paper_2409_00184_b200.render import PointOfView
+    from paper_2409_00184_b200.runtime import predict_next_linear, predict_static
+
+    a = PointOfView([0, 0, 3.0], [0, 0, -1], [0, 1, 0])
+    b = PointOfView([0, 0.1, 2.8], [0, 0, -1], [0, 1, 0])
+    assert predict_static([a, b]) is b and predict_static([]) is None
+    assert predict_next_linear([a]) is a
+    p = predict_next_linear([a, b])
+    np.testing.assert_allclose(p.position, [0, 0.2, 2.6], atol=1e-12)
+    c = PointOfView([0, 0, 3.0], [0, 0.8, 0.6], [0, 1, 0])
+    d = PointOfView([0, 0, 2.9], [0, np.sqrt(0.91), 0.3], [0, 1, 0])
+    np.testing.assert_allclose(predict_next_linear([c, d]).direction, d.direction, atol=1e-12)
+
+
+def test_trajectory_io(tmp_path):
+    from paper_2409_00184_b200.errors import FormatError
+    from paper_2409_00184_b200.runtime import load_trajectory, orbit_trajectory, save_trajectory
+
+    povs = orbit_trajectory(7, radius=2.0)
+    save_trajectory(tmp_path / "t.jsonl", povs)
+    back = load_trajectory(tmp_path / "t.jsonl")
+    for p, q in zip(povs, back):
+        np.testing.assert_allclose(p.position, q.position)
+        np.testing.assert_allclose(p.direction, q.direction)
+    (tmp_path / "bad.jsonl").write_text('{"pos": [0, 0, 1]}\n')
+    with pytest.raises(FormatError):
+        load_trajectory(tmp_path / "bad.jsonl")
