@@ -14,6 +14,7 @@ from __future__ import annotations
 import ctypes as C
 import json
 import math
+import threading
 from dataclasses import dataclass
 from pathlib import Path
 
@@ -321,6 +322,21 @@ def _missing_message(pov, params, cells, key) -> str:
             "the resident set does not cover the visible region")
 
 
+_tls = threading.local()
+
+
+def _pinned_stage(nbytes: int):
+    """This thread's pinned host staging buffer of >= 32 + nbytes bytes (grown on demand)."""
+    import torch
+
+    need = 32 + nbytes
+    buf = getattr(_tls, "stage", None)
+    if buf is None or buf.numel() < need:
+        buf = torch.empty(max(need, 1 << 16), dtype=torch.uint8, pin_memory=True)
+        _tls.stage = buf
+    return buf
+
+
 def render_part(pov, blocks: dict, tf, params, *, band_rows: int | None = None, nparts: int = 1, part: int = 0,
                 device: int | None = None, debug: bool = False, stream=None, out=None, raise_missing=True,
                 host_out: bool = False):
@@ -354,16 +370,17 @@ def render_part(pov, blocks: dict, tf, params, *, band_rows: int | None = None, 
             store.handle, C.byref(fr), sl.ctypes.data_as(C.c_void_p), len(sl), C.c_void_p(out.data_ptr()),
             C.c_void_p(stats.data_ptr()), None if nsamp is None else C.c_void_p(nsamp.data_ptr()),
             None if ohash is None else C.c_void_p(ohash.data_ptr()), C.c_void_p(int(s_obj.cuda_stream))))
-        # one synchronization: stats (and the frame, for host_out) into pinned host memory
+        # one synchronization: stats (and the frame, for host_out) through a
+        # persistent pinned staging buffer of this thread
+        stage = _pinned_stage(rows * W * 4 if host_out else 0)
         with torch.cuda.stream(s_obj):
-            st_h = torch.empty(4, dtype=torch.int64, pin_memory=True)
-            st_h.copy_(stats, non_blocking=True)
+            stage[:32].view(torch.int64).copy_(stats, non_blocking=True)
             if host_out:
-                h = torch.empty((rows, W, 4), dtype=torch.uint8, pin_memory=True)
-                h.copy_(out, non_blocking=True)
-                out = h
+                stage[32:32 + rows * W * 4].view(rows, W, 4).copy_(out, non_blocking=True)
         s_obj.synchronize()
-        st = st_h.numpy()
+        st = stage[:32].view(torch.int64).numpy().copy()
+        if host_out:
+            out = stage[32:32 + rows * W * 4].view(rows, W, 4).clone()
     kms = C.c_float()
     _lib.check(_lib.lib().afam_render_elapsed(store.handle, C.byref(kms)))
     info = {"samples": int(st[0]), "missing_key": int(st[1]), "fp64_samples": int(st[2]),
