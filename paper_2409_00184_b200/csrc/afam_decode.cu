@@ -12,6 +12,8 @@
 // same schedule in float64.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 
 #include "afam_internal.h"
 
@@ -25,9 +27,51 @@ struct DecodeJob {
     const double *b64;
 };
 
-constexpr int kDecodeChunk = 8;
-constexpr int kDecodeThreads = 256;
+constexpr int kDecodeChunk = 65;     // output planes per CTA (a whole 65^3 block)
+constexpr int kDecodeThreads = 416;  // 13 warps: 65 rows = 5 per warp
+constexpr int kAhead = 2;            // planes prefetched beyond the current window
+constexpr int kRing = AFAM_MAX_DEGREE + 1 + kAhead + 1;  // > P + kAhead
 
+// ---- TMA bulk copy + mbarrier (PTX; SASS UBLKCP / SYNCS) ----
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+// 1-D bulk global -> shared copy completing on `bar` (16-byte aligned, size % 16 == 0)
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// Pairs of consecutive elements per lane: a warp covers one row of up to 64
+// elements with two per lane (lane l: 2l, 2l+1) plus lane 0 picking up the
+// 65th (ncp and m are <= 65 for the store's blocks; longer rows loop).
 template <int P, typename T>
 __device__ __forceinline__ void decode_planes(const BlockDesc &d, const int32_t *__restrict__ col0g,
                                               const T *__restrict__ Bg, int m, int k0, int k1,
@@ -41,43 +85,114 @@ __device__ __forceinline__ void decode_planes(const BlockDesc &d, const int32_t 
     for (int i = threadIdx.x; i < m; i += blockDim.x) c0[i] = col0g[i];
     __syncthreads();
     const float *__restrict__ C = d.ctrl;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    const size_t zstride = (size_t)n * pitch;
+    // z-planes of control points stream through a ring of kRing smem slots by
+    // TMA bulk copies (cp.async.bulk, one mbarrier per slot), issued up to
+    // kAhead planes ahead of use so the HBM latency hides behind the previous
+    // output planes' contractions.
+    float *ring = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(c0 + m) + 15) & ~(uintptr_t)15);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(ring + (size_t)kRing * zstride);
+    const uint32_t plane_bytes = (uint32_t)(zstride * sizeof(float));
+    if (threadIdx.x == 0) {
+        for (int r = 0; r < kRing; r++) mbar_init(bar + r, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    // planes are loaded in order from zbase, each exactly once: plane z is the
+    // ((z - zbase) / kRing)-th load into slot (z - zbase) % kRing (its mbarrier phase)
+    const int zbase = c0[k0];
+    const int zlast = min(n - 1, c0[k1 - 1] + P);
+    int issued = zbase - 1;  // highest plane whose load was issued (thread 0)
     for (int k = k0; k < k1; k++) {
         const int z0 = c0[k];
+        if (threadIdx.x == 0) {
+            const int zmax = min(zlast, z0 + P + kAhead);
+            fence_proxy_async();  // earlier generic reads of recycled slots before the async writes
+            for (int z = issued + 1; z <= zmax; z++) {
+                // the slot's previous plane z - kRing < z0 (kRing > P + kAhead) is no longer read
+                uint64_t *bz_ = bar + ((z - zbase) % kRing);
+                mbar_arrive_expect_tx(bz_, plane_bytes);
+                tma_load_1d(ring + (size_t)((z - zbase) % kRing) * zstride, C + (size_t)z * zstride, plane_bytes,
+                            bz_);
+            }
+            issued = max(issued, zmax);
+        }
         T bz[P + 1];
 #pragma unroll
         for (int c = 0; c < P + 1; c++) bz[c] = B[k * 4 + c];
-        // z contraction: S1[a + n*b] = sum_c Bz[k,c] C[a, b, z0+c]
-        for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
-            const int a = idx % n, b = idx / n;
-            const float *p = C + ((size_t)z0 * n + b) * pitch + a;
-            T acc = T(0);
+        const float *planes[P + 1];
 #pragma unroll
-            for (int c = 0; c < P + 1; c++) acc = fma(bz[c], (T)__ldg(p + (size_t)c * n * pitch), acc);
-            S1[idx] = acc;
+        for (int c = 0; c < P + 1; c++) {
+            const int zr = z0 + c - zbase;
+            mbar_wait(bar + (zr % kRing), (uint32_t)((zr / kRing) & 1));
+            planes[c] = ring + (size_t)(zr % kRing) * zstride;
+        }
+        // z contraction: S1[a + n*b] = sum_c Bz[k,c] C[a, b, z0+c] (8-byte smem reads of pitched rows)
+        for (int b = warp; b < n; b += nwarp) {
+            for (int a = 2 * lane; a < n; a += 64) {
+                T s0 = T(0), s1 = T(0);
+#pragma unroll
+                for (int c = 0; c < P + 1; c++) {
+                    const float2 v = *reinterpret_cast<const float2 *>(planes[c] + (size_t)b * pitch + a);
+                    s0 = fma(bz[c], (T)v.x, s0);
+                    s1 = fma(bz[c], (T)v.y, s1);
+                }
+                S1[a + n * b] = s0;
+                if (a + 1 < n) S1[a + 1 + n * b] = s1;
+            }
         }
         __syncthreads();
         // y contraction: S2[a + n*j] = sum_b By[j,b] S1[a + n*(y0_j+b)]
-        for (int idx = threadIdx.x; idx < n * m; idx += blockDim.x) {
-            const int a = idx % n, j = idx / n;
-            const int y0 = c0[j];
-            T acc = T(0);
+        for (int j = warp; j < m; j += nwarp) {
+            const T *s1 = S1 + (size_t)n * c0[j];
+            T by[P + 1];
 #pragma unroll
-            for (int b = 0; b < P + 1; b++) acc = fma(B[j * 4 + b], S1[a + n * (y0 + b)], acc);
-            S2[idx] = acc;
+            for (int b = 0; b < P + 1; b++) by[b] = B[j * 4 + b];
+            for (int a = 2 * lane; a < n; a += 64) {
+                T s0 = T(0), t1 = T(0);
+                const bool two = a + 1 < n;
+#pragma unroll
+                for (int b = 0; b < P + 1; b++) {
+                    s0 = fma(by[b], s1[a + n * b], s0);
+                    if (two) t1 = fma(by[b], s1[a + 1 + n * b], t1);
+                }
+                S2[a + n * j] = s0;
+                if (two) S2[a + 1 + n * j] = t1;
+            }
         }
         __syncthreads();
-        // x contraction + coalesced store: out[i + m*j + m*m*k]
+        // x contraction + coalesced store: out[i + m*j + m*m*k]; the Bx rows of
+        // this lane's outputs stay in registers for all rows j
         float *outk = out + (size_t)k * m * m;
-        for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
-            const int i = idx % m, j = idx / m;
-            const int x0 = c0[i];
-            T acc = T(0);
+        for (int i0 = 2 * lane; i0 < m; i0 += 64) {
+            const bool two = i0 + 1 < m;
+            const int xa = c0[i0], xb = two ? c0[i0 + 1] : xa;
+            T ba[P + 1], bb[P + 1];
 #pragma unroll
-            for (int a = 0; a < P + 1; a++) acc = fma(B[i * 4 + a], S2[x0 + a + n * j], acc);
-            outk[idx] = (float)acc;
+            for (int a = 0; a < P + 1; a++) {
+                ba[a] = B[i0 * 4 + a];
+                bb[a] = two ? B[(i0 + 1) * 4 + a] : T(0);
+            }
+            for (int j = warp; j < m; j += nwarp) {
+                const T *s2 = S2 + (size_t)n * j;
+                T acc0 = T(0), acc1 = T(0);
+#pragma unroll
+                for (int a = 0; a < P + 1; a++) {
+                    acc0 = fma(ba[a], s2[xa + a], acc0);
+                    acc1 = fma(bb[a], s2[xb + a], acc1);
+                }
+                outk[i0 + m * j] = (float)acc0;
+                if (two) outk[i0 + 1 + m * j] = (float)acc1;
+            }
         }
         __syncthreads();
     }
+    // drain: planes loaded but never read (z0 jumping by more than one when m < nspan)
+    // must land before the CTA's shared memory is released
+    if (threadIdx.x == 0)
+        for (int z = max(zbase, issued - kRing + 1); z <= issued; z++)
+            mbar_wait(bar + ((z - zbase) % kRing), (uint32_t)(((z - zbase) / kRing) & 1));
 }
 
 __global__ void __launch_bounds__(kDecodeThreads) decode_grid_kernel(const BlockDesc *__restrict__ descs,
@@ -195,15 +310,21 @@ extern "C" int afam_decode_grid(afam_store *s, const int32_t *slots, int32_t nbl
             AFAM_CUDA(cudaStreamWaitEvent(st, h.ready, 0));
         }
     }
-    const size_t smem = ((size_t)maxn * maxn + (size_t)maxn * m + (size_t)m * 4) * sizeof(double) + (size_t)m * 4 + 16;
-    AFAM_CHECK(smem <= 227 * 1024, AFAM_E_VALUE, "decode of ncp=%d onto m=%d needs %zu B of shared memory", maxn, m,
-               smem);
-    AFAM_CUDA(cudaFuncSetAttribute(decode_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // S1 + S2 + B (float64 worst case) + col0 (padded to 4) + plane ring + mbarriers
+    const size_t maxpitch = (size_t)((maxn + 3) & ~3);
+    const size_t smem = ((size_t)maxn * maxn + (size_t)maxn * m + (size_t)m * 4) * sizeof(double) +
+                        (size_t)((m + 3) & ~3) * 4 + (size_t)kRing * maxn * maxpitch * sizeof(float) +
+                        kRing * sizeof(uint64_t) + 16;
     DecodeJob *d_jobs = nullptr;
     AFAM_CUDA(cudaMallocAsync(&d_jobs, sizeof(DecodeJob) * nblk, st));
     AFAM_CUDA(cudaMemcpyAsync(d_jobs, jobs.data(), sizeof(DecodeJob) * nblk, cudaMemcpyHostToDevice, st));
-    dim3 grid((m + kDecodeChunk - 1) / kDecodeChunk, nblk);
-    decode_grid_kernel<<<grid, kDecodeThreads, smem, st>>>(s->d_desc, d_jobs, m, out);
+    {
+        AFAM_CHECK(smem <= 227 * 1024, AFAM_E_VALUE, "decode of ncp=%d onto m=%d needs %zu B of shared memory", maxn,
+                   m, smem);
+        AFAM_CUDA(cudaFuncSetAttribute(decode_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        dim3 grid((m + kDecodeChunk - 1) / kDecodeChunk, nblk);
+        decode_grid_kernel<<<grid, kDecodeThreads, smem, st>>>(s->d_desc, d_jobs, m, out);
+    }
     AFAM_CUDA(cudaGetLastError());
     AFAM_CUDA(cudaFreeAsync(d_jobs, st));
     return AFAM_OK;
