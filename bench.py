@@ -136,6 +136,42 @@ def build_model(pinned: bool):
     return man, blobs, time.time() - t0
 
 
+def build_model_distributed(rank, dev):
+    """N > 1: rank 0 synthesises the store once; the packed .mfa images are
+    broadcast over NVLink (NCCL) and land in every rank's pinned host buffer
+    (the e2e path streams blocks from there), so host cores are not shared by
+    N copies of the synthesis."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2409_00184_b200 import model, synth
+    from paper_2409_00184_b200.partition import skeleton
+
+    t0 = time.time()
+    man = skeleton(4, 2, 65)
+    man.degree = 3
+    addrs = sorted(man.entries)
+    sizes = [model.serialized_size(synth.ncp_for(a), 3) for a in addrs]
+    total = int(sum(sizes))
+    host = torch.empty(total, dtype=torch.uint8, pin_memory=True)
+    if rank == 0:
+        man0, _ = synth.turbulence_store(alloc=lambda n: host.numpy())
+    dbuf = host.to(dev, non_blocking=False) if rank == 0 else torch.empty(total, dtype=torch.uint8, device=dev)
+    dist.broadcast(dbuf, src=0)
+    if rank != 0:
+        host.copy_(dbuf)
+    del dbuf
+    arr = host.numpy()
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    blobs = {}
+    for i, a in enumerate(addrs):
+        e = man.entries[a]
+        e.ncp, e.nbytes, e.path, e.is_complex = synth.ncp_for(a), sizes[i], a.file_name, True
+        blobs[a] = arr[offs[i]:offs[i + 1]]
+    build_model_distributed.keep = host
+    return man, blobs, time.time() - t0
+
+
 def measure_fma_peak(dev):
     """FP32 FMA peak of this GPU: a dependent-chain-free FFMA kernel in libafam."""
     import ctypes as C
@@ -167,7 +203,10 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    man, blobs, gen_s = build_model(pinned=not args.no_e2e)
+    if world == 1:
+        man, blobs, gen_s = build_model(pinned=not args.no_e2e)
+    else:
+        man, blobs, gen_s = build_model_distributed(rank, dev)
     povs = runtime.orbit_trajectory(100, radius=2.0)
     S = args.size
     params = render.RenderParams(width=S, height=S, sample_distance=1e-3)
@@ -356,7 +395,7 @@ def cpu_sample(man, blobs, povs, tf, params, rows, frame_index):
     host = {a: model.deserialize(bytes(blobs[a]), man.entries[a].ncp, man.entries[a].extent, a.lod) for a in vis}
     H = params.height
     r0 = (H - rows) // 2
-    threads = oracle.max_threads()
+    threads = len(os.sched_getaffinity(0))  # every host core (torchrun sets OMP_NUM_THREADS=1)
     t0 = time.perf_counter()
     _, info = oracle.render(pov, host, tf, params, rows=(r0, r0 + rows), nthreads=threads)
     el = time.perf_counter() - t0
@@ -404,10 +443,18 @@ def main():
             return
         print(json.dumps(run_reference(args)), flush=True)
         return
+    import torch
     import torch.distributed as dist
 
+    if os.environ.get("AFAM_BENCH_SAME_GPU"):  # functional N>1 check on a 1-GPU box (gloo)
+        local_rank = 0
     if world > 1:
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(local_rank)
+        backend = os.environ.get("AFAM_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     res, man, blobs = run_ours(args, rank, world, local_rank)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from paper_2409_00184_b200 import render, runtime

@@ -52,13 +52,16 @@ def gather_bands(local, height: int, band_rows: int, group=None, dst: int = 0):
     if local.shape[0] < rmax:
         send = torch.zeros((rmax,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
         send[: local.shape[0]] = local
+    dev = send.device
+    if send.is_cuda and dist.get_backend(group) == "gloo":  # gloo gathers host tensors
+        send = send.cpu()
     bufs = None
     if rank == dst:
         bufs = [torch.empty_like(send) for _ in range(world)]
     dist.gather(send.contiguous(), bufs, dst=dst, group=group)
     if rank != dst:
         return None
-    return assemble([b[:c] for b, c in zip(bufs, counts)], height, band_rows)
+    return assemble([b[:c].to(dev) for b, c in zip(bufs, counts)], height, band_rows)
 
 
 def render_tiles(pov, blocks: dict, tf, params, *, group=None, band_rows: int = 8, dst: int = 0):
