@@ -41,6 +41,7 @@ struct TfTable {
     int32_t nbp;
     float lut_lo, lut_scale; // bucket = (v - lut_lo) * lut_scale over the TF domain
     int8_t lut[kTfLut];      // last breakpoint <= bucket start (-1: none)
+    uint8_t clean[kTfLut];   // 1: no breakpoint within (a margin of) the bucket, lut is the segment
 };
 
 struct RenderArgs {
@@ -66,8 +67,10 @@ __device__ __forceinline__ float4 tf_eval(const TfTable &T, float v) {
     int bi = (int)((v - T.lut_lo) * T.lut_scale);
     bi = min(max(bi, 0), kTfLut - 1);
     int j = T.lut[bi];
-    while (j + 1 < T.nbp && v >= T.bp[j + 1]) ++j;
-    while (j >= 0 && v < T.bp[j]) --j;
+    if (!T.clean[bi]) {
+        while (j + 1 < T.nbp && v >= T.bp[j + 1]) ++j;
+        while (j >= 0 && v < T.bp[j]) --j;
+    }
     if (j < 0) return T.val[0];
     const float4 a = T.val[j], s = T.slope[j];
     const float dx = v - T.bp[j];
@@ -149,14 +152,17 @@ __device__ __forceinline__ int axis_basis(const BlockLite &b, const BlockDesc *_
     // fast path: interior span of a uniform model, not within 1e-4 spans of a knot
     // no clamp needed here: a sample a hair outside [0, nspan] (rounding at a
     // block face) lands within 1e-4 of an end knot and takes the exact path
+    // (span coordinate in float32 once the float64 offset is formed: for
+    // nspan <= 128 its rounding, < 4e-6 of a span, is far inside the 1e-4
+    // exactness margin and ~1e-7 in value)
     const double dpos = p - b.lo[a];
-    const double tq = dpos * b.scale[a];
-    const int k = min((int)tq, b.nspan - 1);
-    const double fr = tq - (double)k;
+    const float tq = (float)(dpos * b.scale[a]);
+    const int k = min((int)floorf(tq), b.nspan - 1);
+    const float fr = tq - (float)k;
     int s = P + k;
-    const bool uni = b.flags & kFlagUniform;
-    if (uni && fr >= 1e-4 && fr <= 1.0 - 1e-4 && s >= 2 * P - 1 && s <= b.ncp - P) {
-        uniform_basis<P>((float)fr, b.nspan_f, N, E);
+    const bool uni = (b.flags & kFlagUniform) && b.nspan <= 128;
+    if (uni && fr >= 1e-4f && fr <= 1.f - 1e-4f && s >= 2 * P - 1 && s <= b.ncp - P) {
+        uniform_basis<P>(fr, b.nspan_f, N, E);
         return s;
     }
     // exact path: reference parameter (model.py:67) and span search against the stored knots
@@ -441,25 +447,31 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
     GatherCache G;
     G.slot = -1;
 
+    // sample k's position and finest-cell owner (render.py:422-428, :377-380):
+    // float64, reference op order, no contraction
+    auto geometry = [&](int64_t k, double &t, double (&pos)[3], int &own) {
+        t = __dadd_rn(te, __dmul_rn((double)k + 0.5, A.sd));
+        int cidx = 0;
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+            double p = __dadd_rn(A.origin[a], __dmul_rn(t, d[a]));
+            p = p < -1.0 ? -1.0 : (p > 1.0 ? 1.0 : p);  // np.clip (p is never NaN here)
+            pos[a] = p;
+            const double sc = __dmul_rn(__dmul_rn(__dadd_rn(p, 1.0), 0.5), cellsd);
+            int ci = __double2int_rz(sc);
+            ci = min(max(ci, 0), A.cells - 1);
+            cidx = cidx * A.cells + ci;
+        }
+        own = own_grid[cidx];
+    };
+
     if (active) {
         for (int64_t k = 0;; k++) {
-            // render.py:422-423
-            const double t = __dadd_rn(te, __dmul_rn((double)k + 0.5, A.sd));
+            double t, pos[3];
+            int own;
+            geometry(k, t, pos, own);
+            // render.py:423 alive test, before sample k
             if (!(t < tx && (o_max_exact ? Aacc <= o_max : (double)Aacc <= A.o_max))) break;
-            // render.py:427-428, :378-379
-            double pos[3];
-            int cidx = 0;
-#pragma unroll
-            for (int a = 0; a < 3; a++) {
-                double p = __dadd_rn(A.origin[a], __dmul_rn(t, d[a]));
-                p = p < -1.0 ? -1.0 : (p > 1.0 ? 1.0 : p);  // np.clip (p is never NaN here)
-                pos[a] = p;
-                const double sc = __dmul_rn(__dmul_rn(__dadd_rn(p, 1.0), 0.5), cellsd);
-                int ci = __double2int_rz(sc);
-                ci = min(max(ci, 0), A.cells - 1);
-                cidx = cidx * A.cells + ci;
-            }
-            const int own = own_grid[cidx];
             if (own < 0) {  // render.py:430-436
                 miss = ((int64_t)k << 32) | ray;
                 break;
@@ -591,11 +603,16 @@ static void build_tf_table(const afam_frame *F, TfTable &T) {
     const double lo = F->domain_lo, hi = F->domain_hi;
     T.lut_lo = (float)lo;
     T.lut_scale = (float)(kTfLut / (hi - lo));
+    const double w = (hi - lo) / kTfLut, margin = 0.01 * w;
     for (int i = 0; i < kTfLut; i++) {
         const double x = lo + (hi - lo) * i / kTfLut;
         int j = -1;
         while (j + 1 < T.nbp && xs[j + 1] <= x) ++j;
         T.lut[i] = (int8_t)j;
+        bool clean = true;  // no breakpoint near the bucket: the bucket index alone decides the segment
+        for (int q = 0; q < T.nbp; q++)
+            if (xs[q] > x - margin && xs[q] < x + w + margin) clean = false;
+        T.clean[i] = clean;
     }
 }
 
