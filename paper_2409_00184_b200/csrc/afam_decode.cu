@@ -307,7 +307,7 @@ extern "C" int afam_decode_grid(afam_store *s, const int32_t *slots, int32_t nbl
             jobs[b].b32 = op->b32;
             jobs[b].b64 = op->b64;
             maxn = std::max(maxn, (int)h.ncp);
-            AFAM_CUDA(cudaStreamWaitEvent(st, h.ready, 0));
+            AFAM_CUDA(wait_slot(s, sl, st));
         }
     }
     // S1 + S2 + B (float64 worst case) + col0 (padded to 4) + plane ring + mbarriers

@@ -201,36 +201,99 @@ __device__ __forceinline__ void gather(const float *__restrict__ ctrl, int ncp, 
         }
 }
 
+// Same gather from the x-quad layout (ctrl4[(iz*ncp+ix)*ncp+iy] =
+// c[ix..ix+3][iy][iz]): one 16-byte load per (iy, iz) row.
+template <int P>
+__device__ __forceinline__ void gather_quad_rows(const float4 *__restrict__ ctrl4, int ncp, int x0, int y0, int z0,
+                                                 float (&c)[64]) {
+    constexpr int Q = P + 1;
+    const float4 *base = ctrl4 + ((size_t)z0 * ncp + x0) * ncp + y0;
+    const size_t plane = (size_t)ncp * ncp;
+#pragma unroll
+    for (int cz = 0; cz < Q; cz++)
+#pragma unroll
+        for (int by = 0; by < Q; by++) {
+            const float4 r = __ldg(base + cz * plane + by);
+            const float rr[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+            for (int ax = 0; ax < Q; ax++) c[(cz * Q + by) * Q + ax] = rr[ax];
+        }
+}
+
 // One full evaluation (no caching): parameters u in [0,1]^3 -> value and
 // parameter-space gradient (bspline.py:217-229).
+// Uniform B-spline basis on an interior span, local coordinate x in [0,1):
+// the Cox-de Boor values for equally spaced knots, and the difference-form
+// derivative weights E[k] = nspan * L[k] (L: degree p-1 basis), cf. basis_eval.
+template <int P>
+__device__ __forceinline__ void uniform_basis(float x, float ns, float (&N)[P + 1], float (&E)[P]) {
+    const float m = 1.f - x;
+    if (P == 1) {
+        N[0] = m;
+        N[1] = x;
+        E[0] = ns;
+    } else if (P == 2) {
+        const float x2 = x * x;
+        N[0] = 0.5f * m * m;
+        N[1] = fmaf(-1.f, x2, x) + 0.5f;
+        N[2] = 0.5f * x2;
+        E[0] = ns * m;
+        E[1] = ns * x;
+    } else {
+        const float x2 = x * x, x3 = x2 * x, m2 = m * m;
+        const float s6 = 1.f / 6.f;
+        N[0] = s6 * m2 * m;
+        N[1] = fmaf(0.5f, x3, fmaf(-1.f, x2, 2.f / 3.f));
+        N[2] = fmaf(-0.5f, x3, fmaf(0.5f, x2, fmaf(0.5f, x, s6)));
+        N[3] = s6 * x3;
+        const float hn = 0.5f * ns;
+        E[0] = hn * m2;
+        E[1] = ns * (fmaf(-1.f, x2, x) + 0.5f);
+        E[2] = hn * x2;
+    }
+}
+
+// Span + basis (values and difference-form derivative weights) of one axis
+// at parameter u64 (float64, already clipped).  float32 evaluation of a
+// clamped-uniform model takes the closed form on interior spans away from
+// knots (no knot or table loads); everything else searches the stored knots
+// and uses the per-span table.
+template <int P, typename T>
+__device__ __forceinline__ int axis_eval(const BlockDesc &d, int a, double u64, T (&N)[P + 1], T (&E)[P]) {
+    if constexpr (sizeof(T) == 4) {
+        if ((d.flags & kFlagUniform) && d.nspan <= 128) {
+            const float tq = (float)(u64 * (double)d.nspan);
+            const int k = min((int)floorf(tq), d.nspan - 1);
+            const float fr = tq - (float)k;
+            const int s = P + k;
+            if (fr >= 1e-4f && fr <= 1.f - 1e-4f && s >= 2 * P - 1 && s <= d.ncp - P) {
+                uniform_basis<P>(fr, (float)d.nspan, N, E);
+                return s;
+            }
+        }
+    }
+    const int s = find_span(d.knots + a * d.nk, d.ncp, P, d.nspan, u64);
+    Tab<T> t;
+    const size_t off = ((size_t)a * d.nspan + (s - P)) * tab_stride(P);
+    if constexpr (sizeof(T) == 4) load_entry<P>(d.tab32 + off, t);
+    else load_entry<P>(d.tab64 + off, t);
+    basis_eval<P, T>(t, (T)u64, N, E);
+    return s;
+}
+
 template <int P, typename T, bool GRAD>
 __device__ __forceinline__ T eval_uncached(const BlockDesc &d, const double (&u64)[3], T g[3]) {
-    Tab<T> te[3];
-    int s[3];
-    T u[3];
-#pragma unroll
-    for (int a = 0; a < 3; a++) {
-        u[a] = (T)u64[a];
-        s[a] = find_span(d.knots + a * d.nk, d.ncp, P, d.nspan, u64[a]);
-        const size_t off = ((size_t)a * d.nspan + (s[a] - P)) * tab_stride(P);
-        if constexpr (sizeof(T) == 4) load_entry<P>(d.tab32 + off, te[a]);
-        else load_entry<P>(d.tab64 + off, te[a]);
-    }
+    T Nx[P + 1], Dx[P], Ny[P + 1], Dy[P], Nz[P + 1], Dz[P];
+    const int sx = axis_eval<P, T>(d, 0, u64[0], Nx, Dx);
+    const int sy = axis_eval<P, T>(d, 1, u64[1], Ny, Dy);
+    const int sz = axis_eval<P, T>(d, 2, u64[2], Nz, Dz);
     float c[64];
-    gather<P>(d.ctrl, d.ncp, d.pitch, s[0] - P, s[1] - P, s[2] - P, c);
+    gather_quad_rows<P>(d.ctrl4, d.ncp, sx - P, sy - P, sz - P, c);
     if constexpr (GRAD) {
-        T Nx[P + 1], Dx[P], Ny[P + 1], Dy[P], Nz[P + 1], Dz[P];
-        basis_eval<P, T>(te[0], u[0], Nx, Dx);
-        basis_eval<P, T>(te[1], u[1], Ny, Dy);
-        basis_eval<P, T>(te[2], u[2], Nz, Dz);
         T v;
         contract_grad<P, T, float>(c, Nx, Dx, Ny, Dy, Nz, Dz, v, g);
         return v;
     } else {
-        T Nx[P + 1], Ny[P + 1], Nz[P + 1];
-        basis_vals_only<P, T>(te[0], u[0], Nx);
-        basis_vals_only<P, T>(te[1], u[1], Ny);
-        basis_vals_only<P, T>(te[2], u[2], Nz);
         return contract_val<P, T, float>(c, Nx, Ny, Nz);
     }
 }

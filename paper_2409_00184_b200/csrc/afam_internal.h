@@ -104,6 +104,18 @@ struct afam_manifest {
 namespace afam {
 void set_error(const char *fmt, ...);
 int cuda_fail(cudaError_t e, const char *what);
+
+// Order `st` after the slot's upload; uploads already observed complete cost
+// one flag test (caller holds s->mu).
+inline cudaError_t wait_slot(afam_store *s, int32_t slot, cudaStream_t st) {
+    SlotHost &h = s->host[slot];
+    if (!h.pending) return cudaSuccess;
+    if (cudaEventQuery(h.ready) == cudaSuccess) {
+        h.pending = false;
+        return cudaSuccess;
+    }
+    return cudaStreamWaitEvent(st, h.ready, 0);
+}
 }  // namespace afam
 
 #define AFAM_CUDA(call)                                                         \

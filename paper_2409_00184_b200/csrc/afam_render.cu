@@ -83,37 +83,6 @@ __device__ __forceinline__ int frame_row(const RenderArgs &A, int lr) {
     return (b * A.nparts + A.part) * A.band_rows + lr % A.band_rows;
 }
 
-// Uniform B-spline basis on an interior span, local coordinate x in [0,1):
-// the Cox-de Boor values for equally spaced knots, and the difference-form
-// derivative weights E[k] = nspan * L[k] (L: degree p-1 basis), cf. basis_eval.
-template <int P>
-__device__ __forceinline__ void uniform_basis(float x, float ns, float (&N)[P + 1], float (&E)[P]) {
-    const float m = 1.f - x;
-    if (P == 1) {
-        N[0] = m;
-        N[1] = x;
-        E[0] = ns;
-    } else if (P == 2) {
-        const float x2 = x * x;
-        N[0] = 0.5f * m * m;
-        N[1] = fmaf(-1.f, x2, x) + 0.5f;
-        N[2] = 0.5f * x2;
-        E[0] = ns * m;
-        E[1] = ns * x;
-    } else {
-        const float x2 = x * x, x3 = x2 * x, m2 = m * m;
-        const float s6 = 1.f / 6.f;
-        N[0] = s6 * m2 * m;
-        N[1] = fmaf(0.5f, x3, fmaf(-1.f, x2, 2.f / 3.f));
-        N[2] = fmaf(-0.5f, x3, fmaf(0.5f, x2, fmaf(0.5f, x, s6)));
-        N[3] = s6 * x3;
-        const float hn = 0.5f * ns;
-        E[0] = hn * m2;
-        E[1] = ns * (fmaf(-1.f, x2, x) + 0.5f);
-        E[2] = hn * x2;
-    }
-}
-
 // The owner block's fields used per sample (kept in registers).
 struct BlockLite {
     const float4 *ctrl4;
@@ -653,7 +622,7 @@ static int render_minb() {
     static int v = [] {
         const char *e = getenv("AFAM_RENDER_MINB");
         const int m = e ? atoi(e) : 0;
-        return (m == 2 || m == 3) ? m : 4;
+        return (m == 3 || m == 5 || m == 6) ? m : 4;
     }();
     return v;
 }
@@ -674,8 +643,10 @@ template <bool DEBUG, bool SMEM>
 static void launch_render(dim3 g, size_t smem, cudaStream_t st, const BlockDesc *descs, const int16_t *grid,
                           const int32_t *idx, const RenderArgs &A, uint8_t *rgba, afam_render_stats *stats,
                           int32_t *nsamp, uint64_t *ohash) {
-    if (render_minb() == 2)
-        launch_render_v<DEBUG, SMEM, 2>(g, smem, st, descs, grid, idx, A, rgba, stats, nsamp, ohash);
+    if (render_minb() == 5)
+        launch_render_v<DEBUG, SMEM, 5>(g, smem, st, descs, grid, idx, A, rgba, stats, nsamp, ohash);
+    else if (render_minb() == 6)
+        launch_render_v<DEBUG, SMEM, 6>(g, smem, st, descs, grid, idx, A, rgba, stats, nsamp, ohash);
     else if (render_minb() == 4)
         launch_render_v<DEBUG, SMEM, 4>(g, smem, st, descs, grid, idx, A, rgba, stats, nsamp, ohash);
     else
@@ -767,7 +738,7 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
         std::lock_guard<std::mutex> lk(s->mu);
         int rc = build_owner_grid(s, slots, nblocks, cells, grid);
         if (rc) return rc;
-        for (int b = 0; b < nblocks; b++) AFAM_CUDA(cudaStreamWaitEvent(st, s->host[slots[b]].ready, 0));
+        for (int b = 0; b < nblocks; b++) AFAM_CUDA(wait_slot(s, slots[b], st));
     }
     A.cells = cells;
     A.nb = nblocks;
