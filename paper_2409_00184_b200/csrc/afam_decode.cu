@@ -69,24 +69,57 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
 }
 
-// Pairs of consecutive elements per lane: a warp covers one row of up to 64
-// elements with two per lane (lane l: 2l, 2l+1) plus lane 0 picking up the
-// 65th (ncp and m are <= 65 for the store's blocks; longer rows loop).
+constexpr int kMainGroups = 4;  // x-stage columns held per lane: up to 128 (longer rows use the tail path)
+
+__device__ __forceinline__ void st4(float *p, const float (&v)[4]) {
+    *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
+}
+__device__ __forceinline__ void st4(double *p, const double (&v)[4]) {
+    reinterpret_cast<double2 *>(p)[0] = make_double2(v[0], v[1]);
+    reinterpret_cast<double2 *>(p)[1] = make_double2(v[2], v[3]);
+}
+__device__ __forceinline__ void ld4(const float *p, float (&v)[4]) {
+    const float4 t = *reinterpret_cast<const float4 *>(p);
+    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+}
+__device__ __forceinline__ void ld4(const double *p, double (&v)[4]) {
+    const double2 a = reinterpret_cast<const double2 *>(p)[0], b = reinterpret_cast<const double2 *>(p)[1];
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+}
+
+// Three smem-staged banded contractions per output plane, register-blocked:
+// z and y items are 4 consecutive x (16-byte smem traffic), the x stage
+// keeps each lane's Bx rows in registers for every row j.
 template <int P, typename T>
 __device__ __forceinline__ void decode_planes(const BlockDesc &d, const int32_t *__restrict__ col0g,
                                               const T *__restrict__ Bg, int m, int k0, int k1,
                                               float *__restrict__ out, unsigned char *smem) {
-    const int n = d.ncp, pitch = d.pitch;
-    T *S1 = reinterpret_cast<T *>(smem);
-    T *S2 = S1 + (size_t)n * n;
-    T *B = S2 + (size_t)n * m;           // [m][4]
+    constexpr int Q = P + 1;
+    const int n = d.ncp, pitch = d.pitch, nq = pitch >> 2;
+    T *S1 = reinterpret_cast<T *>(smem);  // [n][pitch]
+    T *S2 = S1 + (size_t)n * pitch;       // [m][pitch]
+    T *B = S2 + (size_t)m * pitch;        // [m][4]
     int *c0 = reinterpret_cast<int *>(B + (size_t)m * 4);
     for (int i = threadIdx.x; i < m * 4; i += blockDim.x) B[i] = Bg[i];
     for (int i = threadIdx.x; i < m; i += blockDim.x) c0[i] = col0g[i];
     __syncthreads();
     const float *__restrict__ C = d.ctrl;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    const int tid = threadIdx.x, nth = blockDim.x;
     const size_t zstride = (size_t)n * pitch;
+    // item -> row by float reciprocal: exact for item < 2^20 (error << 0.5/nq)
+    const float inv_nq = 1.f / (float)nq;
+    const int ngroups = min(m / 32, kMainGroups), mainw = 32 * ngroups, tailw = m - mainw;
+    const float inv_tail = tailw > 0 ? 1.f / (float)tailw : 0.f;
+    T bx[kMainGroups][Q];
+    int xi[kMainGroups];
+#pragma unroll
+    for (int t = 0; t < kMainGroups; t++) {
+        const int i = min(lane + 32 * t, m - 1);
+        xi[t] = c0[i];
+#pragma unroll
+        for (int a = 0; a < Q; a++) bx[t][a] = B[i * 4 + a];
+    }
     // z-planes of control points stream through a ring of kRing smem slots by
     // TMA bulk copies (cp.async.bulk, one mbarrier per slot), issued up to
     // kAhead planes ahead of use so the HBM latency hides behind the previous
@@ -128,63 +161,60 @@ __device__ __forceinline__ void decode_planes(const BlockDesc &d, const int32_t 
             mbar_wait(bar + (zr % kRing), (uint32_t)((zr / kRing) & 1));
             planes[c] = ring + (size_t)(zr % kRing) * zstride;
         }
-        // z contraction: S1[a + n*b] = sum_c Bz[k,c] C[a, b, z0+c] (8-byte smem reads of pitched rows)
-        for (int b = warp; b < n; b += nwarp) {
-            for (int a = 2 * lane; a < n; a += 64) {
-                T s0 = T(0), s1 = T(0);
+        // z contraction, 4 consecutive x per item: S1[b][a..a+3] = sum_c Bz[k,c] C[a.., b, z0+c]
+        for (int item = tid; item < n * nq; item += nth) {
+            const int b = (int)(((float)item + 0.5f) * inv_nq), q = item - b * nq;
+            T acc[4] = {T(0), T(0), T(0), T(0)};
 #pragma unroll
-                for (int c = 0; c < P + 1; c++) {
-                    const float2 v = *reinterpret_cast<const float2 *>(planes[c] + (size_t)b * pitch + a);
-                    s0 = fma(bz[c], (T)v.x, s0);
-                    s1 = fma(bz[c], (T)v.y, s1);
-                }
-                S1[a + n * b] = s0;
-                if (a + 1 < n) S1[a + 1 + n * b] = s1;
+            for (int c = 0; c < Q; c++) {
+                const float4 v = *reinterpret_cast<const float4 *>(planes[c] + (size_t)b * pitch + 4 * q);
+                acc[0] = fma(bz[c], (T)v.x, acc[0]);
+                acc[1] = fma(bz[c], (T)v.y, acc[1]);
+                acc[2] = fma(bz[c], (T)v.z, acc[2]);
+                acc[3] = fma(bz[c], (T)v.w, acc[3]);
             }
+            st4(S1 + (size_t)b * pitch + 4 * q, acc);
         }
         __syncthreads();
-        // y contraction: S2[a + n*j] = sum_b By[j,b] S1[a + n*(y0_j+b)]
-        for (int j = warp; j < m; j += nwarp) {
-            const T *s1 = S1 + (size_t)n * c0[j];
-            T by[P + 1];
+        // y contraction: S2[j][a..a+3] = sum_b By[j,b] S1[y0_j+b][a..a+3]
+        for (int item = tid; item < m * nq; item += nth) {
+            const int j = (int)(((float)item + 0.5f) * inv_nq), q = item - j * nq;
+            const T *s1 = S1 + (size_t)c0[j] * pitch + 4 * q;
+            T acc[4] = {T(0), T(0), T(0), T(0)};
 #pragma unroll
-            for (int b = 0; b < P + 1; b++) by[b] = B[j * 4 + b];
-            for (int a = 2 * lane; a < n; a += 64) {
-                T s0 = T(0), t1 = T(0);
-                const bool two = a + 1 < n;
+            for (int bb = 0; bb < Q; bb++) {
+                T v[4];
+                ld4(s1 + (size_t)bb * pitch, v);
+                const T w = B[j * 4 + bb];
 #pragma unroll
-                for (int b = 0; b < P + 1; b++) {
-                    s0 = fma(by[b], s1[a + n * b], s0);
-                    if (two) t1 = fma(by[b], s1[a + 1 + n * b], t1);
-                }
-                S2[a + n * j] = s0;
-                if (two) S2[a + 1 + n * j] = t1;
+                for (int e = 0; e < 4; e++) acc[e] = fma(w, v[e], acc[e]);
             }
+            st4(S2 + (size_t)j * pitch + 4 * q, acc);
         }
         __syncthreads();
-        // x contraction + coalesced store: out[i + m*j + m*m*k]; the Bx rows of
-        // this lane's outputs stay in registers for all rows j
+        // x contraction + coalesced store out[i + m*j + m*m*k]: full-warp columns
+        // i = lane + 32t with their Bx rows in registers, then the m % 32 tail
         float *outk = out + (size_t)k * m * m;
-        for (int i0 = 2 * lane; i0 < m; i0 += 64) {
-            const bool two = i0 + 1 < m;
-            const int xa = c0[i0], xb = two ? c0[i0 + 1] : xa;
-            T ba[P + 1], bb[P + 1];
+        for (int j = warp; j < m; j += nwarp) {
+            const T *s2 = S2 + (size_t)j * pitch;
+            float *orow = outk + (size_t)j * m;
 #pragma unroll
-            for (int a = 0; a < P + 1; a++) {
-                ba[a] = B[i0 * 4 + a];
-                bb[a] = two ? B[(i0 + 1) * 4 + a] : T(0);
-            }
-            for (int j = warp; j < m; j += nwarp) {
-                const T *s2 = S2 + (size_t)n * j;
-                T acc0 = T(0), acc1 = T(0);
+            for (int t = 0; t < kMainGroups; t++) {
+                if (t < ngroups) {
+                    T acc = T(0);
 #pragma unroll
-                for (int a = 0; a < P + 1; a++) {
-                    acc0 = fma(ba[a], s2[xa + a], acc0);
-                    acc1 = fma(bb[a], s2[xb + a], acc1);
+                    for (int a = 0; a < Q; a++) acc = fma(bx[t][a], s2[xi[t] + a], acc);
+                    orow[lane + 32 * t] = (float)acc;
                 }
-                outk[i0 + m * j] = (float)acc0;
-                if (two) outk[i0 + 1 + m * j] = (float)acc1;
             }
+        }
+        for (int item = tid; item < m * tailw; item += nth) {
+            const int j = (int)(((float)item + 0.5f) * inv_tail), i = mainw + (item - j * tailw);
+            const T *s2 = S2 + (size_t)j * pitch + c0[i];
+            T acc = T(0);
+#pragma unroll
+            for (int a = 0; a < Q; a++) acc = fma(B[i * 4 + a], s2[a], acc);
+            outk[(size_t)j * m + i] = (float)acc;
         }
         __syncthreads();
     }
@@ -312,7 +342,7 @@ extern "C" int afam_decode_grid(afam_store *s, const int32_t *slots, int32_t nbl
     }
     // S1 + S2 + B (float64 worst case) + col0 (padded to 4) + plane ring + mbarriers
     const size_t maxpitch = (size_t)((maxn + 3) & ~3);
-    const size_t smem = ((size_t)maxn * maxn + (size_t)maxn * m + (size_t)m * 4) * sizeof(double) +
+    const size_t smem = ((size_t)maxn * maxpitch + (size_t)m * maxpitch + (size_t)m * 4) * sizeof(double) +
                         (size_t)((m + 3) & ~3) * 4 + (size_t)kRing * maxn * maxpitch * sizeof(float) +
                         kRing * sizeof(uint64_t) + 16;
     DecodeJob *d_jobs = nullptr;
