@@ -29,8 +29,7 @@ struct DecodeJob {
 
 constexpr int kDecodeChunk = 65;     // output planes per CTA (a whole 65^3 block)
 constexpr int kDecodeThreads = 416;  // 13 warps: 65 rows = 5 per warp
-constexpr int kAhead = 2;            // planes prefetched beyond the current window
-constexpr int kRing = AFAM_MAX_DEGREE + 1 + kAhead + 1;  // > P + kAhead
+constexpr int kRing = AFAM_MAX_DEGREE + 1;  // plane slots: one window of p+1 planes
 
 // ---- TMA bulk copy + mbarrier (PTX; SASS UBLKCP / SYNCS) ----
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -121,9 +120,10 @@ __device__ __forceinline__ void decode_planes(const BlockDesc &d, const int32_t 
         for (int a = 0; a < Q; a++) bx[t][a] = B[i * 4 + a];
     }
     // z-planes of control points stream through a ring of kRing smem slots by
-    // TMA bulk copies (cp.async.bulk, one mbarrier per slot), issued up to
-    // kAhead planes ahead of use so the HBM latency hides behind the previous
-    // output planes' contractions.
+    // TMA bulk copies (cp.async.bulk, one mbarrier per slot). The ring holds
+    // one window of p+1 planes; the next output plane's new planes are issued
+    // as soon as the Z stage has consumed the current window, so their HBM
+    // latency hides behind the Y and X stages.
     float *ring = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(c0 + m) + 15) & ~(uintptr_t)15);
     uint64_t *bar = reinterpret_cast<uint64_t *>(ring + (size_t)kRing * zstride);
     const uint32_t plane_bytes = (uint32_t)(zstride * sizeof(float));
@@ -137,20 +137,20 @@ __device__ __forceinline__ void decode_planes(const BlockDesc &d, const int32_t 
     const int zbase = c0[k0];
     const int zlast = min(n - 1, c0[k1 - 1] + P);
     int issued = zbase - 1;  // highest plane whose load was issued (thread 0)
+    // issue the loads of planes (issued, zmax]; a slot is recycled only after
+    // every thread passed the barrier behind the z stage that last read it
+    auto issue_upto = [&](int zmax) {
+        fence_proxy_async();  // earlier generic reads of recycled slots before the async writes
+        for (int z = issued + 1; z <= zmax; z++) {
+            uint64_t *bz_ = bar + ((z - zbase) % kRing);
+            mbar_arrive_expect_tx(bz_, plane_bytes);
+            tma_load_1d(ring + (size_t)((z - zbase) % kRing) * zstride, C + (size_t)z * zstride, plane_bytes, bz_);
+        }
+        issued = max(issued, zmax);
+    };
+    if (threadIdx.x == 0) issue_upto(min(zlast, zbase + P));
     for (int k = k0; k < k1; k++) {
         const int z0 = c0[k];
-        if (threadIdx.x == 0) {
-            const int zmax = min(zlast, z0 + P + kAhead);
-            fence_proxy_async();  // earlier generic reads of recycled slots before the async writes
-            for (int z = issued + 1; z <= zmax; z++) {
-                // the slot's previous plane z - kRing < z0 (kRing > P + kAhead) is no longer read
-                uint64_t *bz_ = bar + ((z - zbase) % kRing);
-                mbar_arrive_expect_tx(bz_, plane_bytes);
-                tma_load_1d(ring + (size_t)((z - zbase) % kRing) * zstride, C + (size_t)z * zstride, plane_bytes,
-                            bz_);
-            }
-            issued = max(issued, zmax);
-        }
         T bz[P + 1];
 #pragma unroll
         for (int c = 0; c < P + 1; c++) bz[c] = B[k * 4 + c];
@@ -176,6 +176,9 @@ __device__ __forceinline__ void decode_planes(const BlockDesc &d, const int32_t 
             st4(S1 + (size_t)b * pitch + 4 * q, acc);
         }
         __syncthreads();
+        // the ring planes below the next window are free now: fetch the next
+        // window while the y and x stages run (kRing = P+1 slots suffice)
+        if (threadIdx.x == 0 && k + 1 < k1) issue_upto(min(zlast, c0[k + 1] + P));
         // y contraction: S2[j][a..a+3] = sum_b By[j,b] S1[y0_j+b][a..a+3]
         for (int item = tid; item < m * nq; item += nth) {
             const int j = (int)(((float)item + 0.5f) * inv_nq), q = item - j * nq;
@@ -225,29 +228,27 @@ __device__ __forceinline__ void decode_planes(const BlockDesc &d, const int32_t 
             mbar_wait(bar + ((z - zbase) % kRing), (uint32_t)(((z - zbase) / kRing) & 1));
 }
 
+// One instantiation per arithmetic type so the float kernel is not sized
+// (registers, shared memory) for the float64 path; a CTA whose block has the
+// other precision exits at once.
+template <typename T>
 __global__ void __launch_bounds__(kDecodeThreads) decode_grid_kernel(const BlockDesc *__restrict__ descs,
                                                                       const DecodeJob *__restrict__ jobs, int m,
                                                                       float *__restrict__ out) {
     extern __shared__ __align__(16) unsigned char smem[];
     const DecodeJob jb = jobs[blockIdx.y];
     const BlockDesc d = descs[jb.slot];
+    constexpr bool kF64 = sizeof(T) == 8;
+    if (((d.flags & AFAM_SLOT_FP64) != 0) != kF64) return;
     const int k0 = blockIdx.x * kDecodeChunk;
     const int k1 = min(m, k0 + kDecodeChunk);
     float *o = out + (size_t)blockIdx.y * m * m * m;
-    const bool f64 = d.flags & AFAM_SLOT_FP64;
+    const T *b;
+    if constexpr (kF64) b = jb.b64; else b = jb.b32;
     switch (d.deg) {
-        case 1:
-            if (f64) decode_planes<1, double>(d, jb.col0, jb.b64, m, k0, k1, o, smem);
-            else decode_planes<1, float>(d, jb.col0, jb.b32, m, k0, k1, o, smem);
-            break;
-        case 2:
-            if (f64) decode_planes<2, double>(d, jb.col0, jb.b64, m, k0, k1, o, smem);
-            else decode_planes<2, float>(d, jb.col0, jb.b32, m, k0, k1, o, smem);
-            break;
-        default:
-            if (f64) decode_planes<3, double>(d, jb.col0, jb.b64, m, k0, k1, o, smem);
-            else decode_planes<3, float>(d, jb.col0, jb.b32, m, k0, k1, o, smem);
-            break;
+        case 1: decode_planes<1, T>(d, jb.col0, b, m, k0, k1, o, smem); break;
+        case 2: decode_planes<2, T>(d, jb.col0, b, m, k0, k1, o, smem); break;
+        default: decode_planes<3, T>(d, jb.col0, b, m, k0, k1, o, smem); break;
     }
 }
 
@@ -340,20 +341,31 @@ extern "C" int afam_decode_grid(afam_store *s, const int32_t *slots, int32_t nbl
             AFAM_CUDA(wait_slot(s, sl, st));
         }
     }
-    // S1 + S2 + B (float64 worst case) + col0 (padded to 4) + plane ring + mbarriers
+    // S1 + S2 + B in T + col0 (padded to 4) + plane ring + mbarriers
     const size_t maxpitch = (size_t)((maxn + 3) & ~3);
-    const size_t smem = ((size_t)maxn * maxpitch + (size_t)m * maxpitch + (size_t)m * 4) * sizeof(double) +
-                        (size_t)((m + 3) & ~3) * 4 + (size_t)kRing * maxn * maxpitch * sizeof(float) +
-                        kRing * sizeof(uint64_t) + 16;
+    auto smem_for = [&](size_t tsz) {
+        return ((size_t)maxn * maxpitch + (size_t)m * maxpitch + (size_t)m * 4) * tsz + (size_t)((m + 3) & ~3) * 4 +
+               (size_t)kRing * maxn * maxpitch * sizeof(float) + kRing * sizeof(uint64_t) + 16;
+    };
     DecodeJob *d_jobs = nullptr;
     AFAM_CUDA(cudaMallocAsync(&d_jobs, sizeof(DecodeJob) * nblk, st));
     AFAM_CUDA(cudaMemcpyAsync(d_jobs, jobs.data(), sizeof(DecodeJob) * nblk, cudaMemcpyHostToDevice, st));
+    const dim3 grid((m + kDecodeChunk - 1) / kDecodeChunk, nblk);
     {
+        const size_t smem = smem_for(sizeof(float));
         AFAM_CHECK(smem <= 227 * 1024, AFAM_E_VALUE, "decode of ncp=%d onto m=%d needs %zu B of shared memory", maxn,
                    m, smem);
-        AFAM_CUDA(cudaFuncSetAttribute(decode_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        dim3 grid((m + kDecodeChunk - 1) / kDecodeChunk, nblk);
-        decode_grid_kernel<<<grid, kDecodeThreads, smem, st>>>(s->d_desc, d_jobs, m, out);
+        AFAM_CUDA(cudaFuncSetAttribute(decode_grid_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+        decode_grid_kernel<float><<<grid, kDecodeThreads, smem, st>>>(s->d_desc, d_jobs, m, out);
+    }
+    {
+        const size_t smem = smem_for(sizeof(double));
+        AFAM_CHECK(smem <= 227 * 1024, AFAM_E_VALUE, "decode of ncp=%d onto m=%d needs %zu B of shared memory", maxn,
+                   m, smem);
+        AFAM_CUDA(cudaFuncSetAttribute(decode_grid_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+        decode_grid_kernel<double><<<grid, kDecodeThreads, smem, st>>>(s->d_desc, d_jobs, m, out);
     }
     AFAM_CUDA(cudaGetLastError());
     AFAM_CUDA(cudaFreeAsync(d_jobs, st));
