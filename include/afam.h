@@ -164,6 +164,8 @@ typedef struct {
     int64_t missing_key;   /* (step << 32) | ray of the first sample in an uncovered finest cell, or -1 */
     uint64_t fp64_samples; /* samples decoded on the float64 path */
     uint64_t shaded_samples; /* samples with TF opacity > 0 (gradient + shading evaluated) */
+    uint64_t exact_samples;  /* samples decoded from the float64 position (exact span search) */
+    uint64_t exact_cells;    /* float64 finest-cell evaluations (ray start, cell crossings, near-face samples) */
 } afam_render_stats;
 
 /*

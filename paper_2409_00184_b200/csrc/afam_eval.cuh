@@ -253,6 +253,45 @@ __device__ __forceinline__ void uniform_basis(float x, float ns, float (&N)[P + 
     }
 }
 
+// uniform_basis split into the values and the derivative weights, so the
+// ray march evaluates E only for samples it shades.
+template <int P>
+__device__ __forceinline__ void uniform_N(float x, float (&N)[P + 1]) {
+    const float m = 1.f - x;
+    if (P == 1) {
+        N[0] = m;
+        N[1] = x;
+    } else if (P == 2) {
+        const float x2 = x * x;
+        N[0] = 0.5f * m * m;
+        N[1] = fmaf(-1.f, x2, x) + 0.5f;
+        N[2] = 0.5f * x2;
+    } else {
+        const float x2 = x * x, x3 = x2 * x, m2 = m * m;
+        const float s6 = 1.f / 6.f;
+        N[0] = s6 * m2 * m;
+        N[1] = fmaf(0.5f, x3, fmaf(-1.f, x2, 2.f / 3.f));
+        N[2] = fmaf(-0.5f, x3, fmaf(0.5f, x2, fmaf(0.5f, x, s6)));
+        N[3] = s6 * x3;
+    }
+}
+
+template <int P>
+__device__ __forceinline__ void uniform_E(float x, float ns, float (&E)[P]) {
+    const float m = 1.f - x;
+    if (P == 1) {
+        E[0] = ns;
+    } else if (P == 2) {
+        E[0] = ns * m;
+        E[1] = ns * x;
+    } else {
+        const float x2 = x * x, hn = 0.5f * ns;
+        E[0] = hn * (m * m);
+        E[1] = ns * (fmaf(-1.f, x2, x) + 0.5f);
+        E[2] = hn * x2;
+    }
+}
+
 // Span + basis (values and difference-form derivative weights) of one axis
 // at parameter u64 (float64, already clipped).  float32 evaluation of a
 // clamped-uniform model takes the closed form on interior spans away from

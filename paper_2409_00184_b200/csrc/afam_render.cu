@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <limits>
 #include <vector>
 
 #include "afam_eval.cuh"
@@ -32,19 +33,22 @@
 namespace afam {
 
 constexpr int kTfMaxBp = 2 * AFAM_MAX_TF_POINTS;
-constexpr int kTfLut = 256;
+constexpr int kTfBuckets = 512;
 
 struct TfTable {
-    float4 val[kTfMaxBp];    // (r, g, b, alpha) at breakpoint j
-    float4 slope[kTfMaxBp];  // d/dv on [bp[j], bp[j+1]); 0 past the last breakpoint
-    float bp[kTfMaxBp];      // sorted union of color and opacity control scalars
+    float4 val[kTfMaxBp];     // (r, g, b, alpha) at breakpoint j
+    float4 slope[kTfMaxBp];   // d/dv on [bp[j], bp[j+1]); 0 past the last breakpoint
+    float4 c0[kTfBuckets];    // rgb at the bucket start; .w NaN: a color breakpoint lies in the bucket
+    float4 dc[kTfBuckets];    // rgb increment across the bucket
+    float2 alpha[kTfBuckets]; // (alpha at the bucket start, increment); .y NaN: an opacity breakpoint lies in it
+    float bp[kTfMaxBp];       // sorted union of color and opacity control scalars
+    int8_t lut[kTfBuckets];   // last breakpoint <= bucket start (-1: none)
     int32_t nbp;
-    float lut_lo, lut_scale; // bucket = (v - lut_lo) * lut_scale over the TF domain
-    int8_t lut[kTfLut];      // last breakpoint <= bucket start (-1: none)
-    uint8_t clean[kTfLut];   // 1: no breakpoint within (a margin of) the bucket, lut is the segment
+    float lo, scale;          // bucket coordinate = (v - lo) * scale over the TF domain
+    int32_t pad;
 };
 
-struct RenderArgs {
+struct alignas(16) RenderArgs {
     double origin[3], f[3], r[3], u[3];
     double tan_x, tan_y;
     double sd, o_max;
@@ -54,7 +58,7 @@ struct RenderArgs {
     float power, ambient, diffuse, specular, shininess;
     int32_t power_one;  // power == 1
     float dom_lo, dom_hi;
-    TfTable tf;
+    float o_max_f;      // largest float32 <= o_max: (float)A <= o_max_f iff (double)A <= o_max
     uint32_t flags;
 };
 
@@ -62,15 +66,14 @@ struct RenderArgs {
 // channel is np.interp over its own control points; on the sorted union of
 // all control scalars each channel is linear, so one segment search serves
 // r, g, b and alpha.  Values at the breakpoints are the float64 np.interp
-// values rounded to float32.
+// values rounded to float32.  The hot path reads the per-bucket lines
+// (tf_alpha / tf_color below); this search serves buckets holding a breakpoint.
 __device__ __forceinline__ float4 tf_eval(const TfTable &T, float v) {
-    int bi = (int)((v - T.lut_lo) * T.lut_scale);
-    bi = min(max(bi, 0), kTfLut - 1);
+    int bi = __float2int_rz((v - T.lo) * T.scale);
+    bi = min(max(bi, 0), kTfBuckets - 1);
     int j = T.lut[bi];
-    if (!T.clean[bi]) {
-        while (j + 1 < T.nbp && v >= T.bp[j + 1]) ++j;
-        while (j >= 0 && v < T.bp[j]) --j;
-    }
+    while (j + 1 < T.nbp && v >= T.bp[j + 1]) ++j;
+    while (j >= 0 && v < T.bp[j]) --j;
     if (j < 0) return T.val[0];
     const float4 a = T.val[j], s = T.slope[j];
     const float dx = v - T.bp[j];
@@ -347,24 +350,284 @@ __device__ __forceinline__ void decode_f64(const BlockLite &b, const BlockDesc *
     for (int a = 0; a < 3; a++) g[a] = (float)(gg[a] / span[a]);
 }
 
+// ---------------------------------------------------------------------------
+// K2 march.  The reference's per-sample geometry (render.py:422-428,
+// :377-380) is float64; the kernel evaluates it exactly (same op order, no
+// contraction) only where its result could differ from a cheap float32
+// prediction:
+//  - the sample count comes from one exact search per ray (t_k is monotone
+//    in k, so the alive samples are the prefix k < kend);
+//  - the finest cell of sample k is predicted as sc0 + k*dsc per axis; when
+//    every axis lies farther than `lim` from its current cell's faces the
+//    cell (hence the owner) is unchanged, otherwise the exact float64
+//    position decides (cell crossings, volume faces, rounding ties);
+//  - within a block the span coordinate is tq0 + (k - k0)*dtq from the exact
+//    position at block entry k0 (error < 2e-5 spans).
+// Owner selection therefore stays bit-exact while the common sample runs
+// without float64 arithmetic.
+
+struct RayState {  // per-thread, in local memory: read/written on the exact paths only
+    double d[3];
+    double te;
+    float4 tfv;       // sample_exact results
+    float g[3];
+    int32_t pad;
+};
+
+struct March {
+    int32_t k, kend;
+    float kf;                      // (float)k, exact below 2^24
+    float C0, C1, C2, Aacc;
+    float sc0[3], dsc[3], cen[3];  // finest-cell coordinate prediction, current cell centre
+    float lim;                     // |sc - cen| < lim: same cell (0.5 - rounding margin; < 0 disables)
+    float tq0[3], dtq[3], k0f;     // span-coordinate prediction within the current block
+    int32_t own;
+    uint32_t nshade, ns64, nexact, ncell;
+    uint64_t h;
+};
+
+// The owner block's fields the fast path reads per sample.
+// Internal render flag (AFAM_RENDER_FORCE_EXACT=1 in the environment): every
+// sample on the exact path, for A/B checks of the fast path.
+constexpr uint32_t kRenderForceExact = 0x100u;
+
+struct BlockFast {
+    const float4 *ctrl4;
+    const float *tab32;
+    int32_t ncp, nspan;
+    float nspan_f, inv_span_f[3];
+};
+
+// render.py:422-428 sample position, float64 in the reference op order, and
+// its finest cell (render.py:377-380).
+__device__ __forceinline__ void exact_geometry(const RenderArgs &A, const RayState &R, const int16_t *own_grid,
+                                               int64_t k, double (&p)[3], float (&cen)[3], int32_t &own) {
+    const double t = __dadd_rn(R.te, __dmul_rn((double)k + 0.5, A.sd));
+    const double cellsd = (double)A.cells;
+    int cidx = 0;
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        double q = __dadd_rn(A.origin[a], __dmul_rn(t, R.d[a]));
+        q = q < -1.0 ? -1.0 : (q > 1.0 ? 1.0 : q);  // np.clip (q is never NaN here)
+        p[a] = q;
+        const double sc = __dmul_rn(__dmul_rn(__dadd_rn(q, 1.0), 0.5), cellsd);
+        int ci = __double2int_rz(sc);
+        ci = min(max(ci, 0), A.cells - 1);
+        cen[a] = (float)ci + 0.5f;
+        cidx = cidx * A.cells + ci;
+    }
+    own = own_grid[cidx];
+}
+
+__device__ __forceinline__ void exact_pos(const RenderArgs &A, const RayState &R, int64_t k, double (&p)[3]) {
+    const double t = __dadd_rn(R.te, __dmul_rn((double)k + 0.5, A.sd));
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        const double q = __dadd_rn(A.origin[a], __dmul_rn(t, R.d[a]));
+        p[a] = q < -1.0 ? -1.0 : (q > 1.0 ? 1.0 : q);
+    }
+}
+
+// Per-axis basis of the fast path from the predicted span coordinate tq:
+// span k = floor(tq) (clamped), fraction fr.  Interior spans of a
+// clamped-uniform model use the closed form, the 2(p-1) boundary spans the
+// per-span table.  Returns false (P = 1 only) within 1e-4 of a knot, where
+// the gradient is discontinuous and the exact span must be searched.
+template <int P>
+__device__ __forceinline__ bool axis_fast(const BlockFast &b, int a, float tq, int &k, float &fr, float (&N)[P + 1]) {
+    k = min(max(__float2int_rd(tq), 0), b.nspan - 1);
+    fr = tq - (float)k;
+    if (P == 1 && !(fabsf(fr - 0.5f) < 0.5f - 1e-4f)) return false;
+    if (k >= P - 1 && k <= b.nspan - P) {  // interior span (none when nspan < 2p - 1)
+        uniform_N<P>(fr, N);
+    } else {
+        Tab<float> t;
+        load_entry<P>(b.tab32 + ((size_t)a * b.nspan + k) * tab_stride(P), t);
+        basis_vals_only<P, float>(t, clamp01(tq / b.nspan_f), N);
+    }
+    return true;
+}
+
+template <int P>
+__device__ __forceinline__ void axis_fast_E(const BlockFast &b, int a, int k, float fr, float (&E)[P]) {
+    if (k >= P - 1 && k <= b.nspan - P) {  // interior span (none when nspan < 2p - 1)
+        uniform_E<P>(fr, b.nspan_f, E);
+    } else {
+        Tab<float> t;
+        float N[P + 1];
+        load_entry<P>(b.tab32 + ((size_t)a * b.nspan + k) * tab_stride(P), t);
+        basis_eval<P, float>(t, clamp01(((float)k + fr) / b.nspan_f), N, E);
+    }
+}
+
+// TF opacity of a decoded value from the per-bucket lines (render.py:117-124
+// np.interp); NaN-marked buckets hold a breakpoint and take the segment search.
+__device__ __forceinline__ float tf_alpha(const TfTable &T, float v, int &bi, float &bf) {
+    const float tb = (v - T.lo) * T.scale;
+    bi = min(max(__float2int_rz(tb), 0), kTfBuckets - 1);
+    bf = tb - (float)bi;
+    const float2 l = __ldg(&T.alpha[bi]);
+    float a = fmaf(bf, l.y, l.x);
+    if (isnan(a)) a = tf_eval(T, v).w;
+    return a;
+}
+
+__device__ __forceinline__ float4 tf_color(const TfTable &T, float v, int bi, float bf, float atf) {
+    const float4 c = __ldg(&T.c0[bi]), dc = __ldg(&T.dc[bi]);
+    if (isnan(c.w)) {
+        float4 r = tf_eval(T, v);
+        r.w = atf;
+        return r;
+    }
+    return make_float4(fmaf(bf, dc.x, c.x), fmaf(bf, dc.y, c.y), fmaf(bf, dc.z, c.z), atf);
+}
+
+// Shading and compositing of one sample (render.py:383-395, :451-455).
+__device__ __forceinline__ void composite(const RenderArgs &A, const float (&vdir)[3], float4 tfv,
+                                          const float (&g)[3], March &M) {
+    const float atf = tfv.w;
+    const float as = A.power_one ? 1.f - (1.f - atf) : 1.f - __powf(1.f - atf, A.power);
+    const float gn2 = fmaf(g[2], g[2], fmaf(g[1], g[1], g[0] * g[0]));
+    float ndotl = 0.f;
+    if (gn2 > 1e-24f) {
+        const float ig = rsqrtf(gn2);
+        ndotl = fabsf(g[0] * vdir[0] + g[1] * vdir[1] + g[2] * vdir[2]) * ig;
+    }
+    const float dif = A.diffuse * ndotl;
+    // ndotl**shininess via exp2(shininess * log2(ndotl)) (MUFU.LG2 + MUFU.EX2)
+    const float spec = A.specular * (ndotl > 0.f ? exp2f(A.shininess * __log2f(ndotl))
+                                                 : (A.shininess == 0.f ? 1.f : 0.f));
+    const float lit = A.ambient + dif;
+    const float w = (1.f - M.Aacc) * as;
+    M.C0 = fmaf(w, __saturatef(fmaf(tfv.x, lit, spec)), M.C0);
+    M.C1 = fmaf(w, __saturatef(fmaf(tfv.y, lit, spec)), M.C1);
+    M.C2 = fmaf(w, __saturatef(fmaf(tfv.z, lit, spec)), M.C2);
+    M.Aacc += w;
+}
+
+// One sample of a clamped-uniform float32 block from the predicted span
+// coordinates: value first (x -> y -> z, keeping the x row sums), then the TF
+// opacity; the gradient (difference form) and the colour only when the
+// opacity is positive.  Returns false when the exact path must decode it.
+template <int P>
+__device__ __forceinline__ bool sample_fast(const RenderArgs &A, const TfTable &tf, const BlockFast &b,
+                                            const float (&tq)[3], const float (&vdir)[3], March &M) {
+    constexpr int Q = P + 1;
+    int kx, ky, kz;
+    float fx, fy, fz, Nx[Q], Ny[Q], Nz[Q];
+    if (!axis_fast<P>(b, 0, tq[0], kx, fx, Nx)) return false;
+    if (!axis_fast<P>(b, 1, tq[1], ky, fy, Ny)) return false;
+    if (!axis_fast<P>(b, 2, tq[2], kz, fz, Nz)) return false;
+    // x-quad rows (cz, by) of the (p+1)^3 patch (bspline.py:175-181)
+    const float4 *base = b.ctrl4 + ((size_t)kz * b.ncp + kx) * b.ncp + ky;
+    const size_t plane = (size_t)b.ncp * b.ncp;
+    float rx[Q][Q], ry[Q];
+#pragma unroll
+    for (int cz = 0; cz < Q; cz++) {
+        float ay = 0.f;
+#pragma unroll
+        for (int by = 0; by < Q; by++) {
+            const float4 r = __ldg(base + cz * plane + by);
+            float acc = Nx[0] * r.x;
+            acc = fmaf(Nx[1], r.y, acc);
+            if constexpr (P >= 2) acc = fmaf(Nx[2], r.z, acc);
+            if constexpr (P >= 3) acc = fmaf(Nx[3], r.w, acc);
+            rx[cz][by] = acc;
+            ay = fmaf(Ny[by], acc, ay);
+        }
+        ry[cz] = ay;
+    }
+    float v = 0.f;
+#pragma unroll
+    for (int cz = 0; cz < Q; cz++) v = fmaf(Nz[cz], ry[cz], v);
+    int bi;
+    float bf;
+    const float vc = fminf(fmaxf(v, A.dom_lo), A.dom_hi);
+    const float atf = tf_alpha(tf, vc, bi, bf);
+    if (!(atf > 0.f)) return true;  // a_s = 0: the sample changes neither C nor A
+    ++M.nshade;
+    float Ex[P], Ey[P], Ez[P];
+    axis_fast_E<P>(b, 0, kx, fx, Ex);
+    axis_fast_E<P>(b, 1, ky, fy, Ey);
+    axis_fast_E<P>(b, 2, kz, fz, Ez);
+    float gx = 0.f, gy = 0.f, gz = 0.f;
+#pragma unroll
+    for (int cz = 0; cz < Q; cz++) {
+        float adxy = 0.f, ady = 0.f;
+#pragma unroll
+        for (int by = 0; by < Q; by++) {
+            const float4 r = __ldg(base + cz * plane + by);  // L1 hit
+            float dacc = Ex[0] * (r.y - r.x);
+            if constexpr (P >= 2) dacc = fmaf(Ex[1], r.z - r.y, dacc);
+            if constexpr (P >= 3) dacc = fmaf(Ex[2], r.w - r.z, dacc);
+            adxy = fmaf(Ny[by], dacc, adxy);
+        }
+#pragma unroll
+        for (int q = 0; q < P; q++) ady = fmaf(Ey[q], rx[cz][q + 1] - rx[cz][q], ady);
+        gx = fmaf(Nz[cz], adxy, gx);
+        gy = fmaf(Nz[cz], ady, gy);
+    }
+#pragma unroll
+    for (int q = 0; q < P; q++) gz = fmaf(Ez[q], ry[q + 1] - ry[q], gz);
+    // model.py:79 gradient / span
+    const float g[3] = {gx * b.inv_span_f[0], gy * b.inv_span_f[1], gz * b.inv_span_f[2]};
+    composite(A, vdir, tf_color(tf, vc, bi, bf, atf), g, M);
+    return true;
+}
+
+// One sample on the exact path: float64 position, the reference's span
+// search; float32 (non-uniform knots, P = 1 near a knot) or float64
+// (ill-conditioned slot) arithmetic.  Out of line (rare), so its registers
+// do not weigh on the fast loop; arguments and results go through shared
+// memory (GA: the launch arguments in global memory, tf: the block's shared
+// TF table, R: this ray).
+// Returns 1 when the slot is float64.
+template <int P>
+__device__ __noinline__ int sample_exact(const RenderArgs *GA, const TfTable *tf, RayState *R,
+                                         const BlockDesc *__restrict__ dp,
+                                         int32_t slot, int32_t k) {
+    double pos[3];
+    exact_pos(*GA, *R, k, pos);
+    BlockLite b;
+    load_lite(dp, b);
+    GatherCache G;
+    G.slot = -1;
+    float v, g[3];
+    float4 tfv;
+    const bool f64 = b.flags & AFAM_SLOT_FP64;
+    if (f64) {
+        decode_f64<P>(b, dp, slot, G, pos, v, g);
+        tfv = tf_eval(*tf, fminf(fmaxf(v, GA->dom_lo), GA->dom_hi));
+    } else {
+        decode_f32<P>(b, dp, slot, G, pos, *tf, GA->dom_lo, GA->dom_hi, v, tfv, g);
+    }
+    R->tfv = tfv;
+    R->g[0] = g[0];
+    R->g[1] = g[1];
+    R->g[2] = g[2];
+    return f64 ? 1 : 0;
+}
+
 template <bool DEBUG, bool SMEM_GRID, int MINB>
 __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__restrict__ descs,
                                                         const int16_t *__restrict__ grid,
                                                         const int32_t *__restrict__ idx2slot, const RenderArgs A,
-                                                        uint8_t *__restrict__ rgba, afam_render_stats *stats,
-                                                        int32_t *__restrict__ nsamp, uint64_t *__restrict__ ohash) {
+                                                        const RenderArgs *__restrict__ GA,
+                                                        const TfTable *__restrict__ gtf, uint8_t *__restrict__ rgba,
+                                                        afam_render_stats *stats, int32_t *__restrict__ nsamp,
+                                                        uint64_t *__restrict__ ohash) {
     extern __shared__ __align__(16) unsigned char smem[];
-    TfTable &tf = *reinterpret_cast<TfTable *>(smem);
-    int16_t *sgrid = reinterpret_cast<int16_t *>(smem + sizeof(TfTable));
-    {
-        const int *src = reinterpret_cast<const int *>(&A.tf);
-        int *dst = reinterpret_cast<int *>(&tf);
-        for (int i = threadIdx.x; i < (int)(sizeof(TfTable) / 4); i += blockDim.x) dst[i] = src[i];
-    }
+    // the TF tables stay in global memory (one L1-resident copy per SM, read
+    // through the read-only path), shared memory holds only the owner grid,
+    // so L1 keeps the most room for control-point rows; GA: the launch
+    // arguments in global memory, for the out-of-line exact path
+    const TfTable &tf = *gtf;
+    int16_t *sgrid = reinterpret_cast<int16_t *>(smem);
     if (SMEM_GRID)
         for (int i = threadIdx.x; i < A.cells * A.cells * A.cells; i += blockDim.x) sgrid[i] = grid[i];
     __syncthreads();
     const int16_t *own_grid = SMEM_GRID ? sgrid : grid;
+    RayState R;  // local memory: touched on the exact paths only
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int j = blockIdx.x * 16 + (warp & 1) * 8 + (lane & 7);
@@ -399,117 +662,137 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
     }
     te = fmax(te, A.near_);
     const bool active = inside && te < tx;
+#pragma unroll
+    for (int a = 0; a < 3; a++) R.d[a] = d[a];
+    R.te = te;
 
     const float vdir[3] = {(float)d[0], (float)d[1], (float)d[2]};
-    const double cellsd = (double)A.cells;
-    const float o_max = (float)A.o_max;
-    const bool o_max_exact = (double)o_max == A.o_max;
-    float C0 = 0.f, C1 = 0.f, C2 = 0.f, Aacc = 0.f;
-    uint32_t ns = 0, ns64 = 0, nshade = 0;
-    uint64_t h = 1469598103934665603ULL;
+    March M;
+    M.k = 0;
+    M.kend = 0;
+    M.kf = 0.f;
+    M.C0 = M.C1 = M.C2 = M.Aacc = 0.f;
+    M.nshade = M.ns64 = M.nexact = M.ncell = 0;
+    M.h = 1469598103934665603ULL;
+    M.own = -1;
     int64_t miss = INT64_MAX;
 
-    int32_t cur_own = -1, cur_slot = -1;
-    BlockLite b;
-    b.deg = 0;
-    b.flags = 0;
-    GatherCache G;
-    G.slot = -1;
-
-    // sample k's position and finest-cell owner (render.py:422-428, :377-380):
-    // float64, reference op order, no contraction
-    auto geometry = [&](int64_t k, double &t, double (&pos)[3], int &own) {
-        t = __dadd_rn(te, __dmul_rn((double)k + 0.5, A.sd));
-        int cidx = 0;
+    if (active) {
+        // alive samples: t_k = te + (k + 0.5) sd < tx, a prefix of k (render.py:423)
+        auto tk = [&](int64_t k) { return __dadd_rn(te, __dmul_rn((double)k + 0.5, A.sd)); };
+        int64_t ke = (int64_t)fmax(ceil((tx - te) / A.sd - 0.5), 0.0);
+        while (ke > 0 && !(tk(ke - 1) < tx)) --ke;
+        while (tk(ke) < tx) ++ke;
+        M.kend = (int32_t)min(ke, (int64_t)INT32_MAX);
+        // predicted finest-cell coordinate sc(k) = sc0 + k dsc; the margin
+        // covers float32 rounding of sc0, dsc and the fma (K2)
+        const double hc = 0.5 * (double)A.cells;
+        const double t0 = tk(0);
 #pragma unroll
         for (int a = 0; a < 3; a++) {
-            double p = __dadd_rn(A.origin[a], __dmul_rn(t, d[a]));
-            p = p < -1.0 ? -1.0 : (p > 1.0 ? 1.0 : p);  // np.clip (p is never NaN here)
-            pos[a] = p;
-            const double sc = __dmul_rn(__dmul_rn(__dadd_rn(p, 1.0), 0.5), cellsd);
-            int ci = __double2int_rz(sc);
-            ci = min(max(ci, 0), A.cells - 1);
-            cidx = cidx * A.cells + ci;
+            M.sc0[a] = (float)((A.origin[a] + t0 * d[a] + 1.0) * hc);
+            M.dsc[a] = (float)(A.sd * d[a] * hc);
         }
-        own = own_grid[cidx];
-    };
-
-    if (active) {
-        for (int64_t k = 0;; k++) {
-            double t, pos[3];
-            int own;
-            geometry(k, t, pos, own);
-            // render.py:423 alive test, before sample k
-            if (!(t < tx && (o_max_exact ? Aacc <= o_max : (double)Aacc <= A.o_max))) break;
-            if (own < 0) {  // render.py:430-436
-                miss = ((int64_t)k << 32) | ray;
+        M.lim = ke < (1 << 24) ? 0.5f - (1e-5f + 1e-6f * (float)A.cells) : -1.f;
+        {
+            double p[3];
+            exact_geometry(A, R, own_grid, 0, p, M.cen, M.own);
+        }
+        int32_t cur_own = -1, slot = -1, deg = 0;
+        BlockFast b;
+        bool fast = false;
+        while (M.k < M.kend) {
+            if (M.own < 0) {  // render.py:430-436
+                miss = ((int64_t)M.k << 32) | ray;
                 break;
             }
-            if (own != cur_own) {
-                cur_own = own;
-                cur_slot = __ldg(idx2slot + own);
-                load_lite(descs + cur_slot, b);
+            if (M.own != cur_own) {
+                cur_own = M.own;
+                slot = __ldg(idx2slot + cur_own);
+                const BlockDesc *dp = descs + slot;
+                b.ctrl4 = (const float4 *)__ldg((const unsigned long long *)&dp->ctrl4);
+                b.tab32 = (const float *)__ldg((const unsigned long long *)&dp->tab32);
+                b.ncp = __ldg(&dp->ncp);
+                b.nspan = __ldg(&dp->nspan);
+                b.nspan_f = (float)b.nspan;
+                deg = __ldg(&dp->deg);
+                const uint32_t flags = __ldg(&dp->flags);
+                fast = (flags & kFlagUniform) && !(flags & AFAM_SLOT_FP64) && (deg > 1 || b.nspan <= 128) &&
+                       M.lim > 0.f && !(A.flags & kRenderForceExact);
+                // span-coordinate prediction from the exact entry position
+                double p[3];
+                exact_pos(A, R, M.k, p);
+#pragma unroll
+                for (int a = 0; a < 3; a++) {
+                    b.inv_span_f[a] = __ldg(&dp->inv_span_f[a]);
+                    const double sc = __ldg(&dp->inv_span[a]) * (double)b.nspan;
+                    M.tq0[a] = (float)((p[a] - __ldg(&dp->lo[a])) * sc);
+                    M.dtq[a] = (float)(A.sd * d[a] * sc);
+                }
+                M.k0f = M.kf;
             }
-            float v, g[3];
-            float4 tfv;
-            if (b.flags & AFAM_SLOT_FP64) {
-                ++ns64;
-                if (b.deg == 3) decode_f64<3>(b, descs + cur_slot, cur_slot, G, pos, v, g);
-                else if (b.deg == 2) decode_f64<2>(b, descs + cur_slot, cur_slot, G, pos, v, g);
-                else decode_f64<1>(b, descs + cur_slot, cur_slot, G, pos, v, g);
-                tfv = tf_eval(tf, fminf(fmaxf(v, A.dom_lo), A.dom_hi));
-            } else {
-                if (b.deg == 3) decode_f32<3>(b, descs + cur_slot, cur_slot, G, pos, tf, A.dom_lo, A.dom_hi, v, tfv, g);
-                else if (b.deg == 2)
-                    decode_f32<2>(b, descs + cur_slot, cur_slot, G, pos, tf, A.dom_lo, A.dom_hi, v, tfv, g);
-                else decode_f32<1>(b, descs + cur_slot, cur_slot, G, pos, tf, A.dom_lo, A.dom_hi, v, tfv, g);
+            // one sample per iteration (a flat loop keeps the lanes of a warp
+            // in step across their different block runs)
+            if (DEBUG) M.h = (M.h ^ (uint64_t)(uint32_t)cur_own) * 1099511628211ULL;
+            bool ok = false;
+            if (fast) {
+                const float dk = M.kf - M.k0f;
+                const float tq[3] = {fmaf(dk, M.dtq[0], M.tq0[0]), fmaf(dk, M.dtq[1], M.tq0[1]),
+                                     fmaf(dk, M.dtq[2], M.tq0[2])};
+                if (deg == 3) ok = sample_fast<3>(A, tf, b, tq, vdir, M);
+                else if (deg == 2) ok = sample_fast<2>(A, tf, b, tq, vdir, M);
+                else ok = sample_fast<1>(A, tf, b, tq, vdir, M);
             }
-            ++ns;
-            if (DEBUG) h = (h ^ (uint64_t)(uint32_t)own) * 1099511628211ULL;
-            const float atf = tfv.w;
-            if (!(atf > 0.f)) continue;  // a_s = 0: the sample changes neither C nor A
-            ++nshade;
-            const float col[3] = {tfv.x, tfv.y, tfv.z};
-            // render.py:451 opacity correction
-            const float as = A.power_one ? 1.f - (1.f - atf) : 1.f - __powf(1.f - atf, A.power);
-            // _shade (render.py:383-395)
-            const float gn2 = fmaf(g[2], g[2], fmaf(g[1], g[1], g[0] * g[0]));
-            float ndotl = 0.f;
-            if (gn2 > 1e-24f) {
-                const float ig = rsqrtf(gn2);
-                ndotl = fabsf(g[0] * vdir[0] + g[1] * vdir[1] + g[2] * vdir[2]) * ig;
+            if (!ok) {
+                const BlockDesc *dpx = descs + slot;
+                int f64;
+                if (deg == 3) f64 = sample_exact<3>(GA, &tf, &R, dpx, slot, M.k);
+                else if (deg == 2) f64 = sample_exact<2>(GA, &tf, &R, dpx, slot, M.k);
+                else f64 = sample_exact<1>(GA, &tf, &R, dpx, slot, M.k);
+                M.ns64 += f64;
+                ++M.nexact;
+                const float4 tfv = R.tfv;
+                if (tfv.w > 0.f) {
+                    ++M.nshade;
+                    const float g[3] = {R.g[0], R.g[1], R.g[2]};
+                    composite(A, vdir, tfv, g, M);
+                }
             }
-            const float dif = A.diffuse * ndotl;
-            // ndotl**shininess via exp2(shininess * log2(ndotl)) (MUFU.LG2 + MUFU.EX2)
-            const float spec = A.specular * (ndotl > 0.f ? exp2f(A.shininess * __log2f(ndotl))
-                                                         : (A.shininess == 0.f ? 1.f : 0.f));
-            const float lit = A.ambient + dif;
-            // render.py:453-455 front-to-back composite
-            const float w = (1.f - Aacc) * as;
-            C0 = fmaf(w, __saturatef(fmaf(col[0], lit, spec)), C0);
-            C1 = fmaf(w, __saturatef(fmaf(col[1], lit, spec)), C1);
-            C2 = fmaf(w, __saturatef(fmaf(col[2], lit, spec)), C2);
-            Aacc += w;
+            // render.py:423 alive test before the next sample
+            ++M.k;
+            M.kf += 1.f;
+            if (M.k >= M.kend || !(M.Aacc <= A.o_max_f)) break;
+            bool same = true;
+#pragma unroll
+            for (int a = 0; a < 3; a++) same &= fabsf(fmaf(M.kf, M.dsc[a], M.sc0[a]) - M.cen[a]) < M.lim;
+            if (!same) {
+                double p[3];
+                ++M.ncell;
+                exact_geometry(A, R, own_grid, M.k, p, M.cen, M.own);
+            }
         }
     }
+    const uint32_t ns = (uint32_t)M.k;
     if (inside) {
         // render.py:458-461 quantise (round half to even)
         uchar4 px4;
-        px4.x = (unsigned char)min(max(__float2int_rn(C0 * 255.f), 0), 255);
-        px4.y = (unsigned char)min(max(__float2int_rn(C1 * 255.f), 0), 255);
-        px4.z = (unsigned char)min(max(__float2int_rn(C2 * 255.f), 0), 255);
-        px4.w = (unsigned char)min(max(__float2int_rn(Aacc * 255.f), 0), 255);
+        px4.x = (unsigned char)min(max(__float2int_rn(M.C0 * 255.f), 0), 255);
+        px4.y = (unsigned char)min(max(__float2int_rn(M.C1 * 255.f), 0), 255);
+        px4.z = (unsigned char)min(max(__float2int_rn(M.C2 * 255.f), 0), 255);
+        px4.w = (unsigned char)min(max(__float2int_rn(M.Aacc * 255.f), 0), 255);
         const int64_t local = (int64_t)lr * A.width + j;
         reinterpret_cast<uchar4 *>(rgba)[local] = px4;
         if (DEBUG) {
             nsamp[local] = (int32_t)ns;
-            ohash[local] = h;
+            ohash[local] = M.h;
         }
     }
     // per-warp reductions of the counters
     const uint32_t wsum = __reduce_add_sync(0xffffffffu, ns);
-    const uint32_t wsum64 = __reduce_add_sync(0xffffffffu, ns64);
-    const uint32_t wshade = __reduce_add_sync(0xffffffffu, nshade);
+    const uint32_t wsum64 = __reduce_add_sync(0xffffffffu, M.ns64);
+    const uint32_t wshade = __reduce_add_sync(0xffffffffu, M.nshade);
+    const uint32_t wexact = __reduce_add_sync(0xffffffffu, M.nexact);
+    const uint32_t wcell = __reduce_add_sync(0xffffffffu, M.ncell);
     int64_t wmiss = miss;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -520,6 +803,8 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
         if (wsum) atomicAdd((unsigned long long *)&stats->samples, (unsigned long long)wsum);
         if (wsum64) atomicAdd((unsigned long long *)&stats->fp64_samples, (unsigned long long)wsum64);
         if (wshade) atomicAdd((unsigned long long *)&stats->shaded_samples, (unsigned long long)wshade);
+        if (wexact) atomicAdd((unsigned long long *)&stats->exact_samples, (unsigned long long)wexact);
+        if (wcell) atomicAdd((unsigned long long *)&stats->exact_cells, (unsigned long long)wcell);
         if (wmiss != INT64_MAX) atomicMin((long long *)&stats->missing_key, (long long)wmiss);
     }
 }
@@ -529,6 +814,8 @@ __global__ void init_stats_kernel(afam_render_stats *s) {
     s->fp64_samples = 0;
     s->missing_key = INT64_MAX;
     s->shaded_samples = 0;
+    s->exact_samples = 0;
+    s->exact_cells = 0;
 }
 
 __global__ void finish_stats_kernel(afam_render_stats *s) {
@@ -549,9 +836,11 @@ static double host_interp(double x, const double (*pts)[4], const double (*opts)
 }
 
 static void build_tf_table(const afam_frame *F, TfTable &T) {
-    std::vector<double> xs;
-    for (int k = 0; k < F->ncolor; k++) xs.push_back(F->color[k][0]);
-    for (int k = 0; k < F->nopacity; k++) xs.push_back(F->opacity[k][0]);
+    std::vector<double> xs, xc, xo;
+    for (int k = 0; k < F->ncolor; k++) xc.push_back(F->color[k][0]);
+    for (int k = 0; k < F->nopacity; k++) xo.push_back(F->opacity[k][0]);
+    xs = xc;
+    xs.insert(xs.end(), xo.begin(), xo.end());
     std::sort(xs.begin(), xs.end());
     xs.erase(std::unique(xs.begin(), xs.end()), xs.end());
     T.nbp = (int)xs.size();
@@ -570,18 +859,42 @@ static void build_tf_table(const afam_frame *F, TfTable &T) {
         T.slope[j] = make_float4(s[0], s[1], s[2], s[3]);
     }
     const double lo = F->domain_lo, hi = F->domain_hi;
-    T.lut_lo = (float)lo;
-    T.lut_scale = (float)(kTfLut / (hi - lo));
-    const double w = (hi - lo) / kTfLut, margin = 0.01 * w;
-    for (int i = 0; i < kTfLut; i++) {
-        const double x = lo + (hi - lo) * i / kTfLut;
+    const bool ok = hi > lo;
+    T.lo = (float)lo;
+    T.scale = ok ? (float)(kTfBuckets / (hi - lo)) : 0.f;
+    const double w = ok ? (hi - lo) / kTfBuckets : 0.0, margin = 0.01 * w;
+    const float qnan = std::numeric_limits<float>::quiet_NaN();
+    // a bucket is "clean" for a channel group when none of that group's
+    // control scalars lies within it (plus a margin for the float32 bucket
+    // coordinate): np.interp is then one linear function across the bucket
+    auto clean = [&](const std::vector<double> &pts, double x0, double x1) {
+        for (double q : pts)
+            if (q > x0 - margin && q < x1 + margin) return false;
+        return ok;
+    };
+    for (int i = 0; i < kTfBuckets; i++) {
+        const double x0 = lo + w * i, x1 = lo + w * (i + 1);
         int j = -1;
-        while (j + 1 < T.nbp && xs[j + 1] <= x) ++j;
+        while (j + 1 < T.nbp && xs[j + 1] <= x0) ++j;
         T.lut[i] = (int8_t)j;
-        bool clean = true;  // no breakpoint near the bucket: the bucket index alone decides the segment
-        for (int q = 0; q < T.nbp; q++)
-            if (xs[q] > x - margin && xs[q] < x + w + margin) clean = false;
-        T.clean[i] = clean;
+        if (clean(xo, x0, x1)) {
+            const double a0 = eval(x0, 3), a1 = eval(x1, 3);
+            T.alpha[i] = make_float2((float)a0, (float)(a1 - a0));
+        } else {
+            T.alpha[i] = make_float2(0.f, qnan);
+        }
+        if (clean(xc, x0, x1)) {
+            double c0[3], c1[3];
+            for (int c = 0; c < 3; c++) {
+                c0[c] = eval(x0, c);
+                c1[c] = eval(x1, c);
+            }
+            T.c0[i] = make_float4((float)c0[0], (float)c0[1], (float)c0[2], 0.f);
+            T.dc[i] = make_float4((float)(c1[0] - c0[0]), (float)(c1[1] - c0[1]), (float)(c1[2] - c0[2]), 0.f);
+        } else {
+            T.c0[i] = make_float4(0.f, 0.f, 0.f, qnan);
+            T.dc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
     }
 }
 
@@ -627,30 +940,40 @@ static int render_minb() {
     return v;
 }
 
+struct LaunchArgs {
+    dim3 grid;
+    size_t smem;
+    cudaStream_t st;
+    const BlockDesc *descs;
+    const int16_t *owner;
+    const int32_t *idx;
+    const RenderArgs *gargs;
+    const TfTable *gtf;
+    uint8_t *rgba;
+    afam_render_stats *stats;
+    int32_t *nsamp;
+    uint64_t *ohash;
+};
+
 template <bool DEBUG, bool SMEM, int MINB>
-static void launch_render_v(dim3 g, size_t smem, cudaStream_t st, const BlockDesc *descs, const int16_t *grid,
-                            const int32_t *idx, const RenderArgs &A, uint8_t *rgba, afam_render_stats *stats,
-                            int32_t *nsamp, uint64_t *ohash) {
+static void launch_render_v(const LaunchArgs &L, const RenderArgs &A) {
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(render_kernel<DEBUG, SMEM, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
         configured = true;
     }
-    render_kernel<DEBUG, SMEM, MINB><<<g, 128, smem, st>>>(descs, grid, idx, A, rgba, stats, nsamp, ohash);
+    render_kernel<DEBUG, SMEM, MINB><<<L.grid, 128, L.smem, L.st>>>(L.descs, L.owner, L.idx, A, L.gargs, L.gtf,
+                                                                    L.rgba, L.stats, L.nsamp, L.ohash);
 }
 
 template <bool DEBUG, bool SMEM>
-static void launch_render(dim3 g, size_t smem, cudaStream_t st, const BlockDesc *descs, const int16_t *grid,
-                          const int32_t *idx, const RenderArgs &A, uint8_t *rgba, afam_render_stats *stats,
-                          int32_t *nsamp, uint64_t *ohash) {
-    if (render_minb() == 5)
-        launch_render_v<DEBUG, SMEM, 5>(g, smem, st, descs, grid, idx, A, rgba, stats, nsamp, ohash);
-    else if (render_minb() == 6)
-        launch_render_v<DEBUG, SMEM, 6>(g, smem, st, descs, grid, idx, A, rgba, stats, nsamp, ohash);
-    else if (render_minb() == 4)
-        launch_render_v<DEBUG, SMEM, 4>(g, smem, st, descs, grid, idx, A, rgba, stats, nsamp, ohash);
-    else
-        launch_render_v<DEBUG, SMEM, 3>(g, smem, st, descs, grid, idx, A, rgba, stats, nsamp, ohash);
+static void launch_render(const LaunchArgs &L, const RenderArgs &A) {
+    switch (render_minb()) {
+        case 3: launch_render_v<DEBUG, SMEM, 3>(L, A); break;
+        case 5: launch_render_v<DEBUG, SMEM, 5>(L, A); break;
+        case 6: launch_render_v<DEBUG, SMEM, 6>(L, A); break;
+        default: launch_render_v<DEBUG, SMEM, 4>(L, A); break;
+    }
 }
 
 }  // namespace afam
@@ -729,8 +1052,22 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
     A.shininess = (float)F->shininess;
     A.dom_lo = (float)F->domain_lo;
     A.dom_hi = (float)F->domain_hi;
-    build_tf_table(F, A.tf);
-    A.flags = F->flags;
+    {
+        float of = (float)F->o_max;
+        if ((double)of > F->o_max) of = std::nextafter(of, -INFINITY);
+        A.o_max_f = of;
+    }
+    A.flags = F->flags & AFAM_RENDER_DEBUG;
+    {
+        static const bool force_exact = [] {
+            const char *e = getenv("AFAM_RENDER_FORCE_EXACT");
+            return e && atoi(e) != 0;
+        }();
+        if (force_exact) A.flags |= kRenderForceExact;
+    }
+    TfTable tf;
+    memset(&tf, 0, sizeof(tf));
+    build_tf_table(F, tf);
 
     std::vector<int16_t> grid;
     int32_t cells = 1;
@@ -742,33 +1079,49 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
     }
     A.cells = cells;
     A.nb = nblocks;
-    int16_t *d_grid = nullptr;
-    int32_t *d_idx = nullptr;
+    // one upload: [RenderArgs | TfTable | owner grid | slot of each owner index]
+    auto al = [](size_t v) { return (v + 255) & ~(size_t)255; };
     const size_t gbytes = grid.size() * sizeof(int16_t);
-    const size_t ibytes = std::max<size_t>(1, (size_t)nblocks) * sizeof(int32_t);
-    AFAM_CUDA(cudaMallocAsync(&d_grid, gbytes, st));
-    AFAM_CUDA(cudaMallocAsync(&d_idx, ibytes, st));
-    AFAM_CUDA(cudaMemcpyAsync(d_grid, grid.data(), gbytes, cudaMemcpyHostToDevice, st));
-    if (nblocks) AFAM_CUDA(cudaMemcpyAsync(d_idx, slots, (size_t)nblocks * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    const size_t off_tf = al(sizeof(RenderArgs)), off_grid = off_tf + al(sizeof(TfTable));
+    const size_t off_idx = off_grid + al(gbytes);
+    const size_t total = off_idx + std::max<size_t>(1, (size_t)nblocks) * sizeof(int32_t);
+    std::vector<unsigned char> pack(total, 0);
+    memcpy(pack.data(), &A, sizeof(A));
+    memcpy(pack.data() + off_tf, &tf, sizeof(tf));
+    memcpy(pack.data() + off_grid, grid.data(), gbytes);
+    if (nblocks) memcpy(pack.data() + off_idx, slots, (size_t)nblocks * sizeof(int32_t));
+    unsigned char *d_pack = nullptr;
+    AFAM_CUDA(cudaMallocAsync(&d_pack, total, st));
+    AFAM_CUDA(cudaMemcpyAsync(d_pack, pack.data(), total, cudaMemcpyHostToDevice, st));
     AFAM_CUDA(cudaEventRecord(s->ev_k0, st));
     init_stats_kernel<<<1, 1, 0, st>>>(stats);
     if (A.rows > 0) {
-        dim3 g((A.width + 15) / 16, (A.rows + 7) / 8);
+        LaunchArgs L;
+        L.grid = dim3((A.width + 15) / 16, (A.rows + 7) / 8);
         const bool sg = cells <= kSmemGridMaxCells;
-        const size_t smem = sizeof(TfTable) + (sg ? gbytes : 0);
+        L.smem = sg ? gbytes : 0;
+        L.st = st;
+        L.descs = s->d_desc;
+        L.owner = (const int16_t *)(d_pack + off_grid);
+        L.idx = (const int32_t *)(d_pack + off_idx);
+        L.gargs = (const RenderArgs *)d_pack;
+        L.gtf = (const TfTable *)(d_pack + off_tf);
+        L.rgba = rgba;
+        L.stats = stats;
+        L.nsamp = nsamp;
+        L.ohash = ohash;
         if (debug) {
-            if (sg) launch_render<true, true>(g, smem, st, s->d_desc, d_grid, d_idx, A, rgba, stats, nsamp, ohash);
-            else launch_render<true, false>(g, smem, st, s->d_desc, d_grid, d_idx, A, rgba, stats, nsamp, ohash);
+            if (sg) launch_render<true, true>(L, A);
+            else launch_render<true, false>(L, A);
         } else {
-            if (sg) launch_render<false, true>(g, smem, st, s->d_desc, d_grid, d_idx, A, rgba, stats, nsamp, ohash);
-            else launch_render<false, false>(g, smem, st, s->d_desc, d_grid, d_idx, A, rgba, stats, nsamp, ohash);
+            if (sg) launch_render<false, true>(L, A);
+            else launch_render<false, false>(L, A);
         }
     }
     finish_stats_kernel<<<1, 1, 0, st>>>(stats);
     AFAM_CUDA(cudaEventRecord(s->ev_k1, st));
     AFAM_CUDA(cudaGetLastError());
-    AFAM_CUDA(cudaFreeAsync(d_grid, st));
-    AFAM_CUDA(cudaFreeAsync(d_idx, st));
+    AFAM_CUDA(cudaFreeAsync(d_pack, st));
     return AFAM_OK;
 }
 

@@ -326,10 +326,10 @@ _tls = threading.local()
 
 
 def _pinned_stage(nbytes: int):
-    """This thread's pinned host staging buffer of >= 32 + nbytes bytes (grown on demand)."""
+    """This thread's pinned host staging buffer of >= 64 + nbytes bytes (grown on demand)."""
     import torch
 
-    need = 32 + nbytes
+    need = 64 + nbytes
     buf = getattr(_tls, "stage", None)
     if buf is None or buf.numel() < need:
         buf = torch.empty(max(need, 1 << 16), dtype=torch.uint8, pin_memory=True)
@@ -358,7 +358,7 @@ def render_part(pov, blocks: dict, tf, params, *, band_rows: int | None = None, 
     fr = _frame_struct(pov, tf, params, br, nparts, part, debug)
     if out is None:
         out = torch.empty((rows, W, 4), dtype=torch.uint8, device=dev)
-    stats = torch.empty(4, dtype=torch.int64, device=dev)
+    stats = torch.empty(6, dtype=torch.int64, device=dev)
     nsamp = ohash = None
     if debug:
         nsamp = torch.empty((rows, W), dtype=torch.int32, device=dev)
@@ -374,17 +374,19 @@ def render_part(pov, blocks: dict, tf, params, *, band_rows: int | None = None, 
         # persistent pinned staging buffer of this thread
         stage = _pinned_stage(rows * W * 4 if host_out else 0)
         with torch.cuda.stream(s_obj):
-            stage[:32].view(torch.int64).copy_(stats, non_blocking=True)
+            stage[:48].view(torch.int64).copy_(stats, non_blocking=True)
             if host_out:
-                stage[32:32 + rows * W * 4].view(rows, W, 4).copy_(out, non_blocking=True)
+                stage[64:64 + rows * W * 4].view(rows, W, 4).copy_(out, non_blocking=True)
         s_obj.synchronize()
-        st = stage[:32].view(torch.int64).numpy().copy()
+        st = stage[:48].view(torch.int64).numpy().copy()
         if host_out:
-            out = stage[32:32 + rows * W * 4].view(rows, W, 4).clone()
+            out = stage[64:64 + rows * W * 4].view(rows, W, 4).clone()
     kms = C.c_float()
     _lib.check(_lib.lib().afam_render_elapsed(store.handle, C.byref(kms)))
     info = {"samples": int(st[0]), "missing_key": int(st[1]), "fp64_samples": int(st[2]),
-            "shaded_samples": int(st[3]), "kernel_ms": float(kms.value)}
+            "shaded_samples": int(st[3]), "exact_samples": int(st[4]),
+            "exact_cells": int(st[5]),
+            "kernel_ms": float(kms.value)}
     if raise_missing and info["missing_key"] >= 0:
         cells = C.c_int32()
         _lib.check(_lib.lib().afam_owner_grid(store.handle, sl.ctypes.data_as(C.c_void_p), len(sl), C.byref(cells),
