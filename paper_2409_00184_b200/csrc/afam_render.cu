@@ -357,10 +357,10 @@ __device__ __forceinline__ void decode_f64(const BlockLite &b, const BlockDesc *
 // prediction:
 //  - the sample count comes from one exact search per ray (t_k is monotone
 //    in k, so the alive samples are the prefix k < kend);
-//  - the finest cell of sample k is predicted as sc0 + k*dsc per axis; when
-//    every axis lies farther than `lim` from its current cell's faces the
-//    cell (hence the owner) is unchanged, otherwise the exact float64
-//    position decides (cell crossings, volume faces, rounding ties);
+//  - the finest cell is evaluated exactly at the first sample and then only
+//    at the first sample that could lie within 1e-6 cells of (or across) a
+//    face of the current cell (knext, from the per-axis cell-coordinate
+//    rate; exact_geometry); every sample in between keeps the owner;
 //  - within a block the span coordinate is tq0 + (k - k0)*dtq from the exact
 //    position at block entry k0 (error < 2e-5 spans).
 // Owner selection therefore stays bit-exact while the common sample runs
@@ -378,8 +378,7 @@ struct March {
     int32_t k, kend;
     float kf;                      // (float)k, exact below 2^24
     float C0, C1, C2, Aacc;
-    float sc0[3], dsc[3], cen[3];  // finest-cell coordinate prediction, current cell centre
-    float lim;                     // |sc - cen| < lim: same cell (0.5 - rounding margin; < 0 disables)
+    int32_t knext;                 // next sample whose finest cell is evaluated exactly
     float tq0[3], dtq[3], k0f;     // span-coordinate prediction within the current block
     int32_t own;
     uint32_t nshade, ns64, nexact, ncell;
@@ -399,12 +398,19 @@ struct BlockFast {
 };
 
 // render.py:422-428 sample position, float64 in the reference op order, and
-// its finest cell (render.py:377-380).
+// its finest cell (render.py:377-380).  Also returns knext, the first later
+// sample whose cell could differ: along each axis the cell coordinate
+// sc = ((q+1)/2)*cells moves by sd*d*cells/2 per sample, so every sample
+// before knext lies at least 1e-6 cells inside the current cell's faces --
+// far beyond the float64 rounding of the reference's expression (~1e-14) --
+// and keeps this owner; knext itself is evaluated exactly again.
 __device__ __forceinline__ void exact_geometry(const RenderArgs &A, const RayState &R, const int16_t *own_grid,
-                                               int64_t k, double (&p)[3], float (&cen)[3], int32_t &own) {
+                                               int64_t k, int32_t kend, double (&p)[3], int32_t &own,
+                                               int32_t &knext) {
     const double t = __dadd_rn(R.te, __dmul_rn((double)k + 0.5, A.sd));
     const double cellsd = (double)A.cells;
     int cidx = 0;
+    double steps = 1e18;
 #pragma unroll
     for (int a = 0; a < 3; a++) {
         double q = __dadd_rn(A.origin[a], __dmul_rn(t, R.d[a]));
@@ -413,10 +419,14 @@ __device__ __forceinline__ void exact_geometry(const RenderArgs &A, const RaySta
         const double sc = __dmul_rn(__dmul_rn(__dadd_rn(q, 1.0), 0.5), cellsd);
         int ci = __double2int_rz(sc);
         ci = min(max(ci, 0), A.cells - 1);
-        cen[a] = (float)ci + 0.5f;
         cidx = cidx * A.cells + ci;
+        const double v = A.sd * R.d[a] * (0.5 * cellsd);  // cell coordinate per sample
+        const double dist = v > 0.0 ? (double)(ci + 1) - sc : sc - (double)ci;
+        if (v != 0.0) steps = fmin(steps, (dist - 1e-6) / fabs(v));
     }
     own = own_grid[cidx];
+    const double kn = (double)k + fmax(1.0, ceil(steps));
+    knext = kn < (double)kend ? (int32_t)kn : kend;
 }
 
 __device__ __forceinline__ void exact_pos(const RenderArgs &A, const RayState &R, int64_t k, double (&p)[3]) {
@@ -425,6 +435,39 @@ __device__ __forceinline__ void exact_pos(const RenderArgs &A, const RayState &R
     for (int a = 0; a < 3; a++) {
         const double q = __dadd_rn(A.origin[a], __dmul_rn(t, R.d[a]));
         p[a] = q < -1.0 ? -1.0 : (q > 1.0 ? 1.0 : q);
+    }
+}
+
+// Paired float32 arithmetic (FFMA2/FMUL2/FADD2: two lanes of float math per
+// issue slot; the scalar weight is a broadcast operand).
+__device__ __forceinline__ float2 lo2(const float4 &v) { return make_float2(v.x, v.y); }
+__device__ __forceinline__ float2 hi2(const float4 &v) { return make_float2(v.z, v.w); }
+__device__ __forceinline__ float2 fma2s(float s, float2 x, float2 acc) { return __ffma2_rn(make_float2(s, s), x, acc); }
+__device__ __forceinline__ float2 mul2s(float s, float2 x) { return __fmul2_rn(make_float2(s, s), x); }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+
+// uniform_N (afam_eval.cuh) for two axes at once: the same operations in the
+// same order on float2 lanes, so each lane is bit-identical to uniform_N.
+template <int P>
+__device__ __forceinline__ void uniform_N2(float2 x, float2 (&N)[P + 1]) {
+    const float2 m = __ffma2_rn(x, f2(-1.f), f2(1.f));  // 1 - x
+    if (P == 1) {
+        N[0] = m;
+        N[1] = x;
+    } else if (P == 2) {
+        const float2 x2 = __fmul2_rn(x, x);
+        N[0] = __fmul2_rn(__fmul2_rn(f2(0.5f), m), m);
+        N[1] = __fadd2_rn(__ffma2_rn(f2(-1.f), x2, x), f2(0.5f));
+        N[2] = __fmul2_rn(f2(0.5f), x2);
+    } else {
+        const float2 x2 = __fmul2_rn(x, x), x3 = __fmul2_rn(x2, x), m2 = __fmul2_rn(m, m);
+        const float s6 = 1.f / 6.f;
+        N[0] = __fmul2_rn(__fmul2_rn(f2(s6), m2), m);
+        N[1] = __ffma2_rn(f2(0.5f), x3, __ffma2_rn(f2(-1.f), x2, f2(2.f / 3.f)));
+        N[2] = __ffma2_rn(f2(-0.5f), x3, __ffma2_rn(f2(0.5f), x2, __ffma2_rn(f2(0.5f), x, f2(s6))));
+        N[3] = __fmul2_rn(f2(s6), x3);
     }
 }
 
@@ -446,6 +489,27 @@ __device__ __forceinline__ bool axis_fast(const BlockFast &b, int a, float tq, i
         basis_vals_only<P, float>(t, clamp01(tq / b.nspan_f), N);
     }
     return true;
+}
+
+// axis_fast split: span and fraction (false: P = 1 within 1e-4 of a knot) ...
+template <int P>
+__device__ __forceinline__ bool axis_span(const BlockFast &b, float tq, int &k, float &fr) {
+    k = min(max(__float2int_rd(tq), 0), b.nspan - 1);
+    fr = tq - (float)k;
+    return !(P == 1 && !(fabsf(fr - 0.5f) < 0.5f - 1e-4f));
+}
+
+// ... and the table basis of a clamped boundary span (interior spans: closed form)
+template <int P>
+__device__ __forceinline__ bool span_interior(const BlockFast &b, int k) {
+    return k >= P - 1 && k <= b.nspan - P;  // none when nspan < 2p - 1
+}
+
+template <int P>
+__device__ __forceinline__ void axis_table_N(const BlockFast &b, int a, int k, float tq, float (&N)[P + 1]) {
+    Tab<float> t;
+    load_entry<P>(b.tab32 + ((size_t)a * b.nspan + k) * tab_stride(P), t);
+    basis_vals_only<P, float>(t, clamp01(tq / b.nspan_f), N);
 }
 
 template <int P>
@@ -505,41 +569,100 @@ __device__ __forceinline__ void composite(const RenderArgs &A, const float (&vdi
     M.Aacc += w;
 }
 
+// The (p+1)^3 control points of the current cell, kept in registers across
+// samples as (p+1)^2 x-quad rows (row cz*Q+by = c[x0..x0+3][y0+by][z0+cz],
+// bspline.py:175-181).  A lane re-gathers only when its owner block or one of
+// its three knot spans changed (~1 sample in 4 at LOD-2 span widths), and the
+// L1 data path serves only the lanes that reload.
+struct CellCache {
+    const float4 *key;  // x-quad row (0, 0) of the cached cell; nullptr: empty
+    float4 c[16];
+};
+
+template <int P>
+__device__ __forceinline__ void cell_gather(const BlockFast &b, int kx, int ky, int kz, CellCache &G) {
+    constexpr int Q = P + 1;
+    const float4 *base = b.ctrl4 + ((size_t)kz * b.ncp + kx) * b.ncp + ky;
+    if (base != G.key) {
+        const size_t plane = (size_t)b.ncp * b.ncp;
+#pragma unroll
+        for (int cz = 0; cz < Q; cz++)
+#pragma unroll
+            for (int by = 0; by < Q; by++) G.c[cz * Q + by] = __ldg(base + cz * plane + by);
+        G.key = base;
+    }
+}
+
+// sum_a W[a] X[a] over the x-quad components (x fastest, a = 0..P)
+template <int P>
+__device__ __forceinline__ float dot_x(const float (&W)[P + 1], float2 lo, float2 hi) {
+    float s = W[0] * lo.x;
+    s = fmaf(W[1], lo.y, s);
+    if constexpr (P >= 2) s = fmaf(W[2], hi.x, s);
+    if constexpr (P >= 3) s = fmaf(W[3], hi.y, s);
+    return s;
+}
+
+// sum_q E[q] (X[q+1] - X[q]) over the x-quad components: d/dx in difference form
+template <int P>
+__device__ __forceinline__ float ddot_x(const float (&E)[P], float2 lo, float2 hi) {
+    float s = E[0] * (lo.y - lo.x);
+    if constexpr (P >= 2) s = fmaf(E[1], hi.x - lo.y, s);
+    if constexpr (P >= 3) s = fmaf(E[2], hi.y - hi.x, s);
+    return s;
+}
+
 // One sample of a clamped-uniform float32 block from the predicted span
-// coordinates: value first (x -> y -> z, keeping the x row sums), then the TF
-// opacity; the gradient (difference form) and the colour only when the
-// opacity is positive.  Returns false when the exact path must decode it.
+// coordinates.  Value: y, then z, then x (bspline.py:214 einsum, separable),
+// on x-quad halves with paired FMAs; then the TF opacity.  Only samples the
+// TF makes non-transparent take the gradient (bspline.py:224-228) and the
+// colour: d/dx from the z-contracted quad, d/dz from the kept y partials,
+// d/dy from a z-first pass over the cached cell -- all in difference form
+// (sum E_q (c_{q+1} - c_q)), so a patch that is flat along an axis gives an
+// exactly zero derivative, as the reference's float64 gradient effectively
+// does.  Returns false when the exact path must decode the sample.
 template <int P>
 __device__ __forceinline__ bool sample_fast(const RenderArgs &A, const TfTable &tf, const BlockFast &b,
-                                            const float (&tq)[3], const float (&vdir)[3], March &M) {
+                                            const float (&tq)[3], const float (&vdir)[3], CellCache &G, March &M) {
     constexpr int Q = P + 1;
     int kx, ky, kz;
     float fx, fy, fz, Nx[Q], Ny[Q], Nz[Q];
-    if (!axis_fast<P>(b, 0, tq[0], kx, fx, Nx)) return false;
-    if (!axis_fast<P>(b, 1, tq[1], ky, fy, Ny)) return false;
-    if (!axis_fast<P>(b, 2, tq[2], kz, fz, Nz)) return false;
-    // x-quad rows (cz, by) of the (p+1)^3 patch (bspline.py:175-181)
-    const float4 *base = b.ctrl4 + ((size_t)kz * b.ncp + kx) * b.ncp + ky;
-    const size_t plane = (size_t)b.ncp * b.ncp;
-    float rx[Q][Q], ry[Q];
+    if (!axis_span<P>(b, tq[0], kx, fx) || !axis_span<P>(b, tq[1], ky, fy) || !axis_span<P>(b, tq[2], kz, fz))
+        return false;
+    cell_gather<P>(b, kx, ky, kz, G);
+    {  // x and y closed forms paired, z alone; boundary spans from the table
+        float2 Nxy[Q];
+        uniform_N2<P>(make_float2(fx, fy), Nxy);
+#pragma unroll
+        for (int i = 0; i < Q; i++) {
+            Nx[i] = Nxy[i].x;
+            Ny[i] = Nxy[i].y;
+        }
+        if (!span_interior<P>(b, kx)) axis_table_N<P>(b, 0, kx, tq[0], Nx);
+        if (!span_interior<P>(b, ky)) axis_table_N<P>(b, 1, ky, tq[1], Ny);
+        if (span_interior<P>(b, kz)) uniform_N<P>(fz, Nz);
+        else axis_table_N<P>(b, 2, kz, tq[2], Nz);
+    }
+    // Y[cz] = sum_by Ny[by] c[cz][by] (x-quad), Z = sum_cz Nz[cz] Y[cz]
+    float2 Ylo[Q], Yhi[Q], Zlo, Zhi;
 #pragma unroll
     for (int cz = 0; cz < Q; cz++) {
-        float ay = 0.f;
+        Ylo[cz] = mul2s(Ny[0], lo2(G.c[cz * Q]));
+        Yhi[cz] = mul2s(Ny[0], hi2(G.c[cz * Q]));
 #pragma unroll
-        for (int by = 0; by < Q; by++) {
-            const float4 r = __ldg(base + cz * plane + by);
-            float acc = Nx[0] * r.x;
-            acc = fmaf(Nx[1], r.y, acc);
-            if constexpr (P >= 2) acc = fmaf(Nx[2], r.z, acc);
-            if constexpr (P >= 3) acc = fmaf(Nx[3], r.w, acc);
-            rx[cz][by] = acc;
-            ay = fmaf(Ny[by], acc, ay);
+        for (int by = 1; by < Q; by++) {
+            Ylo[cz] = fma2s(Ny[by], lo2(G.c[cz * Q + by]), Ylo[cz]);
+            Yhi[cz] = fma2s(Ny[by], hi2(G.c[cz * Q + by]), Yhi[cz]);
         }
-        ry[cz] = ay;
     }
-    float v = 0.f;
+    Zlo = mul2s(Nz[0], Ylo[0]);
+    Zhi = mul2s(Nz[0], Yhi[0]);
 #pragma unroll
-    for (int cz = 0; cz < Q; cz++) v = fmaf(Nz[cz], ry[cz], v);
+    for (int cz = 1; cz < Q; cz++) {
+        Zlo = fma2s(Nz[cz], Ylo[cz], Zlo);
+        Zhi = fma2s(Nz[cz], Yhi[cz], Zhi);
+    }
+    const float v = dot_x<P>(Nx, Zlo, Zhi);
     int bi;
     float bf;
     const float vc = fminf(fmaxf(v, A.dom_lo), A.dom_hi);
@@ -550,25 +673,35 @@ __device__ __forceinline__ bool sample_fast(const RenderArgs &A, const TfTable &
     axis_fast_E<P>(b, 0, kx, fx, Ex);
     axis_fast_E<P>(b, 1, ky, fy, Ey);
     axis_fast_E<P>(b, 2, kz, fz, Ez);
-    float gx = 0.f, gy = 0.f, gz = 0.f;
+    const float gx = ddot_x<P>(Ex, Zlo, Zhi);
+    // d/dz: sum_q Ez[q] (Y[q+1] - Y[q]), then x
+    float2 Dlo = mul2s(Ez[0], sub2(Ylo[1], Ylo[0])), Dhi = mul2s(Ez[0], sub2(Yhi[1], Yhi[0]));
 #pragma unroll
-    for (int cz = 0; cz < Q; cz++) {
-        float adxy = 0.f, ady = 0.f;
-#pragma unroll
-        for (int by = 0; by < Q; by++) {
-            const float4 r = __ldg(base + cz * plane + by);  // L1 hit
-            float dacc = Ex[0] * (r.y - r.x);
-            if constexpr (P >= 2) dacc = fmaf(Ex[1], r.z - r.y, dacc);
-            if constexpr (P >= 3) dacc = fmaf(Ex[2], r.w - r.z, dacc);
-            adxy = fmaf(Ny[by], dacc, adxy);
-        }
-#pragma unroll
-        for (int q = 0; q < P; q++) ady = fmaf(Ey[q], rx[cz][q + 1] - rx[cz][q], ady);
-        gx = fmaf(Nz[cz], adxy, gx);
-        gy = fmaf(Nz[cz], ady, gy);
+    for (int q = 1; q < P; q++) {
+        Dlo = fma2s(Ez[q], sub2(Ylo[q + 1], Ylo[q]), Dlo);
+        Dhi = fma2s(Ez[q], sub2(Yhi[q + 1], Yhi[q]), Dhi);
     }
+    const float gz = dot_x<P>(Nx, Dlo, Dhi);
+    // d/dy: W[by] = sum_cz Nz[cz] c[cz][by]; sum_q Ey[q] (W[q+1] - W[q]), then x
+    float2 Wlo[Q], Whi[Q];
 #pragma unroll
-    for (int q = 0; q < P; q++) gz = fmaf(Ez[q], ry[q + 1] - ry[q], gz);
+    for (int by = 0; by < Q; by++) {
+        Wlo[by] = mul2s(Nz[0], lo2(G.c[by]));
+        Whi[by] = mul2s(Nz[0], hi2(G.c[by]));
+#pragma unroll
+        for (int cz = 1; cz < Q; cz++) {
+            Wlo[by] = fma2s(Nz[cz], lo2(G.c[cz * Q + by]), Wlo[by]);
+            Whi[by] = fma2s(Nz[cz], hi2(G.c[cz * Q + by]), Whi[by]);
+        }
+    }
+    Dlo = mul2s(Ey[0], sub2(Wlo[1], Wlo[0]));
+    Dhi = mul2s(Ey[0], sub2(Whi[1], Whi[0]));
+#pragma unroll
+    for (int q = 1; q < P; q++) {
+        Dlo = fma2s(Ey[q], sub2(Wlo[q + 1], Wlo[q]), Dlo);
+        Dhi = fma2s(Ey[q], sub2(Whi[q + 1], Whi[q]), Dhi);
+    }
+    const float gy = dot_x<P>(Nx, Dlo, Dhi);
     // model.py:79 gradient / span
     const float g[3] = {gx * b.inv_span_f[0], gy * b.inv_span_f[1], gz * b.inv_span_f[2]};
     composite(A, vdir, tf_color(tf, vc, bi, bf, atf), g, M);
@@ -608,7 +741,7 @@ __device__ __noinline__ int sample_exact(const RenderArgs *GA, const TfTable *tf
     return f64 ? 1 : 0;
 }
 
-template <bool DEBUG, bool SMEM_GRID, int MINB>
+template <bool DEBUG, bool SMEM_GRID, int FD, int MINB>
 __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__restrict__ descs,
                                                         const int16_t *__restrict__ grid,
                                                         const int32_t *__restrict__ idx2slot, const RenderArgs A,
@@ -684,23 +817,17 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
         while (ke > 0 && !(tk(ke - 1) < tx)) --ke;
         while (tk(ke) < tx) ++ke;
         M.kend = (int32_t)min(ke, (int64_t)INT32_MAX);
-        // predicted finest-cell coordinate sc(k) = sc0 + k dsc; the margin
-        // covers float32 rounding of sc0, dsc and the fma (K2)
-        const double hc = 0.5 * (double)A.cells;
-        const double t0 = tk(0);
-#pragma unroll
-        for (int a = 0; a < 3; a++) {
-            M.sc0[a] = (float)((A.origin[a] + t0 * d[a] + 1.0) * hc);
-            M.dsc[a] = (float)(A.sd * d[a] * hc);
-        }
-        M.lim = ke < (1 << 24) ? 0.5f - (1e-5f + 1e-6f * (float)A.cells) : -1.f;
+        // the float32 sample index kf and span prediction need k < 2^24
+        const bool k24 = ke < (1 << 24);
         {
             double p[3];
-            exact_geometry(A, R, own_grid, 0, p, M.cen, M.own);
+            exact_geometry(A, R, own_grid, 0, M.kend, p, M.own, M.knext);
         }
         int32_t cur_own = -1, slot = -1, deg = 0;
         BlockFast b;
         bool fast = false;
+        CellCache G;
+        G.key = nullptr;
         while (M.k < M.kend) {
             if (M.own < 0) {  // render.py:430-436
                 miss = ((int64_t)M.k << 32) | ray;
@@ -717,8 +844,8 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
                 b.nspan_f = (float)b.nspan;
                 deg = __ldg(&dp->deg);
                 const uint32_t flags = __ldg(&dp->flags);
-                fast = (flags & kFlagUniform) && !(flags & AFAM_SLOT_FP64) && (deg > 1 || b.nspan <= 128) &&
-                       M.lim > 0.f && !(A.flags & kRenderForceExact);
+                fast = deg == FD && (flags & kFlagUniform) && !(flags & AFAM_SLOT_FP64) && (deg > 1 || b.nspan <= 128) &&
+                       k24 && !(A.flags & kRenderForceExact);
                 // span-coordinate prediction from the exact entry position
                 double p[3];
                 exact_pos(A, R, M.k, p);
@@ -739,9 +866,7 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
                 const float dk = M.kf - M.k0f;
                 const float tq[3] = {fmaf(dk, M.dtq[0], M.tq0[0]), fmaf(dk, M.dtq[1], M.tq0[1]),
                                      fmaf(dk, M.dtq[2], M.tq0[2])};
-                if (deg == 3) ok = sample_fast<3>(A, tf, b, tq, vdir, M);
-                else if (deg == 2) ok = sample_fast<2>(A, tf, b, tq, vdir, M);
-                else ok = sample_fast<1>(A, tf, b, tq, vdir, M);
+                ok = sample_fast<FD>(A, tf, b, tq, vdir, G, M);
             }
             if (!ok) {
                 const BlockDesc *dpx = descs + slot;
@@ -762,13 +887,10 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
             ++M.k;
             M.kf += 1.f;
             if (M.k >= M.kend || !(M.Aacc <= A.o_max_f)) break;
-            bool same = true;
-#pragma unroll
-            for (int a = 0; a < 3; a++) same &= fabsf(fmaf(M.kf, M.dsc[a], M.sc0[a]) - M.cen[a]) < M.lim;
-            if (!same) {
+            if (M.k >= M.knext) {
                 double p[3];
                 ++M.ncell;
-                exact_geometry(A, R, own_grid, M.k, p, M.cen, M.own);
+                exact_geometry(A, R, own_grid, M.k, M.kend, p, M.own, M.knext);
             }
         }
     }
@@ -928,14 +1050,14 @@ static int build_owner_grid(afam_store *s, const int32_t *slots, int32_t nb, int
 
 constexpr int kSmemGridMaxCells = 24;  // 24^3 int16 = 27 KB
 
-// Resident CTAs per SM the kernel is compiled for (register budget
-// 65536/(128*MINB)); AFAM_RENDER_MINB=2|3|4 selects the variant (default 4:
-// 128 registers, 16 warps/SM, measured fastest on B200).
+// CTAs per SM the register allocation is sized for (launch bounds), per
+// fast-path degree: the cubic path keeps the cell's 64 control points in
+// registers.  AFAM_RENDER_MINB=2|3|4 overrides it for the cubic kernel.
 static int render_minb() {
     static int v = [] {
         const char *e = getenv("AFAM_RENDER_MINB");
         const int m = e ? atoi(e) : 0;
-        return (m == 3 || m == 5 || m == 6) ? m : 4;
+        return (m == 2 || m == 4) ? m : 3;
     }();
     return v;
 }
@@ -955,24 +1077,29 @@ struct LaunchArgs {
     uint64_t *ohash;
 };
 
-template <bool DEBUG, bool SMEM, int MINB>
+template <bool DEBUG, bool SMEM, int FD, int MINB>
 static void launch_render_v(const LaunchArgs &L, const RenderArgs &A) {
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(render_kernel<DEBUG, SMEM, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        cudaFuncSetAttribute(render_kernel<DEBUG, SMEM, FD, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             64 * 1024);
         configured = true;
     }
-    render_kernel<DEBUG, SMEM, MINB><<<L.grid, 128, L.smem, L.st>>>(L.descs, L.owner, L.idx, A, L.gargs, L.gtf,
-                                                                    L.rgba, L.stats, L.nsamp, L.ohash);
+    render_kernel<DEBUG, SMEM, FD, MINB><<<L.grid, 128, L.smem, L.st>>>(L.descs, L.owner, L.idx, A, L.gargs, L.gtf,
+                                                                        L.rgba, L.stats, L.nsamp, L.ohash);
 }
 
+// fd: the degree the fast path is compiled for (blocks of other degrees take
+// the exact path); debug and non-shared-grid launches use the default bounds.
 template <bool DEBUG, bool SMEM>
-static void launch_render(const LaunchArgs &L, const RenderArgs &A) {
+static void launch_render(const LaunchArgs &L, const RenderArgs &A, int fd) {
+    if (fd == 1) return launch_render_v<DEBUG, SMEM, 1, 4>(L, A);
+    if (fd == 2) return launch_render_v<DEBUG, SMEM, 2, 4>(L, A);
+    if (DEBUG || !SMEM) return launch_render_v<DEBUG, SMEM, 3, 3>(L, A);
     switch (render_minb()) {
-        case 3: launch_render_v<DEBUG, SMEM, 3>(L, A); break;
-        case 5: launch_render_v<DEBUG, SMEM, 5>(L, A); break;
-        case 6: launch_render_v<DEBUG, SMEM, 6>(L, A); break;
-        default: launch_render_v<DEBUG, SMEM, 4>(L, A); break;
+        case 2: launch_render_v<DEBUG, SMEM, 3, 2>(L, A); break;
+        case 4: launch_render_v<DEBUG, SMEM, 3, 4>(L, A); break;
+        default: launch_render_v<DEBUG, SMEM, 3, 3>(L, A); break;
     }
 }
 
@@ -1071,11 +1198,15 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
 
     std::vector<int16_t> grid;
     int32_t cells = 1;
+    int fd = 3;  // fast-path degree: the most common degree among the blocks
     {
         std::lock_guard<std::mutex> lk(s->mu);
         int rc = build_owner_grid(s, slots, nblocks, cells, grid);
         if (rc) return rc;
         for (int b = 0; b < nblocks; b++) AFAM_CUDA(wait_slot(s, slots[b], st));
+        int cnt[4] = {0, 0, 0, 0};
+        for (int b = 0; b < nblocks; b++) cnt[std::min(std::max((int)s->host[slots[b]].deg, 1), 3)]++;
+        fd = cnt[3] >= cnt[2] && cnt[3] >= cnt[1] ? 3 : (cnt[2] >= cnt[1] ? 2 : 1);
     }
     A.cells = cells;
     A.nb = nblocks;
@@ -1111,11 +1242,11 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
         L.nsamp = nsamp;
         L.ohash = ohash;
         if (debug) {
-            if (sg) launch_render<true, true>(L, A);
-            else launch_render<true, false>(L, A);
+            if (sg) launch_render<true, true>(L, A, fd);
+            else launch_render<true, false>(L, A, fd);
         } else {
-            if (sg) launch_render<false, true>(L, A);
-            else launch_render<false, false>(L, A);
+            if (sg) launch_render<false, true>(L, A, fd);
+            else launch_render<false, false>(L, A, fd);
         }
     }
     finish_stats_kernel<<<1, 1, 0, st>>>(stats);
