@@ -381,7 +381,7 @@ struct March {
     int32_t knext;                 // next sample whose finest cell is evaluated exactly
     float tq0[3], dtq[3], k0f;     // span-coordinate prediction within the current block
     int32_t own;
-    uint32_t nshade, ns64, nexact, ncell;
+    uint32_t nshade;
     uint64_t h;
 };
 
@@ -392,9 +392,17 @@ constexpr uint32_t kRenderForceExact = 0x100u;
 
 struct BlockFast {
     const float4 *ctrl4;
-    const float *tab32;
     int32_t ncp, nspan;
-    float nspan_f, inv_span_f[3];
+};
+
+// Per-thread state the sample loop reads rarely (shading, boundary spans,
+// counters of the rare paths), kept in shared memory so the registers go to
+// the cached cell and the per-sample state.
+struct alignas(16) ThreadCold {
+    float4 vdir;         // ray direction (float32), for shading
+    float4 ginv;         // 1/span per axis of the owner block (model.py:79)
+    const float *tab32;  // owner block's per-span basis tables
+    uint32_t ns64, nexact, ncell;
 };
 
 // render.py:422-428 sample position, float64 in the reference op order, and
@@ -476,22 +484,10 @@ __device__ __forceinline__ void uniform_N2(float2 x, float2 (&N)[P + 1]) {
 // clamped-uniform model use the closed form, the 2(p-1) boundary spans the
 // per-span table.  Returns false (P = 1 only) within 1e-4 of a knot, where
 // the gradient is discontinuous and the exact span must be searched.
-template <int P>
-__device__ __forceinline__ bool axis_fast(const BlockFast &b, int a, float tq, int &k, float &fr, float (&N)[P + 1]) {
-    k = min(max(__float2int_rd(tq), 0), b.nspan - 1);
-    fr = tq - (float)k;
-    if (P == 1 && !(fabsf(fr - 0.5f) < 0.5f - 1e-4f)) return false;
-    if (k >= P - 1 && k <= b.nspan - P) {  // interior span (none when nspan < 2p - 1)
-        uniform_N<P>(fr, N);
-    } else {
-        Tab<float> t;
-        load_entry<P>(b.tab32 + ((size_t)a * b.nspan + k) * tab_stride(P), t);
-        basis_vals_only<P, float>(t, clamp01(tq / b.nspan_f), N);
-    }
-    return true;
-}
-
-// axis_fast split: span and fraction (false: P = 1 within 1e-4 of a knot) ...
+// Per-axis span of the fast path from the predicted span coordinate tq:
+// span k = floor(tq) (clamped), fraction fr; false (P = 1 only) within 1e-4
+// of a knot, where the gradient is discontinuous and the exact span must be
+// searched ...
 template <int P>
 __device__ __forceinline__ bool axis_span(const BlockFast &b, float tq, int &k, float &fr) {
     k = min(max(__float2int_rd(tq), 0), b.nspan - 1);
@@ -499,28 +495,32 @@ __device__ __forceinline__ bool axis_span(const BlockFast &b, float tq, int &k, 
     return !(P == 1 && !(fabsf(fr - 0.5f) < 0.5f - 1e-4f));
 }
 
-// ... and the table basis of a clamped boundary span (interior spans: closed form)
+// ... interior spans of a clamped-uniform model use the closed form, the
+// 2(p-1) boundary spans the per-span table
 template <int P>
 __device__ __forceinline__ bool span_interior(const BlockFast &b, int k) {
     return k >= P - 1 && k <= b.nspan - P;  // none when nspan < 2p - 1
 }
 
 template <int P>
-__device__ __forceinline__ void axis_table_N(const BlockFast &b, int a, int k, float tq, float (&N)[P + 1]) {
+__device__ __forceinline__ void axis_table_N(const BlockFast &b, const ThreadCold &C, int a, int k, float tq,
+                                             float (&N)[P + 1]) {
     Tab<float> t;
-    load_entry<P>(b.tab32 + ((size_t)a * b.nspan + k) * tab_stride(P), t);
-    basis_vals_only<P, float>(t, clamp01(tq / b.nspan_f), N);
+    load_entry<P>(C.tab32 + ((size_t)a * b.nspan + k) * tab_stride(P), t);
+    basis_vals_only<P, float>(t, clamp01(tq / (float)b.nspan), N);
 }
 
 template <int P>
-__device__ __forceinline__ void axis_fast_E(const BlockFast &b, int a, int k, float fr, float (&E)[P]) {
+__device__ __forceinline__ void axis_fast_E(const BlockFast &b, const ThreadCold &C, int a, int k, float fr,
+                                            float (&E)[P]) {
+    const float nsf = (float)b.nspan;
     if (k >= P - 1 && k <= b.nspan - P) {  // interior span (none when nspan < 2p - 1)
-        uniform_E<P>(fr, b.nspan_f, E);
+        uniform_E<P>(fr, nsf, E);
     } else {
         Tab<float> t;
         float N[P + 1];
-        load_entry<P>(b.tab32 + ((size_t)a * b.nspan + k) * tab_stride(P), t);
-        basis_eval<P, float>(t, clamp01(((float)k + fr) / b.nspan_f), N, E);
+        load_entry<P>(C.tab32 + ((size_t)a * b.nspan + k) * tab_stride(P), t);
+        basis_eval<P, float>(t, clamp01(((float)k + fr) / nsf), N, E);
     }
 }
 
@@ -547,15 +547,15 @@ __device__ __forceinline__ float4 tf_color(const TfTable &T, float v, int bi, fl
 }
 
 // Shading and compositing of one sample (render.py:383-395, :451-455).
-__device__ __forceinline__ void composite(const RenderArgs &A, const float (&vdir)[3], float4 tfv,
-                                          const float (&g)[3], March &M) {
+__device__ __forceinline__ void composite(const RenderArgs &A, const float4 vdir, float4 tfv, const float (&g)[3],
+                                          March &M) {
     const float atf = tfv.w;
     const float as = A.power_one ? 1.f - (1.f - atf) : 1.f - __powf(1.f - atf, A.power);
     const float gn2 = fmaf(g[2], g[2], fmaf(g[1], g[1], g[0] * g[0]));
     float ndotl = 0.f;
     if (gn2 > 1e-24f) {
         const float ig = rsqrtf(gn2);
-        ndotl = fabsf(g[0] * vdir[0] + g[1] * vdir[1] + g[2] * vdir[2]) * ig;
+        ndotl = fabsf(g[0] * vdir.x + g[1] * vdir.y + g[2] * vdir.z) * ig;
     }
     const float dif = A.diffuse * ndotl;
     // ndotl**shininess via exp2(shininess * log2(ndotl)) (MUFU.LG2 + MUFU.EX2)
@@ -623,7 +623,7 @@ __device__ __forceinline__ float ddot_x(const float (&E)[P], float2 lo, float2 h
 // does.  Returns false when the exact path must decode the sample.
 template <int P>
 __device__ __forceinline__ bool sample_fast(const RenderArgs &A, const TfTable &tf, const BlockFast &b,
-                                            const float (&tq)[3], const float (&vdir)[3], CellCache &G, March &M) {
+                                            const float (&tq)[3], const ThreadCold &C, CellCache &G, March &M) {
     constexpr int Q = P + 1;
     int kx, ky, kz;
     float fx, fy, fz, Nx[Q], Ny[Q], Nz[Q];
@@ -638,10 +638,10 @@ __device__ __forceinline__ bool sample_fast(const RenderArgs &A, const TfTable &
             Nx[i] = Nxy[i].x;
             Ny[i] = Nxy[i].y;
         }
-        if (!span_interior<P>(b, kx)) axis_table_N<P>(b, 0, kx, tq[0], Nx);
-        if (!span_interior<P>(b, ky)) axis_table_N<P>(b, 1, ky, tq[1], Ny);
+        if (!span_interior<P>(b, kx)) axis_table_N<P>(b, C, 0, kx, tq[0], Nx);
+        if (!span_interior<P>(b, ky)) axis_table_N<P>(b, C, 1, ky, tq[1], Ny);
         if (span_interior<P>(b, kz)) uniform_N<P>(fz, Nz);
-        else axis_table_N<P>(b, 2, kz, tq[2], Nz);
+        else axis_table_N<P>(b, C, 2, kz, tq[2], Nz);
     }
     // Y[cz] = sum_by Ny[by] c[cz][by] (x-quad), Z = sum_cz Nz[cz] Y[cz]
     float2 Ylo[Q], Yhi[Q], Zlo, Zhi;
@@ -670,9 +670,9 @@ __device__ __forceinline__ bool sample_fast(const RenderArgs &A, const TfTable &
     if (!(atf > 0.f)) return true;  // a_s = 0: the sample changes neither C nor A
     ++M.nshade;
     float Ex[P], Ey[P], Ez[P];
-    axis_fast_E<P>(b, 0, kx, fx, Ex);
-    axis_fast_E<P>(b, 1, ky, fy, Ey);
-    axis_fast_E<P>(b, 2, kz, fz, Ez);
+    axis_fast_E<P>(b, C, 0, kx, fx, Ex);
+    axis_fast_E<P>(b, C, 1, ky, fy, Ey);
+    axis_fast_E<P>(b, C, 2, kz, fz, Ez);
     const float gx = ddot_x<P>(Ex, Zlo, Zhi);
     // d/dz: sum_q Ez[q] (Y[q+1] - Y[q]), then x
     float2 Dlo = mul2s(Ez[0], sub2(Ylo[1], Ylo[0])), Dhi = mul2s(Ez[0], sub2(Yhi[1], Yhi[0]));
@@ -703,8 +703,9 @@ __device__ __forceinline__ bool sample_fast(const RenderArgs &A, const TfTable &
     }
     const float gy = dot_x<P>(Nx, Dlo, Dhi);
     // model.py:79 gradient / span
-    const float g[3] = {gx * b.inv_span_f[0], gy * b.inv_span_f[1], gz * b.inv_span_f[2]};
-    composite(A, vdir, tf_color(tf, vc, bi, bf, atf), g, M);
+    const float4 gi = C.ginv;
+    const float g[3] = {gx * gi.x, gy * gi.y, gz * gi.z};
+    composite(A, C.vdir, tf_color(tf, vc, bi, bf, atf), g, M);
     return true;
 }
 
@@ -755,7 +756,8 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
     // so L1 keeps the most room for control-point rows; GA: the launch
     // arguments in global memory, for the out-of-line exact path
     const TfTable &tf = *gtf;
-    int16_t *sgrid = reinterpret_cast<int16_t *>(smem);
+    ThreadCold &C = reinterpret_cast<ThreadCold *>(smem)[threadIdx.x];
+    int16_t *sgrid = reinterpret_cast<int16_t *>(smem + 128 * sizeof(ThreadCold));
     if (SMEM_GRID)
         for (int i = threadIdx.x; i < A.cells * A.cells * A.cells; i += blockDim.x) sgrid[i] = grid[i];
     __syncthreads();
@@ -767,7 +769,6 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
     const int lr = blockIdx.y * 8 + (warp >> 1) * 4 + (lane >> 3);
     const bool inside = j < A.width && lr < A.rows;
     const int i = inside ? frame_row(A, lr) : 0;
-    const int64_t ray = (int64_t)i * A.width + j;  // full-frame ray id (render.py:407)
 
     // _ray_grid (render.py:332-337): exact op order, no contraction
     const double xs = __dsub_rn(__dmul_rn(__ddiv_rn((double)j, (double)A.width), 2.0), 1.0);
@@ -799,16 +800,16 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
     for (int a = 0; a < 3; a++) R.d[a] = d[a];
     R.te = te;
 
-    const float vdir[3] = {(float)d[0], (float)d[1], (float)d[2]};
+    C.vdir = make_float4((float)d[0], (float)d[1], (float)d[2], 0.f);
+    C.ns64 = C.nexact = C.ncell = 0;
     March M;
     M.k = 0;
     M.kend = 0;
     M.kf = 0.f;
     M.C0 = M.C1 = M.C2 = M.Aacc = 0.f;
-    M.nshade = M.ns64 = M.nexact = M.ncell = 0;
+    M.nshade = 0;
     M.h = 1469598103934665603ULL;
     M.own = -1;
-    int64_t miss = INT64_MAX;
 
     if (active) {
         // alive samples: t_k = te + (k + 0.5) sd < tx, a prefix of k (render.py:423)
@@ -829,19 +830,15 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
         CellCache G;
         G.key = nullptr;
         while (M.k < M.kend) {
-            if (M.own < 0) {  // render.py:430-436
-                miss = ((int64_t)M.k << 32) | ray;
-                break;
-            }
+            if (M.own < 0) break;  // render.py:430-436 (reported after the loop)
             if (M.own != cur_own) {
                 cur_own = M.own;
                 slot = __ldg(idx2slot + cur_own);
                 const BlockDesc *dp = descs + slot;
                 b.ctrl4 = (const float4 *)__ldg((const unsigned long long *)&dp->ctrl4);
-                b.tab32 = (const float *)__ldg((const unsigned long long *)&dp->tab32);
+                C.tab32 = (const float *)__ldg((const unsigned long long *)&dp->tab32);
                 b.ncp = __ldg(&dp->ncp);
                 b.nspan = __ldg(&dp->nspan);
-                b.nspan_f = (float)b.nspan;
                 deg = __ldg(&dp->deg);
                 const uint32_t flags = __ldg(&dp->flags);
                 fast = deg == FD && (flags & kFlagUniform) && !(flags & AFAM_SLOT_FP64) && (deg > 1 || b.nspan <= 128) &&
@@ -851,11 +848,12 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
                 exact_pos(A, R, M.k, p);
 #pragma unroll
                 for (int a = 0; a < 3; a++) {
-                    b.inv_span_f[a] = __ldg(&dp->inv_span_f[a]);
                     const double sc = __ldg(&dp->inv_span[a]) * (double)b.nspan;
                     M.tq0[a] = (float)((p[a] - __ldg(&dp->lo[a])) * sc);
-                    M.dtq[a] = (float)(A.sd * d[a] * sc);
+                    M.dtq[a] = (float)(A.sd * R.d[a] * sc);
                 }
+                C.ginv = make_float4(__ldg(&dp->inv_span_f[0]), __ldg(&dp->inv_span_f[1]),
+                                     __ldg(&dp->inv_span_f[2]), 0.f);
                 M.k0f = M.kf;
             }
             // one sample per iteration (a flat loop keeps the lanes of a warp
@@ -866,7 +864,7 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
                 const float dk = M.kf - M.k0f;
                 const float tq[3] = {fmaf(dk, M.dtq[0], M.tq0[0]), fmaf(dk, M.dtq[1], M.tq0[1]),
                                      fmaf(dk, M.dtq[2], M.tq0[2])};
-                ok = sample_fast<FD>(A, tf, b, tq, vdir, G, M);
+                ok = sample_fast<FD>(A, tf, b, tq, C, G, M);
             }
             if (!ok) {
                 const BlockDesc *dpx = descs + slot;
@@ -874,13 +872,13 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
                 if (deg == 3) f64 = sample_exact<3>(GA, &tf, &R, dpx, slot, M.k);
                 else if (deg == 2) f64 = sample_exact<2>(GA, &tf, &R, dpx, slot, M.k);
                 else f64 = sample_exact<1>(GA, &tf, &R, dpx, slot, M.k);
-                M.ns64 += f64;
-                ++M.nexact;
+                C.ns64 += f64;
+                ++C.nexact;
                 const float4 tfv = R.tfv;
                 if (tfv.w > 0.f) {
                     ++M.nshade;
                     const float g[3] = {R.g[0], R.g[1], R.g[2]};
-                    composite(A, vdir, tfv, g, M);
+                    composite(A, C.vdir, tfv, g, M);
                 }
             }
             // render.py:423 alive test before the next sample
@@ -889,7 +887,7 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
             if (M.k >= M.kend || !(M.Aacc <= A.o_max_f)) break;
             if (M.k >= M.knext) {
                 double p[3];
-                ++M.ncell;
+                ++C.ncell;
                 exact_geometry(A, R, own_grid, M.k, M.kend, p, M.own, M.knext);
             }
         }
@@ -911,11 +909,12 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
     }
     // per-warp reductions of the counters
     const uint32_t wsum = __reduce_add_sync(0xffffffffu, ns);
-    const uint32_t wsum64 = __reduce_add_sync(0xffffffffu, M.ns64);
+    const uint32_t wsum64 = __reduce_add_sync(0xffffffffu, C.ns64);
     const uint32_t wshade = __reduce_add_sync(0xffffffffu, M.nshade);
-    const uint32_t wexact = __reduce_add_sync(0xffffffffu, M.nexact);
-    const uint32_t wcell = __reduce_add_sync(0xffffffffu, M.ncell);
-    int64_t wmiss = miss;
+    const uint32_t wexact = __reduce_add_sync(0xffffffffu, C.nexact);
+    const uint32_t wcell = __reduce_add_sync(0xffffffffu, C.ncell);
+    // the march stopped at a sample without a resident owner: (step, full-frame ray id)
+    int64_t wmiss = M.own < 0 && M.k < M.kend ? ((int64_t)M.k << 32) | ((int64_t)i * A.width + j) : INT64_MAX;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         const int64_t other = __shfl_xor_sync(0xffffffffu, wmiss, o);
@@ -1230,7 +1229,7 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
         LaunchArgs L;
         L.grid = dim3((A.width + 15) / 16, (A.rows + 7) / 8);
         const bool sg = cells <= kSmemGridMaxCells;
-        L.smem = sg ? gbytes : 0;
+        L.smem = 128 * sizeof(ThreadCold) + (sg ? gbytes : 0);
         L.st = st;
         L.descs = s->d_desc;
         L.owner = (const int16_t *)(d_pack + off_grid);
