@@ -171,8 +171,10 @@ typedef struct {
 /*
  * render.render for the resident blocks slots[0..nblocks) given in sorted
  * BlockAddress order (host array; the finest-cell owner grid of
- * render.py:357-375 is built from their extents).  rgba: device uint8
- * buffer of (rows rendered) x width x 4.  stats: device afam_render_stats
+ * render.py:357-375 is built from their extents).  rgba: uint8 buffer of
+ * (rows rendered) x width x 4, in device memory or in pinned host memory
+ * (cudaHostAlloc; the kernel then writes the pixels straight over the host
+ * link while it marches, so no separate copy-out follows).  stats: device afam_render_stats
  * (zeroed by this call).  Debug (flags & AFAM_RENDER_DEBUG): nsamp[ray]
  * int32 and ohash[ray] uint64 (FNV-1a over owner indices) device buffers.
  */

@@ -77,6 +77,10 @@ struct afam_store {
     float *d_maxabs = nullptr;           // nslots (device)
     std::vector<afam::SlotHost> host;
     cudaEvent_t ev_k0 = nullptr, ev_k1 = nullptr;  // bracket the last afam_render's kernels
+    unsigned char *h_pack = nullptr;                // pinned staging of afam_render's per-frame upload
+    size_t h_pack_cap = 0;
+    cudaEvent_t ev_pack = nullptr;                  // the last upload out of h_pack
+    std::mutex pack_mu;                             // h_pack is shared by concurrent afam_render calls
     std::mutex mu;
     std::map<std::tuple<int, int, int>, afam::DecodeOp> ops;
 

@@ -30,6 +30,32 @@
 
 #include "afam_eval.cuh"
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
+// AFAM_HOST_TIMING=1: per-call host phase times of afam_render on stderr.
+struct HostTimer {
+    static bool on() {
+        static const bool v = [] {
+            const char *e = getenv("AFAM_HOST_TIMING");
+            return e && atoi(e) != 0;
+        }();
+        return v;
+    }
+    std::chrono::steady_clock::time_point t[8];
+    int n = 0;
+    HostTimer() { if (on()) t[n++] = std::chrono::steady_clock::now(); }
+    void mark() { if (on() && n < 8) t[n++] = std::chrono::steady_clock::now(); }
+    void report(const char *what) const {
+        if (!on()) return;
+        fprintf(stderr, "[%s]", what);
+        for (int i = 1; i < n; i++)
+            fprintf(stderr, " %.3f", std::chrono::duration<double, std::milli>(t[i] - t[i - 1]).count());
+        fprintf(stderr, " ms\n");
+    }
+};
+
 namespace afam {
 
 constexpr int kTfMaxBp = 2 * AFAM_MAX_TF_POINTS;
@@ -1149,7 +1175,9 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
     const int nparts = F->nparts > 0 ? F->nparts : 1;
     AFAM_CHECK(F->part >= 0 && F->part < nparts, AFAM_E_VALUE, "part %d outside [0, %d)", F->part, nparts);
     cudaStream_t st = (cudaStream_t)stream;
+    HostTimer ht;
     AFAM_CUDA(cudaSetDevice(s->device));
+    ht.mark();
 
     RenderArgs A;
     memset(&A, 0, sizeof(A));
@@ -1194,6 +1222,7 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
     TfTable tf;
     memset(&tf, 0, sizeof(tf));
     build_tf_table(F, tf);
+    ht.mark();
 
     std::vector<int16_t> grid;
     int32_t cells = 1;
@@ -1207,6 +1236,7 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
         for (int b = 0; b < nblocks; b++) cnt[std::min(std::max((int)s->host[slots[b]].deg, 1), 3)]++;
         fd = cnt[3] >= cnt[2] && cnt[3] >= cnt[1] ? 3 : (cnt[2] >= cnt[1] ? 2 : 1);
     }
+    ht.mark();
     A.cells = cells;
     A.nb = nblocks;
     // one upload: [RenderArgs | TfTable | owner grid | slot of each owner index]
@@ -1215,14 +1245,32 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
     const size_t off_tf = al(sizeof(RenderArgs)), off_grid = off_tf + al(sizeof(TfTable));
     const size_t off_idx = off_grid + al(gbytes);
     const size_t total = off_idx + std::max<size_t>(1, (size_t)nblocks) * sizeof(int32_t);
-    std::vector<unsigned char> pack(total, 0);
-    memcpy(pack.data(), &A, sizeof(A));
-    memcpy(pack.data() + off_tf, &tf, sizeof(tf));
-    memcpy(pack.data() + off_grid, grid.data(), gbytes);
-    if (nblocks) memcpy(pack.data() + off_idx, slots, (size_t)nblocks * sizeof(int32_t));
+    // staged in the store's pinned buffer, so the H2D copy is asynchronous
+    // (a pageable source would block until the stream drains); the previous
+    // frame's copy out of it is fenced by ev_pack
+    std::lock_guard<std::mutex> plk(s->pack_mu);
+    ht.mark();
+    if (s->h_pack_cap < total) {
+        AFAM_CUDA(cudaEventSynchronize(s->ev_pack));
+        if (s->h_pack) AFAM_CUDA(cudaFreeHost(s->h_pack));
+        s->h_pack = nullptr;
+        s->h_pack_cap = 0;
+        AFAM_CUDA(cudaHostAlloc((void **)&s->h_pack, total + (64 << 10), cudaHostAllocDefault));
+        s->h_pack_cap = total + (64 << 10);
+    } else {
+        AFAM_CUDA(cudaEventSynchronize(s->ev_pack));
+    }
+    unsigned char *pack = s->h_pack;
+    memset(pack, 0, total);
+    memcpy(pack, &A, sizeof(A));
+    memcpy(pack + off_tf, &tf, sizeof(tf));
+    memcpy(pack + off_grid, grid.data(), gbytes);
+    if (nblocks) memcpy(pack + off_idx, slots, (size_t)nblocks * sizeof(int32_t));
     unsigned char *d_pack = nullptr;
     AFAM_CUDA(cudaMallocAsync(&d_pack, total, st));
-    AFAM_CUDA(cudaMemcpyAsync(d_pack, pack.data(), total, cudaMemcpyHostToDevice, st));
+    AFAM_CUDA(cudaMemcpyAsync(d_pack, pack, total, cudaMemcpyHostToDevice, st));
+    AFAM_CUDA(cudaEventRecord(s->ev_pack, st));
+    ht.mark();
     AFAM_CUDA(cudaEventRecord(s->ev_k0, st));
     init_stats_kernel<<<1, 1, 0, st>>>(stats);
     if (A.rows > 0) {
@@ -1252,6 +1300,8 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
     AFAM_CUDA(cudaEventRecord(s->ev_k1, st));
     AFAM_CUDA(cudaGetLastError());
     AFAM_CUDA(cudaFreeAsync(d_pack, st));
+    ht.mark();
+    ht.report("afam_render: setdevice, args+tf, grid+waits, pack lock, pack+upload, launches");
     return AFAM_OK;
 }
 

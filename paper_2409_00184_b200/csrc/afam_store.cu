@@ -187,6 +187,16 @@ int afam_store_create(afam_store **out, int device, int32_t slots, int32_t max_n
     for (auto &h : s->host) AFAM_CUDA(cudaEventCreateWithFlags(&h.ready, cudaEventDisableTiming));
     AFAM_CUDA(cudaEventCreate(&s->ev_k0));
     AFAM_CUDA(cudaEventCreate(&s->ev_k1));
+    AFAM_CUDA(cudaEventCreateWithFlags(&s->ev_pack, cudaEventDisableTiming));
+    {
+        // the per-call argument buffers come from the device's stream-ordered
+        // pool (cudaMallocAsync); keep its memory mapped across
+        // synchronizations, or every frame would re-map it (ms per call)
+        cudaMemPool_t pool;
+        AFAM_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t keep = UINT64_MAX;
+        AFAM_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    }
     *out = s;
     return AFAM_OK;
 }
@@ -199,6 +209,8 @@ int afam_store_destroy(afam_store *s) {
         if (h.ready) cudaEventDestroy(h.ready);
     if (s->ev_k0) cudaEventDestroy(s->ev_k0);
     if (s->ev_k1) cudaEventDestroy(s->ev_k1);
+    if (s->ev_pack) cudaEventDestroy(s->ev_pack);
+    if (s->h_pack) cudaFreeHost(s->h_pack);
     for (auto &kv : s->ops) {
         cudaFree(kv.second.b32);
         cudaFree(kv.second.b64);

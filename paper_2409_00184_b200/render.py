@@ -356,8 +356,14 @@ def render_part(pov, blocks: dict, tf, params, *, band_rows: int | None = None, 
     br = H if band_rows is None else int(band_rows)
     rows = int(_lib.lib().afam_frame_rows(H, br, nparts, part))
     fr = _frame_struct(pov, tf, params, br, nparts, part, debug)
+    # host_out: the kernel stores the pixels straight into this thread's
+    # pinned staging buffer (mapped host memory), overlapping the copy-out
+    # with the march; one synchronization covers frame and stats
+    zero_copy = host_out and out is None
+    stage = _pinned_stage(rows * W * 4 if host_out else 0)
     if out is None:
-        out = torch.empty((rows, W, 4), dtype=torch.uint8, device=dev)
+        out = stage[64:64 + rows * W * 4].view(rows, W, 4) if zero_copy else \
+            torch.empty((rows, W, 4), dtype=torch.uint8, device=dev)
     stats = torch.empty(6, dtype=torch.int64, device=dev)
     nsamp = ohash = None
     if debug:
@@ -370,12 +376,9 @@ def render_part(pov, blocks: dict, tf, params, *, band_rows: int | None = None, 
             store.handle, C.byref(fr), sl.ctypes.data_as(C.c_void_p), len(sl), C.c_void_p(out.data_ptr()),
             C.c_void_p(stats.data_ptr()), None if nsamp is None else C.c_void_p(nsamp.data_ptr()),
             None if ohash is None else C.c_void_p(ohash.data_ptr()), C.c_void_p(int(s_obj.cuda_stream))))
-        # one synchronization: stats (and the frame, for host_out) through a
-        # persistent pinned staging buffer of this thread
-        stage = _pinned_stage(rows * W * 4 if host_out else 0)
         with torch.cuda.stream(s_obj):
             stage[:48].view(torch.int64).copy_(stats, non_blocking=True)
-            if host_out:
+            if host_out and not zero_copy:
                 stage[64:64 + rows * W * 4].view(rows, W, 4).copy_(out, non_blocking=True)
         s_obj.synchronize()
         st = stage[:48].view(torch.int64).numpy().copy()
