@@ -119,6 +119,19 @@ int afam_eval_points(afam_store *s, const int32_t *slots, int32_t slot, const do
 int afam_decode_grid(afam_store *s, const int32_t *slots, int32_t nblk, int32_t m, float *out,
                      void *stream);
 
+/* afam_decode_grid with an explicit kernel choice for the float32 slots:
+ * AFAM_DECODE_AUTO (the measured-faster banded CUDA-core kernel unless
+ * AFAM_DECODE_TC=1 is set in the environment), AFAM_DECODE_CUDA_CORES, or
+ * AFAM_DECODE_TENSOR_CORES (tcgen05 3xTF32 x stage; m == 65 and ncp <= 72,
+ * other blocks fall back to the CUDA-core kernel).  Float64 slots always take
+ * the float64 CUDA-core kernel.  *ntc (nullable) receives the number of
+ * blocks given to the tensor-core kernel. */
+#define AFAM_DECODE_AUTO 0
+#define AFAM_DECODE_CUDA_CORES 1
+#define AFAM_DECODE_TENSOR_CORES 2
+int afam_decode_grid_ex(afam_store *s, const int32_t *slots, int32_t nblk, int32_t m, float *out, int32_t path,
+                        int32_t *ntc, void *stream);
+
 /* ------------------------------------------------------------ visibility */
 typedef struct afam_manifest afam_manifest;
 

@@ -74,16 +74,27 @@ def eval_device(store, slots, points, gradient: bool = True, param: bool = False
         return val, d_grad.cpu().numpy().astype(np.float64)
 
 
-def decode_slots(store, slots, m: int) -> np.ndarray:
-    """K3 on resident slots -> (nblk, m, m, m) float64 array indexed [b, i, j, k]."""
+DECODE_PATHS = {"auto": 0, "cuda_cores": 1, "tensor_cores": 2}
+
+
+def decode_slots(store, slots, m: int, path: str = "auto", info: dict | None = None) -> np.ndarray:
+    """K3 on resident slots -> (nblk, m, m, m) float64 array indexed [b, i, j, k].
+    path: "auto" | "cuda_cores" | "tensor_cores" (afam_decode_grid_ex); info,
+    if given, receives {"tensor_core_blocks": n}."""
     torch = _torch()
+    if path not in DECODE_PATHS:
+        raise ValueError(f"unknown decode path {path!r} (use {', '.join(DECODE_PATHS)})")
     slots = np.ascontiguousarray(slots, dtype=np.int32)
     dev = torch.device("cuda", store.device)
     out = torch.empty((len(slots), m, m, m), dtype=torch.float32, device=dev)
+    ntc = C.c_int32(0)
     with torch.cuda.device(dev):
-        _lib.check(_lib.lib().afam_decode_grid(store.handle, slots.ctypes.data_as(C.c_void_p), len(slots), int(m),
-                                               C.c_void_p(out.data_ptr()), C.c_void_p(stream_handle(None, dev))))
+        _lib.check(_lib.lib().afam_decode_grid_ex(store.handle, slots.ctypes.data_as(C.c_void_p), len(slots), int(m),
+                                                  C.c_void_p(out.data_ptr()), DECODE_PATHS[path], C.byref(ntc),
+                                                  C.c_void_p(stream_handle(None, dev))))
         host = out.cpu().numpy()
+    if info is not None:
+        info["tensor_core_blocks"] = int(ntc.value)
     # device layout is x fastest within a block: [b][k][j][i]
     return np.ascontiguousarray(host.transpose(0, 3, 2, 1)).astype(np.float64)
 

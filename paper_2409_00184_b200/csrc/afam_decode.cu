@@ -16,15 +16,17 @@
 #include <cstring>
 
 #include "afam_internal.h"
+#include "afam_umma.cuh"
 
 namespace afam {
 
 struct DecodeJob {
     int32_t slot;
-    int32_t pad;
+    int32_t tc_kp;  // tensor-core path: K extent (ncp rounded up to 8); 0 = CUDA-core path
     const int32_t *col0;
     const float *b32;
     const double *b64;
+    const float *tc_b;
 };
 
 constexpr int kDecodeChunk = 65;     // output planes per CTA (a whole 65^3 block)
@@ -240,6 +242,7 @@ __global__ void __launch_bounds__(kDecodeThreads) decode_grid_kernel(const Block
     const BlockDesc d = descs[jb.slot];
     constexpr bool kF64 = sizeof(T) == 8;
     if (((d.flags & AFAM_SLOT_FP64) != 0) != kF64) return;
+    if (!kF64 && jb.tc_kp > 0) return;  // decoded by decode_tc_kernel
     const int k0 = blockIdx.x * kDecodeChunk;
     const int k1 = min(m, k0 + kDecodeChunk);
     float *o = out + (size_t)blockIdx.y * m * m * m;
@@ -249,6 +252,281 @@ __global__ void __launch_bounds__(kDecodeThreads) decode_grid_kernel(const Block
         case 1: decode_planes<1, T>(d, jb.col0, b, m, k0, k1, o, smem); break;
         case 2: decode_planes<2, T>(d, jb.col0, b, m, k0, k1, o, smem); break;
         default: decode_planes<3, T>(d, jb.col0, b, m, k0, k1, o, smem); break;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Tensor-core grid decode (m == 65, float32 slots).  Per output plane k:
+//   z stage (CUDA cores): S1[y][x] = sum_c Bz[k][c] C[z0+c][y][x] over the
+//     TMA plane ring (as above);
+//   y stage (CUDA cores): S2[j][x] = sum_b By[j][b] S1[y0_j+b][x] for
+//     j < 64, split into tf32 hi/lo and stored as the A operand (64 rows,
+//     K = x, K-major no-swizzle panels);
+//   x stage (tcgen05, kind::tf32, 3xTF32): D[j][i] = sum_x S2[j][x] Bx[i][x]
+//     for i < 64 -- one 64x64 accumulator in TMEM per plane, K = ncp
+//     rounded up to 8, D += A_hi B_hi + A_lo B_hi + A_hi B_lo;
+//   the last lattice row and column (u = 1) select the last control index
+//   exactly (B row m-1 = e_{ncp-1}, checked on the host), so out[k][j][64]
+//   = S2[j][ncp-1] and out[k][64][i] = x-contraction of S1[ncp-1] come from
+//   the CUDA-core stages.
+// Warp-specialised pipeline over the planes: 12 producer warps (z and y
+// stages, A operand), one MMA warp (a single thread issues the tcgen05.mma
+// chain of a plane and commits it to an mbarrier), 4 epilogue warps (TMEM ->
+// shared staging -> 16-byte global stores).  A operands, TMEM accumulators
+// and the u = 1 row/column buffers are double-buffered; mbarriers hand each
+// buffer between the roles (A_full: producers -> MMA; D_full: MMA ->
+// epilogue and producers (A free); E_done: epilogue -> MMA (TMEM free) and
+// producers (row/column buffers free)).
+constexpr int kTcProducerWarps = 12;
+constexpr int kTcMmaWarp = kTcProducerWarps;
+constexpr int kTcEpiWarp0 = kTcProducerWarps + 1;
+constexpr int kTcThreads = 32 * (kTcProducerWarps + 1 + 4);  // 544
+constexpr int kTcRows = 64;      // tensor-core rows / columns per plane (m - 1)
+constexpr int kTcKmax = 72;      // ncp <= 72
+
+struct TcSmem {  // byte offsets of the dynamic shared memory carve-up
+    size_t bs, a, ring, s1, stage, band, col0, xlast, row64, bar, tmem, total;
+};
+
+__host__ __device__ inline size_t tc_align(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+__host__ __device__ inline TcSmem tc_smem(int n, int kp, int m) {
+    const int pitch = (n + 3) & ~3;
+    TcSmem o;
+    size_t off = 0;
+    o.bs = off;    off += 2 * (size_t)kTcRows * kp * 4;         // basis hi, lo
+    o.a = off;     off += 2 * 2 * (size_t)kTcRows * kp * 4;     // 2 buffers x (hi, lo)
+    o.ring = off;  off += (size_t)kRing * n * pitch * 4;        // TMA plane ring
+    o.s1 = off;    off += (size_t)n * pitch * 4;
+    o.stage = off; off += tc_align((size_t)m * m * 4 + 16, 16); // output plane (+ alignment shift)
+    o.band = off;  off += (size_t)m * 4 * 4;
+    o.col0 = off;  off += tc_align((size_t)m * 4, 16);
+    o.xlast = off; off += 2 * kTcRows * 4;
+    o.row64 = off; off += tc_align(2 * (size_t)m * 4, 16);
+    o.bar = off;   off += (kRing + 6) * 8;
+    o.tmem = off;  off += 16;
+    o.total = off;
+    return o;
+}
+
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int P>
+__device__ __forceinline__ void tc_decode_block(const BlockDesc &d, const DecodeJob &jb, int m, float *__restrict__ out,
+                                                size_t out_off, unsigned char *smem) {
+    constexpr int Q = P + 1;
+    const int n = d.ncp, pitch = d.pitch, nq = pitch >> 2, kp = jb.tc_kp, kq = kp >> 2;
+    const TcSmem L = tc_smem(n, kp, m);
+    float *Bs = reinterpret_cast<float *>(smem + L.bs);
+    float *Abuf = reinterpret_cast<float *>(smem + L.a);
+    float *ring = reinterpret_cast<float *>(smem + L.ring);
+    float *S1 = reinterpret_cast<float *>(smem + L.s1);
+    float *stage = reinterpret_cast<float *>(smem + L.stage);
+    float *B = reinterpret_cast<float *>(smem + L.band);
+    int *c0 = reinterpret_cast<int *>(smem + L.col0);
+    float *xlast = reinterpret_cast<float *>(smem + L.xlast);
+    float *row64 = reinterpret_cast<float *>(smem + L.row64);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + L.bar);
+    uint64_t *ring_bar = bar, *a_full = bar + kRing, *d_full = a_full + 2, *e_done = d_full + 2;
+    uint32_t *tmem_base = reinterpret_cast<uint32_t *>(smem + L.tmem);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const size_t abytes = (size_t)kTcRows * kp * 4;  // one operand panel set (hi or lo)
+
+    {  // basis operand (hi, lo) and the banded rows for the CUDA-core stages
+        const float4 *src = reinterpret_cast<const float4 *>(jb.tc_b);
+        float4 *dst = reinterpret_cast<float4 *>(Bs);
+        for (int i = tid; i < 2 * kTcRows * kq; i += blockDim.x) dst[i] = src[i];
+        for (int i = tid; i < m * 4; i += blockDim.x) B[i] = jb.b32[i];
+        for (int i = tid; i < m; i += blockDim.x) c0[i] = jb.col0[i];
+    }
+    if (tid == 0) {
+        for (int r = 0; r < kRing + 6; r++) mbar_init(bar + r, 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) umma::tmem_alloc(tmem_base, 128);
+    umma::fence_async_smem();
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    const uint32_t tbase = *tmem_base;
+
+    if (warp < kTcProducerWarps) {
+        // ---------------- producers: z and y stages on the CUDA cores
+        constexpr int NP = 32 * kTcProducerWarps;
+        const float *__restrict__ C = d.ctrl;
+        const size_t zstride = (size_t)n * pitch;
+        const uint32_t plane_bytes = (uint32_t)(zstride * sizeof(float));
+        const int zbase = c0[0];
+        const int zlast = min(n - 1, c0[m - 1] + P);
+        int issued = zbase - 1;
+        auto issue_upto = [&](int zmax) {
+            fence_proxy_async();
+            for (int z = issued + 1; z <= zmax; z++) {
+                uint64_t *bz_ = ring_bar + ((z - zbase) % kRing);
+                mbar_arrive_expect_tx(bz_, plane_bytes);
+                tma_load_1d(ring + (size_t)((z - zbase) % kRing) * zstride, C + (size_t)z * zstride, plane_bytes,
+                            bz_);
+            }
+            issued = max(issued, zmax);
+        };
+        if (tid == 0) issue_upto(min(zlast, zbase + P));
+        const float inv_nq = 1.f / (float)nq;
+        for (int k = 0; k < m; k++) {
+            const int b = k & 1, u = k >> 1;
+            const int z0 = c0[k];
+            float bz[Q];
+#pragma unroll
+            for (int c = 0; c < Q; c++) bz[c] = B[k * 4 + c];
+            const float *planes[Q];
+#pragma unroll
+            for (int c = 0; c < Q; c++) {
+                const int zr = z0 + c - zbase;
+                mbar_wait(ring_bar + (zr % kRing), (uint32_t)((zr / kRing) & 1));
+                planes[c] = ring + (size_t)(zr % kRing) * zstride;
+            }
+            // z stage: S1[y][x..x+3]
+            for (int item = tid; item < n * nq; item += NP) {
+                const int y = (int)(((float)item + 0.5f) * inv_nq), q = item - y * nq;
+                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int c = 0; c < Q; c++) {
+                    const float4 v = *reinterpret_cast<const float4 *>(planes[c] + (size_t)y * pitch + 4 * q);
+                    acc[0] = fmaf(bz[c], v.x, acc[0]);
+                    acc[1] = fmaf(bz[c], v.y, acc[1]);
+                    acc[2] = fmaf(bz[c], v.z, acc[2]);
+                    acc[3] = fmaf(bz[c], v.w, acc[3]);
+                }
+                st4(S1 + (size_t)y * pitch + 4 * q, acc);
+            }
+            named_sync(1, NP);
+            if (tid == 0 && k + 1 < m) issue_upto(min(zlast, c0[k + 1] + P));
+            if (k >= 2) {  // buffer b: MMAs of plane k-2 done (A free), its epilogue done (row/col free)
+                mbar_wait(d_full + b, (uint32_t)((u - 1) & 1));
+                mbar_wait(e_done + b, (uint32_t)((u - 1) & 1));
+            }
+            // y stage into the A operand (rows j < 64, K = x; zero past ncp)
+            float *Ah = Abuf + (size_t)b * 2 * kTcRows * kp, *Al = Ah + (size_t)kTcRows * kp;
+            for (int item = tid; item < kTcRows * kq; item += NP) {
+                const int q = item >> 6, j = item & (kTcRows - 1);
+                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+                if (q < nq) {
+                    const float *s1 = S1 + (size_t)c0[j] * pitch + 4 * q;
+#pragma unroll
+                    for (int bb = 0; bb < Q; bb++) {
+                        float v[4];
+                        ld4(s1 + (size_t)bb * pitch, v);
+                        const float w = B[j * 4 + bb];
+#pragma unroll
+                        for (int e = 0; e < 4; e++) acc[e] = fmaf(w, v[e], acc[e]);
+                    }
+                    if (q == (n - 1) >> 2) xlast[b * kTcRows + j] = acc[(n - 1) & 3];
+                }
+                float hi[4], lo[4];
+#pragma unroll
+                for (int e = 0; e < 4; e++) umma::split_tf32(acc[e], hi[e], lo[e]);
+                st4(Ah + (size_t)item * 4, hi);
+                st4(Al + (size_t)item * 4, lo);
+            }
+            for (int i = tid; i < m; i += NP) {  // out[k][m-1][i]: x stage of S1[ncp-1] (= S2[m-1])
+                const float *s = S1 + (size_t)(n - 1) * pitch + c0[i];
+                float acc = 0.f;
+#pragma unroll
+                for (int a = 0; a < Q; a++) acc = fmaf(B[i * 4 + a], s[a], acc);
+                row64[b * m + i] = acc;
+            }
+            umma::fence_async_smem();
+            named_sync(1, NP);
+            if (tid == 0) mbar_arrive(a_full + b);
+        }
+        // drain ring loads that were issued but never read
+        if (tid == 0)
+            for (int z = max(zbase, issued - kRing + 1); z <= issued; z++)
+                mbar_wait(ring_bar + ((z - zbase) % kRing), (uint32_t)(((z - zbase) / kRing) & 1));
+    } else if (warp == kTcMmaWarp) {
+        // ---------------- MMA issue: x stage on the tensor core (3xTF32)
+        if (lane == 0) {
+            constexpr uint32_t idesc = umma::idesc_tf32(kTcRows, kTcRows);
+            const uint32_t lbo = kTcRows * 16;
+            const uint32_t bh = umma::smem_addr(Bs), bl = bh + (uint32_t)abytes;
+            const uint64_t dbh0 = umma::desc_kmajor(bh, lbo, 128), dbl0 = umma::desc_kmajor(bl, lbo, 128);
+            for (int k = 0; k < m; k++) {
+                const int b = k & 1, u = k >> 1;
+                mbar_wait(a_full + b, (uint32_t)(u & 1));
+                if (k >= 2) mbar_wait(e_done + b, (uint32_t)((u - 1) & 1));  // TMEM buffer b drained
+                umma::fence_after_sync();
+                const uint32_t ah = umma::smem_addr(Abuf + (size_t)b * 2 * kTcRows * kp);
+                const uint64_t dah0 = umma::desc_kmajor(ah, lbo, 128);
+                const uint64_t dal0 = umma::desc_kmajor(ah + (uint32_t)abytes, lbo, 128);
+                const uint32_t d_tmem = tbase + (uint32_t)(b * kTcRows);
+                for (int ks = 0; ks < kp / 8; ks++) {
+                    const uint64_t off = (uint64_t)((ks * 2 * lbo) >> 4);  // start-address field, 16-B units
+                    umma::mma_tf32(d_tmem, dal0 + off, dbh0 + off, idesc, ks > 0);
+                    umma::mma_tf32(d_tmem, dah0 + off, dbl0 + off, idesc, true);
+                    umma::mma_tf32(d_tmem, dah0 + off, dbh0 + off, idesc, true);
+                }
+                umma::commit(d_full + b);
+            }
+        }
+        __syncwarp();
+    } else {
+        // ---------------- epilogue: TMEM -> staging -> 16-byte global stores
+        constexpr int NE = 128;
+        const int et = tid - 32 * kTcEpiWarp0, sp = warp & 3;  // TMEM sub-partition of this warp
+        for (int k = 0; k < m; k++) {
+            const int b = k & 1, u = k >> 1;
+            const size_t g0 = out_off + (size_t)k * m * m;
+            const int r = (int)(g0 & 3);  // staging shift: stage[r + e] <-> out[g0 + e], 16-B aligned copies
+            mbar_wait(d_full + b, (uint32_t)(u & 1));
+            umma::fence_after_sync();
+#pragma unroll
+            for (int cg = 0; cg < 4; cg++) {  // M = 64 accumulator: row j in TMEM lane (j % 16) + 32 (j / 16)
+                float v[16];
+                umma::tmem_ld16(tbase + ((uint32_t)(32 * sp) << 16) + (uint32_t)(b * kTcRows + 16 * cg), v);
+                if (lane < 16) {
+                    float *row = stage + r + (size_t)(16 * sp + lane) * m + 16 * cg;
+#pragma unroll
+                    for (int c = 0; c < 16; c++) row[c] = v[c];
+                }
+            }
+            for (int j = et; j < kTcRows; j += NE) stage[r + (size_t)j * m + kTcRows] = xlast[b * kTcRows + j];
+            for (int i = et; i < m; i += NE) stage[r + (size_t)kTcRows * m + i] = row64[b * m + i];
+            umma::fence_before_sync();
+            named_sync(2, NE);
+            if (et == 0) mbar_arrive(e_done + b);
+            float *o = out + g0;
+            const int total = m * m, h = (4 - r) & 3;
+            for (int e = et; e < h; e += NE) o[e] = stage[r + e];
+            const int nv = (total - h) >> 2;
+            for (int v = et; v < nv; v += NE)
+                reinterpret_cast<float4 *>(o + h)[v] = reinterpret_cast<const float4 *>(stage + r + h)[v];
+            for (int e = h + 4 * nv + et; e < total; e += NE) o[e] = stage[r + e];
+            named_sync(2, NE);  // staging free for the next plane
+        }
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    if (warp == 0) umma::tmem_dealloc(tbase, 128);
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1) decode_tc_kernel(const BlockDesc *__restrict__ descs,
+                                                                 const DecodeJob *__restrict__ jobs, int m,
+                                                                 float *__restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const DecodeJob jb = jobs[blockIdx.x];
+    if (jb.tc_kp == 0) return;  // no tensor-core operator: CUDA-core path
+    const BlockDesc d = descs[jb.slot];
+    if (d.flags & AFAM_SLOT_FP64) return;  // ill-conditioned: float64 CUDA-core path
+    const size_t off = (size_t)blockIdx.x * m * m * m;
+    switch (d.deg) {
+        case 1: tc_decode_block<1>(d, jb, m, out, off, smem); break;
+        case 2: tc_decode_block<2>(d, jb, m, out, off, smem); break;
+        default: tc_decode_block<3>(d, jb, m, out, off, smem); break;
     }
 }
 
@@ -291,6 +569,18 @@ static void host_band(int ncp, int deg, int m, std::vector<double> &b, std::vect
 
 using namespace afam;
 
+// AFAM_DECODE_AUTO picks the tensor-core decode only with AFAM_DECODE_TC=1
+// in the environment: the banded CUDA-core kernel is faster on B200 (the
+// dense 3xTF32 operands move more shared-memory bytes per plane than the
+// banded x stage, K3).
+static bool tc_default() {
+    static const bool v = [] {
+        const char *e = getenv("AFAM_DECODE_TC");
+        return e && atoi(e) != 0;
+    }();
+    return v;
+}
+
 static int get_op(afam_store *s, int ncp, int deg, int m, DecodeOp **op) {
     auto key = std::make_tuple(ncp, deg, m);
     auto it = s->ops.find(key);
@@ -300,6 +590,36 @@ static int get_op(afam_store *s, int ncp, int deg, int m, DecodeOp **op) {
         host_band(ncp, deg, m, b, c0);
         std::vector<float> b32(b.begin(), b.end());
         DecodeOp o;
+        // tensor-core operator: m == 65, ncp <= 72, and the u = 1 row selecting
+        // the last control point exactly (what lets the CUDA-core stages supply
+        // lattice row/column m-1)
+        if (m == kTcRows + 1 && ncp <= kTcKmax) {
+            // (in float32, as the CUDA-core kernels apply it: Cox-de Boor can
+            // give 1 - 1e-16 at u = 1, which rounds to 1.0f)
+            bool last_ok = c0[m - 1] + deg == ncp - 1 && (float)b[(size_t)(m - 1) * 4 + deg] == 1.0f;
+            for (int a = 0; a < deg; a++) last_ok = last_ok && (float)b[(size_t)(m - 1) * 4 + a] == 0.0f;
+            if (last_ok) {
+                const int kp = (ncp + 7) & ~7;
+                std::vector<float> tb((size_t)2 * kTcRows * kp, 0.f);
+                for (int i = 0; i < kTcRows; i++)
+                    for (int a = 0; a <= deg; a++) {
+                        const int x = c0[i] + a;
+                        const double v = b[(size_t)i * 4 + a];
+                        float hi = (float)v;
+                        uint32_t bits;
+                        memcpy(&bits, &hi, 4);
+                        bits &= 0xFFFFE000u;
+                        memcpy(&hi, &bits, 4);
+                        const float lo = (float)(v - (double)hi);
+                        const size_t e = ((size_t)(x / 4) * kTcRows + i) * 4 + x % 4;
+                        tb[e] = hi;
+                        tb[(size_t)kTcRows * kp + e] = lo;
+                    }
+                AFAM_CUDA(cudaMalloc(&o.tc_b, tb.size() * sizeof(float)));
+                AFAM_CUDA(cudaMemcpy(o.tc_b, tb.data(), tb.size() * sizeof(float), cudaMemcpyHostToDevice));
+                o.tc_kp = kp;
+            }
+        }
         AFAM_CUDA(cudaMalloc(&o.b32, b32.size() * sizeof(float)));
         AFAM_CUDA(cudaMalloc(&o.b64, b.size() * sizeof(double)));
         AFAM_CUDA(cudaMalloc(&o.col0, c0.size() * sizeof(int32_t)));
@@ -314,6 +634,15 @@ static int get_op(afam_store *s, int ncp, int deg, int m, DecodeOp **op) {
 
 extern "C" int afam_decode_grid(afam_store *s, const int32_t *slots, int32_t nblk, int32_t m, float *out,
                                 void *stream) {
+    return afam_decode_grid_ex(s, slots, nblk, m, out, AFAM_DECODE_AUTO, nullptr, stream);
+}
+
+extern "C" int afam_decode_grid_ex(afam_store *s, const int32_t *slots, int32_t nblk, int32_t m, float *out,
+                                   int32_t path, int32_t *ntc_out, void *stream) {
+    AFAM_CHECK(path >= AFAM_DECODE_AUTO && path <= AFAM_DECODE_TENSOR_CORES, AFAM_E_VALUE, "unknown decode path %d",
+               path);
+    const bool use_tc = path == AFAM_DECODE_TENSOR_CORES || (path == AFAM_DECODE_AUTO && tc_default());
+    if (ntc_out) *ntc_out = 0;
     AFAM_CHECK(s, AFAM_E_VALUE, "store is NULL");
     AFAM_CHECK(nblk >= 0, AFAM_E_VALUE, "negative block count");
     if (nblk == 0) return AFAM_OK;
@@ -323,7 +652,7 @@ extern "C" int afam_decode_grid(afam_store *s, const int32_t *slots, int32_t nbl
     cudaStream_t st = (cudaStream_t)stream;
     AFAM_CUDA(cudaSetDevice(s->device));
     std::vector<DecodeJob> jobs(nblk);
-    int maxn = 0;
+    int maxn = 0, ntc = 0, maxkp = 0, maxn_tc = 0;
     {
         std::lock_guard<std::mutex> lk(s->mu);
         for (int b = 0; b < nblk; b++) {
@@ -337,6 +666,13 @@ extern "C" int afam_decode_grid(afam_store *s, const int32_t *slots, int32_t nbl
             jobs[b].col0 = op->col0;
             jobs[b].b32 = op->b32;
             jobs[b].b64 = op->b64;
+            jobs[b].tc_b = op->tc_b;
+            jobs[b].tc_kp = use_tc ? op->tc_kp : 0;  // float64 slots (device flag) stay on the CUDA-core kernel
+            if (jobs[b].tc_kp) {
+                ntc++;
+                maxkp = std::max(maxkp, (int)jobs[b].tc_kp);
+                maxn_tc = std::max(maxn_tc, (int)h.ncp);
+            }
             maxn = std::max(maxn, (int)h.ncp);
             AFAM_CUDA(wait_slot(s, sl, st));
         }
@@ -351,7 +687,14 @@ extern "C" int afam_decode_grid(afam_store *s, const int32_t *slots, int32_t nbl
     AFAM_CUDA(cudaMallocAsync(&d_jobs, sizeof(DecodeJob) * nblk, st));
     AFAM_CUDA(cudaMemcpyAsync(d_jobs, jobs.data(), sizeof(DecodeJob) * nblk, cudaMemcpyHostToDevice, st));
     const dim3 grid((m + kDecodeChunk - 1) / kDecodeChunk, nblk);
-    {
+    if (ntc_out) *ntc_out = ntc;
+    if (ntc > 0) {
+        const size_t smem = tc_smem(maxn_tc, maxkp, m).total;
+        AFAM_CHECK(smem <= 227 * 1024, AFAM_E_VALUE, "tensor-core decode needs %zu B of shared memory", smem);
+        AFAM_CUDA(cudaFuncSetAttribute(decode_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        decode_tc_kernel<<<nblk, kTcThreads, smem, st>>>(s->d_desc, d_jobs, m, out);
+    }
+    if (ntc < nblk) {
         const size_t smem = smem_for(sizeof(float));
         AFAM_CHECK(smem <= 227 * 1024, AFAM_E_VALUE, "decode of ncp=%d onto m=%d needs %zu B of shared memory", maxn,
                    m, smem);

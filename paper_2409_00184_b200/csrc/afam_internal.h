@@ -63,6 +63,11 @@ struct DecodeOp {  // banded collocation matrix of bspline.py:98-125 for (ncp, d
     float *b32 = nullptr;   // [m][4]
     double *b64 = nullptr;  // [m][4]
     int32_t *col0 = nullptr;// [m] first nonzero column (span - deg)
+    // tensor-core decode (afam_decode.cu, m == 65, ncp <= 72): the first m-1
+    // rows of B dense over K = kp columns (kp = ncp rounded up to 8), split
+    // into tf32 hi and lo parts, in the K-major no-swizzle operand layout
+    float *tc_b = nullptr;  // [2][kp/4][m-1][4]: hi panels, then lo panels
+    int32_t tc_kp = 0;      // 0: the tensor-core path does not apply
 };
 
 }  // namespace afam

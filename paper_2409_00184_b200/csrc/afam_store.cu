@@ -215,6 +215,7 @@ int afam_store_destroy(afam_store *s) {
         cudaFree(kv.second.b32);
         cudaFree(kv.second.b64);
         cudaFree(kv.second.col0);
+        if (kv.second.tc_b) cudaFree(kv.second.tc_b);
     }
     cudaFree(s->arena);
     cudaFree(s->d_desc);

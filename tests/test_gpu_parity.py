@@ -163,6 +163,49 @@ def test_decode_ill_conditioned_vs_oracle(cuda, oracle):
         assert np.abs(got[b] - want).max() <= VALUE_TOL
 
 
+@pytest.mark.parametrize("degree", [1, 2, 3])
+def test_decode_tensor_cores_vs_oracle(cuda, oracle, degree):
+    """K3 tcgen05 path (3xTF32 x stage) on the 65^3 lattice: every block given
+    to the tensor cores, values within 1e-5 of the float64 oracle and of the
+    CUDA-core kernel."""
+    from paper_2409_00184_b200 import synth
+    from paper_2409_00184_b200.bspline import decode_slots
+    from paper_2409_00184_b200.device import DeviceStore
+
+    sizes = [degree + 2, 17, 33, 40, 48, 57, 60, 64 if degree < 3 else 52]
+    man, blobs = synth.field_store(levels=1, coarsest=2, micro=65, degree=degree,
+                                   ncp_of=lambda a: sizes[(a.ijk[0] * 2 + a.ijk[1]) * 2 + a.ijk[2]])
+    ds = DeviceStore(len(blobs), 65)
+    addrs = sorted(blobs)
+    slots = [ds.load_mfa(blobs[a], man.entries[a].ncp, man.entries[a].extent, a.lod).slot for a in addrs]
+    info = {}
+    got = decode_slots(ds, slots, 65, path="tensor_cores", info=info)
+    assert info["tensor_core_blocks"] == len(slots)
+    ref = decode_slots(ds, slots, 65, path="cuda_cores")
+    for b, s in enumerate(slots):
+        ctrl, _ = ds.read(s)
+        want = oracle.decode_grid(ctrl, degree, 65)
+        assert np.abs(got[b] - want).max() <= VALUE_TOL, (b, ctrl.shape[0])
+        assert np.abs(got[b] - ref[b]).max() <= VALUE_TOL
+
+
+def test_decode_tensor_cores_other_lattice_falls_back(cuda, oracle):
+    """m != 65: the tensor-core request falls back to the CUDA-core kernel."""
+    from paper_2409_00184_b200 import synth
+    from paper_2409_00184_b200.bspline import decode_slots
+    from paper_2409_00184_b200.device import DeviceStore
+
+    man, blobs = synth.field_store(levels=1, coarsest=1, micro=9, degree=3, ncp_of=lambda a: 7)
+    ds = DeviceStore(len(blobs), 9)
+    a = sorted(blobs)[0]
+    slot = ds.load_mfa(blobs[a], man.entries[a].ncp, man.entries[a].extent, a.lod).slot
+    info = {}
+    got = decode_slots(ds, [slot], 33, path="tensor_cores", info=info)
+    assert info["tensor_core_blocks"] == 0
+    ctrl, _ = ds.read(slot)
+    assert np.abs(got[0] - oracle.decode_grid(ctrl, 3, 33)).max() <= VALUE_TOL
+
+
 # ----------------------------------------------------------------- K2 render
 FRAME_NAMES = list(npz("frames.npz")["names"])
 
