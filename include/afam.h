@@ -18,6 +18,8 @@
  *   afam_decode_grid      MicroModel.decode_grid,                 model.py:89-93,
  *                         bspline.decode_tensor_product           bspline.py:162-172
  *   afam_select_visible   render.select_visible                   render.py:281-320
+ *   afam_fit_rmse         encoder._fit_and_measure / error_rmse   encoder.py:74-83,
+ *                         model.fit, bspline.fit_tensor_product   model.py:96-107, bspline.py:109-159
  *   afam_render           render.render                           render.py:398-466
  *
  * Status -> Python exception (reference errors.py:12-25):
@@ -131,6 +133,28 @@ int afam_decode_grid(afam_store *s, const int32_t *slots, int32_t nblk, int32_t 
 #define AFAM_DECODE_TENSOR_CORES 2
 int afam_decode_grid_ex(afam_store *s, const int32_t *slots, int32_t nblk, int32_t m, float *out, int32_t path,
                         int32_t *ntc, void *stream);
+
+/* ------------------------------------------------- encoder inner loop */
+/*
+ * Batched in-level search step (reference encoder.in_level_search /
+ * _fit_and_measure, encoder.py:74-156): for job j, fit block job_block[j]
+ * of samples (device float32, nblk blocks of m^3, [i][j][k] C order) with
+ * job_ncp[j] control points per axis (endpoint-pinned separable least
+ * squares, bspline.py:109-159, float64), round the coefficients to float32
+ * (model.py:96-107), decode them on the m^3 lattice (bspline.py:162-172,
+ * float64) and return the RMSE against the samples in rmse[j] (host array;
+ * the call synchronizes).  ctrl (device, nullable): job j's float32
+ * coefficients [a][b][c] (C order) at ctrl + ctrl_off[j] (host offsets).
+ * The store supplies the device and caches the per-(ncp, degree, m) operators.
+ */
+int afam_fit_rmse(afam_store *s, const float *samples, int32_t nblk, int32_t m, int32_t degree,
+                  const int32_t *job_block, const int32_t *job_ncp, int32_t njobs, double *rmse, float *ctrl,
+                  const int64_t *ctrl_off, void *stream);
+
+/* The fit operator F (ncp x m: coefficients = F @ samples along one axis) and
+ * the dense collocation matrix B (m x ncp) of (ncp, degree, m), host float64
+ * (either pointer may be NULL). */
+int afam_fit_operator(int32_t ncp, int32_t degree, int32_t m, double *fit, double *dec);
 
 /* ------------------------------------------------------------ visibility */
 typedef struct afam_manifest afam_manifest;

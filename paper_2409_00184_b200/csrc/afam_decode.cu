@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_tc_kernel(const BlockDes
 // Host: the banded rows of bspline._axis_operator's B for (ncp, deg, m):
 // params linspace(0, 1, m), clamped uniform float64 knots
 // (bspline.py:29-38, :98-125), Cox-de Boor with the reference's divisors.
-static void host_band(int ncp, int deg, int m, std::vector<double> &b, std::vector<int32_t> &col0) {
+void host_band(int ncp, int deg, int m, std::vector<double> &b, std::vector<int32_t> &col0) {
     const int nk = ncp + deg + 1;
     std::vector<double> kv(nk);
     for (int i = 0; i <= deg; i++) kv[i] = 0.0;

@@ -70,6 +70,16 @@ struct DecodeOp {  // banded collocation matrix of bspline.py:98-125 for (ncp, d
     int32_t tc_kp = 0;      // 0: the tensor-core path does not apply
 };
 
+// Banded rows of the collocation matrix of bspline.py:98-125 for (ncp, deg,
+// m): params linspace(0, 1, m), fresh float64 clamped uniform knots; row i
+// holds N[col0[i] .. col0[i] + deg] (afam_decode.cu).
+void host_band(int ncp, int deg, int m, std::vector<double> &b, std::vector<int32_t> &col0);
+
+struct FitOp {  // endpoint-pinned least-squares fit operator (bspline.py:109-159), device
+    double *fit = nullptr;  // [ncp][m]: coefficients = fit @ samples along one axis
+    double *dec = nullptr;  // [m][ncp]: dense collocation matrix (decode along one axis)
+};
+
 }  // namespace afam
 
 struct afam_store {
@@ -88,6 +98,7 @@ struct afam_store {
     std::mutex pack_mu;                             // h_pack is shared by concurrent afam_render calls
     std::mutex mu;
     std::map<std::tuple<int, int, int>, afam::DecodeOp> ops;
+    std::map<std::tuple<int, int, int>, afam::FitOp> fit_ops;  // (ncp, deg, m)
 
     char *slot_base(int32_t slot) const { return arena + (size_t)slot * slot_bytes; }
     uint8_t *raw_ptr(int32_t slot) const { return (uint8_t *)slot_base(slot); }

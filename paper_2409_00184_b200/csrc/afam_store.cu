@@ -217,6 +217,10 @@ int afam_store_destroy(afam_store *s) {
         cudaFree(kv.second.col0);
         if (kv.second.tc_b) cudaFree(kv.second.tc_b);
     }
+    for (auto &kv : s->fit_ops) {
+        cudaFree(kv.second.fit);
+        cudaFree(kv.second.dec);
+    }
     cudaFree(s->arena);
     cudaFree(s->d_desc);
     cudaFree(s->d_maxabs);
