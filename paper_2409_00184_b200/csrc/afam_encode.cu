@@ -136,6 +136,123 @@ __global__ void __launch_bounds__(kFitThreads) contract_rotate_kernel(const FitJ
     }
 }
 
+// Register-tiled variant for operator extents <= 65 (the 65^3 micro-blocks
+// of the configs): a CTA computes all output rows for 64 input columns, each
+// thread a 4 x 4 (rows x columns) tile from the transposed operator and the
+// input tile in shared memory (16 DFMA per 8 shared loads).
+constexpr int kFitRT2 = 64;
+constexpr int kFitMaxN2 = 65;
+
+__device__ __forceinline__ int fit_R(int stage, int m, int ncp) {
+    switch (stage) {
+        case 0: return m * m;
+        case 1: return m * ncp;
+        case 2: return ncp * ncp;
+        case 3: return ncp * ncp;
+        case 4: return ncp * m;
+        default: return m * m;
+    }
+}
+
+__global__ void __launch_bounds__(kFitThreads, 2) contract_tiled_kernel(const FitJob *__restrict__ jobs, int m,
+                                                                       int stage) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const FitJob J = jobs[blockIdx.y];
+    const int ncp = J.ncp;
+    const bool dec = stage >= 3;
+    const int n0 = dec ? ncp : m, nout = dec ? m : ncp;
+    const int R = fit_R(stage, m, ncp);
+    const int r0 = blockIdx.x * kFitRT2;
+    if (r0 >= R) return;
+    const int rt = min(kFitRT2, R - r0);
+    const int np = (nout + 3) & ~3;                      // padded row count of the transposed operator
+    double *sOpT = reinterpret_cast<double *>(smem);     // [n0][np]
+    double *sIn = sOpT + (size_t)n0 * np;                // [n0][kFitRT2]
+    double *sOut = sIn + (size_t)n0 * kFitRT2;           // [kFitRT2][nout]
+    const double *op = dec ? J.op_dec : J.op_fit;        // [nout][n0]
+    for (int e = threadIdx.x; e < n0 * np; e += blockDim.x) {
+        const int k = e / np, a = e % np;
+        sOpT[e] = a < nout ? op[(size_t)a * n0 + k] : 0.0;
+    }
+    const double *in64 = nullptr;
+    switch (stage) {
+        case 1: in64 = J.buf0; break;
+        case 2: in64 = J.buf1; break;
+        case 3: in64 = J.buf0; break;
+        case 4: in64 = J.buf1; break;
+        case 5: in64 = J.buf0; break;
+        default: break;
+    }
+    for (int e = threadIdx.x; e < n0 * kFitRT2; e += blockDim.x) {
+        const int k = e / kFitRT2, r = e % kFitRT2;
+        double v = 0.0;
+        if (r < rt) {
+            const size_t g = (size_t)k * R + r0 + r;
+            v = stage == 0 ? (double)J.samples[g] : in64[g];
+        }
+        sIn[e] = v;
+    }
+    __syncthreads();
+    const int tc = threadIdx.x & 15, tr = threadIdx.x >> 4;  // 4-column group, 4-row group
+    for (int ab = 0; ab < nout; ab += 64) {
+        const int a0 = ab + 4 * tr;
+        if (a0 < np) {
+            double acc[4][4];
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+#pragma unroll
+                for (int j = 0; j < 4; j++) acc[i][j] = 0.0;
+            for (int k = 0; k < n0; k++) {
+                const double2 o01 = *reinterpret_cast<const double2 *>(sOpT + (size_t)k * np + a0);
+                const double2 o23 = *reinterpret_cast<const double2 *>(sOpT + (size_t)k * np + a0 + 2);
+                const double2 x01 = *reinterpret_cast<const double2 *>(sIn + (size_t)k * kFitRT2 + 4 * tc);
+                const double2 x23 = *reinterpret_cast<const double2 *>(sIn + (size_t)k * kFitRT2 + 4 * tc + 2);
+                const double o[4] = {o01.x, o01.y, o23.x, o23.y}, x[4] = {x01.x, x01.y, x23.x, x23.y};
+#pragma unroll
+                for (int i = 0; i < 4; i++)
+#pragma unroll
+                    for (int j = 0; j < 4; j++) acc[i][j] = fma(o[i], x[j], acc[i][j]);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+#pragma unroll
+                for (int j = 0; j < 4; j++)
+                    if (a0 + i < nout) sOut[(4 * tc + j) * nout + a0 + i] = acc[i][j];
+        }
+    }
+    __syncthreads();
+    const int total = rt * nout;
+    const size_t obase = (size_t)r0 * nout;
+    if (stage == 5) {
+        double sum = 0.0;
+        for (int e = threadIdx.x; e < total; e += blockDim.x) {
+            const double d = sOut[e] - (double)J.samples[obase + e];
+            sum = fma(d, d, sum);
+        }
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        __shared__ double wsum[kFitThreads / 32];
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        if (lane == 0) wsum[warp] = sum;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < kFitThreads / 32; w++) t += wsum[w];
+            atomicAdd(J.sse, t);
+        }
+        return;
+    }
+    double *out = stage == 0 ? J.buf0 : (stage == 1 ? J.buf1 : (stage == 2 ? J.buf0 : (stage == 3 ? J.buf1 : J.buf0)));
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {
+        double v = sOut[e];
+        if (stage == 2) {  // model.fit stores float32 coefficients (model.py:103)
+            const float f = (float)v;
+            if (J.ctrl) J.ctrl[obase + e] = f;
+            v = (double)f;
+        }
+        out[obase + e] = v;
+    }
+}
+
 // Host: _axis_operator (bspline.py:109-125) as an explicit matrix.  With B
 // the m x ncp collocation matrix and Bi its interior columns, the pinned fit
 // of data d is c_0 = d_0, c_{ncp-1} = d_{m-1}, interior
@@ -274,13 +391,25 @@ extern "C" int afam_fit_rmse(afam_store *s, const float *samples, int32_t nblk, 
     FitJob *d_jobs = nullptr;
     AFAM_CUDA(cudaMallocAsync(&d_jobs, sizeof(FitJob) * njobs, st));
     AFAM_CUDA(cudaMemcpyAsync(d_jobs, jobs.data(), sizeof(FitJob) * njobs, cudaMemcpyHostToDevice, st));
-    const size_t smem = ((size_t)m * m + (size_t)m * kFitRT + (size_t)kFitRT * m) * sizeof(double);
-    AFAM_CUDA(cudaFuncSetAttribute(contract_rotate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     // the widest R of each stage (over the batch's ncp) sizes the grid; CTAs past a job's R exit
     const int Rmax[6] = {m * m, m * maxncp, maxncp * maxncp, maxncp * maxncp, maxncp * m, m * m};
-    for (int stage = 0; stage < 6; stage++) {
-        dim3 grid((Rmax[stage] + kFitRT - 1) / kFitRT, njobs);
-        contract_rotate_kernel<<<grid, kFitThreads, smem, st>>>(d_jobs, m, stage);
+    if (m <= kFitMaxN2) {
+        const int mp = (m + 3) & ~3;
+        const size_t smem = ((size_t)m * mp + (size_t)m * kFitRT2 + (size_t)kFitRT2 * m) * sizeof(double);
+        AFAM_CUDA(cudaFuncSetAttribute(contract_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+        for (int stage = 0; stage < 6; stage++) {
+            dim3 grid((Rmax[stage] + kFitRT2 - 1) / kFitRT2, njobs);
+            contract_tiled_kernel<<<grid, kFitThreads, smem, st>>>(d_jobs, m, stage);
+        }
+    } else {
+        const size_t smem = ((size_t)m * m + (size_t)m * kFitRT + (size_t)kFitRT * m) * sizeof(double);
+        AFAM_CUDA(cudaFuncSetAttribute(contract_rotate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+        for (int stage = 0; stage < 6; stage++) {
+            dim3 grid((Rmax[stage] + kFitRT - 1) / kFitRT, njobs);
+            contract_rotate_kernel<<<grid, kFitThreads, smem, st>>>(d_jobs, m, stage);
+        }
     }
     AFAM_CUDA(cudaGetLastError());
     // rmse = sqrt(sse / m^3) (encoder.error_rmse: sqrt(mean(diff^2)))
