@@ -80,6 +80,16 @@ int afam_store_slots(const afam_store *s, int32_t *slots, int32_t *max_ncp);
 int afam_store_put_mfa(afam_store *s, int32_t slot, const uint8_t *bytes, uint64_t nbytes, int32_t ncp,
                        const double extent[6], void *stream);
 
+/* Upload one .mfa file straight from disk: read into a pinned staging ring
+ * (no pageable copy), validate like store.load_model (missing file, length,
+ * degree byte: AFAM_E_FORMAT; non-finite control points: AFAM_E_VALUE), then
+ * the asynchronous H2D copy and realignment of afam_store_put_mfa.
+ * *degree (nullable) receives the file's degree byte.
+ * Replaces store.load_model_bytes + model.deserialize (store.py:33-47,
+ * model.py:121-148) for the device loader. */
+int afam_store_put_file(afam_store *s, int32_t slot, const char *path, int32_t ncp, const double extent[6],
+                        int32_t *degree, void *stream);
+
 /* Upload an already-decoded model: knots (3, ncp+degree+1) float32 full
  * clamped vectors, ctrl ncp^3 float32 x-fastest. */
 int afam_store_put(afam_store *s, int32_t slot, int32_t degree, int32_t ncp, const float *knots,

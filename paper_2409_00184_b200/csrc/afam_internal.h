@@ -96,6 +96,13 @@ struct afam_store {
     size_t h_pack_cap = 0;
     cudaEvent_t ev_pack = nullptr;                  // the last upload out of h_pack
     std::mutex pack_mu;                             // h_pack is shared by concurrent afam_render calls
+    // afam_store_put_file: ring of pinned staging buffers (file -> pinned -> H2D)
+    static constexpr int kFileRing = 4;
+    unsigned char *h_file[kFileRing] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev_file[kFileRing] = {nullptr, nullptr, nullptr, nullptr};
+    int file_next = 0;
+    std::mutex file_mu[kFileRing];
+    std::mutex file_ring_mu;
     std::mutex mu;
     std::map<std::tuple<int, int, int>, afam::DecodeOp> ops;
     std::map<std::tuple<int, int, int>, afam::FitOp> fit_ops;  // (ncp, deg, m)

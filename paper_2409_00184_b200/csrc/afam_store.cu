@@ -6,6 +6,11 @@
 // at byte 1+12(ncp+d), FORMAT.md:24-30), so the raw file image is copied
 // H2D verbatim and realigned on device by unpack_ctrl_kernel /
 // build_tables_kernel; no host-side repacking.
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <cerrno>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -210,6 +215,10 @@ int afam_store_destroy(afam_store *s) {
     if (s->ev_k0) cudaEventDestroy(s->ev_k0);
     if (s->ev_k1) cudaEventDestroy(s->ev_k1);
     if (s->ev_pack) cudaEventDestroy(s->ev_pack);
+    for (int b = 0; b < afam_store::kFileRing; b++) {
+        if (s->h_file[b]) cudaFreeHost(s->h_file[b]);
+        if (s->ev_file[b]) cudaEventDestroy(s->ev_file[b]);
+    }
     if (s->h_pack) cudaFreeHost(s->h_pack);
     for (auto &kv : s->ops) {
         cudaFree(kv.second.b32);
@@ -309,6 +318,82 @@ int afam_store_put_mfa(afam_store *s, int32_t slot, const uint8_t *bytes, uint64
     AFAM_CUDA(cudaStreamWaitEvent(st, s->host[slot].ready, 0));
     AFAM_CUDA(cudaMemcpyAsync(s->raw_ptr(slot), bytes, nbytes, cudaMemcpyHostToDevice, st));
     return launch_unpack(s, slot, deg, ncp, 1, 0, 1 + 12ull * (ncp + deg), extent, st);
+}
+
+// model.py MicroModel: non-finite control points are a ValueError.  Host
+// scan of the little-endian float32 payload by exponent bits (vectorizes).
+static bool all_finite_le_f32(const uint8_t *p, size_t count) {
+    uint32_t bad = 0;
+    for (size_t i = 0; i < count; i++) {
+        uint32_t u;
+        memcpy(&u, p + 4 * i, 4);
+        bad |= (uint32_t)((u & 0x7f800000u) == 0x7f800000u);
+    }
+    return bad == 0;
+}
+
+int afam_store_put_file(afam_store *s, int32_t slot, const char *path, int32_t ncp, const double extent[6],
+                        int32_t *degree, void *stream) {
+    AFAM_CHECK(s && path, AFAM_E_VALUE, "NULL argument to afam_store_put_file");
+    int rc = check_put(s, slot, 1, ncp, extent);
+    if (rc) return rc;
+    AFAM_CUDA(cudaSetDevice(s->device));
+    int b;
+    {
+        std::lock_guard<std::mutex> lk(s->file_ring_mu);
+        b = s->file_next;
+        s->file_next = (s->file_next + 1) % afam_store::kFileRing;
+    }
+    std::lock_guard<std::mutex> blk(s->file_mu[b]);
+    if (!s->h_file[b]) {
+        AFAM_CUDA(cudaHostAlloc((void **)&s->h_file[b], s->raw_bytes, cudaHostAllocDefault));
+        AFAM_CUDA(cudaEventCreateWithFlags(&s->ev_file[b], cudaEventDisableTiming));
+    } else {
+        AFAM_CUDA(cudaEventSynchronize(s->ev_file[b]));  // the buffer's previous H2D copy is done
+    }
+    // store.load_model_bytes (store.py:33-41): a missing file is a FormatError
+    const int fd = open(path, O_RDONLY);
+    AFAM_CHECK(fd >= 0, AFAM_E_FORMAT, "missing model file %s", path);
+    struct stat sb;
+    if (fstat(fd, &sb) != 0) {
+        close(fd);
+        AFAM_CHECK(false, AFAM_E_FORMAT, "cannot stat model file %s", path);
+    }
+    const uint64_t nbytes = (uint64_t)sb.st_size;
+    if (nbytes < 1 || nbytes > s->raw_bytes) {
+        close(fd);
+        AFAM_CHECK(nbytes >= 1, AFAM_E_FORMAT, "empty micro-model byte string");
+        // longer than any model of this store's max ncp: length mismatch below
+    }
+    const size_t want = std::min<size_t>(nbytes, s->raw_bytes);
+    size_t got = 0;
+    while (got < want) {
+        const ssize_t r = read(fd, s->h_file[b] + got, want - got);
+        if (r < 0 && errno == EINTR) continue;
+        if (r <= 0) break;
+        got += (size_t)r;
+    }
+    close(fd);
+    AFAM_CHECK(got == want, AFAM_E_FORMAT, "short read of model file %s", path);
+    const uint8_t *bytes = s->h_file[b];
+    const int deg = bytes[0];
+    // model.py:123-133
+    AFAM_CHECK(deg < ncp, AFAM_E_FORMAT, "degree byte %d >= ncp %d", deg, ncp);
+    const size_t expected = serialized_size(ncp, deg);
+    AFAM_CHECK(nbytes == expected, AFAM_E_FORMAT,
+               "micro-model length mismatch: expected %zu bytes for ncp=%d, degree=%d, found %llu", expected, ncp,
+               deg, (unsigned long long)nbytes);
+    const uint64_t coff = 1 + 12ull * (ncp + deg);
+    AFAM_CHECK(all_finite_le_f32(bytes + coff, (size_t)ncp * ncp * ncp), AFAM_E_VALUE, "non-finite control points");
+    rc = check_put(s, slot, deg, ncp, extent);
+    if (rc) return rc;
+    if (degree) *degree = deg;
+    cudaStream_t st = (cudaStream_t)stream;
+    std::lock_guard<std::mutex> lk(s->mu);
+    AFAM_CUDA(cudaStreamWaitEvent(st, s->host[slot].ready, 0));
+    AFAM_CUDA(cudaMemcpyAsync(s->raw_ptr(slot), bytes, nbytes, cudaMemcpyHostToDevice, st));
+    AFAM_CUDA(cudaEventRecord(s->ev_file[b], st));
+    return launch_unpack(s, slot, deg, ncp, 1, 0, coff, extent, st);
 }
 
 int afam_store_put(afam_store *s, int32_t slot, int32_t degree, int32_t ncp, const float *knots,

@@ -132,6 +132,26 @@ class DeviceStore:
                                                  int(ncp), ext.ctypes.data_as(C.c_void_p),
                                                  C.c_void_p(stream_handle(stream, self.device))))
 
+    def put_file(self, slot: int, path, ncp: int, extent, stream=None) -> int:
+        """Upload one .mfa file from disk through the native pinned staging
+        ring (afam_store_put_file); returns the file's degree byte."""
+        ext = _extent6(extent)
+        deg = C.c_int32(0)
+        _lib.check(_lib.lib().afam_store_put_file(self._h, int(slot), str(path).encode(), int(ncp),
+                                                  ext.ctypes.data_as(C.c_void_p), C.byref(deg),
+                                                  C.c_void_p(stream_handle(stream, self.device))))
+        return int(deg.value)
+
+    def load_file(self, path, ncp: int, extent, lod: int, stream=None) -> DeviceBlock:
+        slot = self.alloc()
+        try:
+            deg = self.put_file(slot, path, ncp, extent, stream)
+        except Exception:
+            with self._lock:
+                self._free.append(slot)
+            raise
+        return DeviceBlock(self, slot, extent, lod, deg, ncp)
+
     def put_model(self, slot: int, model, stream=None) -> None:
         ctrl = np.ascontiguousarray(np.asarray(model.control, dtype=np.float32).ravel(order="F"))
         knots = np.ascontiguousarray(np.asarray(model.knots, dtype=np.float32))

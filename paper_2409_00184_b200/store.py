@@ -54,12 +54,20 @@ def store_size_bytes(store_root, manifest) -> int:
 
 
 def device_loader(store_root, manifest, dstore, stream=None, source=None):
-    """addr -> DeviceBlock.  `source(addr) -> bytes` overrides the file read
-    (e.g. an in-memory / pinned host store)."""
+    """addr -> DeviceBlock.  Block files are read natively into pinned
+    staging and uploaded asynchronously (afam_store_put_file);
+    `source(addr) -> bytes` overrides the file read (e.g. an in-memory /
+    pinned host store)."""
 
     def load(addr):
-        data = source(addr) if source is not None else load_model_bytes(store_root, manifest, addr)
-        ent = manifest.entries[addr]
+        ent = manifest.entries.get(addr)
+        if source is None:
+            if ent is None or not ent.path:
+                raise FormatError(f"manifest has no model file for block {addr.key}")
+            return dstore.load_file(Path(store_root) / ent.path, ent.ncp, ent.extent, addr.lod, stream)
+        data = source(addr)
+        if ent is None:
+            raise FormatError(f"manifest has no model file for block {addr.key}")
         model.parse_header(data, ent.ncp)  # FormatError semantics of model.deserialize
         buf = np.frombuffer(data, dtype=np.uint8) if not isinstance(data, np.ndarray) else data
         ctrl = np.frombuffer(buf, dtype="<f4", offset=1 + 12 * (ent.ncp + int(buf[0])), count=ent.ncp ** 3)

@@ -82,3 +82,51 @@ def test_linear_prefetch_reduces_misses_on_dolly(disk_store):
     on, _ = _cache(root, man, 500)
     _, frames_on, _ = runtime.replay(povs, man, on, tf, params, prefetch="linear")
     assert off.misses > 0 and on.misses < off.misses
+
+
+def test_file_loader_round_trip_and_errors(disk_store, tmp_path):
+    """afam_store_put_file (native pinned-staging reader) uploads exactly the
+    file's model and keeps store.load_model's error semantics (store.py:33-47,
+    model.py:121-148): missing / truncated file or bad degree byte ->
+    FormatError, non-finite control points -> ValueError."""
+    import shutil
+
+    from paper_2409_00184_b200 import model, store
+    from paper_2409_00184_b200.device import DeviceStore
+    from paper_2409_00184_b200.errors import FormatError
+
+    root, man = disk_store
+    ds = DeviceStore(4, 9)
+    load = store.device_loader(root, man, ds)
+    for a in man.addresses()[:3]:
+        blk = load(a)
+        want = store.load_model(root, man, a)
+        ctrl, knots = ds.read(blk.slot)
+        np.testing.assert_array_equal(ctrl, want.control)
+        np.testing.assert_array_equal(knots, want.knots)
+        assert blk.degree == want.degree and blk.ncp == want.ncp
+        ds.release(blk.slot)
+    # corrupt copies of one block file
+    a = man.addresses()[0]
+    work = tmp_path / "s"
+    shutil.copytree(root, work)
+    path = work / man.entries[a].path
+    data = bytearray(path.read_bytes())
+    bad = store.device_loader(work, man, ds)
+    path.write_bytes(bytes(data[:-4]))
+    with pytest.raises(FormatError, match="length mismatch"):
+        bad(a)
+    path.write_bytes(bytes([man.entries[a].ncp]) + bytes(data[1:]))
+    with pytest.raises(FormatError, match="degree byte"):
+        bad(a)
+    nan = bytearray(data)
+    off = 1 + 12 * (man.entries[a].ncp + data[0])
+    nan[off:off + 4] = np.array([np.nan], dtype="<f4").tobytes()
+    path.write_bytes(bytes(nan))
+    with pytest.raises(ValueError, match="non-finite"):
+        bad(a)
+    path.unlink()
+    with pytest.raises(FormatError, match="missing model file"):
+        bad(a)
+    assert ds.free_slots() == 4
+    assert model is not None
