@@ -77,6 +77,7 @@ SIGNATURES = [
     ("afam_store_create", C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int32, C.c_int32, C.c_double]),
     ("afam_store_destroy", C.c_int, [C.c_void_p]),
     ("afam_store_slots", C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    ("afam_store_put_ds", C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]),
     ("afam_store_put_file", C.c_int, [C.c_void_p, C.c_int32, C.c_char_p, C.c_int32, C.c_void_p, C.c_void_p,
                                       C.c_void_p]),
     ("afam_store_put_mfa", C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_uint64, C.c_int32, C.c_void_p,

@@ -658,6 +658,7 @@ extern "C" int afam_decode_grid_ex(afam_store *s, const int32_t *slots, int32_t 
         for (int b = 0; b < nblk; b++) {
             const int32_t sl = slots[b];
             AFAM_CHECK(sl >= 0 && sl < s->nslots && s->host[sl].valid, AFAM_E_VALUE, "slot %d is empty", sl);
+            AFAM_CHECK(!s->host[sl].ds, AFAM_E_VALUE, "slot %d holds a DS block (no spline to decode)", sl);
             const SlotHost &h = s->host[sl];
             DecodeOp *op = nullptr;
             int rc = get_op(s, h.ncp, h.deg, m, &op);

@@ -42,7 +42,8 @@ struct alignas(16) BlockDesc {
     int32_t nspan;        // ncp - deg
     uint32_t flags;       // AFAM_SLOT_* | kFlagUniform
     float max_abs;
-    int32_t pad[3];
+    int32_t ds_n[3];      // AFAM_SLOT_DS: interior lattice dims (ghost width in `deg`,
+                          // raw samples at `ctrl`, gradient grids [3][nz][ny][nx] at `ctrl4`)
 };
 
 // Internal desc flag: all three knot vectors are the clamped uniform ones
@@ -55,6 +56,7 @@ struct SlotHost {
     bool valid = false;
     bool pending = false;  // upload possibly still in flight (ready not yet observed)
     int32_t ncp = 0, deg = 0;
+    bool ds = false;       // down-sampled raw block (AFAM_SLOT_DS)
     double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     cudaEvent_t ready = nullptr;  // recorded after the upload kernels
 };

@@ -87,6 +87,7 @@ extern "C" int afam_eval_points(afam_store *s, const int32_t *slots, int32_t slo
         std::lock_guard<std::mutex> lk(s->mu);
         if (!slots) {
             AFAM_CHECK(slot >= 0 && slot < s->nslots && s->host[slot].valid, AFAM_E_VALUE, "slot %d is empty", slot);
+            AFAM_CHECK(!s->host[slot].ds, AFAM_E_VALUE, "slot %d holds a DS block (no spline to evaluate)", slot);
             AFAM_CUDA(cudaStreamWaitEvent(st, s->host[slot].ready, 0));
         } else {
             // the caller passes resident slots only; order after every upload still in flight

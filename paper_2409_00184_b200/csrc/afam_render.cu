@@ -735,6 +735,70 @@ __device__ __forceinline__ bool sample_fast(const RenderArgs &A, const TfTable &
     return true;
 }
 
+// ---------------------------------------------------------------------------
+// Down-sampled (DS) baseline blocks (reference downsample.py, DsBlock):
+// values by trilinear interpolation of the raw (ghosted) samples, gradients
+// by trilinear interpolation of the clipped-index central-difference grids
+// (built at upload), both at the continuous interior-lattice index
+// u * (n - 1), u = clip((p - lo) / span, 0, 1) (downsample.py:107-129).
+struct DsFast {
+    const float *samp;  // (nx+2g)(ny+2g)(nz+2g), x fastest
+    const float *grid;  // [3][nz][ny][nx]
+    int32_t n[3], g;
+};
+
+// downsample._trilinear (downsample.py:131-146) on a dims[0] x dims[1] x
+// dims[2] grid (x fastest) at continuous index x, float32, same op order.
+__device__ __forceinline__ float ds_trilinear(const float *__restrict__ grid, const int (&dims)[3],
+                                              const float (&x)[3]) {
+    int i0[3], i1[3];
+    float f[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        const int top = dims[a] - 1;
+        const int b = min(max(__float2int_rd(x[a]), 0), max(top - 1, 0));
+        f[a] = x[a] - (float)b;
+        i0[a] = b;
+        i1[a] = min(b + 1, top);
+    }
+    const size_t sy = (size_t)dims[0], sz = (size_t)dims[0] * dims[1];
+    auto at = [&](int i, int j, int k) { return __ldg(grid + (size_t)k * sz + (size_t)j * sy + i); };
+    const float gx = 1.f - f[0], gy = 1.f - f[1], gz = 1.f - f[2];
+    const float c00 = at(i0[0], i0[1], i0[2]) * gx + at(i1[0], i0[1], i0[2]) * f[0];
+    const float c10 = at(i0[0], i1[1], i0[2]) * gx + at(i1[0], i1[1], i0[2]) * f[0];
+    const float c01 = at(i0[0], i0[1], i1[2]) * gx + at(i1[0], i0[1], i1[2]) * f[0];
+    const float c11 = at(i0[0], i1[1], i1[2]) * gx + at(i1[0], i1[1], i1[2]) * f[0];
+    const float c0 = c00 * gy + c10 * f[1];
+    const float c1 = c01 * gy + c11 * f[1];
+    return c0 * gz + c1 * f[2];
+}
+
+// One DS sample from the predicted continuous interior index tq.
+__device__ __forceinline__ void sample_ds(const RenderArgs &A, const TfTable &tf, const DsFast &b,
+                                          const float (&tq)[3], const ThreadCold &C, March &M) {
+    float xi[3], xs[3];
+    int ds[3], dn[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        xi[a] = fminf(fmaxf(tq[a], 0.f), (float)(b.n[a] - 1));
+        xs[a] = xi[a] + (float)b.g;
+        dn[a] = b.n[a];
+        ds[a] = b.n[a] + 2 * b.g;
+    }
+    const float v = ds_trilinear(b.samp, ds, xs);
+    int bi;
+    float bf;
+    const float vc = fminf(fmaxf(v, A.dom_lo), A.dom_hi);
+    const float atf = tf_alpha(tf, vc, bi, bf);
+    if (!(atf > 0.f)) return;
+    ++M.nshade;
+    const size_t plane = (size_t)dn[0] * dn[1] * dn[2];
+    const float4 gi = C.ginv;  // (n - 1) / span per axis
+    const float g[3] = {ds_trilinear(b.grid, dn, xi) * gi.x, ds_trilinear(b.grid + plane, dn, xi) * gi.y,
+                        ds_trilinear(b.grid + 2 * plane, dn, xi) * gi.z};
+    composite(A, C.vdir, tf_color(tf, vc, bi, bf, atf), g, M);
+}
+
 // One sample on the exact path: float64 position, the reference's span
 // search; float32 (non-uniform knots, P = 1 near a knot) or float64
 // (ill-conditioned slot) arithmetic.  Out of line (rare), so its registers
@@ -855,12 +919,32 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
         bool fast = false;
         CellCache G;
         G.key = nullptr;
+        DsFast dsb;
         while (M.k < M.kend) {
             if (M.own < 0) break;  // render.py:430-436 (reported after the loop)
             if (M.own != cur_own) {
                 cur_own = M.own;
                 slot = __ldg(idx2slot + cur_own);
                 const BlockDesc *dp = descs + slot;
+                if constexpr (FD == 0) {  // DS blocks (AFAM_SLOT_DS)
+                    dsb.samp = (const float *)__ldg((const unsigned long long *)&dp->ctrl);
+                    dsb.grid = (const float *)__ldg((const unsigned long long *)&dp->ctrl4);
+                    dsb.g = __ldg(&dp->deg);
+                    double p[3];
+                    exact_pos(A, R, M.k, p);
+                    float gs[3];
+#pragma unroll
+                    for (int a = 0; a < 3; a++) {
+                        dsb.n[a] = __ldg(&dp->ds_n[a]);
+                        const double sc = __ldg(&dp->inv_span[a]) * (double)(dsb.n[a] - 1);
+                        M.tq0[a] = (float)((p[a] - __ldg(&dp->lo[a])) * sc);
+                        M.dtq[a] = (float)(A.sd * R.d[a] * sc);
+                        gs[a] = (float)sc;
+                    }
+                    C.ginv = make_float4(gs[0], gs[1], gs[2], 0.f);
+                    M.k0f = M.kf;
+                    fast = true;
+                } else {
                 b.ctrl4 = (const float4 *)__ldg((const unsigned long long *)&dp->ctrl4);
                 C.tab32 = (const float *)__ldg((const unsigned long long *)&dp->tab32);
                 b.ncp = __ldg(&dp->ncp);
@@ -881,16 +965,23 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
                 C.ginv = make_float4(__ldg(&dp->inv_span_f[0]), __ldg(&dp->inv_span_f[1]),
                                      __ldg(&dp->inv_span_f[2]), 0.f);
                 M.k0f = M.kf;
+                }
             }
             // one sample per iteration (a flat loop keeps the lanes of a warp
             // in step across their different block runs)
             if (DEBUG) M.h = (M.h ^ (uint64_t)(uint32_t)cur_own) * 1099511628211ULL;
             bool ok = false;
-            if (fast) {
+            if constexpr (FD == 0) {
                 const float dk = M.kf - M.k0f;
                 const float tq[3] = {fmaf(dk, M.dtq[0], M.tq0[0]), fmaf(dk, M.dtq[1], M.tq0[1]),
                                      fmaf(dk, M.dtq[2], M.tq0[2])};
-                ok = sample_fast<FD>(A, tf, b, tq, C, G, M);
+                sample_ds(A, tf, dsb, tq, C, M);
+                ok = true;
+            } else if (fast) {
+                const float dk = M.kf - M.k0f;
+                const float tq[3] = {fmaf(dk, M.dtq[0], M.tq0[0]), fmaf(dk, M.dtq[1], M.tq0[1]),
+                                     fmaf(dk, M.dtq[2], M.tq0[2])};
+                ok = sample_fast<(FD > 0 ? FD : 1)>(A, tf, b, tq, C, G, M);
             }
             if (!ok) {
                 const BlockDesc *dpx = descs + slot;
@@ -1118,6 +1209,7 @@ static void launch_render_v(const LaunchArgs &L, const RenderArgs &A) {
 // the exact path); debug and non-shared-grid launches use the default bounds.
 template <bool DEBUG, bool SMEM>
 static void launch_render(const LaunchArgs &L, const RenderArgs &A, int fd) {
+    if (fd == 0) return launch_render_v<DEBUG, SMEM, 0, 4>(L, A);  // DS blocks
     if (fd == 1) return launch_render_v<DEBUG, SMEM, 1, 4>(L, A);
     if (fd == 2) return launch_render_v<DEBUG, SMEM, 2, 4>(L, A);
     if (DEBUG || !SMEM) return launch_render_v<DEBUG, SMEM, 3, 3>(L, A);
@@ -1232,9 +1324,17 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
         int rc = build_owner_grid(s, slots, nblocks, cells, grid);
         if (rc) return rc;
         for (int b = 0; b < nblocks; b++) AFAM_CUDA(wait_slot(s, slots[b], st));
-        int cnt[4] = {0, 0, 0, 0};
-        for (int b = 0; b < nblocks; b++) cnt[std::min(std::max((int)s->host[slots[b]].deg, 1), 3)]++;
-        fd = cnt[3] >= cnt[2] && cnt[3] >= cnt[1] ? 3 : (cnt[2] >= cnt[1] ? 2 : 1);
+        int cnt[4] = {0, 0, 0, 0}, nds = 0;
+        for (int b = 0; b < nblocks; b++) {
+            if (s->host[slots[b]].ds) {
+                ++nds;
+                continue;
+            }
+            cnt[std::min(std::max((int)s->host[slots[b]].deg, 1), 3)]++;
+        }
+        AFAM_CHECK(nds == 0 || nds == nblocks, AFAM_E_VALUE,
+                   "resident blocks mix spline models and DS blocks (%d of %d DS)", nds, nblocks);
+        fd = nds ? 0 : (cnt[3] >= cnt[2] && cnt[3] >= cnt[1] ? 3 : (cnt[2] >= cnt[1] ? 2 : 1));
     }
     ht.mark();
     A.cells = cells;

@@ -282,9 +282,26 @@ static int launch_unpack(afam_store *s, int32_t slot, int deg, int ncp, uint64_t
     h.pending = true;
     h.ncp = ncp;
     h.deg = deg;
+    h.ds = false;
     for (int a = 0; a < 3; a++) { h.lo[a] = extent[2 * a]; h.hi[a] = extent[2 * a + 1]; }
     AFAM_CUDA(cudaEventRecord(h.ready, st));
     return AFAM_OK;
+}
+
+// DS gradient grids (reference downsample.py:83-105, DsBlock._gradient_grids):
+// at every interior lattice point, per axis, (s[idx+1] - s[idx-1]) / 2 with
+// the indices clipped to the ghosted array, in float64, stored float32.
+__global__ void ds_gradient_kernel(const float *__restrict__ samp, int gx, int gy, int gz, int ghost, int nx, int ny,
+                                   int nz, float *__restrict__ grid) {
+    const int64_t total = (int64_t)nx * ny * nz;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(e % nx), j = (int)((e / nx) % ny), k = (int)(e / ((int64_t)nx * ny));
+        const int I = i + ghost, J = j + ghost, K = k + ghost;
+        auto at = [&](int a, int b, int c) { return (double)samp[((int64_t)c * gy + b) * gx + a]; };
+        grid[e] = (float)((at(min(I + 1, gx - 1), J, K) - at(max(I - 1, 0), J, K)) / 2.0);
+        grid[total + e] = (float)((at(I, min(J + 1, gy - 1), K) - at(I, max(J - 1, 0), K)) / 2.0);
+        grid[2 * total + e] = (float)((at(I, J, min(K + 1, gz - 1)) - at(I, J, max(K - 1, 0))) / 2.0);
+    }
 }
 
 static int check_put(afam_store *s, int32_t slot, int deg, int ncp, const double *extent) {
@@ -396,6 +413,69 @@ int afam_store_put_file(afam_store *s, int32_t slot, const char *path, int32_t n
     return launch_unpack(s, slot, deg, ncp, 1, 0, coff, extent, st);
 }
 
+int afam_store_put_ds(afam_store *s, int32_t slot, const uint8_t *bytes, uint64_t nbytes, const double extent[6],
+                      void *stream) {
+    AFAM_CHECK(s, AFAM_E_VALUE, "store is NULL");
+    AFAM_CHECK(slot >= 0 && slot < s->nslots, AFAM_E_VALUE, "slot %d outside [0, %d)", slot, s->nslots);
+    AFAM_CHECK(bytes && nbytes >= 16, AFAM_E_FORMAT, "truncated block file: header missing");
+    uint32_t hd[4];
+    memcpy(hd, bytes, 16);
+    const uint64_t expected = 16 + (uint64_t)hd[0] * hd[1] * hd[2] * 4;
+    AFAM_CHECK(nbytes == expected, AFAM_E_FORMAT,
+               "block length mismatch: expected %llu bytes for dims (%u,%u,%u), found %llu",
+               (unsigned long long)expected, hd[0], hd[1], hd[2], (unsigned long long)nbytes);
+    const int g = (int)hd[3];
+    AFAM_CHECK(g == 0 || g == 1, AFAM_E_VALUE, "ghost width must be 0 or 1");
+    for (int a = 0; a < 3; a++)
+        AFAM_CHECK((int64_t)hd[a] > 2 * g + 1, AFAM_E_VALUE, "sample array (%u, %u, %u) too small for ghost %d", hd[0],
+                   hd[1], hd[2], g);
+    AFAM_CHECK(extent, AFAM_E_VALUE, "extent is NULL");
+    for (int a = 0; a < 3; a++)
+        AFAM_CHECK(extent[2 * a + 1] > extent[2 * a], AFAM_E_VALUE, "degenerate extent");
+    const int nx = (int)hd[0] - 2 * g, ny = (int)hd[1] - 2 * g, nz = (int)hd[2] - 2 * g;
+    AFAM_CHECK(nbytes <= s->raw_bytes && (uint64_t)3 * nx * ny * nz <= 4 * s->ctrl4_elems, AFAM_E_CAPACITY,
+               "DS block (%u, %u, %u) exceeds the store's slot size (max_ncp %d)", hd[0], hd[1], hd[2], s->max_ncp);
+    cudaStream_t st = (cudaStream_t)stream;
+    std::lock_guard<std::mutex> lk(s->mu);
+    AFAM_CUDA(cudaSetDevice(s->device));
+    AFAM_CUDA(cudaStreamWaitEvent(st, s->host[slot].ready, 0));
+    AFAM_CUDA(cudaMemcpyAsync(s->raw_ptr(slot), bytes, nbytes, cudaMemcpyHostToDevice, st));
+    const float *samp = reinterpret_cast<const float *>(s->raw_ptr(slot) + 16);
+    float *grid = reinterpret_cast<float *>(s->ctrl4_ptr(slot));
+    const int64_t total = (int64_t)nx * ny * nz;
+    ds_gradient_kernel<<<(int)std::min<int64_t>((total + 255) / 256, 1184), 256, 0, st>>>(
+        samp, (int)hd[0], (int)hd[1], (int)hd[2], g, nx, ny, nz, grid);
+    BlockDesc d{};
+    d.ctrl = samp;
+    d.ctrl4 = reinterpret_cast<const float4 *>(grid);
+    for (int a = 0; a < 3; a++) {
+        d.lo[a] = extent[2 * a];
+        d.span[a] = extent[2 * a + 1] - extent[2 * a];
+        d.inv_span[a] = 1.0 / d.span[a];
+        d.lo_f[a] = (float)d.lo[a];
+        d.inv_span_f[a] = (float)d.inv_span[a];
+    }
+    d.deg = g;
+    d.ds_n[0] = nx;
+    d.ds_n[1] = ny;
+    d.ds_n[2] = nz;
+    d.ncp = std::max(nx, std::max(ny, nz));
+    d.flags = AFAM_SLOT_VALID | AFAM_SLOT_DS;
+    // the descriptor goes up by value on the same stream (pinned staging not needed for 144 B:
+    // cudaMemcpyAsync from this stack copy completes before the call returns for pageable memory)
+    AFAM_CUDA(cudaMemcpyAsync(s->d_desc + slot, &d, sizeof(d), cudaMemcpyHostToDevice, st));
+    AFAM_CUDA(cudaGetLastError());
+    SlotHost &h = s->host[slot];
+    h.valid = true;
+    h.pending = true;
+    h.ncp = d.ncp;
+    h.deg = g;
+    h.ds = true;
+    for (int a = 0; a < 3; a++) { h.lo[a] = extent[2 * a]; h.hi[a] = extent[2 * a + 1]; }
+    AFAM_CUDA(cudaEventRecord(h.ready, st));
+    return AFAM_OK;
+}
+
 int afam_store_put(afam_store *s, int32_t slot, int32_t degree, int32_t ncp, const float *knots,
                    const float *ctrl, const double extent[6], void *stream) {
     int rc = check_put(s, slot, degree, ncp, extent);
@@ -443,6 +523,7 @@ int afam_store_read(afam_store *s, int32_t slot, float *ctrl, float *knots) {
     AFAM_CHECK(slot >= 0 && slot < s->nslots, AFAM_E_VALUE, "slot %d outside [0, %d)", slot, s->nslots);
     SlotHost &h = s->host[slot];
     AFAM_CHECK(h.valid, AFAM_E_VALUE, "slot %d is empty", slot);
+    AFAM_CHECK(!h.ds, AFAM_E_VALUE, "slot %d holds a DS block", slot);
     AFAM_CUDA(cudaSetDevice(s->device));
     AFAM_CUDA(cudaEventSynchronize(h.ready));
     const int ncp = h.ncp, P = pitch_for(ncp);

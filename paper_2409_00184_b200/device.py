@@ -44,16 +44,17 @@ def stream_handle(stream=None, device=None) -> int:
 class DeviceBlock:
     """Handle to a model resident in a DeviceStore slot."""
 
-    __slots__ = ("store", "slot", "extent", "lod", "degree", "ncp", "nbytes", "__weakref__")
+    __slots__ = ("store", "slot", "extent", "lod", "degree", "ncp", "nbytes", "kind", "__weakref__")
 
-    def __init__(self, store, slot, extent, lod, degree, ncp):
+    def __init__(self, store, slot, extent, lod, degree, ncp, kind: str = "mfa", nbytes: int | None = None):
         self.store = store
         self.slot = int(slot)
         self.extent = np.asarray(extent, dtype=np.float64).reshape(3, 2)
         self.lod = int(lod)
-        self.degree = int(degree)
-        self.ncp = int(ncp)
-        self.nbytes = serialized_size(self.ncp, self.degree)
+        self.degree = int(degree)  # DS blocks: the ghost width
+        self.ncp = int(ncp)        # DS blocks: the largest interior lattice dim
+        self.kind = kind
+        self.nbytes = int(nbytes) if nbytes is not None else serialized_size(self.ncp, self.degree)
 
     def values_at(self, points):
         from .bspline import eval_device
@@ -152,6 +153,26 @@ class DeviceStore:
             raise
         return DeviceBlock(self, slot, extent, lod, deg, ncp)
 
+    def put_ds(self, slot: int, data, extent, stream=None) -> None:
+        """Upload one DS block file image (afam_store_put_ds)."""
+        buf = np.frombuffer(data, dtype=np.uint8) if not isinstance(data, np.ndarray) else data
+        _lib.check(_lib.lib().afam_store_put_ds(self._h, int(slot), buf.ctypes.data_as(C.c_void_p), buf.size,
+                                                _extent6(extent).ctypes.data_as(C.c_void_p),
+                                                C.c_void_p(stream_handle(stream, self.device))))
+
+    def load_ds(self, data, extent, lod: int, stream=None) -> DeviceBlock:
+        import struct
+
+        slot = self.alloc()
+        try:
+            self.put_ds(slot, data, extent, stream)
+        except Exception:
+            with self._lock:
+                self._free.append(slot)
+            raise
+        nx, ny, nz, g = struct.unpack_from("<4I", bytes(data[:16]))
+        return DeviceBlock(self, slot, extent, lod, g, max(nx, ny, nz) - 2 * g, kind="ds", nbytes=len(data))
+
     def put_model(self, slot: int, model, stream=None) -> None:
         ctrl = np.ascontiguousarray(np.asarray(model.control, dtype=np.float32).ravel(order="F"))
         knots = np.ascontiguousarray(np.asarray(model.knots, dtype=np.float32))
@@ -240,6 +261,26 @@ class _ScratchStore:
             self.lru[key] = (ref, blk)
             return blk
 
+    def get_ds(self, block, serialize) -> DeviceBlock:
+        """Upload (or reuse) a host DS block, keyed like get()."""
+        key = id(block)
+        with self.lock:
+            hit = self.lru.get(key)
+            if hit is not None and hit[0] is not None and hit[0]() is block:
+                self.lru.move_to_end(key)
+                return hit[1]
+            if hit is not None:
+                self._drop(key)
+            while self.store.free_slots() == 0:
+                self._drop(next(iter(self.lru)))
+            blk = self.store.load_ds(serialize(block), block.extent, block.lod)
+            try:
+                ref = weakref.ref(block)
+            except TypeError:
+                ref = None
+            self.lru[key] = (ref, blk)
+            return blk
+
     def _drop(self, key):
         _, blk = self.lru.pop(key)
         self.store.release(blk.slot)
@@ -266,10 +307,21 @@ def as_device_blocks(values, device: int = 0):
         return next(iter(stores.values())), [v.slot for v in values]
     if not hosts and not values:
         return scratch_store(9, device).store, []
+    from .downsample import DsBlock, serialize_ds
+
+    if hosts and all(isinstance(v, DsBlock) for v in hosts):  # DS baseline blocks
+        edge = max(max(v.samples.shape) for v in hosts) if hosts else 9
+        sc = scratch_store(edge, device)
+        slots = []
+        for v in values:
+            if isinstance(v, DeviceBlock):
+                raise TypeError("cannot mix resident DeviceBlocks with host DS blocks in one render")
+            slots.append(sc.get_ds(v, serialize_ds).slot)
+        return sc.store, slots
     for v in hosts:
         if not (hasattr(v, "control") and hasattr(v, "knots") and hasattr(v, "degree") and hasattr(v, "extent")):
-            raise TypeError(f"block {type(v).__name__} is not a spline micro-model; the B200 path decodes "
-                            "MicroModel/DeviceBlock blocks only (no CPU fallback)")
+            raise TypeError(f"block {type(v).__name__} is not a spline micro-model or DS block; the B200 path "
+                            "decodes MicroModel/DsBlock/DeviceBlock blocks only (no CPU fallback)")
     max_ncp = max(int(v.ncp) if isinstance(v, DeviceBlock) else int(np.asarray(v.control).shape[0]) for v in values)
     sc = scratch_store(max_ncp, device)
     pinned = set(id(v) for v in values)

@@ -1,0 +1,116 @@
+"""Down-sampled (DS) baseline (reference downsample.py): store format and
+build on the CPU; GPU render of DS blocks (AFAM_SLOT_DS, trilinear values
+and central-difference gradients) against the reference's own frames
+(tests/golden/gen_ds_golden.py)."""
+
+import json
+
+import numpy as np
+import pytest
+
+from helpers import npz
+
+Z = npz("ds.npz")
+NAMES = [str(n) for n in Z["names"]]
+
+
+def _store(g):
+    from paper_2409_00184_b200 import downsample, partition
+
+    man = partition.LODManifest.from_json(json.loads(bytes(Z[f"store_g{g}_manifest"]).decode()))
+    blob = bytes(Z[f"store_g{g}_blob"])
+    offs = Z[f"store_g{g}_offsets"]
+    raw, blocks = {}, {}
+    for i, key in enumerate(Z[f"store_g{g}_keys"]):
+        a = partition.BlockAddress.from_key(str(key))
+        raw[a] = blob[offs[i]:offs[i + 1]]
+        blocks[a] = downsample.deserialize_ds(raw[a], man.entries[a].extent, a.lod)
+    return man, raw, blocks
+
+
+def test_ds_store_round_trip_and_errors():
+    from paper_2409_00184_b200 import downsample
+    from paper_2409_00184_b200.errors import FormatError
+
+    man, raw, blocks = _store(1)
+    assert man.kind == "ds" and man.ghost == 1
+    for a, data in raw.items():
+        assert downsample.serialize_ds(blocks[a]) == data
+        assert blocks[a].nbytes == len(data) == man.entries[a].nbytes
+    data = next(iter(raw.values()))
+    with pytest.raises(FormatError, match="header missing"):
+        downsample.deserialize_ds(data[:8], [[-1, 1]] * 3, 1)
+    with pytest.raises(FormatError, match="length mismatch"):
+        downsample.deserialize_ds(data[:-4], [[-1, 1]] * 3, 1)
+    bad = bytearray(data)
+    bad[12:16] = (2).to_bytes(4, "little")
+    with pytest.raises(ValueError, match="ghost width"):
+        downsample.deserialize_ds(bytes(bad), [[-1, 1]] * 3, 1)
+
+
+def test_build_ds_store_matches_reference_bytes():
+    """build_ds_store on the golden 33^3 volume reproduces the reference's
+    block files byte for byte (ghosted, edge-clamped strided samples)."""
+    from types import SimpleNamespace
+
+    from paper_2409_00184_b200 import downsample
+
+    ez = npz("encoder.npz")
+    vol = SimpleNamespace(samples=ez["vol_samples"], bounds=ez["vol_bounds"])
+    for g in (0, 1):
+        man_ref, raw, _ = _store(g)
+        man, blocks = downsample.build_ds_store(vol, levels=2, micro_dims=9, coarsest=2, ghost=g)
+        assert sorted(blocks) == sorted(raw)
+        for a in raw:
+            assert downsample.serialize_ds(blocks[a]) == raw[a], (g, a)
+            np.testing.assert_array_equal(man.entries[a].extent, man_ref.entries[a].extent)
+
+
+def _cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", NAMES)
+def test_render_ds_vs_reference_frames(name, oracle):
+    _cuda()
+    from paper_2409_00184_b200 import render
+
+    g = int(Z[f"{name}_ghost"])
+    man, _, blocks = _store(g)
+    pv = Z[f"{name}_pov"]
+    pov = render.PointOfView(pv[0:3], pv[3:6], pv[6:9], float(pv[9]))
+    w, h, sd, omax, ref, near, amb, dif, spe, shi = [float(v) for v in Z[f"{name}_params"]]
+    params = render.RenderParams(width=int(w), height=int(h), sample_distance=sd, o_max=omax,
+                                 reference_step=None if np.isnan(ref) else ref, near=near, ambient=amb,
+                                 diffuse=dif, specular=spe, shininess=shi)
+    vis = render.select_visible(pov, man, params.aspect)
+    assert [(a.lod, *a.ijk) for a in vis] == [tuple(r) for r in Z[f"{name}_vis"]]
+    frame = render.render(pov, {a: blocks[a] for a in vis}, render.TransferFunction.ml_preset(), params)
+    assert render.render.last_stats["samples"] == int(Z[f"{name}_samples"])
+    assert oracle.psnr(frame.rgba, Z[f"{name}_rgba"]) >= 60.0
+
+
+@pytest.mark.gpu
+def test_ds_device_loader_replay(tmp_path):
+    """make_loader on a DS store with a DeviceStore: HBM-resident DS slots,
+    replay frames equal a direct render of host DS blocks."""
+    _cuda()
+    from paper_2409_00184_b200 import downsample, render, runtime
+    from paper_2409_00184_b200.device import DeviceStore
+
+    man, raw, blocks = _store(1)
+    downsample.write_ds_store(tmp_path, man, raw)
+    ds = DeviceStore(20, 11)
+    cache = runtime.ModelCache(16, runtime.make_loader(tmp_path, man, ds))
+    povs = runtime.orbit_trajectory(3, radius=2.5)
+    params = render.RenderParams(width=24, height=24, sample_distance=0.02)
+    tf = render.TransferFunction.ml_preset()
+    _, frames, agg = runtime.replay(povs, man, cache, tf, params, prefetch="off")
+    assert agg["frames"] == 3
+    for pov, fr in zip(povs, frames):
+        vis = render.select_visible(pov, man, params.aspect)
+        want = render.render(pov, {a: blocks[a] for a in vis}, tf, params)
+        np.testing.assert_array_equal(fr.rgba, want.rgba)
