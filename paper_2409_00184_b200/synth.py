@@ -171,3 +171,34 @@ def field_store(levels: int, coarsest: int, micro: int, degree: int, ncp_of, fn=
         ent = man.entries[addr]
         ent.ncp, ent.nbytes, ent.path = ncp, len(blob), addr.file_name
     return man, blobs
+
+
+def turbulence_ds_blocks(addrs, levels: int = 4, coarsest: int = 2, micro: int = 65, ghost: int = 1, K: int = 48,
+                         seed: int = SEED, kmax: float = 12.0):
+    """{addr: DS block file image} of the same synthetic turbulence field as
+    turbulence_store, sampled directly on each block's micro lattice plus the
+    ghost layer (clamped at the volume faces, as downsample.build_ds_store),
+    for the DS-vs-spline comparison (paper Fig. 15)."""
+    import struct
+
+    man = skeleton(levels, coarsest, micro)
+    kvec, A = _modes(K, seed, kmax)
+    rng = np.random.default_rng(seed + 1)
+    pts = rng.uniform(-1, 1, size=(1 << 15, 3))
+    vals = np.real(np.exp(2j * np.pi * pts @ kvec.T) @ A)
+    vmin, vmax = float(vals.min()), float(vals.max())
+    scale = 0.96 / (vmax - vmin)
+    offset = 0.02 - vmin * scale
+    out = {}
+    for addr in addrs:
+        ext = man.entries[addr].extent
+        E = []
+        for a in range(3):
+            step = (ext[a, 1] - ext[a, 0]) / (micro - 1)
+            xs = np.clip(ext[a, 0] + step * np.arange(-ghost, micro + ghost), -1.0, 1.0)
+            E.append(np.exp(2j * np.pi * np.outer(xs, kvec[:, a])))  # (n, K)
+        n = micro + 2 * ghost
+        G = (E[1][:, None, :] * E[2][None, :, :]).reshape(n * n, -1)
+        v = np.real((E[0] * A[None, :]) @ G.T).reshape(n, n, n) * scale + offset
+        out[addr] = struct.pack("<4I", n, n, n, ghost) + v.astype("<f4").ravel(order="F").tobytes()
+    return out
