@@ -31,6 +31,8 @@ struct FitJob {
     const float *samples;   // [m][m][m] float32 (block b of the batch)
     const double *op_fit;   // [ncp][m]
     const double *op_dec;   // [m][ncp]
+    const double *opT_fit;  // [m][ncp4] transposed, zero-padded
+    const double *opT_dec;  // [ncp][m4]
     double *buf0, *buf1;    // ping-pong intermediates (>= m^3 doubles each)
     float *ctrl;            // nullable: [ncp][ncp][ncp] float32 coefficients out
     double *sse;            // sum of squared errors (accumulated)
@@ -169,10 +171,10 @@ __global__ void __launch_bounds__(kFitThreads, 2) contract_tiled_kernel(const Fi
     double *sOpT = reinterpret_cast<double *>(smem);     // [n0][np]
     double *sIn = sOpT + (size_t)n0 * np;                // [n0][kFitRT2]
     double *sOut = sIn + (size_t)n0 * kFitRT2;           // [kFitRT2][nout]
-    const double *op = dec ? J.op_dec : J.op_fit;        // [nout][n0]
-    for (int e = threadIdx.x; e < n0 * np; e += blockDim.x) {
-        const int k = e / np, a = e % np;
-        sOpT[e] = a < nout ? op[(size_t)a * n0 + k] : 0.0;
+    {  // transposed, padded operator [n0][np]: a straight 16-byte copy
+        const double2 *src = reinterpret_cast<const double2 *>(dec ? J.opT_dec : J.opT_fit);
+        double2 *dst = reinterpret_cast<double2 *>(sOpT);
+        for (int e = threadIdx.x; e < n0 * np / 2; e += blockDim.x) dst[e] = src[e];
     }
     const double *in64 = nullptr;
     switch (stage) {
@@ -325,6 +327,18 @@ static int get_fit_op(afam_store *s, int ncp, int deg, int m, FitOp **op) {
         AFAM_CUDA(cudaMalloc(&o.dec, Bd.size() * sizeof(double)));
         AFAM_CUDA(cudaMemcpy(o.fit, F.data(), F.size() * sizeof(double), cudaMemcpyHostToDevice));
         AFAM_CUDA(cudaMemcpy(o.dec, Bd.data(), Bd.size() * sizeof(double), cudaMemcpyHostToDevice));
+        // transposed, zero-padded copies for the tiled kernel
+        const int ncp4 = (ncp + 3) & ~3, m4 = (m + 3) & ~3;
+        std::vector<double> FT((size_t)m * ncp4, 0.0), BT((size_t)ncp * m4, 0.0);
+        for (int a = 0; a < ncp; a++)
+            for (int i = 0; i < m; i++) {
+                FT[(size_t)i * ncp4 + a] = F[(size_t)a * m + i];
+                BT[(size_t)a * m4 + i] = Bd[(size_t)i * ncp + a];
+            }
+        AFAM_CUDA(cudaMalloc(&o.fitT, FT.size() * sizeof(double)));
+        AFAM_CUDA(cudaMalloc(&o.decT, BT.size() * sizeof(double)));
+        AFAM_CUDA(cudaMemcpy(o.fitT, FT.data(), FT.size() * sizeof(double), cudaMemcpyHostToDevice));
+        AFAM_CUDA(cudaMemcpy(o.decT, BT.data(), BT.size() * sizeof(double), cudaMemcpyHostToDevice));
         it = s->fit_ops.emplace(key, o).first;
     }
     *op = &it->second;
@@ -380,6 +394,8 @@ extern "C" int afam_fit_rmse(afam_store *s, const float *samples, int32_t nblk, 
             J.samples = samples + (size_t)b * cube;
             J.op_fit = op->fit;
             J.op_dec = op->dec;
+            J.opT_fit = op->fitT;
+            J.opT_dec = op->decT;
             J.buf0 = work + (size_t)j * 2 * cube;
             J.buf1 = J.buf0 + cube;
             J.ctrl = ctrl ? ctrl + ctrl_off[j] : nullptr;

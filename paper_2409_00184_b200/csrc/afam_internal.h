@@ -78,8 +78,10 @@ struct DecodeOp {  // banded collocation matrix of bspline.py:98-125 for (ncp, d
 void host_band(int ncp, int deg, int m, std::vector<double> &b, std::vector<int32_t> &col0);
 
 struct FitOp {  // endpoint-pinned least-squares fit operator (bspline.py:109-159), device
-    double *fit = nullptr;  // [ncp][m]: coefficients = fit @ samples along one axis
-    double *dec = nullptr;  // [m][ncp]: dense collocation matrix (decode along one axis)
+    double *fit = nullptr;   // [ncp][m]: coefficients = fit @ samples along one axis
+    double *dec = nullptr;   // [m][ncp]: dense collocation matrix (decode along one axis)
+    double *fitT = nullptr;  // [m][ncp rounded up to 4]: fit transposed, zero-padded (tiled kernel)
+    double *decT = nullptr;  // [ncp][m rounded up to 4]: dec transposed, zero-padded
 };
 
 }  // namespace afam

@@ -229,6 +229,8 @@ int afam_store_destroy(afam_store *s) {
     for (auto &kv : s->fit_ops) {
         cudaFree(kv.second.fit);
         cudaFree(kv.second.dec);
+        cudaFree(kv.second.fitT);
+        cudaFree(kv.second.decT);
     }
     cudaFree(s->arena);
     cudaFree(s->d_desc);

@@ -88,16 +88,21 @@ def fit_rmse_batch(samples, degree: int, jobs, want_ctrl: bool = False, device: 
     import torch
 
     _lib.require_device()
-    blocks = [np.ascontiguousarray(s, dtype=np.float32) for s in samples]
-    if not blocks:
-        return np.zeros(0), ([] if want_ctrl else None)
-    m = blocks[0].shape[0]
-    if any(b.shape != (m, m, m) for b in blocks):
-        raise ValueError("fit_rmse_batch needs cubic sample grids of one edge length")
+    dev = torch.device("cuda", device)
+    if isinstance(samples, torch.Tensor):  # already resident: (nblk, m, m, m) float32 on `device`
+        d_samples = samples.contiguous()
+        nblk, m = int(d_samples.shape[0]), int(d_samples.shape[1])
+    else:
+        blocks = [np.ascontiguousarray(s, dtype=np.float32) for s in samples]
+        if not blocks:
+            return np.zeros(0), ([] if want_ctrl else None)
+        m = blocks[0].shape[0]
+        if any(b.shape != (m, m, m) for b in blocks):
+            raise ValueError("fit_rmse_batch needs cubic sample grids of one edge length")
+        nblk = len(blocks)
+        d_samples = torch.from_numpy(np.stack(blocks)).to(dev)
     jobs = [(int(b), int(n)) for b, n in jobs]
     store = _op_store(device)
-    dev = torch.device("cuda", device)
-    d_samples = torch.from_numpy(np.stack(blocks)).to(dev)
     per = max(1, min(65535, WORK_BYTES // (16 * m ** 3)))
     rmse = np.zeros(len(jobs))
     ctrls = [] if want_ctrl else None
@@ -114,7 +119,7 @@ def fit_rmse_batch(samples, degree: int, jobs, want_ctrl: bool = False, device: 
                 offs = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
                 d_ctrl = torch.empty(int(sizes.sum()), dtype=torch.float32, device=dev)
             _lib.check(_lib.lib().afam_fit_rmse(
-                store.handle, C.c_void_p(d_samples.data_ptr()), len(blocks), m, int(degree),
+                store.handle, C.c_void_p(d_samples.data_ptr()), nblk, m, int(degree),
                 jb.ctypes.data_as(C.c_void_p), jn.ctypes.data_as(C.c_void_p), len(chunk),
                 out.ctypes.data_as(C.c_void_p), None if d_ctrl is None else C.c_void_p(d_ctrl.data_ptr()),
                 None if offs is None else offs.ctypes.data_as(C.c_void_p), C.c_void_p(stream.cuda_stream)))
@@ -151,6 +156,13 @@ def search_blocks(samples, error_bound: float, degree: int, extents=None, lods=N
     extents = extents if extents is not None else [((0.0, 1.0),) * 3] * nb
     lods = lods if lods is not None else [1] * nb
     profiles = [ErrorProfile() for _ in range(nb)]
+    import torch
+
+    _lib.require_device()
+    if any(np.shape(b) != (n, n, n) for b in blocks):
+        raise ValueError("search_blocks needs cubic sample grids of one edge length")
+    blocks = torch.from_numpy(np.stack([np.asarray(b, dtype=np.float32) for b in blocks])).to(
+        torch.device("cuda", device))  # uploaded once for every probe round
     if assume_monotone:
         lo, hi = [ncp_min] * nb, [n] * nb
         while True:

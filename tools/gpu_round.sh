@@ -1,5 +1,6 @@
-# One GPU session: parity tests, bench (ours + reference arm), kernel microbenchmarks,
-# ncu launch list and --set full captures of K2 and K3. Outputs under gpurun_out/.
+# One GPU session: parity tests, smoke, bench (ours + reference arm), kernel
+# microbenchmarks, ncu launch list and --set full captures of K2, K3 and the
+# encoder kernel.  Outputs under gpurun_out/.
 cd $GRAFT_REPO_ROOT
 TAG=${TAG:-r01}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu,power.draw --format=csv
@@ -8,7 +9,11 @@ timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; echo "bench rc=$?"
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err; echo "ref rc=$?"
 timeout 600 python tools/bench_kernels.py > gpurun_out/kernels_$TAG.jsonl 2> gpurun_out/kernels_$TAG.err; echo "kernels rc=$?"
+AFAM_DECODE_TC=1 timeout 600 python tools/bench_kernels.py 2>/dev/null | head -1 | sed 's/"K3 decode_grid"/"K3 decode_grid (tensor cores)"/' >> gpurun_out/kernels_$TAG.jsonl
+timeout 600 python tools/bench_encoder.py >> gpurun_out/kernels_$TAG.jsonl 2>> gpurun_out/kernels_$TAG.err
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/bench_ncu_$TAG.log 2>&1; echo "ncu list rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:render_kernel -s 3 -c 1 -o gpurun_out/prof_render_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_render_$TAG.log 2>&1; echo "ncu render rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:decode -c 2 -o gpurun_out/prof_decode_$TAG python tools/bench_kernels.py > gpurun_out/ncu_decode_$TAG.log 2>&1; echo "ncu decode rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:decode_grid_kernel -c 1 -o gpurun_out/prof_decode_$TAG python tools/bench_kernels.py > gpurun_out/ncu_decode_$TAG.log 2>&1; echo "ncu decode rc=$?"
+AFAM_DECODE_TC=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:decode_tc -c 1 -o gpurun_out/prof_decode_tc_$TAG python tools/bench_kernels.py > gpurun_out/ncu_decode_tc_$TAG.log 2>&1; echo "ncu decode tc rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:contract_tiled -s 12 -c 1 -o gpurun_out/prof_encoder_$TAG python tools/bench_encoder.py > gpurun_out/ncu_encoder_$TAG.log 2>&1; echo "ncu encoder rc=$?"
 head -c 3000 gpurun_out/bench_$TAG.json; echo; head -c 1500 gpurun_out/bench_ref_$TAG.json; echo; cat gpurun_out/kernels_$TAG.jsonl
