@@ -32,11 +32,19 @@ DOMAIN_LO, DOMAIN_HI = -1.0, 1.0
 
 def pov_basis(pov):
     """(forward, right, up) of any pov-like object with the reference's numpy
-    op order (render.py:68-73); direction is used as stored (already unit)."""
+    op order (render.py:68-73); direction is used as stored (already unit).
+    Cached on PointOfView objects (immutable), which the replay loop asks
+    for several times per frame."""
+    cached = getattr(pov, "_afam_basis", None)
+    if cached is not None:
+        return cached
     fwd = np.asarray(pov.direction, dtype=np.float64)
     right = np.cross(fwd, np.asarray(pov.up, dtype=np.float64))
     right = right / np.linalg.norm(right)
-    return fwd, right, np.cross(right, fwd)
+    out = (fwd, right, np.cross(right, fwd))
+    if isinstance(pov, PointOfView):
+        object.__setattr__(pov, "_afam_basis", out)
+    return out
 
 
 @dataclass(frozen=True, eq=False)
@@ -223,6 +231,11 @@ class NativeManifest:
         self.levels = manifest.levels
         self.capacity = int(sum(int(b) ** 3 for b in bpa))
         self._out = np.zeros((self.capacity, 4), dtype=np.int32)
+        # interned addresses: flat index off[lod-1] + (i*bpa + j)*bpa + k -> BlockAddress
+        self._bpa = np.asarray(bpa, dtype=np.int64)
+        self._off = np.concatenate([[0], np.cumsum(self._bpa ** 3)[:-1]]).astype(np.int64)
+        self._addrs = [BlockAddress(l + 1, (i, j, k)) for l, b in enumerate(bpa.tolist())
+                       for i in range(b) for j in range(b) for k in range(b)]
 
     def __del__(self):
         try:
@@ -243,7 +256,11 @@ class NativeManifest:
             u.ctypes.data_as(C.c_void_p), math.tan(math.radians(pov.fov_y) / 2.0), float(aspect), float(near),
             None if rr is None else rr.ctypes.data_as(C.c_void_p), 0 if rr is None else rr.size,
             self._out.ctypes.data_as(C.c_void_p), self.capacity, C.byref(n)))
-        return [BlockAddress(int(q[0]), (int(q[1]), int(q[2]), int(q[3]))) for q in self._out[: n.value]]
+        q = self._out[: n.value].astype(np.int64)
+        lv = q[:, 0] - 1
+        b = self._bpa[lv]
+        idx = self._off[lv] + (q[:, 1] * b + q[:, 2]) * b + q[:, 3]
+        return [self._addrs[t] for t in idx.tolist()]
 
 
 def _native(manifest) -> NativeManifest:
