@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-rows", type=int, default=24, help="rows of the frame in the CPU sample")
+    ap.add_argument("--gather", default="fused", choices=["fused", "nccl"],
+                    help="N > 1: band gather fused into the render kernel (peer stores) or an NCCL gather")
     return ap.parse_args()
 
 
@@ -227,23 +229,48 @@ def run_ours(args, rank, world, local_rank):
                             device=dev)
     from paper_2409_00184_b200 import tiles
 
+    # N > 1: the band gather is fused into the render kernel -- every rank
+    # stores its pixels straight into rank 0's frame over NVLink (CUDA IPC,
+    # tiles.PeerFrame); the NCCL gather is the fallback (or --gather nccl)
+    peer = None
+    if world > 1 and args.gather == "fused":
+        ok = torch.ones(1, device=dev)
+        try:
+            peer = tiles.PeerFrame(S, S, device=local_rank)
+        except Exception as exc:  # noqa: BLE001
+            print(f"rank {rank}: fused gather unavailable ({exc}); using the NCCL gather", file=sys.stderr)
+            ok.zero_()
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if ok.item() < 1:
+            if peer is not None:
+                peer.close()
+            peer = None
+    gather_kind = "single GPU" if world == 1 else ("fused: peer stores over NVLink" if peer else "NCCL gather")
+
     def step(k):
-        """One frame: render this rank's bands, gather them to rank 0.  Device
-        time = the render kernels (CUDA events recorded by afam_render on the
-        render stream around its launches) + the NCCL gather (events on the
-        same stream).  Host preparation is reported separately."""
+        """One frame: render this rank's bands and bring them to rank 0.
+        Device time = the render kernels (CUDA events recorded by afam_render
+        on the render stream around its launches) + the NCCL gather when the
+        gather is not fused (events on the same stream).  Host preparation is
+        reported separately."""
         pov = povs[k % len(povs)]
         vis = render.select_visible(pov, man, params.aspect)
         blocks = {a: resident_all[a] for a in vis}
         ev0 = torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
-        _, info, _ = render.render_part(pov, blocks, tf, params, band_rows=band, nparts=world, part=rank,
-                                        device=local_rank, out=frame_out)
+        if peer is not None:
+            _, info, _ = render.render_part(pov, blocks, tf, params, band_rows=band, nparts=world, part=rank,
+                                            device=local_rank, out_ptr=peer.ptr)
+        else:
+            _, info, _ = render.render_part(pov, blocks, tf, params, band_rows=band, nparts=world, part=rank,
+                                            device=local_rank, out=frame_out)
         ev1, ev2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev1.record(stream)
-        if world > 1:  # NCCL gather of the RGBA8 bands to rank 0 + un-permute there
+        if world > 1 and peer is None:  # NCCL gather of the RGBA8 bands to rank 0 + un-permute there
             tiles.gather_bands(frame_out, S, band)
         ev2.record(stream)
+        if peer is not None:
+            dist.barrier()  # every rank's kernel (and its peer stores) done before rank 0 uses the frame
         return ev0, ev1, ev2, info, len(vis)
 
     times, ktimes, envelope, samples, fp64s, shaded, nvis = [], [], [], 0, 0, 0, []
@@ -310,7 +337,7 @@ def run_ours(args, rank, world, local_rank):
               "scaling": "strong", "vs_baseline": None, "dtype": "f32 (f64 geometry; f64 decode on "
                                                                  "ill-conditioned blocks)",
               "data": "synthetic (seeded turbulence, fitted like the reference encoder)",
-              "config": dict(WORKLOAD, parallelism=f"image bands x{world}", frame_ms=step_ms,
+              "config": dict(WORKLOAD, parallelism=f"image bands x{world}", gather=gather_kind, frame_ms=step_ms,
                              kernel_ms=kern_ms, host_envelope_ms=float(np.mean(envelope)),
                              visible_blocks_mean=float(np.mean(nvis)),
                              fp64_sample_frac=total_fp64 / max(1.0, total_samples), gen_s=round(gen_s, 1),
@@ -321,6 +348,9 @@ def run_ours(args, rank, world, local_rank):
     # -- e2e through the public runtime API: ModelCache(200) + linear prefetch, pinned host source
     if not args.no_e2e:
         result["e2e"] = run_e2e(args, man, blobs, povs, tf, params, rank, world, local_rank)
+    if peer is not None:
+        dist.barrier()
+        peer.close()
     del resident_all, ds
     return result, man, blobs
 

@@ -49,6 +49,7 @@ extern "C" {
 /* Per-slot flags (afam_store_info). */
 #define AFAM_SLOT_VALID 1u
 #define AFAM_SLOT_FP64 2u     /* ill-conditioned: evaluated in float64 */
+#define AFAM_SLOT_DS 4u       /* down-sampled raw block (trilinear), afam_store_put_ds */
 
 const char *afam_last_error(void);
 int afam_version(void);
@@ -79,6 +80,17 @@ int afam_store_slots(const afam_store *s, int32_t *slots, int32_t *max_ncp);
  */
 int afam_store_put_mfa(afam_store *s, int32_t slot, const uint8_t *bytes, uint64_t nbytes, int32_t ncp,
                        const double extent[6], void *stream);
+
+/* Upload one down-sampled (DS) block file image (reference downsample.py:
+ * 16-byte header of uint32 (nx, ny, nz, ghost) then nx*ny*nz float32 LE,
+ * x fastest; serialize_ds / deserialize_ds, downsample.py:140-161) into
+ * `slot`.  Errors as deserialize_ds / DsBlock: truncated header or length
+ * mismatch -> AFAM_E_FORMAT; ghost not 0/1 or dims <= 2*ghost+1 ->
+ * AFAM_E_VALUE; larger than a slot -> AFAM_E_CAPACITY.  The device keeps the
+ * raw samples and builds the clipped-index central-difference gradient
+ * grids (DsBlock._gradient_grids) for the trilinear render path. */
+int afam_store_put_ds(afam_store *s, int32_t slot, const uint8_t *bytes, uint64_t nbytes, const double extent[6],
+                      void *stream);
 
 /* Upload one .mfa file straight from disk: read into a pinned staging ring
  * (no pageable copy), validate like store.load_model (missing file, length,
@@ -205,6 +217,9 @@ typedef struct {
 } afam_frame;
 
 #define AFAM_RENDER_DEBUG 1u   /* write per-ray sample counts + owner hashes */
+#define AFAM_RENDER_FULL_FRAME 2u  /* rgba is the whole height x width frame: this part's rows land
+                                      at their frame rows (e.g. another GPU's frame buffer mapped
+                                      over NVLink with afam_ipc_open) */
 
 typedef struct {
     uint64_t samples;      /* decoded samples (value+gradient evaluations) */
@@ -227,6 +242,20 @@ typedef struct {
  */
 int afam_render(afam_store *s, const afam_frame *frame, const int32_t *slots, int32_t nblocks, uint8_t *rgba,
                 afam_render_stats *stats, int32_t *nsamp, uint64_t *ohash, void *stream);
+
+/* CUDA IPC of a device buffer between the processes of one node (the fused
+ * image-band gather: every rank's render kernel stores its pixels straight
+ * into rank 0's frame buffer over NVLink).  handle: 64 bytes.  afam_ipc_open
+ * maps a peer's buffer (peer access enabled lazily); afam_ipc_close unmaps. */
+int afam_ipc_get_handle(const void *dev_ptr, uint8_t *handle);
+int afam_ipc_open(const uint8_t *handle, int32_t device, void **dev_ptr);
+int afam_ipc_close(void *dev_ptr);
+/* A plain cudaMalloc'ed device buffer (its own allocation, so its IPC handle
+ * maps exactly this buffer) and its release. */
+int afam_device_alloc(int32_t device, uint64_t bytes, void **dev_ptr);
+int afam_device_free(void *dev_ptr);
+/* Synchronous device -> host copy (reading such a buffer back). */
+int afam_copy_to_host(void *host, const void *dev_ptr, uint64_t bytes);
 
 /* Device time (ms) of the kernels of the last afam_render on this store
  * (CUDA events recorded on its stream around the launches); waits for them. */

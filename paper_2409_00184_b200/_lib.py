@@ -28,6 +28,7 @@ AFAM_SLOT_FP64 = 2
 AFAM_EVAL_PARAM = 1
 AFAM_EVAL_OUT_F64 = 2
 AFAM_RENDER_DEBUG = 1
+AFAM_RENDER_FULL_FRAME = 2
 
 _lib = None
 
@@ -103,6 +104,12 @@ SIGNATURES = [
                                       C.POINTER(C.c_int32)]),
     ("afam_render", C.c_int, [C.c_void_p, C.POINTER(AfamFrame), C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
                               C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("afam_ipc_get_handle", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("afam_ipc_open", C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p)]),
+    ("afam_ipc_close", C.c_int, [C.c_void_p]),
+    ("afam_device_alloc", C.c_int, [C.c_int32, C.c_uint64, C.POINTER(C.c_void_p)]),
+    ("afam_device_free", C.c_int, [C.c_void_p]),
+    ("afam_copy_to_host", C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
     ("afam_render_elapsed", C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
     ("afam_frame_rows", C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
     ("afam_owner_grid", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.c_void_p,

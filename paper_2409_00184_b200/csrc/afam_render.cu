@@ -1018,7 +1018,9 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
         px4.z = (unsigned char)min(max(__float2int_rn(M.C2 * 255.f), 0), 255);
         px4.w = (unsigned char)min(max(__float2int_rn(M.Aacc * 255.f), 0), 255);
         const int64_t local = (int64_t)lr * A.width + j;
-        reinterpret_cast<uchar4 *>(rgba)[local] = px4;
+        // full-frame output: this part's rows at their frame rows (a peer GPU's frame over NVLink)
+        const int64_t dst = (A.flags & AFAM_RENDER_FULL_FRAME) ? (int64_t)i * A.width + j : local;
+        reinterpret_cast<uchar4 *>(rgba)[dst] = px4;
         if (DEBUG) {
             nsamp[local] = (int32_t)ns;
             ohash[local] = M.h;
@@ -1303,7 +1305,7 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
         if ((double)of > F->o_max) of = std::nextafter(of, -INFINITY);
         A.o_max_f = of;
     }
-    A.flags = F->flags & AFAM_RENDER_DEBUG;
+    A.flags = F->flags & (AFAM_RENDER_DEBUG | AFAM_RENDER_FULL_FRAME);
     {
         static const bool force_exact = [] {
             const char *e = getenv("AFAM_RENDER_FORCE_EXACT");
@@ -1402,6 +1404,48 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
     AFAM_CUDA(cudaFreeAsync(d_pack, st));
     ht.mark();
     ht.report("afam_render: setdevice, args+tf, grid+waits, pack lock, pack+upload, launches");
+    return AFAM_OK;
+}
+
+extern "C" int afam_ipc_get_handle(const void *dev_ptr, uint8_t *handle) {
+    AFAM_CHECK(dev_ptr && handle, AFAM_E_VALUE, "NULL argument to afam_ipc_get_handle");
+    cudaIpcMemHandle_t h;
+    AFAM_CUDA(cudaIpcGetMemHandle(&h, const_cast<void *>(dev_ptr)));
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    memcpy(handle, &h, sizeof(h));
+    return AFAM_OK;
+}
+
+extern "C" int afam_ipc_open(const uint8_t *handle, int32_t device, void **dev_ptr) {
+    AFAM_CHECK(handle && dev_ptr, AFAM_E_VALUE, "NULL argument to afam_ipc_open");
+    AFAM_CUDA(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    AFAM_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return AFAM_OK;
+}
+
+extern "C" int afam_device_alloc(int32_t device, uint64_t bytes, void **dev_ptr) {
+    AFAM_CHECK(dev_ptr && bytes > 0, AFAM_E_VALUE, "bad argument to afam_device_alloc");
+    AFAM_CUDA(cudaSetDevice(device));
+    AFAM_CUDA(cudaMalloc(dev_ptr, bytes));
+    return AFAM_OK;
+}
+
+extern "C" int afam_device_free(void *dev_ptr) {
+    if (dev_ptr) AFAM_CUDA(cudaFree(dev_ptr));
+    return AFAM_OK;
+}
+
+extern "C" int afam_copy_to_host(void *host, const void *dev_ptr, uint64_t bytes) {
+    AFAM_CHECK(host && dev_ptr, AFAM_E_VALUE, "NULL argument to afam_copy_to_host");
+    AFAM_CUDA(cudaMemcpy(host, dev_ptr, bytes, cudaMemcpyDeviceToHost));
+    return AFAM_OK;
+}
+
+extern "C" int afam_ipc_close(void *dev_ptr) {
+    AFAM_CHECK(dev_ptr, AFAM_E_VALUE, "NULL argument to afam_ipc_close");
+    AFAM_CUDA(cudaIpcCloseMemHandle(dev_ptr));
     return AFAM_OK;
 }
 

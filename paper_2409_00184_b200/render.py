@@ -286,7 +286,7 @@ def camera_setup(pov, params) -> dict:
     return {"f": f, "r": r, "u": u, "tan_y": tan_y, "tan_x": tan_y * params.aspect}
 
 
-def _frame_struct(pov, tf, params, band_rows, nparts, part, debug) -> _lib.AfamFrame:
+def _frame_struct(pov, tf, params, band_rows, nparts, part, debug, full_frame=False) -> _lib.AfamFrame:
     fr = _lib.AfamFrame()
     cam = camera_setup(pov, params)
     for a in range(3):
@@ -308,7 +308,7 @@ def _frame_struct(pov, tf, params, band_rows, nparts, part, debug) -> _lib.AfamF
     for k in range(op.shape[0]):
         fr.opacity[k][0], fr.opacity[k][1] = float(op[k, 0]), float(op[k, 1])
     fr.domain_lo, fr.domain_hi = float(tf.domain[0]), float(tf.domain[1])
-    fr.flags = _lib.AFAM_RENDER_DEBUG if debug else 0
+    fr.flags = (_lib.AFAM_RENDER_DEBUG if debug else 0) | (_lib.AFAM_RENDER_FULL_FRAME if full_frame else 0)
     return fr
 
 
@@ -356,11 +356,14 @@ def _pinned_stage(nbytes: int):
 
 def render_part(pov, blocks: dict, tf, params, *, band_rows: int | None = None, nparts: int = 1, part: int = 0,
                 device: int | None = None, debug: bool = False, stream=None, out=None, raise_missing=True,
-                host_out: bool = False):
+                host_out: bool = False, out_ptr: int | None = None):
     """Render this part's row bands on the GPU.  Returns (rgba tensor (rows,
     W, 4) uint8 -- on the device, or in pinned host memory with host_out --,
     stats host dict, debug tensors or None).  Rows are the bands b with
-    b % nparts == part, packed in band order."""
+    b % nparts == part, packed in band order.  With out_ptr (a device
+    address of a whole H x W x 4 frame, e.g. rank 0's frame mapped over
+    NVLink, tiles.PeerFrame) the rows land at their frame rows instead and
+    the returned tensor is None."""
     import torch
 
     from .device import as_device_blocks, stream_handle
@@ -372,13 +375,15 @@ def render_part(pov, blocks: dict, tf, params, *, band_rows: int | None = None, 
     H, W = int(params.height), int(params.width)
     br = H if band_rows is None else int(band_rows)
     rows = int(_lib.lib().afam_frame_rows(H, br, nparts, part))
-    fr = _frame_struct(pov, tf, params, br, nparts, part, debug)
+    fr = _frame_struct(pov, tf, params, br, nparts, part, debug, full_frame=out_ptr is not None)
     # host_out: the kernel stores the pixels straight into this thread's
     # pinned staging buffer (mapped host memory), overlapping the copy-out
     # with the march; one synchronization covers frame and stats
+    if out_ptr is not None and host_out:
+        raise ValueError("out_ptr and host_out are exclusive")
     zero_copy = host_out and out is None
     stage = _pinned_stage(rows * W * 4 if host_out else 0)
-    if out is None:
+    if out is None and out_ptr is None:
         out = stage[64:64 + rows * W * 4].view(rows, W, 4) if zero_copy else \
             torch.empty((rows, W, 4), dtype=torch.uint8, device=dev)
     stats = torch.empty(6, dtype=torch.int64, device=dev)
@@ -390,7 +395,8 @@ def render_part(pov, blocks: dict, tf, params, *, band_rows: int | None = None, 
     with torch.cuda.device(dev):
         s_obj = stream if stream is not None else torch.cuda.current_stream(dev)
         _lib.check(_lib.lib().afam_render(
-            store.handle, C.byref(fr), sl.ctypes.data_as(C.c_void_p), len(sl), C.c_void_p(out.data_ptr()),
+            store.handle, C.byref(fr), sl.ctypes.data_as(C.c_void_p), len(sl),
+            C.c_void_p(out_ptr if out_ptr is not None else out.data_ptr()),
             C.c_void_p(stats.data_ptr()), None if nsamp is None else C.c_void_p(nsamp.data_ptr()),
             None if ohash is None else C.c_void_p(ohash.data_ptr()), C.c_void_p(int(s_obj.cuda_stream))))
         with torch.cuda.stream(s_obj):

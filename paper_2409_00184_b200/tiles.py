@@ -12,7 +12,7 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["part_rows", "assemble", "gather_bands", "render_tiles"]
+__all__ = ["part_rows", "assemble", "gather_bands", "render_tiles", "PeerFrame", "render_tiles_fused"]
 
 
 def part_rows(height: int, band_rows: int, nparts: int, part: int) -> np.ndarray:
@@ -86,3 +86,99 @@ def render_tiles(pov, blocks: dict, tf, params, *, group=None, band_rows: int = 
 
 
 render_tiles.last_stats = None
+
+
+class PeerFrame:
+    """Rank `dst`'s (height, width, 4) uint8 frame buffer mapped into every
+    rank of the group over NVLink (CUDA IPC, afam_ipc_*): the fused band
+    gather -- each rank's render kernel stores its rows straight into this
+    buffer (AFAM_RENDER_FULL_FRAME), so no separate collective moves pixels.
+    The handle travels once through torch.distributed."""
+
+    def __init__(self, height: int, width: int, group=None, dst: int = 0, device: int | None = None):
+        import ctypes as C
+
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib
+
+        self.height, self.width, self.dst = int(height), int(width), int(dst)
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.nbytes = self.height * self.width * 4
+        self._own = self.rank == self.dst
+        ptr = C.c_void_p()
+        handle = None
+        if self._own:
+            _lib.check(_lib.lib().afam_device_alloc(self.device, self.nbytes, C.byref(ptr)))
+            hb = (C.c_uint8 * 64)()
+            _lib.check(_lib.lib().afam_ipc_get_handle(ptr, hb))
+            handle = bytes(hb)
+        if dist.is_initialized() and dist.get_world_size(group) > 1:
+            obj = [handle]
+            dist.broadcast_object_list(obj, src=dist.get_global_rank(group, self.dst) if group else self.dst,
+                                       group=group, device=torch.device("cuda", self.device)
+                                       if dist.get_backend(group) == "nccl" else None)
+            handle = obj[0]
+            if not self._own:
+                hb = (C.c_uint8 * 64).from_buffer_copy(handle)
+                _lib.check(_lib.lib().afam_ipc_open(hb, self.device, C.byref(ptr)))
+        self.ptr = int(ptr.value)
+
+    def frame(self):
+        """The assembled frame as a host (H, W, 4) uint8 array (rank dst only)."""
+        import ctypes as C
+
+        import numpy as np
+        import torch
+
+        if not self._own:
+            raise RuntimeError("only the destination rank reads the frame")
+        from . import _lib
+
+        out = np.empty((self.height, self.width, 4), dtype=np.uint8)
+        torch.cuda.synchronize(self.device)
+        _lib.check(_lib.lib().afam_copy_to_host(out.ctypes.data_as(C.c_void_p), C.c_void_p(self.ptr), self.nbytes))
+        return out
+
+    def close(self):
+        from . import _lib
+
+        if self.ptr:
+            if self._own:
+                _lib.lib().afam_device_free(self.ptr)
+            else:
+                _lib.lib().afam_ipc_close(self.ptr)
+            self.ptr = 0
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def render_tiles_fused(pov, blocks: dict, tf, params, peer: PeerFrame, *, group=None, band_rows: int = 8):
+    """render_tiles with the band gather fused into the render kernel: every
+    rank renders its bands (b % world == rank) straight into `peer`, the
+    destination rank's frame, over NVLink; one barrier orders the writes
+    before the destination reads.  Returns the Frame on the destination rank
+    (None elsewhere)."""
+    import torch.distributed as dist
+
+    from .render import Frame, render_part
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    _, info, _ = render_part(pov, blocks, tf, params, band_rows=band_rows, nparts=world, part=rank,
+                             out_ptr=peer.ptr)
+    render_tiles_fused.last_stats = info
+    if world > 1:
+        dist.barrier(group)  # every rank's kernel (and its peer stores) completed
+    if rank != peer.dst:
+        return None
+    return Frame(int(params.width), int(params.height), peer.frame())
+
+
+render_tiles_fused.last_stats = None
