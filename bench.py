@@ -195,6 +195,32 @@ def measure_fma_peak(dev):
 
 
 # ------------------------------------------------------------------ ours
+def make_peer(args, world, rank, size, local_rank, dev):
+    """N > 1: rank 0's frame mapped into every rank (fused band gather), or
+    None (NCCL gather) when --gather nccl or when any rank cannot map it."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2409_00184_b200 import tiles
+
+    if args.gather != "fused":
+        return None
+    ok = torch.ones(1, device=dev)
+    peer = None
+    try:
+        peer = tiles.PeerFrame(size, size, device=local_rank)
+    except Exception as exc:  # noqa: BLE001
+        print(f"rank {rank}: fused gather unavailable ({exc}); using the NCCL gather", file=sys.stderr)
+        ok.zero_()
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if ok.item() < 1:
+        if peer is not None:
+            peer.close()
+        return None
+    return peer
+
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -232,19 +258,7 @@ def run_ours(args, rank, world, local_rank):
     # N > 1: the band gather is fused into the render kernel -- every rank
     # stores its pixels straight into rank 0's frame over NVLink (CUDA IPC,
     # tiles.PeerFrame); the NCCL gather is the fallback (or --gather nccl)
-    peer = None
-    if world > 1 and args.gather == "fused":
-        ok = torch.ones(1, device=dev)
-        try:
-            peer = tiles.PeerFrame(S, S, device=local_rank)
-        except Exception as exc:  # noqa: BLE001
-            print(f"rank {rank}: fused gather unavailable ({exc}); using the NCCL gather", file=sys.stderr)
-            ok.zero_()
-        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-        if ok.item() < 1:
-            if peer is not None:
-                peer.close()
-            peer = None
+    peer = make_peer(args, world, rank, S, local_rank, dev) if world > 1 else None
     gather_kind = "single GPU" if world == 1 else ("fused: peer stores over NVLink" if peer else "NCCL gather")
 
     def step(k):
@@ -371,11 +385,19 @@ def run_e2e(args, man, blobs, povs, tf, params, rank, world, local_rank):
 
     from paper_2409_00184_b200 import tiles
 
+    peer = make_peer(args, world, rank, params.height, local_rank, torch.device("cuda", local_rank)) \
+        if world > 1 else None
+
     def draw(pov, resident, tf_, params_):
-        # public API: tiles.render_tiles == render.render on one GPU; the
-        # Frame (host RGBA8) is the step's result read back to the host
-        frame = tiles.render_tiles(pov, resident, tf_, params_, band_rows=band)
-        draw.samples += tiles.render_tiles.last_stats["samples"]
+        # public API: tiles.render_tiles == render.render on one GPU (N > 1:
+        # the fused band gather into rank 0's frame); the Frame (host RGBA8)
+        # is the step's result read back to the host
+        if peer is not None:
+            frame = tiles.render_tiles_fused(pov, resident, tf_, params_, peer, band_rows=band)
+            draw.samples += tiles.render_tiles_fused.last_stats["samples"]
+        else:
+            frame = tiles.render_tiles(pov, resident, tf_, params_, band_rows=band)
+            draw.samples += tiles.render_tiles.last_stats["samples"]
         if frame is not None:
             draw.d2h += frame.rgba.nbytes
         return frame
@@ -405,6 +427,9 @@ def run_e2e(args, man, blobs, povs, tf, params, rank, world, local_rank):
         dist.all_reduce(m, op=dist.ReduceOp.MAX)
         tot = torch.stack([s[0], m[1]])
     h2d = (c1["bytes_loaded"] - c0["bytes_loaded"]) / nsteps
+    if peer is not None:
+        dist.barrier()
+        peer.close()
     return {"value": float(tot[0]) / float(tot[1]), "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": draw.d2h / nsteps, "steps": nsteps,
             "api": "runtime.replay(ModelCache(200), prefetch='linear') -> render_part -> Frame bytes on host",
