@@ -1,0 +1,145 @@
+"""Closed-form and structural properties of the GPU render path, mirroring
+the reference's own render tests (reference tests/test_render.py:239-362) on
+spline models: opacity correction, front-to-back order, transparent
+background, saturation, the early-termination bound, determinism and pixel
+co-location under resolution doubling."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def _models(fn, levels=1, coarsest=1, micro=9, degree=3, ncp=7):
+    from paper_2409_00184_b200 import model, synth
+
+    # bounds [-1, 1]^3 so fn sees normalized scene coordinates
+    man, blobs = synth.field_store(levels=levels, coarsest=coarsest, micro=micro, degree=degree,
+                                   ncp_of=lambda a: ncp, fn=fn, bounds=((-1.0, 1.0),) * 3)
+    return man, {a: model.deserialize(b, man.entries[a].ncp, man.entries[a].extent, a.lod)
+                 for a, b in blobs.items()}
+
+
+def _head_on(dist=4.0):
+    from paper_2409_00184_b200 import render
+
+    return render.PointOfView([0, 0, dist], [0, 0, -1], [0, 1, 0])
+
+
+def _render(man, models, pov, tf, params):
+    from paper_2409_00184_b200 import render
+
+    vis = render.select_visible(pov, man, params.aspect)
+    return render.render(pov, {a: models[a] for a in vis}, tf, params)
+
+
+def _const(v):
+    return lambda x, y, z: np.full(np.shape(x), v)
+
+
+def test_opacity_correction_power(gpu):
+    """reference_step twice the sample distance halves the exponent
+    (render.py:411-414): 20 samples of a constant a_tf compose to
+    1 - (1 - a_s)^20 with a_s = 1 - (1 - a_tf)^0.5."""
+    from paper_2409_00184_b200 import render
+
+    a_tf = 0.3
+    man, models = _models(_const(0.5))
+    tf = render.TransferFunction(color_points=[[0.0, 1, 1, 1], [1.0, 1, 1, 1]],
+                                 opacity_points=[[0.0, a_tf], [1.0, a_tf]])
+    params = render.RenderParams(width=2, height=2, sample_distance=0.1, reference_step=0.2, o_max=1.0)
+    fr = _render(man, models, _head_on(), tf, params)
+    a_s = 1.0 - (1.0 - a_tf) ** 0.5
+    assert abs(int(fr.rgba[1, 1, 3]) - np.rint(255 * (1.0 - (1.0 - a_s) ** 20))) <= 1
+    assert render.render.last_stats["samples"] >= 20
+
+
+def test_front_to_back_order(gpu):
+    """An opaque TF shows the first sample only (z = 0.95 on the head-on
+    ray): v = (z + 1) / 2 = 0.975, shaded with the headlight along the
+    gradient (ndotl = 1): c = v * (0.1 + 0.7) + 0.2."""
+    from paper_2409_00184_b200 import render
+
+    man, models = _models(lambda x, y, z: (np.asarray(z, dtype=float) + 1.0) / 2.0)
+    tf = render.TransferFunction(color_points=[[0.0, 0, 0, 0], [1.0, 1, 1, 1]],
+                                 opacity_points=[[0.0, 1.0], [1.0, 1.0]])
+    params = render.RenderParams(width=2, height=2, sample_distance=0.1, o_max=1.0)
+    fr = _render(man, models, _head_on(), tf, params)
+    v = 0.975
+    want = np.rint(255 * min(1.0, v * 0.8 + 0.2))
+    assert abs(int(fr.rgba[1, 1, 0]) - want) <= 1
+    assert fr.rgba[1, 1, 3] == 255
+
+
+def test_zero_opacity_and_background_are_transparent_black(gpu):
+    from paper_2409_00184_b200 import render
+
+    man, models = _models(_const(0.5))
+    tf0 = render.TransferFunction(color_points=[[0.0, 1, 1, 1], [1.0, 1, 1, 1]],
+                                  opacity_points=[[0.0, 0.0], [1.0, 0.0]])
+    fr = _render(man, models, _head_on(), tf0, render.RenderParams(width=8, height=8, sample_distance=0.05))
+    assert np.all(fr.rgba == 0)
+    far = render.PointOfView([0, 0, 30.0], [0, 0, -1], [0, 1, 0], 45.0)
+    fr = _render(man, models, far, render.TransferFunction.ml_preset(),
+                 render.RenderParams(width=16, height=16, sample_distance=0.05))
+    assert np.all(fr.rgba[0, 0] == 0) and np.all(fr.rgba[-1, -1] == 0)
+
+
+def test_alpha_saturates(gpu):
+    from paper_2409_00184_b200 import render
+
+    man, models = _models(_const(0.5))
+    tf = render.TransferFunction(color_points=[[0.0, 0.5, 0.5, 0.5], [1.0, 0.5, 0.5, 0.5]],
+                                 opacity_points=[[0.0, 1.0], [1.0, 1.0]])
+    fr = _render(man, models, _head_on(), tf, render.RenderParams(width=2, height=2, sample_distance=0.1, o_max=1.0))
+    assert fr.rgba[1, 1, 3] == 255
+
+
+@pytest.fixture(scope="module")
+def ml_store(gpu):
+    from paper_2409_00184_b200 import synth
+
+    def ml(x, y, z):  # Marschner-Lobb over the normalized scene
+        return synth.ml_value((np.asarray(x) + 1) * 3.5, (np.asarray(y) + 1) * 3.5, (np.asarray(z) + 1) * 3.5)
+
+    return _models(ml, levels=2, coarsest=1, micro=17, degree=3, ncp=15)
+
+
+def test_early_termination_bound(ml_store):
+    """o_max = 0.99 leaves at most 1% of the composite unaccumulated
+    (reference tests/test_render.py:320-331)."""
+    from paper_2409_00184_b200 import render
+
+    man, models = ml_store
+    tf = render.TransferFunction.ml_preset()
+    full = _render(man, models, _head_on(3.0), tf, render.RenderParams(width=32, height=32, sample_distance=0.01,
+                                                                        o_max=1.0))
+    cut = _render(man, models, _head_on(3.0), tf, render.RenderParams(width=32, height=32, sample_distance=0.01,
+                                                                       o_max=0.99))
+    diff = np.abs(full.rgba.astype(int) - cut.rgba.astype(int))
+    assert diff.max() <= np.ceil(0.01 * 255) + 1
+
+
+def test_determinism_and_resolution_doubling(ml_store):
+    """The same call twice gives the same bytes; pixel (i, j) of a frame is
+    pixel (2i, 2j) of the frame at twice the resolution (pixel corners,
+    render.py:323-337)."""
+    from paper_2409_00184_b200 import render
+
+    man, models = ml_store
+    tf = render.TransferFunction.ml_preset()
+    pov = render.PointOfView([0.4, 0.3, 2.0], [-0.1, -0.1, -1.0], [0, 1, 0])
+    p16 = render.RenderParams(width=16, height=16, sample_distance=0.02)
+    a = _render(man, models, pov, tf, p16)
+    b = _render(man, models, pov, tf, p16)
+    np.testing.assert_array_equal(a.rgba, b.rgba)
+    hi = _render(man, models, pov, tf, render.RenderParams(width=32, height=32, sample_distance=0.02))
+    np.testing.assert_array_equal(hi.rgba[::2, ::2], a.rgba)
