@@ -97,6 +97,8 @@ SIGNATURES = [
     ("afam_fit_rmse", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                 C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("afam_fit_operator", C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
+    ("afam_png_deflate", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_uint64,
+                                   C.POINTER(C.c_uint64), C.POINTER(C.c_uint32), C.c_void_p]),
     ("afam_manifest_create", C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.c_void_p, C.c_void_p]),
     ("afam_manifest_destroy", C.c_int, [C.c_void_p]),
     ("afam_select_visible", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double,
@@ -155,3 +157,11 @@ def require_device() -> None:
     n = lib().afam_device_count()
     if n < 1:
         raise RuntimeError("no CUDA device visible: the B200 path has no CPU fallback")
+
+
+def device_available() -> bool:
+    """True when libafam sees a CUDA device."""
+    try:
+        return lib().afam_device_count() > 0
+    except Exception:  # noqa: BLE001
+        return False

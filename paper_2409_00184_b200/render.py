@@ -194,6 +194,16 @@ class Frame:
         return cls(width=img.width, height=img.height, rgba=np.asarray(img, dtype=np.uint8))
 
     def to_png_bytes(self) -> bytes:
+        """PNG of the frame (render.py:216-221).  With a CUDA device the image
+        data is filtered and deflated on the GPU (png_bytes_gpu); the decoded
+        pixels are identical either way."""
+        from . import _lib
+
+        if _lib.device_available():
+            return png_bytes_gpu(self.rgba)
+        return self._to_png_bytes_pil()
+
+    def _to_png_bytes_pil(self) -> bytes:
         import io
 
         from PIL import Image
@@ -201,6 +211,39 @@ class Frame:
         out = io.BytesIO()
         Image.fromarray(self.rgba, mode="RGBA").save(out, format="PNG")
         return out.getvalue()
+
+
+def png_bytes_gpu(rgba) -> bytes:
+    """PNG bytes of an (H, W, 4) uint8 RGBA frame (host array or CUDA tensor):
+    afam_png_deflate makes the zlib payload on the GPU, the host wraps the
+    chunks (IHDR, IDAT, IEND with CRC-32)."""
+    import struct
+    import zlib
+
+    import torch
+
+    if isinstance(rgba, torch.Tensor) and rgba.is_cuda:
+        d = rgba.contiguous()
+    else:
+        d = torch.from_numpy(np.ascontiguousarray(rgba, dtype=np.uint8)).cuda()
+    H, W = int(d.shape[0]), int(d.shape[1])
+    if d.shape[2] != 4 or d.dtype != torch.uint8:
+        raise ValueError(f"expected (H, W, 4) uint8 RGBA, got {tuple(d.shape)} {d.dtype}")
+    cap = int(((4 * W + 1) * 9 // 8 + 16) * H + 1024)
+    out = torch.empty(cap, dtype=torch.uint8, device=d.device)
+    nbytes, adler = C.c_uint64(), C.c_uint32()
+    with torch.cuda.device(d.device):
+        _lib.check(_lib.lib().afam_png_deflate(C.c_void_p(d.data_ptr()), W, H, C.c_void_p(out.data_ptr()), cap,
+                                               C.byref(nbytes), C.byref(adler),
+                                               C.c_void_p(torch.cuda.current_stream(d.device).cuda_stream)))
+    body = out[: nbytes.value].cpu().numpy().tobytes()
+    idat = b"\x78\x01" + body + struct.pack(">I", adler.value)
+
+    def chunk(kind: bytes, data: bytes) -> bytes:
+        return struct.pack(">I", len(data)) + kind + data + struct.pack(">I", zlib.crc32(kind + data) & 0xFFFFFFFF)
+
+    ihdr = struct.pack(">IIBBBBB", W, H, 8, 6, 0, 0, 0)
+    return b"\x89PNG\r\n\x1a\n" + chunk(b"IHDR", ihdr) + chunk(b"IDAT", idat) + chunk(b"IEND", b"")
 
 
 # ------------------------------------------------------------- visibility
