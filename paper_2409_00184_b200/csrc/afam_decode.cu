@@ -88,6 +88,28 @@ __device__ __forceinline__ void ld4(const double *p, double (&v)[4]) {
     v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
 }
 
+// acc[0..3] += w * v[0..3]: paired FMAs (FFMA2) in float32, scalar in float64
+__device__ __forceinline__ void fma4(float w, float4 v, float (&acc)[4]) {
+    const float2 lo = __ffma2_rn(make_float2(w, w), make_float2(v.x, v.y), make_float2(acc[0], acc[1]));
+    const float2 hi = __ffma2_rn(make_float2(w, w), make_float2(v.z, v.w), make_float2(acc[2], acc[3]));
+    acc[0] = lo.x; acc[1] = lo.y; acc[2] = hi.x; acc[3] = hi.y;
+}
+__device__ __forceinline__ void fma4(double w, float4 v, double (&acc)[4]) {
+    acc[0] = fma(w, (double)v.x, acc[0]);
+    acc[1] = fma(w, (double)v.y, acc[1]);
+    acc[2] = fma(w, (double)v.z, acc[2]);
+    acc[3] = fma(w, (double)v.w, acc[3]);
+}
+__device__ __forceinline__ void fma4(float w, const float *p, float (&acc)[4]) {
+    fma4(w, *reinterpret_cast<const float4 *>(p), acc);
+}
+__device__ __forceinline__ void fma4(double w, const double *p, double (&acc)[4]) {
+    double v[4];
+    ld4(p, v);
+#pragma unroll
+    for (int e = 0; e < 4; e++) acc[e] = fma(w, v[e], acc[e]);
+}
+
 // Three smem-staged banded contractions per output plane, register-blocked:
 // z and y items are 4 consecutive x (16-byte smem traffic), the x stage
 // keeps each lane's Bx rows in registers for every row j.
@@ -169,11 +191,7 @@ __device__ __forceinline__ void decode_planes(const BlockDesc &d, const int32_t 
             T acc[4] = {T(0), T(0), T(0), T(0)};
 #pragma unroll
             for (int c = 0; c < Q; c++) {
-                const float4 v = *reinterpret_cast<const float4 *>(planes[c] + (size_t)b * pitch + 4 * q);
-                acc[0] = fma(bz[c], (T)v.x, acc[0]);
-                acc[1] = fma(bz[c], (T)v.y, acc[1]);
-                acc[2] = fma(bz[c], (T)v.z, acc[2]);
-                acc[3] = fma(bz[c], (T)v.w, acc[3]);
+                fma4(bz[c], *reinterpret_cast<const float4 *>(planes[c] + (size_t)b * pitch + 4 * q), acc);
             }
             st4(S1 + (size_t)b * pitch + 4 * q, acc);
         }
@@ -187,20 +205,30 @@ __device__ __forceinline__ void decode_planes(const BlockDesc &d, const int32_t 
             const T *s1 = S1 + (size_t)c0[j] * pitch + 4 * q;
             T acc[4] = {T(0), T(0), T(0), T(0)};
 #pragma unroll
-            for (int bb = 0; bb < Q; bb++) {
-                T v[4];
-                ld4(s1 + (size_t)bb * pitch, v);
-                const T w = B[j * 4 + bb];
-#pragma unroll
-                for (int e = 0; e < 4; e++) acc[e] = fma(w, v[e], acc[e]);
-            }
+            for (int bb = 0; bb < Q; bb++) fma4(B[j * 4 + bb], s1 + (size_t)bb * pitch, acc);
             st4(S2 + (size_t)j * pitch + 4 * q, acc);
         }
         __syncthreads();
         // x contraction + coalesced store out[i + m*j + m*m*k]: full-warp columns
         // i = lane + 32t with their Bx rows in registers, then the m % 32 tail
         float *outk = out + (size_t)k * m * m;
+        if constexpr (sizeof(T) == 4) {
+            if (ngroups == 2) {  // m in [64, 95]: both column groups in one paired FMA chain (FFMA2)
+                for (int j = warp; j < m; j += nwarp) {
+                    const float *s2 = reinterpret_cast<const float *>(S2) + (size_t)j * pitch;
+                    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int a = 0; a < Q; a++)
+                        acc = __ffma2_rn(make_float2(bx[0][a], bx[1][a]), make_float2(s2[xi[0] + a], s2[xi[1] + a]),
+                                         acc);
+                    float *orow = outk + (size_t)j * m;
+                    orow[lane] = acc.x;
+                    orow[lane + 32] = acc.y;
+                }
+            }
+        }
         for (int j = warp; j < m; j += nwarp) {
+            if (sizeof(T) == 4 && ngroups == 2) break;  // done above
             const T *s2 = S2 + (size_t)j * pitch;
             float *orow = outk + (size_t)j * m;
 #pragma unroll
