@@ -422,13 +422,8 @@ __device__ __forceinline__ void tc_decode_block(const BlockDesc &d, const Decode
                 const int y = (int)(((float)item + 0.5f) * inv_nq), q = item - y * nq;
                 float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-                for (int c = 0; c < Q; c++) {
-                    const float4 v = *reinterpret_cast<const float4 *>(planes[c] + (size_t)y * pitch + 4 * q);
-                    acc[0] = fmaf(bz[c], v.x, acc[0]);
-                    acc[1] = fmaf(bz[c], v.y, acc[1]);
-                    acc[2] = fmaf(bz[c], v.z, acc[2]);
-                    acc[3] = fmaf(bz[c], v.w, acc[3]);
-                }
+                for (int c = 0; c < Q; c++)
+                    fma4(bz[c], *reinterpret_cast<const float4 *>(planes[c] + (size_t)y * pitch + 4 * q), acc);
                 st4(S1 + (size_t)y * pitch + 4 * q, acc);
             }
             named_sync(1, NP);
@@ -445,13 +440,7 @@ __device__ __forceinline__ void tc_decode_block(const BlockDesc &d, const Decode
                 if (q < nq) {
                     const float *s1 = S1 + (size_t)c0[j] * pitch + 4 * q;
 #pragma unroll
-                    for (int bb = 0; bb < Q; bb++) {
-                        float v[4];
-                        ld4(s1 + (size_t)bb * pitch, v);
-                        const float w = B[j * 4 + bb];
-#pragma unroll
-                        for (int e = 0; e < 4; e++) acc[e] = fmaf(w, v[e], acc[e]);
-                    }
+                    for (int bb = 0; bb < Q; bb++) fma4(B[j * 4 + bb], s1 + (size_t)bb * pitch, acc);
                     if (q == (n - 1) >> 2) xlast[b * kTcRows + j] = acc[(n - 1) & 3];
                 }
                 float hi[4], lo[4];
