@@ -142,27 +142,35 @@ def _make_model(ctrl, degree, extent, lod) -> model.MicroModel:
 def search_blocks(samples, error_bound: float, degree: int, extents=None, lods=None,
                   assume_monotone: bool = False, device: int = 0) -> list:
     """in_level_search for many blocks of one edge length at once (one GPU
-    batch per sweep / bisection round).  Returns [SearchResult]."""
+    batch per sweep / bisection round).  `samples`: a list of cubic host
+    arrays or a resident (nblocks, m, m, m) float32 CUDA tensor.  Returns
+    [SearchResult]."""
+    import torch
+
     if error_bound <= 0:
         raise ValueError("error bound must be positive")
-    blocks = [np.asarray(s) for s in samples]
+    on_device = isinstance(samples, torch.Tensor)
+    blocks = samples if on_device else [np.asarray(s) for s in samples]
     nb = len(blocks)
     if nb == 0:
         return []
-    n = blocks[0].shape[0]
+    n = int(blocks[0].shape[0])
     ncp_min = degree + 1
     if n < ncp_min:
         raise ValueError(f"block edge {n} below minimum NCP {ncp_min}")
     extents = extents if extents is not None else [((0.0, 1.0),) * 3] * nb
     lods = lods if lods is not None else [1] * nb
     profiles = [ErrorProfile() for _ in range(nb)]
-    import torch
-
     _lib.require_device()
-    if any(np.shape(b) != (n, n, n) for b in blocks):
-        raise ValueError("search_blocks needs cubic sample grids of one edge length")
-    blocks = torch.from_numpy(np.stack([np.asarray(b, dtype=np.float32) for b in blocks])).to(
-        torch.device("cuda", device))  # uploaded once for every probe round
+    if on_device:  # (nb, n, n, n) float32, already resident
+        if tuple(blocks.shape[1:]) != (n, n, n) or blocks.dtype != torch.float32:
+            raise ValueError("search_blocks needs a (nblocks, m, m, m) float32 tensor")
+        blocks = blocks.contiguous()
+    else:
+        if any(np.shape(b) != (n, n, n) for b in blocks):
+            raise ValueError("search_blocks needs cubic sample grids of one edge length")
+        blocks = torch.from_numpy(np.stack([np.asarray(b, dtype=np.float32) for b in blocks])).to(
+            torch.device("cuda", device))  # uploaded once for every probe round
     if assume_monotone:
         lo, hi = [ncp_min] * nb, [n] * nb
         while True:
