@@ -179,11 +179,12 @@ int afam_fit_rmse(afam_store *s, const float *samples, int32_t nblk, int32_t m, 
 int afam_fit_operator(int32_t ncp, int32_t degree, int32_t m, double *fit, double *dec);
 
 /* ----------------------------------------------------------- frame egress */
-/* The deflate stream (one fixed-Huffman block: per-row PNG filter + literals
- * and distance-1 runs) of the PNG image data of an RGBA8 frame (device,
- * height x width x 4, row 0 at the top); replaces the zlib pass of
- * Frame.to_png_bytes (render.py:216-221).  out: device buffer, 4-byte
- * aligned, >= 1.2 * (4*width+1) * height + 64 bytes; *out_bytes: the stream
+/* The deflate stream (one dynamic-Huffman block built from the frame's
+ * symbol histogram: per-row PNG filter + literals and distance-1 runs) of
+ * the PNG image data of an RGBA8 frame (device, height x width x 4, row 0 at
+ * the top); replaces the zlib pass of Frame.to_png_bytes (render.py:216-221).
+ * out: device buffer, 4-byte aligned, >= ((4*width+1)*15/8 + 16) * height +
+ * 2048 bytes; *out_bytes: the stream
  * length; *adler: Adler-32 of the filtered data (the zlib trailer).  The call
  * synchronizes its stream. */
 int afam_png_deflate(const uint8_t *rgba, int32_t width, int32_t height, uint8_t *out, uint64_t out_cap,

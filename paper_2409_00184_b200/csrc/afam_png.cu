@@ -2,24 +2,27 @@
 // PNG of an RGBA8 frame (reference Frame.to_png_bytes, render.py:216-221,
 // which spends 36-345 ms in zlib level 6 per 1024^2 frame).
 //
-// One thread per image row: PNG filter chosen per row (None / Sub / Up, by
-// the smallest sum of |residual| as libpng's heuristic), then the filtered
-// row -- filter byte first -- is coded with the fixed deflate Huffman codes
-// (RFC 1951 3.2.6): literals, plus runs of the previous byte as (length,
-// distance 1) matches, which is what flat and transparent regions become
-// after filtering.  Every row emits into its own scratch bitstream; an
-// exclusive scan of the row bit lengths places them, and a scatter kernel
-// ORs each row's words in at its bit offset behind the 3-bit block header
-// (BFINAL = 1, BTYPE = fixed); the end-of-block code closes the stream.
-// Adler-32 of the filtered data comes from per-row (sum, weighted sum)
-// pairs combined on the host.
+// One thread per image row.  Pass 1 picks the PNG filter of the row (None /
+// Sub / Up, smallest sum of |residual|, libpng's heuristic), tokenizes the
+// filtered row -- filter byte first -- into literals and runs of the
+// previous byte ((length, distance 1) matches, what flat and transparent
+// regions become after filtering) and counts the literal/length symbols of
+// the frame.  The host builds one length-limited canonical Huffman code from
+// that histogram (RFC 1951 3.2.2) and the dynamic block header (3.2.7).
+// Pass 2 codes every row into its own scratch bitstream; an exclusive scan
+// of the row bit lengths places the rows behind the header, a scatter
+// kernel ORs them in, and the end-of-block code closes the block.  Adler-32
+// of the filtered data comes from per-row (sum, weighted sum) pairs.
 #include <algorithm>
 #include <cstring>
+#include <queue>
 #include <vector>
 
 #include "afam_internal.h"
 
 namespace afam {
+
+constexpr int kLitLen = 286;  // literal/length alphabet (0..285)
 
 struct BitWriter {
     uint32_t *out;
@@ -27,6 +30,7 @@ struct BitWriter {
     int nb = 0;
     uint64_t total = 0;
     __device__ __forceinline__ void put(uint32_t bits, int n) {  // n <= 32, LSB-first
+        if (n == 0) return;
         buf |= (uint64_t)bits << nb;
         nb += n;
         total += n;
@@ -43,36 +47,16 @@ struct BitWriter {
     }
 };
 
-__device__ __forceinline__ uint32_t bitrev(uint32_t v, int n) { return __brev(v) >> (32 - n); }
-
-// fixed Huffman code of a literal/length symbol, MSB-first bits reversed for the LSB-first stream
-__device__ __forceinline__ void put_litlen(BitWriter &w, int sym) {
-    if (sym < 144) w.put(bitrev(0x30 + sym, 8), 8);
-    else if (sym < 256) w.put(bitrev(0x190 + (sym - 144), 9), 9);
-    else if (sym < 280) w.put(bitrev(sym - 256, 7), 7);
-    else w.put(bitrev(0xC0 + (sym - 280), 8), 8);
-}
-
-// a match of `len` (3..258) bytes at distance 1
-__device__ __forceinline__ void put_match_d1(BitWriter &w, int len) {
-    if (len == 258) {
-        put_litlen(w, 285);
-    } else {
-        // length codes 257..284: base lengths and extra bits
-        int code, extra, base;
-        if (len <= 10) { code = 257 + (len - 3); extra = 0; base = len; }
-        else {
-            int e = 1, b = 11;
-            while (len >= b + (4 << e)) { b += 4 << e; e++; }  // groups of 4 codes per extra-bit count
-            const int idx = (len - b) >> e;
-            code = 265 + 4 * (e - 1) + idx;
-            extra = e;
-            base = b + (idx << e);
-        }
-        put_litlen(w, code);
-        if (extra) w.put((uint32_t)(len - base), extra);
-    }
-    w.put(0, 5);  // distance code 0 (distance 1), 5 bits, no extra bits
+// length code (257..285), its extra bits and their value for a match length 3..258
+__device__ __forceinline__ void length_code(int len, int &code, int &extra, int &xval) {
+    if (len == 258) { code = 285; extra = 0; xval = 0; return; }
+    if (len <= 10) { code = 257 + (len - 3); extra = 0; xval = 0; return; }
+    int e = 1, b = 11;
+    while (len >= b + (4 << e)) { b += 4 << e; e++; }  // groups of 4 codes per extra-bit count
+    const int idx = (len - b) >> e;
+    code = 265 + 4 * (e - 1) + idx;
+    extra = e;
+    xval = len - (b + (idx << e));
 }
 
 __device__ __forceinline__ int filt(int f, const uint8_t *row, const uint8_t *prev, int x) {
@@ -82,56 +66,81 @@ __device__ __forceinline__ int filt(int f, const uint8_t *row, const uint8_t *pr
     return (f == 1 ? v - a : (f == 2 ? v - b : v)) & 0xFF;
 }
 
-__global__ void png_rows_kernel(const uint8_t *__restrict__ rgba, int width, int height, uint32_t *__restrict__ scratch,
-                                int words_per_row, uint64_t *__restrict__ row_bits, uint64_t *__restrict__ adler_ab) {
+// pass 1 (codes == nullptr): filter choice, symbol histogram, Adler pieces;
+// pass 2: code the row with the frame's table (codes[s] bit-reversed, lens[s])
+__global__ void png_rows_kernel(const uint8_t *__restrict__ rgba, int width, int height, uint8_t *__restrict__ filters,
+                                unsigned int *__restrict__ hist, const uint32_t *__restrict__ codes,
+                                const uint8_t *__restrict__ lens, uint32_t *__restrict__ scratch, int words_per_row,
+                                uint64_t *__restrict__ row_bits, uint64_t *__restrict__ adler_ab) {
     const int y = blockIdx.x * blockDim.x + threadIdx.x;
     if (y >= height) return;
     const int n = 4 * width;
     const uint8_t *row = rgba + (size_t)y * n;
     const uint8_t *prev = y > 0 ? row - n : nullptr;
-    // filter choice: minimum sum of |signed residual| over None, Sub, Up
-    uint64_t cost[3] = {0, 0, 0};
-    for (int x = 0; x < n; x++)
-        for (int f = 0; f < 3; f++) {
-            const int r = filt(f, row, prev, x);
-            cost[f] += r < 128 ? r : 256 - r;
-        }
-    const int f = cost[1] < cost[0] ? (cost[2] < cost[1] ? 2 : 1) : (cost[2] < cost[0] ? 2 : 0);
+    const bool encode = codes != nullptr;
+    int f;
+    if (!encode) {
+        uint64_t cost[3] = {0, 0, 0};
+        for (int x = 0; x < n; x++)
+#pragma unroll
+            for (int ff = 0; ff < 3; ff++) {
+                const int r = filt(ff, row, prev, x);
+                cost[ff] += r < 128 ? r : 256 - r;
+            }
+        f = cost[1] < cost[0] ? (cost[2] < cost[1] ? 2 : 1) : (cost[2] < cost[0] ? 2 : 0);
+        filters[y] = (uint8_t)f;
+    } else {
+        f = filters[y];
+    }
     BitWriter w;
     w.out = scratch + (size_t)y * words_per_row;
-    // Adler-32 pieces of this row's data (filter byte + filtered bytes)
+    auto sym = [&](int s) {
+        if (encode) w.put(codes[s], lens[s]);
+        else atomicAdd(hist + s, 1u);
+    };
     const uint64_t m = (uint64_t)n + 1;
     uint64_t A = (uint64_t)f, B = m * (uint64_t)f;
-    put_litlen(w, f);
+    sym(f);
     int last = f;
     int x = 0;
     while (x < n) {
         const int r = filt(f, row, prev, x);
-        // run of the previous byte?
         int len = 0;
-        if (r == last) {
+        if (r == last) {  // a run of the previous byte
             len = 1;
             while (x + len < n && len < 258 && filt(f, row, prev, x + len) == last) len++;
         }
         if (len >= 3) {
-            put_match_d1(w, len);
-            for (int k = 0; k < len; k++) {
-                A += (uint64_t)last;
-                B += (m - 1 - (uint64_t)(x + k)) * (uint64_t)last;
+            int code, extra, xval;
+            length_code(len, code, extra, xval);
+            sym(code);
+            if (encode) {
+                w.put((uint32_t)xval, extra);
+                w.put(0, 1);  // the single distance code (distance 1): one bit
+            }
+            if (!encode) {
+                A += (uint64_t)len * (uint64_t)last;
+                // sum over k of (m - 1 - (x + k)) = len * (m - 1 - x) - len (len - 1) / 2
+                B += ((uint64_t)len * (m - 1 - (uint64_t)x) - (uint64_t)len * (len - 1) / 2) * (uint64_t)last;
             }
             x += len;
         } else {
-            put_litlen(w, r);
-            A += (uint64_t)r;
-            B += (m - 1 - (uint64_t)x) * (uint64_t)r;
+            sym(r);
+            if (!encode) {
+                A += (uint64_t)r;
+                B += (m - 1 - (uint64_t)x) * (uint64_t)r;
+            }
             last = r;
             x++;
         }
     }
-    w.flush();
-    row_bits[y] = w.total;
-    adler_ab[2 * y] = A;
-    adler_ab[2 * y + 1] = B;
+    if (encode) {
+        w.flush();
+        row_bits[y] = w.total;
+    } else {
+        adler_ab[2 * y] = A;
+        adler_ab[2 * y + 1] = B;
+    }
 }
 
 // exclusive scan of the row bit lengths (height is small: one thread)
@@ -147,7 +156,7 @@ __global__ void png_scan_kernel(const uint64_t *__restrict__ row_bits, int heigh
 
 __global__ void png_scatter_kernel(const uint32_t *__restrict__ scratch, int words_per_row,
                                    const uint64_t *__restrict__ row_bits, const uint64_t *__restrict__ row_off,
-                                   int height, uint32_t *__restrict__ out) {
+                                   uint32_t *__restrict__ out) {
     const int y = blockIdx.y;
     const uint64_t nbits = row_bits[y];
     const int nw = (int)((nbits + 31) / 32);
@@ -163,6 +172,138 @@ __global__ void png_scatter_kernel(const uint32_t *__restrict__ scratch, int wor
     }
 }
 
+// ---------------------------------------------------------------- host side
+struct HostBits {
+    std::vector<uint8_t> bytes;
+    uint64_t nbits = 0;
+    void put(uint32_t v, int n) {
+        for (int i = 0; i < n; i++, nbits++) {
+            if ((nbits >> 3) >= bytes.size()) bytes.push_back(0);
+            if ((v >> i) & 1u) bytes[nbits >> 3] |= (uint8_t)(1u << (nbits & 7));
+        }
+    }
+};
+
+static uint32_t rev_bits(uint32_t v, int n) {
+    uint32_t r = 0;
+    for (int i = 0; i < n; i++) r |= ((v >> i) & 1u) << (n - 1 - i);
+    return r;
+}
+
+// Huffman code lengths for `freq` (zero-frequency symbols get 0), limited to
+// max_len by halving the frequencies until the tree fits.
+static std::vector<int> huff_lengths(std::vector<uint64_t> freq, int max_len) {
+    const int ns = (int)freq.size();
+    std::vector<int> len(ns, 0);
+    for (;;) {
+        struct Node { uint64_t w; int id; };
+        auto cmp = [](const Node &a, const Node &b) { return a.w > b.w || (a.w == b.w && a.id > b.id); };
+        std::priority_queue<Node, std::vector<Node>, decltype(cmp)> pq(cmp);
+        std::vector<int> parent;
+        int nodes = 0;
+        std::vector<int> leaf_of(ns, -1);
+        for (int s = 0; s < ns; s++)
+            if (freq[s]) {
+                leaf_of[s] = nodes;
+                pq.push({freq[s], nodes++});
+                parent.push_back(-1);
+            }
+        std::fill(len.begin(), len.end(), 0);
+        if (nodes == 0) return len;
+        if (nodes == 1) {
+            for (int s = 0; s < ns; s++)
+                if (freq[s]) len[s] = 1;
+            return len;
+        }
+        while (pq.size() > 1) {
+            const Node a = pq.top(); pq.pop();
+            const Node b = pq.top(); pq.pop();
+            parent.push_back(-1);
+            parent[a.id] = nodes;
+            parent[b.id] = nodes;
+            pq.push({a.w + b.w, nodes++});
+        }
+        int maxl = 0;
+        for (int s = 0; s < ns; s++)
+            if (leaf_of[s] >= 0) {
+                int d = 0;
+                for (int v = leaf_of[s]; parent[v] >= 0; v = parent[v]) d++;
+                len[s] = d;
+                maxl = std::max(maxl, d);
+            }
+        if (maxl <= max_len) return len;
+        for (auto &f : freq)
+            if (f) f = (f + 1) / 2;
+    }
+}
+
+// canonical codes (RFC 1951 3.2.2), bit-reversed for the LSB-first stream
+static std::vector<uint32_t> canon_codes(const std::vector<int> &len) {
+    int maxl = 0;
+    for (int l : len) maxl = std::max(maxl, l);
+    std::vector<int> bl(maxl + 1, 0);
+    for (int l : len)
+        if (l) bl[l]++;
+    std::vector<uint32_t> next(maxl + 2, 0);
+    uint32_t code = 0;
+    for (int b = 1; b <= maxl; b++) {
+        code = (code + (uint32_t)bl[b - 1]) << 1;
+        next[b] = code;
+    }
+    std::vector<uint32_t> out(len.size(), 0);
+    for (size_t s = 0; s < len.size(); s++)
+        if (len[s]) out[s] = rev_bits(next[len[s]]++, len[s]);
+    return out;
+}
+
+// dynamic block header (RFC 1951 3.2.7) for literal/length lengths `ll` and
+// the single distance code 0 of length 1
+static void write_header(HostBits &h, const std::vector<int> &ll) {
+    int hlit = kLitLen;
+    while (hlit > 257 && ll[hlit - 1] == 0) hlit--;
+    std::vector<int> seq(ll.begin(), ll.begin() + hlit);
+    seq.push_back(1);  // distance code 0: length 1 (HDIST = 0 -> one code)
+    // run-length code the lengths with symbols 16 / 17 / 18
+    struct Tok { int sym, xbits, xval; };
+    std::vector<Tok> toks;
+    for (size_t i = 0; i < seq.size();) {
+        const int v = seq[i];
+        size_t r = 1;
+        while (i + r < seq.size() && seq[i + r] == v) r++;
+        if (v == 0 && r >= 3) {
+            size_t left = r;
+            while (left >= 11) { const int k = (int)std::min<size_t>(left, 138); toks.push_back({18, 7, k - 11}); left -= k; }
+            if (left >= 3) { toks.push_back({17, 3, (int)left - 3}); left = 0; }
+            while (left--) toks.push_back({0, 0, 0});
+        } else if (v != 0 && r >= 4) {
+            toks.push_back({v, 0, 0});
+            size_t left = r - 1;
+            while (left >= 3) { const int k = (int)std::min<size_t>(left, 6); toks.push_back({16, 2, k - 3}); left -= k; }
+            while (left--) toks.push_back({v, 0, 0});
+        } else {
+            for (size_t k = 0; k < r; k++) toks.push_back({v, 0, 0});
+        }
+        i += r;
+    }
+    std::vector<uint64_t> cf(19, 0);
+    for (auto &t : toks) cf[t.sym]++;
+    const std::vector<int> cl = huff_lengths(cf, 7);
+    const std::vector<uint32_t> cc = canon_codes(cl);
+    static const int order[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
+    int hclen = 19;
+    while (hclen > 4 && cl[order[hclen - 1]] == 0) hclen--;
+    h.put(1, 1);  // BFINAL
+    h.put(2, 2);  // BTYPE = 10 (dynamic)
+    h.put((uint32_t)(hlit - 257), 5);
+    h.put(0, 5);  // HDIST = 1 code
+    h.put((uint32_t)(hclen - 4), 4);
+    for (int i = 0; i < hclen; i++) h.put((uint32_t)cl[order[i]], 3);
+    for (auto &t : toks) {
+        h.put(cc[t.sym], cl[t.sym]);
+        if (t.xbits) h.put((uint32_t)t.xval, t.xbits);
+    }
+}
+
 }  // namespace afam
 
 using namespace afam;
@@ -174,45 +315,84 @@ extern "C" int afam_png_deflate(const uint8_t *rgba, int32_t width, int32_t heig
     AFAM_CHECK(((uintptr_t)out & 3) == 0, AFAM_E_VALUE, "output buffer must be 4-byte aligned");
     cudaStream_t st = (cudaStream_t)stream;
     const int n = 4 * width + 1;
-    // worst case 9 bits per byte + slack, in 32-bit words
-    const int wpr = (int)(((uint64_t)n * 9 + 63) / 32) + 1;
-    const uint64_t worst_bits = 3 + (uint64_t)height * wpr * 32 + 7;
+    // worst case 15 bits per byte (a 15-bit literal code) + slack, in 32-bit words
+    const int wpr = (int)(((uint64_t)n * 15 + 63) / 32) + 1;
+    const uint64_t header_max = 8 * 1024;
+    const uint64_t worst_bits = header_max + (uint64_t)height * wpr * 32 + 15;
     AFAM_CHECK(out_cap * 8 >= worst_bits + 64, AFAM_E_CAPACITY, "PNG output buffer too small (%llu bytes)",
                (unsigned long long)out_cap);
     uint32_t *scratch = nullptr;
     uint64_t *meta = nullptr;  // row_bits[h], row_off[h], adler_ab[2h], total[1]
+    unsigned int *hist = nullptr;
+    uint32_t *codes = nullptr;
+    uint8_t *small = nullptr;  // filters[h], lens[286]
     AFAM_CUDA(cudaMallocAsync(&scratch, sizeof(uint32_t) * (size_t)wpr * height, st));
     AFAM_CUDA(cudaMallocAsync(&meta, sizeof(uint64_t) * ((size_t)4 * height + 1), st));
+    AFAM_CUDA(cudaMallocAsync(&hist, sizeof(unsigned int) * kLitLen + sizeof(uint32_t) * kLitLen, st));
+    AFAM_CUDA(cudaMallocAsync(&small, (size_t)height + kLitLen, st));
+    codes = reinterpret_cast<uint32_t *>(hist + kLitLen);
+    uint8_t *filters = small, *lens = small + height;
     uint64_t *row_bits = meta, *row_off = meta + height, *adler_ab = meta + 2 * height, *total = meta + 4 * height;
+    AFAM_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned int) * kLitLen, st));
+    const int tpb = 64, nblk = (height + tpb - 1) / tpb;
+    png_rows_kernel<<<nblk, tpb, 0, st>>>(rgba, width, height, filters, hist, nullptr, nullptr, scratch, wpr, row_bits,
+                                          adler_ab);
+    std::vector<unsigned int> h(kLitLen);
+    std::vector<uint64_t> ab((size_t)2 * height);
+    AFAM_CUDA(cudaMemcpyAsync(h.data(), hist, sizeof(unsigned int) * kLitLen, cudaMemcpyDeviceToHost, st));
+    AFAM_CUDA(cudaMemcpyAsync(ab.data(), adler_ab, sizeof(uint64_t) * 2 * height, cudaMemcpyDeviceToHost, st));
+    AFAM_CUDA(cudaStreamSynchronize(st));
+    // the frame's code: literal/length lengths from the histogram (+ end of block)
+    std::vector<uint64_t> freq(h.begin(), h.end());
+    freq[256] = 1;
+    const std::vector<int> ll = huff_lengths(freq, 15);
+    const std::vector<uint32_t> cc = canon_codes(ll);
+    HostBits hb;
+    write_header(hb, ll);
+    std::vector<uint8_t> hl(kLitLen);
+    for (int s = 0; s < kLitLen; s++) hl[s] = (uint8_t)ll[s];
+    AFAM_CUDA(cudaMemcpyAsync(codes, cc.data(), sizeof(uint32_t) * kLitLen, cudaMemcpyHostToDevice, st));
+    AFAM_CUDA(cudaMemcpyAsync(lens, hl.data(), kLitLen, cudaMemcpyHostToDevice, st));
     const uint64_t out_words = (worst_bits + 31) / 32 + 1;
     AFAM_CUDA(cudaMemsetAsync(out, 0, out_words * 4, st));
-    png_rows_kernel<<<(height + 63) / 64, 64, 0, st>>>(rgba, width, height, scratch, wpr, row_bits, adler_ab);
-    png_scan_kernel<<<1, 1, 0, st>>>(row_bits, height, 3, row_off, total);
-    png_scatter_kernel<<<dim3(4, height), 128, 0, st>>>(scratch, wpr, row_bits, row_off, height,
+    png_rows_kernel<<<nblk, tpb, 0, st>>>(rgba, width, height, filters, nullptr, codes, lens, scratch, wpr, row_bits,
+                                          adler_ab);
+    png_scan_kernel<<<1, 1, 0, st>>>(row_bits, height, hb.nbits, row_off, total);
+    png_scatter_kernel<<<dim3(4, height), 128, 0, st>>>(scratch, wpr, row_bits, row_off,
                                                        reinterpret_cast<uint32_t *>(out));
     AFAM_CUDA(cudaGetLastError());
-    std::vector<uint64_t> host((size_t)2 * height + 1);
-    AFAM_CUDA(cudaMemcpyAsync(host.data(), adler_ab, sizeof(uint64_t) * 2 * height, cudaMemcpyDeviceToHost, st));
-    AFAM_CUDA(cudaMemcpyAsync(host.data() + 2 * height, total, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    uint64_t body_end = 0;
+    AFAM_CUDA(cudaMemcpyAsync(&body_end, total, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
     AFAM_CUDA(cudaStreamSynchronize(st));
-    // header bits: BFINAL = 1, BTYPE = 01 (fixed) -> value 0b011 in the first 3 bits
-    uint32_t first;
-    AFAM_CUDA(cudaMemcpy(&first, out, 4, cudaMemcpyDeviceToHost));
-    first |= 3u;
-    AFAM_CUDA(cudaMemcpy(out, &first, 4, cudaMemcpyHostToDevice));
-    // end of block: symbol 256 = 7 zero bits (the buffer is zeroed): just count them
-    const uint64_t bits = host[2 * height] + 7;
-    *out_bytes = (bits + 7) / 8;
+    // header bits in front (OR into the first bytes) and the end-of-block code behind
+    {
+        const size_t nb = (hb.nbits + 7) / 8;
+        std::vector<uint8_t> head(nb);
+        AFAM_CUDA(cudaMemcpy(head.data(), out, nb, cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < nb; i++) head[i] |= hb.bytes[i];
+        AFAM_CUDA(cudaMemcpy(out, head.data(), nb, cudaMemcpyHostToDevice));
+        HostBits tail;
+        tail.nbits = body_end & 7;  // position inside the last byte
+        tail.bytes.assign(1, 0);
+        tail.put(cc[256], ll[256]);
+        const size_t tb = (tail.nbits + 7) / 8;
+        std::vector<uint8_t> last(tb);
+        AFAM_CUDA(cudaMemcpy(last.data(), out + (body_end >> 3), tb, cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < tb; i++) last[i] |= tail.bytes[i];
+        AFAM_CUDA(cudaMemcpy(out + (body_end >> 3), last.data(), tb, cudaMemcpyHostToDevice));
+        *out_bytes = (body_end + (uint64_t)ll[256] + 7) / 8;
+    }
     // Adler-32 over the rows in order
     const uint64_t MOD = 65521;
     uint64_t s1 = 1, s2 = 0;
-    const uint64_t m = (uint64_t)n;
     for (int y = 0; y < height; y++) {
-        s2 = (s2 + (m % MOD) * s1 + host[2 * y + 1] % MOD) % MOD;
-        s1 = (s1 + host[2 * y] % MOD) % MOD;
+        s2 = (s2 + ((uint64_t)n % MOD) * s1 + ab[2 * y + 1] % MOD) % MOD;
+        s1 = (s1 + ab[2 * y] % MOD) % MOD;
     }
     *adler = (uint32_t)((s2 << 16) | s1);
     AFAM_CUDA(cudaFreeAsync(scratch, st));
     AFAM_CUDA(cudaFreeAsync(meta, st));
+    AFAM_CUDA(cudaFreeAsync(hist, st));
+    AFAM_CUDA(cudaFreeAsync(small, st));
     return AFAM_OK;
 }

@@ -229,7 +229,7 @@ def png_bytes_gpu(rgba) -> bytes:
     H, W = int(d.shape[0]), int(d.shape[1])
     if d.shape[2] != 4 or d.dtype != torch.uint8:
         raise ValueError(f"expected (H, W, 4) uint8 RGBA, got {tuple(d.shape)} {d.dtype}")
-    cap = int(((4 * W + 1) * 9 // 8 + 16) * H + 1024)
+    cap = int(((4 * W + 1) * 15 // 8 + 16) * H + 2048)
     out = torch.empty(cap, dtype=torch.uint8, device=d.device)
     nbytes, adler = C.c_uint64(), C.c_uint32()
     with torch.cuda.device(d.device):
