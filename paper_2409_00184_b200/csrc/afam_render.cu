@@ -528,9 +528,46 @@ __device__ __forceinline__ bool span_interior(const BlockFast &b, int k) {
     return k >= P - 1 && k <= b.nspan - P;  // none when nspan < 2p - 1
 }
 
+// Closed form of the cubic clamped-uniform basis on the two spans at either
+// end (nspan >= 6): in the span's local coordinate f the knots are
+// 0,0,0,0,1,2,3,4,... (span 0, 1) and the mirror image at the other end, so
+// every block shares these polynomials (power basis, ascending; E_q is the
+// difference-form weight sum_{i>q} dN_i/df).  Checked against exact
+// rational Cox-de Boor in DESIGN.md's derivation script.
+__constant__ float kBndN[2][4][4] = {
+    {{1.f, -3.f, 3.f, -1.f}, {0.f, 3.f, -4.5f, 1.75f}, {0.f, 0.f, 1.5f, -11.f / 12.f}, {0.f, 0.f, 0.f, 1.f / 6.f}},
+    {{0.25f, -0.75f, 0.75f, -0.25f}, {7.f / 12.f, 0.25f, -1.25f, 7.f / 12.f}, {1.f / 6.f, 0.5f, 0.5f, -0.5f},
+     {0.f, 0.f, 0.f, 1.f / 6.f}}};
+__constant__ float kBndE[2][3][3] = {{{3.f, -6.f, 3.f}, {0.f, 3.f, -2.25f}, {0.f, 0.f, 0.5f}},
+                                     {{0.75f, -1.5f, 0.75f}, {0.5f, 1.f, -1.f}, {0.f, 0.f, 0.5f}}};
+
+// span class of a cubic boundary span k (not interior): 0/1 from the left
+// end, mirrored from the right end
+__device__ __forceinline__ void bnd_class(const BlockFast &b, int k, int &cls, bool &mirror) {
+    mirror = k > 1;
+    cls = mirror ? b.nspan - 1 - k : k;
+}
+
 template <int P>
 __device__ __forceinline__ void axis_table_N(const BlockFast &b, const ThreadCold &C, int a, int k, float tq,
                                              float (&N)[P + 1]) {
+    if constexpr (P == 3) {
+        if (b.nspan >= 6) {
+            int cls;
+            bool mirror;
+            bnd_class(b, k, cls, mirror);
+            const float fr = tq - (float)k;
+            const float f = mirror ? 1.f - fr : fr;
+            float n[4];
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+                n[i] = fmaf(fmaf(fmaf(kBndN[cls][i][3], f, kBndN[cls][i][2]), f, kBndN[cls][i][1]), f,
+                            kBndN[cls][i][0]);
+#pragma unroll
+            for (int i = 0; i < 4; i++) N[i] = mirror ? n[3 - i] : n[i];
+            return;
+        }
+    }
     Tab<float> t;
     load_entry<P>(C.tab32 + ((size_t)a * b.nspan + k) * tab_stride(P), t);
     basis_vals_only<P, float>(t, clamp01(tq / (float)b.nspan), N);
@@ -542,6 +579,16 @@ __device__ __forceinline__ void axis_fast_E(const BlockFast &b, const ThreadCold
     const float nsf = (float)b.nspan;
     if (k >= P - 1 && k <= b.nspan - P) {  // interior span (none when nspan < 2p - 1)
         uniform_E<P>(fr, nsf, E);
+    } else if (P == 3 && b.nspan >= 6) {
+        int cls;
+        bool mirror;
+        bnd_class(b, k, cls, mirror);
+        const float f = mirror ? 1.f - fr : fr;
+        float e[3];
+#pragma unroll
+        for (int q = 0; q < 3; q++) e[q] = nsf * fmaf(fmaf(kBndE[cls][q][2], f, kBndE[cls][q][1]), f, kBndE[cls][q][0]);
+#pragma unroll
+        for (int q = 0; q < P; q++) E[q] = mirror ? e[2 - q] : e[q];
     } else {
         Tab<float> t;
         float N[P + 1];
