@@ -599,11 +599,17 @@ __device__ __forceinline__ void axis_fast_E(const BlockFast &b, const ThreadCold
 
 // TF opacity of a decoded value from the per-bucket lines (render.py:117-124
 // np.interp); NaN-marked buckets hold a breakpoint and take the segment search.
+// The kernel's dynamic shared memory: [ThreadCold x 128 | TF opacity lines | owner grid]
+extern __shared__ __align__(16) unsigned char afam_render_smem[];
+constexpr size_t kSmemAlphaOff = 128 * sizeof(ThreadCold);
+constexpr size_t kSmemGridOff = kSmemAlphaOff + kTfBuckets * sizeof(float2);
+
 __device__ __forceinline__ float tf_alpha(const TfTable &T, float v, int &bi, float &bf) {
     const float tb = (v - T.lo) * T.scale;
     bi = min(max(__float2int_rz(tb), 0), kTfBuckets - 1);
     bf = tb - (float)bi;
-    const float2 l = __ldg(&T.alpha[bi]);
+    // opacity lines staged in shared memory (the per-sample critical path)
+    const float2 l = reinterpret_cast<const float2 *>(afam_render_smem + kSmemAlphaOff)[bi];
     float a = fmaf(bf, l.y, l.x);
     if (isnan(a)) a = tf_eval(T, v).w;
     return a;
@@ -894,7 +900,9 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
     // arguments in global memory, for the out-of-line exact path
     const TfTable &tf = *gtf;
     ThreadCold &C = reinterpret_cast<ThreadCold *>(smem)[threadIdx.x];
-    int16_t *sgrid = reinterpret_cast<int16_t *>(smem + 128 * sizeof(ThreadCold));
+    int16_t *sgrid = reinterpret_cast<int16_t *>(smem + kSmemGridOff);
+    for (int i = threadIdx.x; i < kTfBuckets; i += blockDim.x)
+        reinterpret_cast<float2 *>(smem + kSmemAlphaOff)[i] = gtf->alpha[i];
     if (SMEM_GRID)
         for (int i = threadIdx.x; i < A.cells * A.cells * A.cells; i += blockDim.x) sgrid[i] = grid[i];
     __syncthreads();
@@ -1426,7 +1434,7 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
         LaunchArgs L;
         L.grid = dim3((A.width + 15) / 16, (A.rows + 7) / 8);
         const bool sg = cells <= kSmemGridMaxCells;
-        L.smem = 128 * sizeof(ThreadCold) + (sg ? gbytes : 0);
+        L.smem = kSmemGridOff + (sg ? gbytes : 0);
         L.st = st;
         L.descs = s->d_desc;
         L.owner = (const int16_t *)(d_pack + off_grid);
