@@ -318,27 +318,6 @@ static int check_put(afam_store *s, int32_t slot, int deg, int ncp, const double
     return AFAM_OK;
 }
 
-int afam_store_put_mfa(afam_store *s, int32_t slot, const uint8_t *bytes, uint64_t nbytes, int32_t ncp,
-                       const double extent[6], void *stream) {
-    AFAM_CHECK(bytes && nbytes >= 1, AFAM_E_FORMAT, "empty micro-model byte string");
-    const int deg = bytes[0];
-    // model.py:123-133
-    AFAM_CHECK(deg < ncp, AFAM_E_FORMAT, "degree byte %d >= ncp %d", deg, ncp);
-    const size_t expected = serialized_size(ncp, deg);
-    AFAM_CHECK(nbytes == expected, AFAM_E_FORMAT,
-               "micro-model length mismatch: expected %zu bytes for ncp=%d, degree=%d, found %llu", expected,
-               ncp, deg, (unsigned long long)nbytes);
-    int rc = check_put(s, slot, deg, ncp, extent);
-    if (rc) return rc;
-    cudaStream_t st = (cudaStream_t)stream;
-    std::lock_guard<std::mutex> lk(s->mu);
-    AFAM_CUDA(cudaSetDevice(s->device));
-    // the previous upload into this slot (possibly on another stream) must be done
-    AFAM_CUDA(cudaStreamWaitEvent(st, s->host[slot].ready, 0));
-    AFAM_CUDA(cudaMemcpyAsync(s->raw_ptr(slot), bytes, nbytes, cudaMemcpyHostToDevice, st));
-    return launch_unpack(s, slot, deg, ncp, 1, 0, 1 + 12ull * (ncp + deg), extent, st);
-}
-
 // model.py MicroModel: non-finite control points are a ValueError.  Host
 // scan of the little-endian float32 payload by exponent bits (vectorizes).
 static bool all_finite_le_f32(const uint8_t *p, size_t count) {
@@ -350,6 +329,31 @@ static bool all_finite_le_f32(const uint8_t *p, size_t count) {
     }
     return bad == 0;
 }
+
+int afam_store_put_mfa(afam_store *s, int32_t slot, const uint8_t *bytes, uint64_t nbytes, int32_t ncp,
+                       const double extent[6], void *stream) {
+    AFAM_CHECK(bytes && nbytes >= 1, AFAM_E_FORMAT, "empty micro-model byte string");
+    const int deg = bytes[0];
+    // model.py:123-133
+    AFAM_CHECK(deg < ncp, AFAM_E_FORMAT, "degree byte %d >= ncp %d", deg, ncp);
+    const size_t expected = serialized_size(ncp, deg);
+    AFAM_CHECK(nbytes == expected, AFAM_E_FORMAT,
+               "micro-model length mismatch: expected %zu bytes for ncp=%d, degree=%d, found %llu", expected,
+               ncp, deg, (unsigned long long)nbytes);
+    // model.py MicroModel: non-finite control points are a ValueError
+    AFAM_CHECK(all_finite_le_f32(bytes + 1 + 12ull * (ncp + deg), (size_t)ncp * ncp * ncp), AFAM_E_VALUE,
+               "non-finite control points");
+    int rc = check_put(s, slot, deg, ncp, extent);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    std::lock_guard<std::mutex> lk(s->mu);
+    AFAM_CUDA(cudaSetDevice(s->device));
+    // the previous upload into this slot (possibly on another stream) must be done
+    AFAM_CUDA(cudaStreamWaitEvent(st, s->host[slot].ready, 0));
+    AFAM_CUDA(cudaMemcpyAsync(s->raw_ptr(slot), bytes, nbytes, cudaMemcpyHostToDevice, st));
+    return launch_unpack(s, slot, deg, ncp, 1, 0, 1 + 12ull * (ncp + deg), extent, st);
+}
+
 
 int afam_store_put_file(afam_store *s, int32_t slot, const char *path, int32_t ncp, const double extent[6],
                         int32_t *degree, void *stream) {

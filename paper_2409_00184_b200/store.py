@@ -68,11 +68,9 @@ def device_loader(store_root, manifest, dstore, stream=None, source=None):
         data = source(addr)
         if ent is None:
             raise FormatError(f"manifest has no model file for block {addr.key}")
-        model.parse_header(data, ent.ncp)  # FormatError semantics of model.deserialize
+        # afam_store_put_mfa validates like model.deserialize (FormatError on
+        # length / degree byte, ValueError on non-finite control points)
         buf = np.frombuffer(data, dtype=np.uint8) if not isinstance(data, np.ndarray) else data
-        ctrl = np.frombuffer(buf, dtype="<f4", offset=1 + 12 * (ent.ncp + int(buf[0])), count=ent.ncp ** 3)
-        if not np.isfinite(ctrl).all():
-            raise ValueError("non-finite control points")
         return dstore.load_mfa(buf, ent.ncp, ent.extent, addr.lod, stream)
 
     return load
