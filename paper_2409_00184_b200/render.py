@@ -397,6 +397,25 @@ def _pinned_stage(nbytes: int):
     return buf
 
 
+_streams: dict = {}
+
+
+def _render_stream(dev):
+    """A high-priority stream per (device, thread) for the render kernel:
+    block uploads of the prefetch thread (default-priority loader streams)
+    then yield the SMs to the frame.  render_part synchronizes it before
+    returning, so callers see finished results as with their own stream."""
+    import torch
+
+    key = (dev.index, threading.get_ident())
+    s = _streams.get(key)
+    if s is None:
+        lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
+        s = torch.cuda.Stream(device=dev, priority=min(lo, hi))
+        _streams[key] = s
+    return s
+
+
 def render_part(pov, blocks: dict, tf, params, *, band_rows: int | None = None, nparts: int = 1, part: int = 0,
                 device: int | None = None, debug: bool = False, stream=None, out=None, raise_missing=True,
                 host_out: bool = False, out_ptr: int | None = None):
@@ -436,7 +455,7 @@ def render_part(pov, blocks: dict, tf, params, *, band_rows: int | None = None, 
         ohash = torch.empty((rows, W), dtype=torch.int64, device=dev)
     sl = np.ascontiguousarray(slots, dtype=np.int32)
     with torch.cuda.device(dev):
-        s_obj = stream if stream is not None else torch.cuda.current_stream(dev)
+        s_obj = stream if stream is not None else _render_stream(dev)
         _lib.check(_lib.lib().afam_render(
             store.handle, C.byref(fr), sl.ctypes.data_as(C.c_void_p), len(sl),
             C.c_void_p(out_ptr if out_ptr is not None else out.data_ptr()),
