@@ -137,8 +137,22 @@ def evaluate_points_with_gradient(coeff, degree: int, u, knots=None):
 
 def decode_tensor_product(coeff, degree: int, dims) -> np.ndarray:
     """Decode onto the uniform dims lattice (reference bspline.py:162-172)."""
-    d = tuple(int(v) for v in dims)
-    if d[0] != d[1] or d[1] != d[2]:
-        raise ValueError(f"decode dims must be cubic on the device path, got {d}")
     store, (slot,) = as_device_blocks([_as_model(coeff, degree, None)])
-    return decode_slots(store, [slot], d[0])[0]
+    return decode_block(store, slot, dims)
+
+
+def decode_block(store, slot: int, dims) -> np.ndarray:
+    """One resident block on the uniform dims lattice, float64 [i, j, k].
+    Cubic dims take K3 (afam_decode_grid_ex); other shapes evaluate the
+    lattice parameters linspace(0, 1, d) per axis with K1 (param mode), the
+    reference's u grid (bspline.py:117)."""
+    d = tuple(int(v) for v in np.broadcast_to(np.asarray(dims), (3,)))
+    if min(d) < 1:
+        raise ValueError(f"decode dims must be positive, got {d}")
+    if d[0] == d[1] == d[2] and d[0] >= 2:
+        return decode_slots(store, [slot], d[0])[0]
+    axes = [np.linspace(0.0, 1.0, n) for n in d]
+    u = np.stack(np.meshgrid(*axes, indexing="ij"), axis=-1).reshape(-1, 3)
+    return eval_device(store, int(slot), u, gradient=False, param=True).reshape(d)
+
+

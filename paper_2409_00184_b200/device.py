@@ -67,20 +67,12 @@ class DeviceBlock:
         return eval_device(self.store, self.slot, points, gradient=True)[1]
 
     def decode_grid(self, dims):
-        from .bspline import decode_slots
+        from .bspline import decode_block
 
-        m = _cubic_dims(dims)
-        return decode_slots(self.store, [self.slot], m)[0]
+        return decode_block(self.store, self.slot, dims)
 
     def __repr__(self):
         return f"DeviceBlock(slot={self.slot}, lod={self.lod}, ncp={self.ncp}, degree={self.degree})"
-
-
-def _cubic_dims(dims) -> int:
-    d = tuple(int(v) for v in np.broadcast_to(np.asarray(dims), (3,)))
-    if d[0] != d[1] or d[1] != d[2]:
-        raise ValueError(f"decode dims must be cubic on the device path, got {d}")
-    return d[0]
 
 
 def _extent6(extent) -> np.ndarray:

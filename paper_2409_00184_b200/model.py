@@ -97,11 +97,10 @@ class MicroModel:
         return eval_device(store, slot, points, gradient=True)[1]
 
     def decode_grid(self, dims) -> np.ndarray:
-        from .bspline import decode_slots
-        from .device import _cubic_dims
+        from .bspline import decode_block
 
         store, slot = self._resident()
-        return decode_slots(store, [slot], _cubic_dims(dims))[0]
+        return decode_block(store, slot, dims)
 
 
 def serialize(model) -> bytes:

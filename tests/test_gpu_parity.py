@@ -131,6 +131,27 @@ def test_decode_grid_vs_reference_golden(cuda):
         assert np.abs(got - want).max() <= VALUE_TOL * max(1.0, float(np.abs(want).max()))
 
 
+def test_decode_non_cubic_dims_vs_oracle(cuda, oracle):
+    """decode_grid / decode_tensor_product on non-cubic dims (the reference
+    accepts any dims triple, bspline.py:162-172): linspace(0, 1, 9) and
+    linspace(0, 1, 5) are exact sub-lattices of linspace(0, 1, 17), so the
+    (9, 17, 5) decode is the oracle's 17^3 decode strided."""
+    from paper_2409_00184_b200 import bspline, model
+
+    rng = np.random.default_rng(11)
+    for degree, ncp in ((2, 7), (3, 12), (1, 5)):
+        ctrl = rng.random((ncp, ncp, ncp)).astype(np.float32)
+        want = oracle.decode_grid(ctrl, degree, 17)[::2, :, ::4]
+        got = bspline.decode_tensor_product(ctrl, degree, (9, 17, 5))
+        assert got.shape == (9, 17, 5)
+        assert np.abs(got - want).max() <= VALUE_TOL
+        knots = np.repeat(bspline.clamped_knots(ncp, degree)[None, :], 3, axis=0).astype(np.float32)
+        mm = model.MicroModel(degree, knots, ctrl, [[-1, 1]] * 3, 1)
+        assert np.abs(mm.decode_grid((9, 17, 5)) - want).max() <= VALUE_TOL
+        one = mm.decode_grid((1, 17, 17))  # a single u = 0 plane
+        assert np.abs(one - oracle.decode_grid(ctrl, degree, 17)[:1]).max() <= VALUE_TOL
+
+
 def test_decode_config1_all_blocks_vs_oracle(cuda, oracle):
     """BASELINE config 1: all 729 blocks of the 64^3 ML store, 8^3 lattice."""
     from paper_2409_00184_b200.bspline import decode_slots

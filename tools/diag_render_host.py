@@ -1,5 +1,5 @@
-"""Break down render_part's host wall time (no replay, blocks resident)."""
-import ctypes as C
+"""Where the host time of render.render() goes on resident config-3 blocks:
+total call vs kernel_ms, and the cost of materialising the 4 MB frame."""
 import sys
 import time
 
@@ -8,7 +8,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import bench  # noqa: E402
-from paper_2409_00184_b200 import _lib, render, runtime  # noqa: E402
+from paper_2409_00184_b200 import render, runtime  # noqa: E402
 from paper_2409_00184_b200.device import DeviceStore  # noqa: E402
 
 man, blobs, _ = bench.build_model(pinned=False)
@@ -18,40 +18,25 @@ tf = render.TransferFunction.ml_preset()
 need = sorted({a for k in range(3, 23) for a in render.select_visible(povs[k], man)})
 ds = DeviceStore(len(need) + 1, 65)
 res = {a: ds.load_mfa(blobs[a], man.entries[a].ncp, man.entries[a].extent, a.lod) for a in need}
+frames = [{a: res[a] for a in render.select_visible(povs[k], man)} for k in range(3, 23)]
+for k in range(3):
+    render.render(povs[3 + k], frames[k], tf, params)
 torch.cuda.synchronize()
-lib = _lib.lib()
-orig = lib.afam_render
-T = {"c_call": [], "sync": []}
-
-
-class Wrap:
-    def __call__(self, *a):
-        t0 = time.perf_counter()
-        r = orig(*a)
-        T["c_call"].append((time.perf_counter() - t0) * 1e3)
-        return r
-
-
-lib.afam_render = Wrap()
-orig_sync = torch.cuda.Stream.synchronize
-
-
-def sync(self):
+tot, kern = [], []
+for k in range(20):
     t0 = time.perf_counter()
-    orig_sync(self)
-    T["sync"].append((time.perf_counter() - t0) * 1e3)
-
-
-torch.cuda.Stream.synchronize = sync
-for host_out in (False, True):
-    for key in T:
-        T[key].clear()
-    walls, kms = [], []
-    for k in range(3, 23):
-        blocks = {a: res[a] for a in render.select_visible(povs[k], man)}
+    fr = render.render(povs[3 + k], frames[k], tf, params)
+    tot.append((time.perf_counter() - t0) * 1e3)
+    kern.append(render.render.last_stats["kernel_ms"])
+print("render() %.3f ms, kernel %.3f ms" % (np.median(tot), np.median(kern)))
+src = torch.empty(4 << 20, dtype=torch.uint8, pin_memory=True)
+for name, fn in (("clone pinned->torch", lambda: src.clone()),
+                 ("np.empty+copyto", lambda: np.copyto(np.empty(4 << 20, np.uint8), src.numpy())),
+                 ("np.array copy", lambda: np.array(src.numpy()))):
+    ts = []
+    for _ in range(30):
         t0 = time.perf_counter()
-        out, info, _ = render.render_part(povs[k], blocks, tf, params, host_out=host_out)
-        walls.append((time.perf_counter() - t0) * 1e3)
-        kms.append(info["kernel_ms"])
-    print(f"host_out={host_out}: wall {np.mean(walls[2:]):.3f} ms, kernel {np.mean(kms[2:]):.3f} ms, "
-          f"afam_render call {np.mean(T['c_call'][2:]):.3f} ms, sync {np.mean(T['sync'][2:]):.3f} ms", flush=True)
+        x = fn()
+        ts.append((time.perf_counter() - t0) * 1e3)
+        del x
+    print("%s %.3f ms" % (name, np.median(ts)))
