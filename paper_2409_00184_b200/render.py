@@ -426,6 +426,55 @@ def render_part(pov, blocks: dict, tf, params, *, band_rows: int | None = None, 
     address of a whole H x W x 4 frame, e.g. rank 0's frame mapped over
     NVLink, tiles.PeerFrame) the rows land at their frame rows instead and
     the returned tensor is None."""
+    return submit_part(pov, blocks, tf, params, band_rows=band_rows, nparts=nparts, part=part, device=device,
+                       debug=debug, stream=stream, out=out, raise_missing=raise_missing, host_out=host_out,
+                       out_ptr=out_ptr).result()
+
+
+class PendingPart:
+    """A launched render_part: `done()` polls the GPU (no host wait),
+    `result()` waits and returns render_part's (rgba, info, debug)."""
+
+    def __init__(self, **kw):
+        self.__dict__.update(kw)
+        self._res = None
+
+    def done(self) -> bool:
+        return self._res is not None or self.event.query()
+
+    def result(self):
+        if self._res is not None:
+            return self._res
+        import torch
+
+        with torch.cuda.device(self.dev):
+            self.s_obj.synchronize()
+            st = self.stage[:48].view(torch.int64).numpy().copy()
+            out = self.out
+            if self.host_out:
+                out = self.stage[64:64 + self.nbytes].view(self.rows, self.W, 4).clone()
+        kms = C.c_float()
+        _lib.check(_lib.lib().afam_render_elapsed(self.store.handle, C.byref(kms)))
+        info = {"samples": int(st[0]), "missing_key": int(st[1]), "fp64_samples": int(st[2]),
+                "shaded_samples": int(st[3]), "exact_samples": int(st[4]),
+                "exact_cells": int(st[5]),
+                "kernel_ms": float(kms.value)}
+        if self.raise_missing and info["missing_key"] >= 0:
+            cells = C.c_int32()
+            _lib.check(_lib.lib().afam_owner_grid(self.store.handle, self.sl.ctypes.data_as(C.c_void_p),
+                                                  len(self.sl), C.byref(cells), None, 0))
+            raise MissingBlockError(_missing_message(self.pov, self.params, cells.value, info["missing_key"]))
+        dbg = {"nsamp": self.nsamp, "ohash": self.ohash} if self.debug else None
+        self._res = (out, info, dbg)
+        return self._res
+
+
+def submit_part(pov, blocks: dict, tf, params, *, band_rows: int | None = None, nparts: int = 1, part: int = 0,
+                device: int | None = None, debug: bool = False, stream=None, out=None, raise_missing=True,
+                host_out: bool = False, out_ptr: int | None = None) -> PendingPart:
+    """render_part without the wait: launches the frame's kernels and
+    returns a PendingPart, so the caller's thread can do host work (the
+    replay prefetch) while the GPU marches."""
     import torch
 
     from .device import as_device_blocks, stream_handle
@@ -465,31 +514,40 @@ def render_part(pov, blocks: dict, tf, params, *, band_rows: int | None = None, 
             stage[:48].view(torch.int64).copy_(stats, non_blocking=True)
             if host_out and not zero_copy:
                 stage[64:64 + rows * W * 4].view(rows, W, 4).copy_(out, non_blocking=True)
-        s_obj.synchronize()
-        st = stage[:48].view(torch.int64).numpy().copy()
-        if host_out:
-            out = stage[64:64 + rows * W * 4].view(rows, W, 4).clone()
-    kms = C.c_float()
-    _lib.check(_lib.lib().afam_render_elapsed(store.handle, C.byref(kms)))
-    info = {"samples": int(st[0]), "missing_key": int(st[1]), "fp64_samples": int(st[2]),
-            "shaded_samples": int(st[3]), "exact_samples": int(st[4]),
-            "exact_cells": int(st[5]),
-            "kernel_ms": float(kms.value)}
-    if raise_missing and info["missing_key"] >= 0:
-        cells = C.c_int32()
-        _lib.check(_lib.lib().afam_owner_grid(store.handle, sl.ctypes.data_as(C.c_void_p), len(sl), C.byref(cells),
-                                              None, 0))
-        raise MissingBlockError(_missing_message(pov, params, cells.value, info["missing_key"]))
-    dbg = {"nsamp": nsamp, "ohash": ohash} if debug else None
-    return out, info, dbg
+            event = torch.cuda.Event()
+            event.record(s_obj)
+    return PendingPart(dev=dev, s_obj=s_obj, stage=stage, out=out, host_out=host_out, nbytes=rows * W * 4,
+                       rows=rows, W=W, store=store, sl=sl, pov=pov, params=params, raise_missing=raise_missing,
+                       debug=debug, nsamp=nsamp, ohash=ohash, stats=stats, event=event)
+
+
+class PendingFrame:
+    """render.submit's handle: `done()` polls, `result()` returns the Frame
+    (and sets `on.last_stats`)."""
+
+    def __init__(self, part: PendingPart, params, on, finish=None):
+        self.part, self.params, self.on, self.finish = part, params, on, finish
+
+    def done(self) -> bool:
+        return self.part.done()
+
+    def result(self):
+        out, info, _ = self.part.result()
+        self.on.last_stats = info
+        if self.finish is not None:
+            return self.finish(out, info)
+        return Frame(width=int(self.params.width), height=int(self.params.height), rgba=out.numpy())
+
+
+def submit(pov, blocks: dict, tf, params) -> PendingFrame:
+    """render() split at the GPU wait: launch the frame, return a handle."""
+    return PendingFrame(submit_part(pov, blocks, tf, params, host_out=True), params, render)
 
 
 def render(pov, blocks: dict, tf, params) -> Frame:
     """Front-to-back composite of the resident blocks (render.py:398-466) on the GPU."""
-    out, info, _ = render_part(pov, blocks, tf, params, host_out=True)
-    frame = Frame(width=int(params.width), height=int(params.height), rgba=out.numpy())
-    render.last_stats = info
-    return frame
+    return submit(pov, blocks, tf, params).result()
 
 
+render.submit = submit
 render.last_stats = None

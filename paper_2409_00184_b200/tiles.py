@@ -68,23 +68,31 @@ def render_tiles(pov, blocks: dict, tf, params, *, group=None, band_rows: int = 
     """render.render across the ranks of `group`: returns the Frame on `dst`
     (None on the other ranks).  Without torch.distributed initialised it is
     a single-GPU render."""
+    return submit_tiles(pov, blocks, tf, params, group=group, band_rows=band_rows, dst=dst).result()
+
+
+def submit_tiles(pov, blocks: dict, tf, params, *, group=None, band_rows: int = 8, dst: int = 0):
+    """render_tiles split at the GPU wait (render.PendingFrame): the band
+    gather runs in result()."""
     import torch.distributed as dist
 
-    from .render import Frame, render_part
+    from .render import Frame, PendingFrame, submit_part
 
     if not (dist.is_available() and dist.is_initialized()):
-        out, info, _ = render_part(pov, blocks, tf, params, host_out=True)
-        render_tiles.last_stats = info
-        return Frame(int(params.width), int(params.height), out.numpy())
+        return PendingFrame(submit_part(pov, blocks, tf, params, host_out=True), params, render_tiles)
     world, rank = dist.get_world_size(group), dist.get_rank(group)
-    out, info, _ = render_part(pov, blocks, tf, params, band_rows=band_rows, nparts=world, part=rank)
-    render_tiles.last_stats = info
-    full = gather_bands(out, int(params.height), band_rows, group, dst)
-    if full is None:
-        return None
-    return Frame(int(params.width), int(params.height), full.cpu().numpy())
+
+    def finish(out, info):
+        full = gather_bands(out, int(params.height), band_rows, group, dst)
+        if full is None:
+            return None
+        return Frame(int(params.width), int(params.height), full.cpu().numpy())
+
+    return PendingFrame(submit_part(pov, blocks, tf, params, band_rows=band_rows, nparts=world, part=rank),
+                        params, render_tiles, finish)
 
 
+render_tiles.submit = submit_tiles
 render_tiles.last_stats = None
 
 
@@ -165,20 +173,28 @@ def render_tiles_fused(pov, blocks: dict, tf, params, peer: PeerFrame, *, group=
     destination rank's frame, over NVLink; one barrier orders the writes
     before the destination reads.  Returns the Frame on the destination rank
     (None elsewhere)."""
+    return submit_tiles_fused(pov, blocks, tf, params, peer, group=group, band_rows=band_rows).result()
+
+
+def submit_tiles_fused(pov, blocks: dict, tf, params, peer: PeerFrame, *, group=None, band_rows: int = 8):
+    """render_tiles_fused split at the GPU wait (render.PendingFrame)."""
     import torch.distributed as dist
 
-    from .render import Frame, render_part
+    from .render import Frame, PendingFrame, submit_part
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
-    _, info, _ = render_part(pov, blocks, tf, params, band_rows=band_rows, nparts=world, part=rank,
-                             out_ptr=peer.ptr)
-    render_tiles_fused.last_stats = info
-    if world > 1:
-        dist.barrier(group)  # every rank's kernel (and its peer stores) completed
-    if rank != peer.dst:
-        return None
-    return Frame(int(params.width), int(params.height), peer.frame())
+
+    def finish(out, info):
+        if world > 1:
+            dist.barrier(group)  # every rank's kernel (and its peer stores) completed
+        if rank != peer.dst:
+            return None
+        return Frame(int(params.width), int(params.height), peer.frame())
+
+    return PendingFrame(submit_part(pov, blocks, tf, params, band_rows=band_rows, nparts=world, part=rank,
+                                    out_ptr=peer.ptr), params, render_tiles_fused, finish)
 
 
+render_tiles_fused.submit = submit_tiles_fused
 render_tiles_fused.last_stats = None
