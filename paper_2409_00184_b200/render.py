@@ -431,6 +431,10 @@ def render_part(pov, blocks: dict, tf, params, *, band_rows: int | None = None, 
                        out_ptr=out_ptr).result()
 
 
+def _addr_key(a):
+    return (a.lod, a.ijk)
+
+
 class PendingPart:
     """A launched render_part: `done()` polls the GPU (no host wait),
     `result()` waits and returns render_part's (rgba, info, debug)."""
@@ -479,7 +483,10 @@ def submit_part(pov, blocks: dict, tf, params, *, band_rows: int | None = None, 
 
     from .device import as_device_blocks, stream_handle
 
-    addrs = sorted(blocks)
+    try:  # (lod, i, j, k) order as BlockAddress.__lt__, without a Python compare per pair
+        addrs = sorted(blocks, key=_addr_key)
+    except AttributeError:
+        addrs = sorted(blocks)
     dev_index = torch.cuda.current_device() if device is None else int(device)
     store, slots = as_device_blocks([blocks[a] for a in addrs], dev_index)
     dev = torch.device("cuda", store.device)
