@@ -419,6 +419,8 @@ constexpr uint32_t kRenderForceExact = 0x100u;
 struct BlockFast {
     const float4 *ctrl4;
     int32_t ncp, nspan;
+    int32_t plane;  // ncp^2: x-quad rows per z plane
+    uint32_t nint;  // interior spans (k in [p-1, nspan-p]): max(nspan - 2p + 2, 0)
 };
 
 // Per-thread state the sample loop reads rarely (shading, boundary spans,
@@ -525,7 +527,7 @@ __device__ __forceinline__ bool axis_span(const BlockFast &b, float tq, int &k, 
 // 2(p-1) boundary spans the per-span table
 template <int P>
 __device__ __forceinline__ bool span_interior(const BlockFast &b, int k) {
-    return k >= P - 1 && k <= b.nspan - P;  // none when nspan < 2p - 1
+    return (uint32_t)(k - (P - 1)) < b.nint;  // k in [p-1, nspan-p]; none when nspan < 2p - 1
 }
 
 // Closed form of the cubic clamped-uniform basis on the two spans at either
@@ -577,7 +579,7 @@ template <int P>
 __device__ __forceinline__ void axis_fast_E(const BlockFast &b, const ThreadCold &C, int a, int k, float fr,
                                             float (&E)[P]) {
     const float nsf = (float)b.nspan;
-    if (k >= P - 1 && k <= b.nspan - P) {  // interior span (none when nspan < 2p - 1)
+    if (span_interior<P>(b, k)) {
         uniform_E<P>(fr, nsf, E);
     } else if (P == 3 && b.nspan >= 6) {
         int cls;
@@ -654,21 +656,21 @@ __device__ __forceinline__ void composite(const RenderArgs &A, const float4 vdir
 // its three knot spans changed (~1 sample in 4 at LOD-2 span widths), and the
 // L1 data path serves only the lanes that reload.
 struct CellCache {
-    const float4 *key;  // x-quad row (0, 0) of the cached cell; nullptr: empty
+    int32_t key;  // x-quad row index of the cached cell's (0, 0) row in the owner block; -1: empty
     float4 c[16];
 };
 
 template <int P>
 __device__ __forceinline__ void cell_gather(const BlockFast &b, int kx, int ky, int kz, CellCache &G) {
     constexpr int Q = P + 1;
-    const float4 *base = b.ctrl4 + ((size_t)kz * b.ncp + kx) * b.ncp + ky;
-    if (base != G.key) {
-        const size_t plane = (size_t)b.ncp * b.ncp;
+    const int32_t id = (kz * b.ncp + kx) * b.ncp + ky;  // < 72^3: 32-bit index math on the hit path
+    if (id != G.key) {
+        const float4 *base = b.ctrl4 + id;
 #pragma unroll
         for (int cz = 0; cz < Q; cz++)
 #pragma unroll
-            for (int by = 0; by < Q; by++) G.c[cz * Q + by] = __ldg(base + cz * plane + by);
-        G.key = base;
+            for (int by = 0; by < Q; by++) G.c[cz * Q + by] = __ldg(base + cz * b.plane + by);
+        G.key = id;
     }
 }
 
@@ -717,10 +719,15 @@ __device__ __forceinline__ bool sample_fast(const RenderArgs &A, const TfTable &
             Nx[i] = Nxy[i].x;
             Ny[i] = Nxy[i].y;
         }
-        if (!span_interior<P>(b, kx)) axis_table_N<P>(b, C, 0, kx, tq[0], Nx);
-        if (!span_interior<P>(b, ky)) axis_table_N<P>(b, C, 1, ky, tq[1], Ny);
-        if (span_interior<P>(b, kz)) uniform_N<P>(fz, Nz);
-        else axis_table_N<P>(b, C, 2, kz, tq[2], Nz);
+        const bool inx = span_interior<P>(b, kx), iny = span_interior<P>(b, ky), inz = span_interior<P>(b, kz);
+        if (inx & iny & inz) {  // the common case: one branch
+            uniform_N<P>(fz, Nz);
+        } else {
+            if (!inx) axis_table_N<P>(b, C, 0, kx, tq[0], Nx);
+            if (!iny) axis_table_N<P>(b, C, 1, ky, tq[1], Ny);
+            if (inz) uniform_N<P>(fz, Nz);
+            else axis_table_N<P>(b, C, 2, kz, tq[2], Nz);
+        }
     }
     // Y[cz] = sum_by Ny[by] c[cz][by] (x-quad), Z = sum_cz Nz[cz] Y[cz]
     float2 Ylo[Q], Yhi[Q], Zlo, Zhi;
@@ -973,7 +980,7 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
         BlockFast b;
         bool fast = false;
         CellCache G;
-        G.key = nullptr;
+        G.key = -1;
         DsFast dsb;
         while (M.k < M.kend) {
             if (M.own < 0) break;  // render.py:430-436 (reported after the loop)
@@ -1004,6 +1011,9 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
                 C.tab32 = (const float *)__ldg((const unsigned long long *)&dp->tab32);
                 b.ncp = __ldg(&dp->ncp);
                 b.nspan = __ldg(&dp->nspan);
+                b.plane = b.ncp * b.ncp;
+                b.nint = (uint32_t)max(b.nspan - 2 * (FD > 0 ? FD : 1) + 2, 0);
+                G.key = -1;
                 deg = __ldg(&dp->deg);
                 const uint32_t flags = __ldg(&dp->flags);
                 fast = deg == FD && (flags & kFlagUniform) && !(flags & AFAM_SLOT_FP64) && (deg > 1 || b.nspan <= 128) &&
