@@ -148,7 +148,10 @@ __device__ __forceinline__ void decode_planes(const BlockDesc &d, const int32_t 
     // one window of p+1 planes; the next output plane's new planes are issued
     // as soon as the Z stage has consumed the current window, so their HBM
     // latency hides behind the Y and X stages.
-    float *ring = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(c0 + m) + 15) & ~(uintptr_t)15);
+    // ring offset from the shared base (integer math keeps the shared address
+    // space visible to the compiler: LDS with 32-bit addressing, not generic loads)
+    const size_t ring_off = ((size_t)(reinterpret_cast<unsigned char *>(c0 + m) - smem) + 15) & ~(size_t)15;
+    float *ring = reinterpret_cast<float *>(smem + ring_off);
     uint64_t *bar = reinterpret_cast<uint64_t *>(ring + (size_t)kRing * zstride);
     const uint32_t plane_bytes = (uint32_t)(zstride * sizeof(float));
     if (threadIdx.x == 0) {
