@@ -1378,9 +1378,37 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
         }();
         if (force_exact) A.flags |= kRenderForceExact;
     }
-    TfTable tf;
-    memset(&tf, 0, sizeof(tf));
-    build_tf_table(F, tf);
+    // the TF table depends only on the TF's control points and domain: a
+    // per-thread copy is rebuilt only when they change (replay renders every
+    // frame with the same TF)
+    struct TfCache {
+        bool valid = false;
+        double key[2 + 4 * AFAM_MAX_TF_POINTS + 2 * AFAM_MAX_TF_POINTS + 2];
+        TfTable table;
+    };
+    static thread_local TfCache tfc;
+    double key[sizeof(tfc.key) / sizeof(double)];
+    {
+        memset(key, 0, sizeof(key));
+        int o = 0;
+        key[o++] = F->ncolor;
+        key[o++] = F->nopacity;
+        for (int k = 0; k < F->ncolor; k++)
+            for (int c = 0; c < 4; c++) key[o + 4 * k + c] = F->color[k][c];
+        o += 4 * AFAM_MAX_TF_POINTS;
+        for (int k = 0; k < F->nopacity; k++)
+            for (int c = 0; c < 2; c++) key[o + 2 * k + c] = F->opacity[k][c];
+        o += 2 * AFAM_MAX_TF_POINTS;
+        key[o++] = F->domain_lo;
+        key[o++] = F->domain_hi;
+    }
+    if (!tfc.valid || memcmp(key, tfc.key, sizeof(key)) != 0) {
+        memset(&tfc.table, 0, sizeof(tfc.table));
+        build_tf_table(F, tfc.table);
+        memcpy(tfc.key, key, sizeof(key));
+        tfc.valid = true;
+    }
+    const TfTable &tf = tfc.table;
     ht.mark();
 
     std::vector<int16_t> grid;

@@ -330,6 +330,29 @@ def camera_setup(pov, params) -> dict:
 
 
 def _frame_struct(pov, tf, params, band_rows, nparts, part, debug, full_frame=False) -> _lib.AfamFrame:
+    # the TF and shading fields change rarely: a per-thread template keyed by
+    # their values is copied and only the camera / band fields are set
+    cp, op = np.asarray(tf.color_points, np.float64), np.asarray(tf.opacity_points, np.float64)
+    key = (cp.tobytes(), op.tobytes(), cp.shape, op.shape, tuple(float(v) for v in tf.domain),
+           float(params.sample_distance), params.reference_step, float(params.o_max), float(params.near),
+           float(params.ambient), float(params.diffuse), float(params.specular), float(params.shininess))
+    cache = getattr(_tls, "frame_tmpl", None)
+    if cache is None or cache[0] != key:
+        cache = (key, _frame_struct_full(pov, tf, params, band_rows, nparts, part, debug, full_frame))
+        _tls.frame_tmpl = cache
+    fr = _lib.AfamFrame.from_buffer_copy(cache[1])
+    cam = camera_setup(pov, params)
+    for a in range(3):
+        fr.origin[a] = float(pov.position[a])
+        fr.f[a], fr.r[a], fr.u[a] = float(cam["f"][a]), float(cam["r"][a]), float(cam["u"][a])
+    fr.tan_x, fr.tan_y = cam["tan_x"], cam["tan_y"]
+    fr.width, fr.height = int(params.width), int(params.height)
+    fr.band_rows, fr.nparts, fr.part = int(band_rows), int(nparts), int(part)
+    fr.flags = (_lib.AFAM_RENDER_DEBUG if debug else 0) | (_lib.AFAM_RENDER_FULL_FRAME if full_frame else 0)
+    return fr
+
+
+def _frame_struct_full(pov, tf, params, band_rows, nparts, part, debug, full_frame=False) -> _lib.AfamFrame:
     fr = _lib.AfamFrame()
     cam = camera_setup(pov, params)
     for a in range(3):
@@ -431,6 +454,19 @@ def render_part(pov, blocks: dict, tf, params, *, band_rows: int | None = None, 
                        out_ptr=out_ptr).result()
 
 
+def _thread_stats(dev):
+    """This thread's device stats buffer and completion event (one frame in
+    flight per thread: submit_part's handle is consumed before the next)."""
+    import torch
+
+    key = ("stats", dev.index)
+    st = getattr(_tls, "stats", None)
+    if st is None or st[0] != key:
+        st = (key, torch.empty(6, dtype=torch.int64, device=dev), torch.cuda.Event())
+        _tls.stats = st
+    return st[1], st[2]
+
+
 def _addr_key(a):
     return (a.lod, a.ijk)
 
@@ -504,7 +540,7 @@ def submit_part(pov, blocks: dict, tf, params, *, band_rows: int | None = None, 
     if out is None and out_ptr is None:
         out = stage[64:64 + rows * W * 4].view(rows, W, 4) if zero_copy else \
             torch.empty((rows, W, 4), dtype=torch.uint8, device=dev)
-    stats = torch.empty(6, dtype=torch.int64, device=dev)
+    stats, event = _thread_stats(dev)
     nsamp = ohash = None
     if debug:
         nsamp = torch.empty((rows, W), dtype=torch.int32, device=dev)
@@ -521,7 +557,6 @@ def submit_part(pov, blocks: dict, tf, params, *, band_rows: int | None = None, 
             stage[:48].view(torch.int64).copy_(stats, non_blocking=True)
             if host_out and not zero_copy:
                 stage[64:64 + rows * W * 4].view(rows, W, 4).copy_(out, non_blocking=True)
-            event = torch.cuda.Event()
             event.record(s_obj)
     return PendingPart(dev=dev, s_obj=s_obj, stage=stage, out=out, host_out=host_out, nbytes=rows * W * 4,
                        rows=rows, W=W, store=store, sl=sl, pov=pov, params=params, raise_missing=raise_missing,
