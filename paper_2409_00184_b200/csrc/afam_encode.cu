@@ -27,44 +27,55 @@ constexpr int kFitThreads = 256;
 constexpr int kFitRT = 32;     // input columns per CTA tile
 constexpr int kFitMaxN = 129;  // operator extents supported (ncp, m <= 129)
 
+// Sample grids are [d0][d1][d2] (C order, bspline.fit_tensor_product's axes
+// 0, 1, 2); every axis t has its own operators for its extent d_t.
 struct FitJob {
-    const float *samples;   // [m][m][m] float32 (block b of the batch)
-    const double *op_fit;   // [ncp][m]
-    const double *op_dec;   // [m][ncp]
-    const double *opT_fit;  // [m][ncp4] transposed, zero-padded
-    const double *opT_dec;  // [ncp][m4]
-    double *buf0, *buf1;    // ping-pong intermediates (>= m^3 doubles each)
-    float *ctrl;            // nullable: [ncp][ncp][ncp] float32 coefficients out
-    double *sse;            // sum of squared errors (accumulated)
+    const float *samples;      // [d0][d1][d2] float32 (block b of the batch)
+    const double *op_fit[3];   // axis t: [ncp][d_t]
+    const double *op_dec[3];   // axis t: [d_t][ncp]
+    const double *opT_fit[3];  // axis t: [d_t][ncp4] transposed, zero-padded
+    const double *opT_dec[3];  // axis t: [ncp][d_t4]
+    double *buf0, *buf1;       // ping-pong intermediates (>= d0 d1 d2 doubles each)
+    float *ctrl;               // nullable: [ncp][ncp][ncp] float32 coefficients out
+    double *sse;               // sum of squared errors (accumulated)
     int32_t ncp, pad;
 };
+
+struct FitDims {
+    int32_t d[3];
+};
+
+// Stage s contracts axis s % 3 (fit: d_t -> ncp, decode: ncp -> d_t); R is
+// the product of the two other current extents.
+__device__ __forceinline__ int fit_R(int stage, const FitDims &D, int ncp) {
+    switch (stage) {
+        case 0: return D.d[1] * D.d[2];
+        case 1: return D.d[2] * ncp;
+        case 2: return ncp * ncp;
+        case 3: return ncp * ncp;
+        case 4: return ncp * D.d[0];
+        default: return D.d[0] * D.d[1];
+    }
+}
 
 // One contraction of every job: in [n0][R] (slowest axis contracted) ->
 // out [R][nout].  Stage selects operator and operand types:
 //   0: samples (f32) x fit op,  1-2: f64 x fit op (2 rounds the result to
 //   float32 and optionally emits it),  3: coefficients x decode op,
 //   4: f64 x decode op,  5: f64 x decode op -> squared error vs samples.
-__global__ void __launch_bounds__(kFitThreads) contract_rotate_kernel(const FitJob *__restrict__ jobs, int m,
+__global__ void __launch_bounds__(kFitThreads) contract_rotate_kernel(const FitJob *__restrict__ jobs, FitDims D,
                                                                       int stage) {
     extern __shared__ __align__(16) unsigned char smem[];
     const FitJob J = jobs[blockIdx.y];
     const int ncp = J.ncp;
     const bool dec = stage >= 3;
-    const int n0 = dec ? ncp : m, nout = dec ? m : ncp;
-    // R = product of the two other extents at this stage
-    int R;
-    switch (stage) {
-        case 0: R = m * m; break;
-        case 1: R = m * ncp; break;
-        case 2: R = ncp * ncp; break;
-        case 3: R = ncp * ncp; break;
-        case 4: R = ncp * m; break;
-        default: R = m * m; break;
-    }
+    const int ax = stage % 3, dt = D.d[ax];
+    const int n0 = dec ? ncp : dt, nout = dec ? dt : ncp;
+    const int R = fit_R(stage, D, ncp);
     const int r0 = blockIdx.x * kFitRT;
     if (r0 >= R) return;
     const int rt = min(kFitRT, R - r0);
-    const double *op = dec ? J.op_dec : J.op_fit;
+    const double *op = dec ? J.op_dec[ax] : J.op_fit[ax];
     double *sOp = reinterpret_cast<double *>(smem);          // [nout][n0]
     double *sIn = sOp + (size_t)nout * n0;                   // [n0][kFitRT]
     double *sOut = sIn + (size_t)n0 * kFitRT;                // [kFitRT][nout]
@@ -145,25 +156,15 @@ __global__ void __launch_bounds__(kFitThreads) contract_rotate_kernel(const FitJ
 constexpr int kFitRT2 = 64;
 constexpr int kFitMaxN2 = 65;
 
-__device__ __forceinline__ int fit_R(int stage, int m, int ncp) {
-    switch (stage) {
-        case 0: return m * m;
-        case 1: return m * ncp;
-        case 2: return ncp * ncp;
-        case 3: return ncp * ncp;
-        case 4: return ncp * m;
-        default: return m * m;
-    }
-}
-
-__global__ void __launch_bounds__(kFitThreads, 2) contract_tiled_kernel(const FitJob *__restrict__ jobs, int m,
+__global__ void __launch_bounds__(kFitThreads, 2) contract_tiled_kernel(const FitJob *__restrict__ jobs, FitDims D,
                                                                        int stage) {
     extern __shared__ __align__(16) unsigned char smem[];
     const FitJob J = jobs[blockIdx.y];
     const int ncp = J.ncp;
     const bool dec = stage >= 3;
-    const int n0 = dec ? ncp : m, nout = dec ? m : ncp;
-    const int R = fit_R(stage, m, ncp);
+    const int ax = stage % 3, dt = D.d[ax];
+    const int n0 = dec ? ncp : dt, nout = dec ? dt : ncp;
+    const int R = fit_R(stage, D, ncp);
     const int r0 = blockIdx.x * kFitRT2;
     if (r0 >= R) return;
     const int rt = min(kFitRT2, R - r0);
@@ -172,7 +173,7 @@ __global__ void __launch_bounds__(kFitThreads, 2) contract_tiled_kernel(const Fi
     double *sIn = sOpT + (size_t)n0 * np;                // [n0][kFitRT2]
     double *sOut = sIn + (size_t)n0 * kFitRT2;           // [kFitRT2][nout]
     {  // transposed, padded operator [n0][np]: a straight 16-byte copy
-        const double2 *src = reinterpret_cast<const double2 *>(dec ? J.opT_dec : J.opT_fit);
+        const double2 *src = reinterpret_cast<const double2 *>(dec ? J.opT_dec[ax] : J.opT_fit[ax]);
         double2 *dst = reinterpret_cast<double2 *>(sOpT);
         for (int e = threadIdx.x; e < n0 * np / 2; e += blockDim.x) dst[e] = src[e];
     }
@@ -361,19 +362,27 @@ extern "C" int afam_fit_operator(int32_t ncp, int32_t degree, int32_t m, double 
     return AFAM_OK;
 }
 
-extern "C" int afam_fit_rmse(afam_store *s, const float *samples, int32_t nblk, int32_t m, int32_t degree,
-                             const int32_t *job_block, const int32_t *job_ncp, int32_t njobs, double *rmse,
-                             float *ctrl, const int64_t *ctrl_off, void *stream) {
-    AFAM_CHECK(s && samples && job_block && job_ncp && rmse, AFAM_E_VALUE, "NULL argument to afam_fit_rmse");
+extern "C" int afam_fit_rmse3(afam_store *s, const float *samples, int32_t nblk, const int32_t *dims,
+                              int32_t degree, const int32_t *job_block, const int32_t *job_ncp, int32_t njobs,
+                              double *rmse, float *ctrl, const int64_t *ctrl_off, void *stream) {
+    AFAM_CHECK(s && samples && dims && job_block && job_ncp && rmse, AFAM_E_VALUE, "NULL argument to afam_fit_rmse");
     AFAM_CHECK(degree >= 1 && degree <= AFAM_MAX_DEGREE, AFAM_E_VALUE, "degree %d outside [1, %d]", degree,
                AFAM_MAX_DEGREE);
-    AFAM_CHECK(m >= 2 && m <= kFitMaxN, AFAM_E_VALUE, "block edge %d outside [2, %d]", m, kFitMaxN);
+    FitDims D;
+    int maxd = 0, mind = 1 << 30;
+    for (int t = 0; t < 3; t++) {
+        D.d[t] = dims[t];
+        AFAM_CHECK(dims[t] >= 2 && dims[t] <= kFitMaxN, AFAM_E_VALUE, "block extent %d outside [2, %d]", dims[t],
+                   kFitMaxN);
+        maxd = std::max(maxd, dims[t]);
+        mind = std::min(mind, dims[t]);
+    }
     AFAM_CHECK(njobs >= 0 && njobs <= 65535, AFAM_E_VALUE, "at most 65535 jobs per call");
     AFAM_CHECK(!ctrl || ctrl_off, AFAM_E_VALUE, "ctrl needs ctrl_off");
     if (njobs == 0) return AFAM_OK;
     cudaStream_t st = (cudaStream_t)stream;
     AFAM_CUDA(cudaSetDevice(s->device));
-    const size_t cube = (size_t)m * m * m;
+    const size_t cube = (size_t)dims[0] * dims[1] * dims[2];
     std::vector<FitJob> jobs(njobs);
     double *work = nullptr, *sse = nullptr;
     AFAM_CUDA(cudaMallocAsync(&work, 2 * cube * sizeof(double) * njobs, st));
@@ -385,17 +394,20 @@ extern "C" int afam_fit_rmse(afam_store *s, const float *samples, int32_t nblk, 
         for (int j = 0; j < njobs; j++) {
             const int b = job_block[j], ncp = job_ncp[j];
             AFAM_CHECK(b >= 0 && b < nblk, AFAM_E_VALUE, "job %d: block %d outside [0, %d)", j, b, nblk);
-            AFAM_CHECK(ncp >= degree + 1 && ncp <= m, AFAM_E_VALUE, "ncp must be in [%d, %d], got %d",
-                       degree + 1, m, ncp);
-            FitOp *op = nullptr;
-            int rc = get_fit_op(s, ncp, degree, m, &op);
-            if (rc) return rc;
+            // bspline.fit_tensor_product: degree + 1 <= ncp <= m on every axis
+            AFAM_CHECK(ncp >= degree + 1 && ncp <= mind, AFAM_E_VALUE, "ncp must be in [%d, %d], got %d",
+                       degree + 1, mind, ncp);
             FitJob &J = jobs[j];
+            for (int t = 0; t < 3; t++) {
+                FitOp *op = nullptr;
+                int rc = get_fit_op(s, ncp, degree, dims[t], &op);
+                if (rc) return rc;
+                J.op_fit[t] = op->fit;
+                J.op_dec[t] = op->dec;
+                J.opT_fit[t] = op->fitT;
+                J.opT_dec[t] = op->decT;
+            }
             J.samples = samples + (size_t)b * cube;
-            J.op_fit = op->fit;
-            J.op_dec = op->dec;
-            J.opT_fit = op->fitT;
-            J.opT_dec = op->decT;
             J.buf0 = work + (size_t)j * 2 * cube;
             J.buf1 = J.buf0 + cube;
             J.ctrl = ctrl ? ctrl + ctrl_off[j] : nullptr;
@@ -408,27 +420,29 @@ extern "C" int afam_fit_rmse(afam_store *s, const float *samples, int32_t nblk, 
     AFAM_CUDA(cudaMallocAsync(&d_jobs, sizeof(FitJob) * njobs, st));
     AFAM_CUDA(cudaMemcpyAsync(d_jobs, jobs.data(), sizeof(FitJob) * njobs, cudaMemcpyHostToDevice, st));
     // the widest R of each stage (over the batch's ncp) sizes the grid; CTAs past a job's R exit
-    const int Rmax[6] = {m * m, m * maxncp, maxncp * maxncp, maxncp * maxncp, maxncp * m, m * m};
-    if (m <= kFitMaxN2) {
-        const int mp = (m + 3) & ~3;
-        const size_t smem = ((size_t)m * mp + (size_t)m * kFitRT2 + (size_t)kFitRT2 * m) * sizeof(double);
+    const int Rmax[6] = {dims[1] * dims[2], dims[2] * maxncp, maxncp * maxncp, maxncp * maxncp, maxncp * dims[0],
+                         dims[0] * dims[1]};
+    if (maxd <= kFitMaxN2) {
+        const int mp = (maxd + 3) & ~3;
+        const size_t smem = ((size_t)maxd * mp + (size_t)maxd * kFitRT2 + (size_t)kFitRT2 * maxd) * sizeof(double);
         AFAM_CUDA(cudaFuncSetAttribute(contract_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
         for (int stage = 0; stage < 6; stage++) {
             dim3 grid((Rmax[stage] + kFitRT2 - 1) / kFitRT2, njobs);
-            contract_tiled_kernel<<<grid, kFitThreads, smem, st>>>(d_jobs, m, stage);
+            contract_tiled_kernel<<<grid, kFitThreads, smem, st>>>(d_jobs, D, stage);
         }
     } else {
-        const size_t smem = ((size_t)m * m + (size_t)m * kFitRT + (size_t)kFitRT * m) * sizeof(double);
+        const size_t smem =
+            ((size_t)maxd * maxd + (size_t)maxd * kFitRT + (size_t)kFitRT * maxd) * sizeof(double);
         AFAM_CUDA(cudaFuncSetAttribute(contract_rotate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
         for (int stage = 0; stage < 6; stage++) {
             dim3 grid((Rmax[stage] + kFitRT - 1) / kFitRT, njobs);
-            contract_rotate_kernel<<<grid, kFitThreads, smem, st>>>(d_jobs, m, stage);
+            contract_rotate_kernel<<<grid, kFitThreads, smem, st>>>(d_jobs, D, stage);
         }
     }
     AFAM_CUDA(cudaGetLastError());
-    // rmse = sqrt(sse / m^3) (encoder.error_rmse: sqrt(mean(diff^2)))
+    // rmse = sqrt(sse / (d0 d1 d2)) (encoder.error_rmse: sqrt(mean(diff^2)))
     std::vector<double> h(njobs);
     AFAM_CUDA(cudaMemcpyAsync(h.data(), sse, sizeof(double) * njobs, cudaMemcpyDeviceToHost, st));
     AFAM_CUDA(cudaStreamSynchronize(st));
@@ -437,4 +451,11 @@ extern "C" int afam_fit_rmse(afam_store *s, const float *samples, int32_t nblk, 
     AFAM_CUDA(cudaFreeAsync(sse, st));
     AFAM_CUDA(cudaFreeAsync(work, st));
     return AFAM_OK;
+}
+
+extern "C" int afam_fit_rmse(afam_store *s, const float *samples, int32_t nblk, int32_t m, int32_t degree,
+                             const int32_t *job_block, const int32_t *job_ncp, int32_t njobs, double *rmse,
+                             float *ctrl, const int64_t *ctrl_off, void *stream) {
+    const int32_t dims[3] = {m, m, m};
+    return afam_fit_rmse3(s, samples, nblk, dims, degree, job_block, job_ncp, njobs, rmse, ctrl, ctrl_off, stream);
 }

@@ -82,28 +82,36 @@ def _op_store(device: int):
 
 
 def fit_rmse_batch(samples, degree: int, jobs, want_ctrl: bool = False, device: int = 0):
-    """Run (block index, ncp) jobs over a list of cubic float32 sample grids
-    (all m^3).  Returns rmse (njobs,) and, with want_ctrl, the list of float32
-    (ncp, ncp, ncp) coefficient grids (C order, [a, b, c] = x, y, z)."""
+    """Run (block index, ncp) jobs over a list of float32 sample grids of one
+    shape (d0, d1, d2) (bspline.fit_tensor_product fits any 3-D grid; cubic
+    in the configs).  Returns rmse (njobs,) and, with want_ctrl, the list of
+    float32 (ncp, ncp, ncp) coefficient grids (C order, [a, b, c] = x, y, z)."""
     import torch
 
     _lib.require_device()
     dev = torch.device("cuda", device)
-    if isinstance(samples, torch.Tensor):  # already resident: (nblk, m, m, m) float32 on `device`
+    if isinstance(samples, torch.Tensor):  # already resident: (nblk, d0, d1, d2) float32 on `device`
         d_samples = samples.contiguous()
-        nblk, m = int(d_samples.shape[0]), int(d_samples.shape[1])
+        nblk, dims = int(d_samples.shape[0]), tuple(int(v) for v in d_samples.shape[1:])
     else:
         blocks = [np.ascontiguousarray(s, dtype=np.float32) for s in samples]
         if not blocks:
             return np.zeros(0), ([] if want_ctrl else None)
-        m = blocks[0].shape[0]
-        if any(b.shape != (m, m, m) for b in blocks):
-            raise ValueError("fit_rmse_batch needs cubic sample grids of one edge length")
+        dims = tuple(blocks[0].shape)
+        if len(dims) != 3:
+            raise ValueError("expected a 3D sample grid")
+        if any(b.shape != dims for b in blocks):
+            raise ValueError("fit_rmse_batch needs sample grids of one shape")
         nblk = len(blocks)
         d_samples = torch.from_numpy(np.stack(blocks)).to(dev)
     jobs = [(int(b), int(n)) for b, n in jobs]
+    for _, n in jobs:  # bspline.fit_tensor_product's check, axis by axis
+        for axis, d in enumerate(dims):
+            if not degree + 1 <= n <= d:
+                raise ValueError(f"ncp must be in [{degree + 1}, {d}] for axis {axis}, got {n}")
+    c_dims = (C.c_int32 * 3)(*dims)
     store = _op_store(device)
-    per = max(1, min(65535, WORK_BYTES // (16 * m ** 3)))
+    per = max(1, min(65535, WORK_BYTES // (16 * int(np.prod(dims)))))
     rmse = np.zeros(len(jobs))
     ctrls = [] if want_ctrl else None
     with torch.cuda.device(dev):
@@ -118,8 +126,8 @@ def fit_rmse_batch(samples, degree: int, jobs, want_ctrl: bool = False, device: 
                 sizes = jn.astype(np.int64) ** 3
                 offs = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
                 d_ctrl = torch.empty(int(sizes.sum()), dtype=torch.float32, device=dev)
-            _lib.check(_lib.lib().afam_fit_rmse(
-                store.handle, C.c_void_p(d_samples.data_ptr()), nblk, m, int(degree),
+            _lib.check(_lib.lib().afam_fit_rmse3(
+                store.handle, C.c_void_p(d_samples.data_ptr()), nblk, c_dims, int(degree),
                 jb.ctypes.data_as(C.c_void_p), jn.ctypes.data_as(C.c_void_p), len(chunk),
                 out.ctypes.data_as(C.c_void_p), None if d_ctrl is None else C.c_void_p(d_ctrl.data_ptr()),
                 None if offs is None else offs.ctypes.data_as(C.c_void_p), C.c_void_p(stream.cuda_stream)))
@@ -141,10 +149,10 @@ def _make_model(ctrl, degree, extent, lod) -> model.MicroModel:
 
 def search_blocks(samples, error_bound: float, degree: int, extents=None, lods=None,
                   assume_monotone: bool = False, device: int = 0) -> list:
-    """in_level_search for many blocks of one edge length at once (one GPU
-    batch per sweep / bisection round).  `samples`: a list of cubic host
-    arrays or a resident (nblocks, m, m, m) float32 CUDA tensor.  Returns
-    [SearchResult]."""
+    """in_level_search for many blocks of one shape at once (one GPU batch per
+    sweep / bisection round).  `samples`: a list of host arrays or a
+    resident (nblocks, d0, d1, d2) float32 CUDA tensor; NCPs run up to the
+    edge d0 as the reference's (encoder.py:104).  Returns [SearchResult]."""
     import torch
 
     if error_bound <= 0:
@@ -162,13 +170,14 @@ def search_blocks(samples, error_bound: float, degree: int, extents=None, lods=N
     lods = lods if lods is not None else [1] * nb
     profiles = [ErrorProfile() for _ in range(nb)]
     _lib.require_device()
-    if on_device:  # (nb, n, n, n) float32, already resident
-        if tuple(blocks.shape[1:]) != (n, n, n) or blocks.dtype != torch.float32:
-            raise ValueError("search_blocks needs a (nblocks, m, m, m) float32 tensor")
+    shape = tuple(int(v) for v in blocks[0].shape)
+    if on_device:  # (nb, d0, d1, d2) float32, already resident
+        if blocks.dim() != 4 or blocks.dtype != torch.float32:
+            raise ValueError("search_blocks needs a (nblocks, d0, d1, d2) float32 tensor")
         blocks = blocks.contiguous()
     else:
-        if any(np.shape(b) != (n, n, n) for b in blocks):
-            raise ValueError("search_blocks needs cubic sample grids of one edge length")
+        if any(np.shape(b) != shape for b in blocks):
+            raise ValueError("search_blocks needs sample grids of one shape")
         blocks = torch.from_numpy(np.stack([np.asarray(b, dtype=np.float32) for b in blocks])).to(
             torch.device("cuda", device))  # uploaded once for every probe round
     if assume_monotone:
