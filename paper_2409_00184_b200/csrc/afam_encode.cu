@@ -45,6 +45,13 @@ struct FitDims {
     int32_t d[3];
 };
 
+// element `ax` of a 3-array without a dynamic index (which would copy the
+// job / the kernel parameter to local memory)
+template <typename T>
+__device__ __forceinline__ T sel3(const T (&v)[3], int ax) {
+    return ax == 0 ? v[0] : (ax == 1 ? v[1] : v[2]);
+}
+
 // Stage s contracts axis s % 3 (fit: d_t -> ncp, decode: ncp -> d_t); R is
 // the product of the two other current extents.
 __device__ __forceinline__ int fit_R(int stage, const FitDims &D, int ncp) {
@@ -69,13 +76,13 @@ __global__ void __launch_bounds__(kFitThreads) contract_rotate_kernel(const FitJ
     const FitJob J = jobs[blockIdx.y];
     const int ncp = J.ncp;
     const bool dec = stage >= 3;
-    const int ax = stage % 3, dt = D.d[ax];
+    const int ax = stage % 3, dt = sel3(D.d, ax);
     const int n0 = dec ? ncp : dt, nout = dec ? dt : ncp;
     const int R = fit_R(stage, D, ncp);
     const int r0 = blockIdx.x * kFitRT;
     if (r0 >= R) return;
     const int rt = min(kFitRT, R - r0);
-    const double *op = dec ? J.op_dec[ax] : J.op_fit[ax];
+    const double *op = dec ? sel3(J.op_dec, ax) : sel3(J.op_fit, ax);
     double *sOp = reinterpret_cast<double *>(smem);          // [nout][n0]
     double *sIn = sOp + (size_t)nout * n0;                   // [n0][kFitRT]
     double *sOut = sIn + (size_t)n0 * kFitRT;                // [kFitRT][nout]
@@ -162,7 +169,7 @@ __global__ void __launch_bounds__(kFitThreads, 2) contract_tiled_kernel(const Fi
     const FitJob J = jobs[blockIdx.y];
     const int ncp = J.ncp;
     const bool dec = stage >= 3;
-    const int ax = stage % 3, dt = D.d[ax];
+    const int ax = stage % 3, dt = sel3(D.d, ax);
     const int n0 = dec ? ncp : dt, nout = dec ? dt : ncp;
     const int R = fit_R(stage, D, ncp);
     const int r0 = blockIdx.x * kFitRT2;
@@ -173,7 +180,7 @@ __global__ void __launch_bounds__(kFitThreads, 2) contract_tiled_kernel(const Fi
     double *sIn = sOpT + (size_t)n0 * np;                // [n0][kFitRT2]
     double *sOut = sIn + (size_t)n0 * kFitRT2;           // [kFitRT2][nout]
     {  // transposed, padded operator [n0][np]: a straight 16-byte copy
-        const double2 *src = reinterpret_cast<const double2 *>(dec ? J.opT_dec[ax] : J.opT_fit[ax]);
+        const double2 *src = reinterpret_cast<const double2 *>(dec ? sel3(J.opT_dec, ax) : sel3(J.opT_fit, ax));
         double2 *dst = reinterpret_cast<double2 *>(sOpT);
         for (int e = threadIdx.x; e < n0 * np / 2; e += blockDim.x) dst[e] = src[e];
     }
