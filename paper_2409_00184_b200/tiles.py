@@ -117,12 +117,15 @@ class PeerFrame:
         self.nbytes = self.height * self.width * 4
         self._own = self.rank == self.dst
         ptr = C.c_void_p()
-        handle = None
+        handle, err = None, None
         if self._own:
-            _lib.check(_lib.lib().afam_device_alloc(self.device, self.nbytes, C.byref(ptr)))
-            hb = (C.c_uint8 * 64)()
-            _lib.check(_lib.lib().afam_ipc_get_handle(ptr, hb))
-            handle = bytes(hb)
+            try:  # a failure still takes part in the broadcast below, so no rank waits forever
+                _lib.check(_lib.lib().afam_device_alloc(self.device, self.nbytes, C.byref(ptr)))
+                hb = (C.c_uint8 * 64)()
+                _lib.check(_lib.lib().afam_ipc_get_handle(ptr, hb))
+                handle = bytes(hb)
+            except Exception as exc:  # noqa: BLE001
+                err = exc
         if dist.is_initialized() and dist.get_world_size(group) > 1:
             obj = [handle]
             dist.broadcast_object_list(obj, src=dist.get_global_rank(group, self.dst) if group else self.dst,
@@ -130,8 +133,14 @@ class PeerFrame:
                                        if dist.get_backend(group) == "nccl" else None)
             handle = obj[0]
             if not self._own:
+                if handle is None:
+                    raise RuntimeError(f"rank {self.dst} could not export its frame buffer")
                 hb = (C.c_uint8 * 64).from_buffer_copy(handle)
                 _lib.check(_lib.lib().afam_ipc_open(hb, self.device, C.byref(ptr)))
+        if err is not None:
+            if ptr.value:
+                _lib.lib().afam_device_free(ptr)
+            raise err
         self.ptr = int(ptr.value)
 
     def frame(self):
