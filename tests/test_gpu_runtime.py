@@ -75,7 +75,10 @@ def test_linear_prefetch_reduces_misses_on_dolly(disk_store):
 
     root, man = disk_store
     tf = render.TransferFunction.ml_preset()
-    params = render.RenderParams(width=24, height=24, sample_distance=0.02)
+    # the prefetch loads only while the frame is on the GPU (the reference's
+    # rendering_done check, runtime.py:186): frames big enough that a few
+    # 9^3 block uploads fit in one
+    params = render.RenderParams(width=256, height=256, sample_distance=0.002)
     povs = [render.PointOfView([0.3, 0.2, 3.2 - 0.05 * i], [0, 0, -1], [0, 1, 0]) for i in range(40)]
     off, _ = _cache(root, man, 500)
     runtime.replay(povs, man, off, tf, params, prefetch="off", keep_frames=False)
