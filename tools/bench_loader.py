@@ -42,6 +42,21 @@ for kind in ("memory", "files"):
         samples[0] += tiles.render_tiles.last_stats["samples"]
         return fr
 
+    class Counted:  # split at the GPU wait, as bench.py's e2e draw (prefetch while the GPU marches)
+        def __init__(self, pending):
+            self.pending = pending
+
+        def done(self):
+            return self.pending.done()
+
+        def result(self):
+            fr = self.pending.result()
+            samples[0] += tiles.render_tiles.last_stats["samples"]
+            return fr
+
+    draw.submit = lambda pov, resident, tf_, params_: Counted(
+        tiles.submit_tiles(pov, resident, tf_, params_, band_rows=8))
+
     runtime.replay(povs[:3], sub, cache, tf, params, prefetch="linear", keep_frames=False, render_fn=draw)
     samples[0] = 0
     c0 = cache.counters()
