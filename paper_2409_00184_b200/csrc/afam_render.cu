@@ -1245,6 +1245,16 @@ static int render_minb() {
     return v;
 }
 
+// A/B override of the p = 2 fast path's CTAs per SM (AFAM_RENDER_MINB2=3|4|5)
+static int render_minb2() {
+    static int v = [] {
+        const char *e = getenv("AFAM_RENDER_MINB2");
+        const int m = e ? atoi(e) : 0;
+        return (m == 3 || m == 5) ? m : 4;
+    }();
+    return v;
+}
+
 struct LaunchArgs {
     dim3 grid;
     size_t smem;
@@ -1278,7 +1288,11 @@ template <bool DEBUG, bool SMEM>
 static void launch_render(const LaunchArgs &L, const RenderArgs &A, int fd) {
     if (fd == 0) return launch_render_v<DEBUG, SMEM, 0, 4>(L, A);  // DS blocks
     if (fd == 1) return launch_render_v<DEBUG, SMEM, 1, 4>(L, A);
-    if (fd == 2) return launch_render_v<DEBUG, SMEM, 2, 4>(L, A);
+    if (fd == 2) {
+        if (!DEBUG && SMEM && render_minb2() == 3) return launch_render_v<DEBUG, SMEM, 2, 3>(L, A);
+        if (!DEBUG && SMEM && render_minb2() == 5) return launch_render_v<DEBUG, SMEM, 2, 5>(L, A);
+        return launch_render_v<DEBUG, SMEM, 2, 4>(L, A);
+    }
     if (DEBUG || !SMEM) return launch_render_v<DEBUG, SMEM, 3, 3>(L, A);
     switch (render_minb()) {
         case 2: launch_render_v<DEBUG, SMEM, 3, 2>(L, A); break;
