@@ -130,8 +130,8 @@ __device__ __forceinline__ void decode_planes(const BlockDesc &d, const int32_t 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
     const int tid = threadIdx.x, nth = blockDim.x;
     const size_t zstride = (size_t)n * pitch;
-    // item -> row by float reciprocal: exact for item < 2^20 (error << 0.5/nq)
-    const float inv_nq = 1.f / (float)nq;
+    // z / y items: thread = (row group g_, x quad q_); groups * nq <= nth threads work
+    const int groups = nth / nq, q_ = tid % nq, g_ = tid / nq, gstride = groups * pitch;
     const int ngroups = min(m / 32, kMainGroups), mainw = 32 * ngroups, tailw = m - mainw;
     const float inv_tail = tailw > 0 ? 1.f / (float)tailw : 0.f;
     T bx[kMainGroups][Q];
@@ -188,29 +188,28 @@ __device__ __forceinline__ void decode_planes(const BlockDesc &d, const int32_t 
             mbar_wait(bar + (zr % kRing), (uint32_t)((zr / kRing) & 1));
             planes[c] = ring + (size_t)(zr % kRing) * zstride;
         }
-        // z contraction, 4 consecutive x per item: S1[b][a..a+3] = sum_c Bz[k,c] C[a.., b, z0+c]
-        for (int item = tid; item < n * nq; item += nth) {
-            const int b = (int)(((float)item + 0.5f) * inv_nq), q = item - b * nq;
-            T acc[4] = {T(0), T(0), T(0), T(0)};
+        // z contraction, 4 consecutive x per item: S1[b][a..a+3] = sum_c Bz[k,c] C[a.., b, z0+c];
+        // thread (group g, quad q) takes rows b = g, g + groups, ... (no per-item division)
+        if (g_ < groups)
+            for (int off = g_ * pitch + 4 * q_; off < n * pitch; off += gstride) {
+                T acc[4] = {T(0), T(0), T(0), T(0)};
 #pragma unroll
-            for (int c = 0; c < Q; c++) {
-                fma4(bz[c], *reinterpret_cast<const float4 *>(planes[c] + (size_t)b * pitch + 4 * q), acc);
+                for (int c = 0; c < Q; c++) fma4(bz[c], *reinterpret_cast<const float4 *>(planes[c] + off), acc);
+                st4(S1 + off, acc);
             }
-            st4(S1 + (size_t)b * pitch + 4 * q, acc);
-        }
         __syncthreads();
         // the ring planes below the next window are free now: fetch the next
         // window while the y and x stages run (kRing = P+1 slots suffice)
         if (threadIdx.x == 0 && k + 1 < k1) issue_upto(min(zlast, c0[k + 1] + P));
         // y contraction: S2[j][a..a+3] = sum_b By[j,b] S1[y0_j+b][a..a+3]
-        for (int item = tid; item < m * nq; item += nth) {
-            const int j = (int)(((float)item + 0.5f) * inv_nq), q = item - j * nq;
-            const T *s1 = S1 + (size_t)c0[j] * pitch + 4 * q;
-            T acc[4] = {T(0), T(0), T(0), T(0)};
+        if (g_ < groups)
+            for (int j = g_; j < m; j += groups) {
+                const T *s1 = S1 + c0[j] * pitch + 4 * q_;
+                T acc[4] = {T(0), T(0), T(0), T(0)};
 #pragma unroll
-            for (int bb = 0; bb < Q; bb++) fma4(B[j * 4 + bb], s1 + (size_t)bb * pitch, acc);
-            st4(S2 + (size_t)j * pitch + 4 * q, acc);
-        }
+                for (int bb = 0; bb < Q; bb++) fma4(B[j * 4 + bb], s1 + bb * pitch, acc);
+                st4(S2 + j * pitch + 4 * q_, acc);
+            }
         __syncthreads();
         // x contraction + coalesced store out[i + m*j + m*m*k]: full-warp columns
         // i = lane + 32t with their Bx rows in registers, then the m % 32 tail
