@@ -190,3 +190,41 @@ def test_trajectory_io(tmp_path):
     (tmp_path / "bad.jsonl").write_text('{"pos": [0, 0, 1]}\n')
     with pytest.raises(FormatError):
         load_trajectory(tmp_path / "bad.jsonl")
+
+
+def test_replay_with_submit_prefetches_while_frame_in_flight(manifest):
+    """replay with a render function that splits at its GPU wait
+    (`render_fn.submit` -> handle with done()/result()): the prefetch runs on
+    the frame thread and loads only while done() is False (the reference's
+    rendering_done check, runtime.py:186); frames, timings and the hit/miss
+    accounting are the thread path's."""
+    from paper_2409_00184_b200.render import PointOfView
+    from paper_2409_00184_b200.runtime import ModelCache, replay
+
+    povs = [PointOfView([0.3, 0.2, 3.2 - 0.15 * i], [0, 0, -1], [0, 1, 0]) for i in range(20)]
+
+    class Pending:
+        def __init__(self, budget):
+            self.polls, self.budget = 0, budget
+
+        def done(self):  # "the GPU" finishes after `budget` polls
+            self.polls += 1
+            return self.polls > self.budget
+
+        def result(self):
+            return ("frame", self.polls)
+
+    def draw(pov, resident, tf, params):
+        raise AssertionError("replay must use submit")
+
+    for budget, expect_loads in ((0, False), (10 ** 6, True)):
+        draw.submit = lambda pov, resident, tf, params, b=budget: Pending(b)
+        cache = ModelCache(500, load_blob)
+        params = type("P", (), {"aspect": 1.0})()
+        timings, frames, agg = replay(povs, manifest, cache, None, params, prefetch="linear", render_fn=draw)
+        assert len(frames) == len(povs) and all(f[0] == "frame" for f in frames)
+        assert agg["frames"] == len(povs)
+        loaded = sum(t.prefetch_models_loaded for t in timings)
+        assert (loaded > 0) == expect_loads
+        for t in timings:
+            assert t.input_latency_ms == pytest.approx(t.caching_ms + t.rendering_ms, abs=1e-6)
