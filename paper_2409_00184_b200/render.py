@@ -471,13 +471,20 @@ def _addr_key(a):
     return (a.lod, a.ijk)
 
 
+_inflight: dict = {}  # thread ident -> its uncollected PendingPart (one per thread)
+
+
 class PendingPart:
     """A launched render_part: `done()` polls the GPU (no host wait),
-    `result()` waits and returns render_part's (rgba, info, debug)."""
+    `result()` waits and returns render_part's (rgba, info, debug).  A thread
+    has at most one uncollected frame: the staging buffer, stats buffer and
+    completion event are per thread."""
 
     def __init__(self, **kw):
         self.__dict__.update(kw)
         self._res = None
+        self._owner = threading.get_ident()
+        _inflight[self._owner] = self
 
     def done(self) -> bool:
         return self._res is not None or self.event.query()
@@ -486,6 +493,11 @@ class PendingPart:
         if self._res is not None:
             return self._res
         import torch
+
+        if getattr(self, "_superseded", False):
+            raise RuntimeError("this frame's buffers were reused by a later submit on the same thread")
+        if _inflight.get(self._owner) is self:
+            del _inflight[self._owner]
 
         with torch.cuda.device(self.dev):
             self.s_obj.synchronize()
@@ -519,6 +531,10 @@ def submit_part(pov, blocks: dict, tf, params, *, band_rows: int | None = None, 
 
     from .device import as_device_blocks, stream_handle
 
+    prev = _inflight.pop(threading.get_ident(), None)
+    if prev is not None:  # an uncollected frame of this thread: let it finish, then its buffers are reused
+        prev.s_obj.synchronize()
+        prev._superseded = True
     try:  # (lod, i, j, k) order as BlockAddress.__lt__, without a Python compare per pair
         addrs = sorted(blocks, key=_addr_key)
     except AttributeError:
