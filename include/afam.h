@@ -175,8 +175,10 @@ int afam_fit_rmse(afam_store *s, const float *samples, int32_t nblk, int32_t m, 
 
 /* afam_fit_rmse on non-cubic sample grids: samples are nblk blocks of
  * dims[0] x dims[1] x dims[2] ([i][j][k] C order; bspline.fit_tensor_product
- * fits any 3-D grid, one ncp on every axis, degree + 1 <= ncp <= min(dims)),
- * decoded back on the same lattice.  afam_fit_rmse(m) is dims = (m, m, m). */
+ * fits any 3-D grid, one ncp on every axis, degree + 1 <= ncp <= min(dims),
+ * bspline.py:128-147; encoder.in_level_search sweeps NCPs up to dims[0],
+ * encoder.py:104), decoded back on the same lattice (bspline.py:162-172).
+ * afam_fit_rmse(m) is dims = (m, m, m). */
 int afam_fit_rmse3(afam_store *s, const float *samples, int32_t nblk, const int32_t *dims, int32_t degree,
                    const int32_t *job_block, const int32_t *job_ncp, int32_t njobs, double *rmse, float *ctrl,
                    const int64_t *ctrl_off, void *stream);
