@@ -23,6 +23,56 @@ __device__ __forceinline__ T eval_dispatch(const BlockDesc &d, const double (&u)
     }
 }
 
+// DS baseline blocks (AFAM_SLOT_DS, reference downsample.py:101-138):
+// trilinear interpolation at continuous lattice indices x (_trilinear:
+// base = clip(floor(x), 0, max(top - 1, 0)), neighbours min(base + 1, top)),
+// in float64 from the float32 grid g of dims (nx, ny, nz), x fastest.
+__device__ __forceinline__ double ds_trilinear(const float *__restrict__ g, const int (&dims)[3],
+                                               const double (&x)[3]) {
+    int b0[3], b1[3];
+    double f[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        const int top = dims[a] - 1;
+        const int b = min(max((int)floor(x[a]), 0), max(top - 1, 0));
+        b0[a] = b;
+        b1[a] = min(b + 1, top);
+        f[a] = x[a] - (double)b;
+    }
+    auto at = [&](int i, int j, int k) { return (double)__ldg(g + ((size_t)k * dims[1] + j) * dims[0] + i); };
+    // the reference's order: x, then y, then z, each as a (1 - f) + b f
+    const double c00 = at(b0[0], b0[1], b0[2]) * (1.0 - f[0]) + at(b1[0], b0[1], b0[2]) * f[0];
+    const double c10 = at(b0[0], b1[1], b0[2]) * (1.0 - f[0]) + at(b1[0], b1[1], b0[2]) * f[0];
+    const double c01 = at(b0[0], b0[1], b1[2]) * (1.0 - f[0]) + at(b1[0], b0[1], b1[2]) * f[0];
+    const double c11 = at(b0[0], b1[1], b1[2]) * (1.0 - f[0]) + at(b1[0], b1[1], b1[2]) * f[0];
+    const double c0 = c00 * (1.0 - f[1]) + c10 * f[1];
+    const double c1 = c01 * (1.0 - f[1]) + c11 * f[1];
+    return c0 * (1.0 - f[2]) + c1 * f[2];
+}
+
+template <bool GRAD, typename OT>
+__device__ __forceinline__ void eval_ds(const BlockDesc &d, const double *__restrict__ pts, int64_t i, OT *val,
+                                        OT *grad) {
+    const int g = d.deg;  // ghost width
+    const int n[3] = {d.ds_n[0], d.ds_n[1], d.ds_n[2]};
+    const int nr[3] = {n[0] + 2 * g, n[1] + 2 * g, n[2] + 2 * g};
+    double x[3], xg[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) {  // _continuous_index: clip((p - lo) / span, 0, 1) * (n - 1)
+        const double p = __ldg(pts + 3 * i + a);
+        x[a] = clamp01(__ddiv_rn(__dsub_rn(p, d.lo[a]), d.span[a])) * (double)(n[a] - 1);
+        xg[a] = x[a] + (double)g;
+    }
+    val[i] = (OT)ds_trilinear(d.ctrl, nr, xg);
+    if (GRAD) {
+        const size_t plane = (size_t)n[0] * n[1] * n[2];
+        const float *grids = reinterpret_cast<const float *>(d.ctrl4);
+#pragma unroll
+        for (int a = 0; a < 3; a++)  // central-difference grids x (n - 1) / span (downsample.py:118-128)
+            grad[3 * i + a] = (OT)(ds_trilinear(grids + a * plane, n, x) * ((double)(n[a] - 1) / d.span[a]));
+    }
+}
+
 template <bool GRAD, typename OT>
 __global__ void __launch_bounds__(256) eval_points_kernel(const BlockDesc *__restrict__ descs,
                                                           const int32_t *__restrict__ slots, int32_t slot,
@@ -33,6 +83,10 @@ __global__ void __launch_bounds__(256) eval_points_kernel(const BlockDesc *__res
     if (i >= n) return;
     const int32_t sl = slots ? __ldg(slots + i) : slot;
     const BlockDesc d = load_desc(descs + sl);
+    if (d.flags & AFAM_SLOT_DS) {  // world points only (DS blocks have no parameter space)
+        eval_ds<GRAD, OT>(d, pts, i, val, grad);
+        return;
+    }
     const bool param = flags & AFAM_EVAL_PARAM;
     double u[3];
 #pragma unroll
@@ -87,7 +141,8 @@ extern "C" int afam_eval_points(afam_store *s, const int32_t *slots, int32_t slo
         std::lock_guard<std::mutex> lk(s->mu);
         if (!slots) {
             AFAM_CHECK(slot >= 0 && slot < s->nslots && s->host[slot].valid, AFAM_E_VALUE, "slot %d is empty", slot);
-            AFAM_CHECK(!s->host[slot].ds, AFAM_E_VALUE, "slot %d holds a DS block (no spline to evaluate)", slot);
+            AFAM_CHECK(!s->host[slot].ds || !(flags & AFAM_EVAL_PARAM), AFAM_E_VALUE,
+                       "slot %d holds a DS block: parameter-space evaluation needs a spline", slot);
             AFAM_CUDA(cudaStreamWaitEvent(st, s->host[slot].ready, 0));
         } else {
             // the caller passes resident slots only; order after every upload still in flight

@@ -114,3 +114,29 @@ def test_ds_device_loader_replay(tmp_path):
         vis = render.select_visible(pov, man, params.aspect)
         want = render.render(pov, {a: blocks[a] for a in vis}, tf, params)
         np.testing.assert_array_equal(fr.rgba, want.rgba)
+
+
+@pytest.mark.gpu
+def test_ds_point_queries_vs_reference():
+    """DsBlock.values_at / gradients_at on the GPU (K1's DS branch) against
+    the reference's trilinear queries (tests/golden/gen_ds_points_golden.py),
+    ghost 0 and 1, points inside and around each block (clipped)."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from helpers import npz
+
+    from paper_2409_00184_b200 import downsample
+
+    z = npz("ds_points.npz")
+    for k in range(int(z["nblocks"])):
+        b = downsample.DsBlock(z[f"b{k}_samples"], int(z[f"b{k}_ghost"]), z[f"b{k}_extent"], int(z[f"b{k}_lod"]))
+        pts = z[f"b{k}_points"]
+        v = b.values_at(pts)
+        g = b.gradients_at(pts)
+        want_v, want_g = z[f"b{k}_values"], z[f"b{k}_grads"]
+        rng = max(1.0, float(np.abs(want_v).max()))
+        assert np.abs(v - want_v).max() <= 1e-12 * rng, k
+        # the central-difference grids are built once at upload and held in
+        # float32 (as the DS render reads them): ~1e-8 relative vs float64
+        assert np.abs(g - want_g).max() <= 1e-6 * max(1.0, float(np.abs(want_g).max())), k
