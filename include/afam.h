@@ -128,7 +128,9 @@ int afam_store_read(afam_store *s, int32_t slot, float *ctrl, float *knots);
  * (u = clip((p-lo)/(hi-lo), 0, 1), gradient divided by the extent span);
  * with AFAM_EVAL_PARAM the points are parameters (bspline.evaluate_points).
  * val (n) / grad (n x 3) are device buffers of float32 (or float64 with
- * AFAM_EVAL_OUT_F64); grad may be NULL.
+ * AFAM_EVAL_OUT_F64); grad may be NULL.  AFAM_SLOT_DS slots answer world
+ * points with the DS baseline's trilinear queries (DsBlock.values_at /
+ * gradients_at, downsample.py:101-138); they have no parameter space.
  */
 int afam_eval_points(afam_store *s, const int32_t *slots, int32_t slot, const double *pts, int64_t n,
                      void *val, void *grad, uint32_t flags, void *stream);
