@@ -732,5 +732,9 @@ extern "C" int afam_decode_grid_ex(afam_store *s, const int32_t *slots, int32_t 
     }
     AFAM_CUDA(cudaGetLastError());
     AFAM_CUDA(cudaFreeAsync(d_jobs, st));
+    ThreadCtx *tc = thread_ctx(s->device);
+    AFAM_CHECK(tc, AFAM_E_CUDA, "per-thread state unavailable");
+    AFAM_CUDA(cudaEventRecord(tc->read, st));
+    mark_readers(s, slots, nblk, tc->read);  // later uploads into these slots wait for the decode
     return AFAM_OK;
 }

@@ -59,7 +59,22 @@ struct SlotHost {
     bool ds = false;       // down-sampled raw block (AFAM_SLOT_DS)
     double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     cudaEvent_t ready = nullptr;  // recorded after the upload kernels
+    cudaEvent_t reader = nullptr; // the last kernel reading the slot (a ThreadCtx event): uploads wait on it
 };
+
+// Per (calling thread, device) state of the frame path: the timing bracket
+// of this thread's last afam_render, its pinned argument staging, and the
+// event its point-query / decode launches record.  Two threads rendering
+// from one store never share these (no lock, no overwritten kernel time).
+// Never destroyed: slots may still name `k1` / `read` as their reader.
+struct ThreadCtx {
+    cudaEvent_t k0 = nullptr, k1 = nullptr;  // bracket the last afam_render's kernels (timing)
+    unsigned char *pack = nullptr;           // pinned staging of afam_render's per-frame upload
+    size_t pack_cap = 0;
+    cudaEvent_t ev_pack = nullptr;           // the last upload out of `pack`
+    cudaEvent_t read = nullptr;              // recorded after afam_eval_points / afam_decode_grid launches
+};
+ThreadCtx *thread_ctx(int device);  // afam_store.cu
 
 struct DecodeOp {  // banded collocation matrix of bspline.py:98-125 for (ncp, deg, m)
     float *b32 = nullptr;   // [m][4]
@@ -95,11 +110,6 @@ struct afam_store {
     afam::BlockDesc *d_desc = nullptr;   // nslots descriptors (device)
     float *d_maxabs = nullptr;           // nslots (device)
     std::vector<afam::SlotHost> host;
-    cudaEvent_t ev_k0 = nullptr, ev_k1 = nullptr;  // bracket the last afam_render's kernels
-    unsigned char *h_pack = nullptr;                // pinned staging of afam_render's per-frame upload
-    size_t h_pack_cap = 0;
-    cudaEvent_t ev_pack = nullptr;                  // the last upload out of h_pack
-    std::mutex pack_mu;                             // h_pack is shared by concurrent afam_render calls
     // afam_store_put_file: ring of pinned staging buffers (file -> pinned -> H2D)
     static constexpr int kFileRing = 4;
     unsigned char *h_file[kFileRing] = {nullptr, nullptr, nullptr, nullptr};
@@ -146,6 +156,21 @@ inline cudaError_t wait_slot(afam_store *s, int32_t slot, cudaStream_t st) {
         return cudaSuccess;
     }
     return cudaStreamWaitEvent(st, h.ready, 0);
+}
+
+// Order an upload into `slot` on `st` after the kernels still reading the
+// slot's previous contents (caller holds s->mu).
+inline cudaError_t wait_readers(afam_store *s, int32_t slot, cudaStream_t st) {
+    cudaEvent_t r = s->host[slot].reader;
+    return r ? cudaStreamWaitEvent(st, r, 0) : cudaSuccess;
+}
+
+// Name `ev` (recorded after the launches that read these slots) as their
+// last reader.
+inline void mark_readers(afam_store *s, const int32_t *slots, int32_t n, cudaEvent_t ev) {
+    std::lock_guard<std::mutex> lk(s->mu);
+    for (int32_t b = 0; b < n; b++)
+        if (slots[b] >= 0 && slots[b] < s->nslots) s->host[slots[b]].reader = ev;
 }
 }  // namespace afam
 

@@ -157,5 +157,17 @@ extern "C" int afam_eval_points(afam_store *s, const int32_t *slots, int32_t slo
     if (flags & AFAM_EVAL_OUT_F64) launch<double>(s->d_desc, slots, slot, pts, n, val, grad, flags, st);
     else launch<float>(s->d_desc, slots, slot, pts, n, val, grad, flags, st);
     AFAM_CUDA(cudaGetLastError());
+    // later uploads into the slots read here wait for this launch (the
+    // per-point slot ids are device data: every valid slot is marked)
+    ThreadCtx *tc = thread_ctx(s->device);
+    AFAM_CHECK(tc, AFAM_E_CUDA, "per-thread state unavailable");
+    AFAM_CUDA(cudaEventRecord(tc->read, st));
+    if (!slots) {
+        mark_readers(s, &slot, 1, tc->read);
+    } else {
+        std::lock_guard<std::mutex> lk(s->mu);
+        for (int32_t k = 0; k < s->nslots; k++)
+            if (s->host[k].valid) s->host[k].reader = tc->read;
+    }
     return AFAM_OK;
 }

@@ -1454,22 +1454,23 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
     const size_t off_tf = al(sizeof(RenderArgs)), off_grid = off_tf + al(sizeof(TfTable));
     const size_t off_idx = off_grid + al(gbytes);
     const size_t total = off_idx + std::max<size_t>(1, (size_t)nblocks) * sizeof(int32_t);
-    // staged in the store's pinned buffer, so the H2D copy is asynchronous
-    // (a pageable source would block until the stream drains); the previous
-    // frame's copy out of it is fenced by ev_pack
-    std::lock_guard<std::mutex> plk(s->pack_mu);
+    // staged in this thread's pinned buffer, so the H2D copy is asynchronous
+    // (a pageable source would block until the stream drains); the thread's
+    // previous frame's copy out of it is fenced by ev_pack
+    ThreadCtx *tc = thread_ctx(s->device);
+    AFAM_CHECK(tc, AFAM_E_CUDA, "per-thread render state unavailable");
     ht.mark();
-    if (s->h_pack_cap < total) {
-        AFAM_CUDA(cudaEventSynchronize(s->ev_pack));
-        if (s->h_pack) AFAM_CUDA(cudaFreeHost(s->h_pack));
-        s->h_pack = nullptr;
-        s->h_pack_cap = 0;
-        AFAM_CUDA(cudaHostAlloc((void **)&s->h_pack, total + (64 << 10), cudaHostAllocDefault));
-        s->h_pack_cap = total + (64 << 10);
+    if (tc->pack_cap < total) {
+        AFAM_CUDA(cudaEventSynchronize(tc->ev_pack));
+        if (tc->pack) AFAM_CUDA(cudaFreeHost(tc->pack));
+        tc->pack = nullptr;
+        tc->pack_cap = 0;
+        AFAM_CUDA(cudaHostAlloc((void **)&tc->pack, total + (64 << 10), cudaHostAllocDefault));
+        tc->pack_cap = total + (64 << 10);
     } else {
-        AFAM_CUDA(cudaEventSynchronize(s->ev_pack));
+        AFAM_CUDA(cudaEventSynchronize(tc->ev_pack));
     }
-    unsigned char *pack = s->h_pack;
+    unsigned char *pack = tc->pack;
     memset(pack, 0, total);
     memcpy(pack, &A, sizeof(A));
     memcpy(pack + off_tf, &tf, sizeof(tf));
@@ -1478,9 +1479,9 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
     unsigned char *d_pack = nullptr;
     AFAM_CUDA(cudaMallocAsync(&d_pack, total, st));
     AFAM_CUDA(cudaMemcpyAsync(d_pack, pack, total, cudaMemcpyHostToDevice, st));
-    AFAM_CUDA(cudaEventRecord(s->ev_pack, st));
+    AFAM_CUDA(cudaEventRecord(tc->ev_pack, st));
     ht.mark();
-    AFAM_CUDA(cudaEventRecord(s->ev_k0, st));
+    AFAM_CUDA(cudaEventRecord(tc->k0, st));
     init_stats_kernel<<<1, 1, 0, st>>>(stats);
     if (A.rows > 0) {
         LaunchArgs L;
@@ -1506,8 +1507,9 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
         }
     }
     finish_stats_kernel<<<1, 1, 0, st>>>(stats);
-    AFAM_CUDA(cudaEventRecord(s->ev_k1, st));
+    AFAM_CUDA(cudaEventRecord(tc->k1, st));
     AFAM_CUDA(cudaGetLastError());
+    mark_readers(s, slots, nblocks, tc->k1);  // uploads into these slots now wait for this frame
     AFAM_CUDA(cudaFreeAsync(d_pack, st));
     ht.mark();
     ht.report("afam_render: setdevice, args+tf, grid+waits, pack lock, pack+upload, launches");
@@ -1559,7 +1561,9 @@ extern "C" int afam_ipc_close(void *dev_ptr) {
 extern "C" int afam_render_elapsed(afam_store *s, float *ms) {
     AFAM_CHECK(s && ms, AFAM_E_VALUE, "NULL argument to afam_render_elapsed");
     AFAM_CUDA(cudaSetDevice(s->device));
-    AFAM_CUDA(cudaEventSynchronize(s->ev_k1));
-    AFAM_CUDA(cudaEventElapsedTime(ms, s->ev_k0, s->ev_k1));
+    ThreadCtx *tc = thread_ctx(s->device);
+    AFAM_CHECK(tc, AFAM_E_CUDA, "per-thread render state unavailable");
+    AFAM_CUDA(cudaEventSynchronize(tc->k1));
+    AFAM_CUDA(cudaEventElapsedTime(ms, tc->k0, tc->k1));
     return AFAM_OK;
 }

@@ -35,6 +35,23 @@ int cuda_fail(cudaError_t e, const char *what) {
     return AFAM_E_CUDA;
 }
 
+// One ThreadCtx per (thread, device), created on first use (the caller has
+// selected `device`) and kept for the life of the process.
+ThreadCtx *thread_ctx(int device) {
+    static thread_local std::map<int, ThreadCtx *> ctx;
+    auto it = ctx.find(device);
+    if (it != ctx.end()) return it->second;
+    ThreadCtx *c = new ThreadCtx();
+    if (cudaEventCreate(&c->k0) != cudaSuccess || cudaEventCreate(&c->k1) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_pack, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->read, cudaEventDisableTiming) != cudaSuccess) {
+        set_error("cannot create the per-thread render events");
+        return nullptr;
+    }
+    ctx[device] = c;
+    return c;
+}
+
 static __device__ __forceinline__ float load_le_f32(const uint8_t *p) {
     uint32_t v = (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
     return __uint_as_float(v);
@@ -190,9 +207,6 @@ int afam_store_create(afam_store **out, int device, int32_t slots, int32_t max_n
     AFAM_CUDA(cudaMalloc(&s->d_maxabs, sizeof(float) * slots));
     s->host.resize(slots);
     for (auto &h : s->host) AFAM_CUDA(cudaEventCreateWithFlags(&h.ready, cudaEventDisableTiming));
-    AFAM_CUDA(cudaEventCreate(&s->ev_k0));
-    AFAM_CUDA(cudaEventCreate(&s->ev_k1));
-    AFAM_CUDA(cudaEventCreateWithFlags(&s->ev_pack, cudaEventDisableTiming));
     {
         // the per-call argument buffers come from the device's stream-ordered
         // pool (cudaMallocAsync); keep its memory mapped across
@@ -212,14 +226,10 @@ int afam_store_destroy(afam_store *s) {
     cudaDeviceSynchronize();
     for (auto &h : s->host)
         if (h.ready) cudaEventDestroy(h.ready);
-    if (s->ev_k0) cudaEventDestroy(s->ev_k0);
-    if (s->ev_k1) cudaEventDestroy(s->ev_k1);
-    if (s->ev_pack) cudaEventDestroy(s->ev_pack);
     for (int b = 0; b < afam_store::kFileRing; b++) {
         if (s->h_file[b]) cudaFreeHost(s->h_file[b]);
         if (s->ev_file[b]) cudaEventDestroy(s->ev_file[b]);
     }
-    if (s->h_pack) cudaFreeHost(s->h_pack);
     for (auto &kv : s->ops) {
         cudaFree(kv.second.b32);
         cudaFree(kv.second.b64);
@@ -350,6 +360,7 @@ int afam_store_put_mfa(afam_store *s, int32_t slot, const uint8_t *bytes, uint64
     AFAM_CUDA(cudaSetDevice(s->device));
     // the previous upload into this slot (possibly on another stream) must be done
     AFAM_CUDA(cudaStreamWaitEvent(st, s->host[slot].ready, 0));
+    AFAM_CUDA(wait_readers(s, slot, st));
     AFAM_CUDA(cudaMemcpyAsync(s->raw_ptr(slot), bytes, nbytes, cudaMemcpyHostToDevice, st));
     return launch_unpack(s, slot, deg, ncp, 1, 0, 1 + 12ull * (ncp + deg), extent, st);
 }
@@ -414,6 +425,7 @@ int afam_store_put_file(afam_store *s, int32_t slot, const char *path, int32_t n
     cudaStream_t st = (cudaStream_t)stream;
     std::lock_guard<std::mutex> lk(s->mu);
     AFAM_CUDA(cudaStreamWaitEvent(st, s->host[slot].ready, 0));
+    AFAM_CUDA(wait_readers(s, slot, st));
     AFAM_CUDA(cudaMemcpyAsync(s->raw_ptr(slot), bytes, nbytes, cudaMemcpyHostToDevice, st));
     AFAM_CUDA(cudaEventRecord(s->ev_file[b], st));
     return launch_unpack(s, slot, deg, ncp, 1, 0, coff, extent, st);
@@ -445,6 +457,7 @@ int afam_store_put_ds(afam_store *s, int32_t slot, const uint8_t *bytes, uint64_
     std::lock_guard<std::mutex> lk(s->mu);
     AFAM_CUDA(cudaSetDevice(s->device));
     AFAM_CUDA(cudaStreamWaitEvent(st, s->host[slot].ready, 0));
+    AFAM_CUDA(wait_readers(s, slot, st));
     AFAM_CUDA(cudaMemcpyAsync(s->raw_ptr(slot), bytes, nbytes, cudaMemcpyHostToDevice, st));
     const float *samp = reinterpret_cast<const float *>(s->raw_ptr(slot) + 16);
     float *grid = reinterpret_cast<float *>(s->ctrl4_ptr(slot));
@@ -494,6 +507,7 @@ int afam_store_put(afam_store *s, int32_t slot, int32_t degree, int32_t ncp, con
     const size_t cb = sizeof(float) * (size_t)ncp * ncp * ncp;
     const uint64_t koff = 0, coff = (kb + 15) & ~(size_t)15;
     AFAM_CUDA(cudaStreamWaitEvent(st, s->host[slot].ready, 0));
+    AFAM_CUDA(wait_readers(s, slot, st));
     AFAM_CUDA(cudaMemcpyAsync(s->raw_ptr(slot) + koff, knots, kb, cudaMemcpyHostToDevice, st));
     AFAM_CUDA(cudaMemcpyAsync(s->raw_ptr(slot) + coff, ctrl, cb, cudaMemcpyHostToDevice, st));
     return launch_unpack(s, slot, degree, ncp, koff, 1, coff, extent, st);

@@ -253,8 +253,9 @@ class _ScratchStore:
             self.lru[key] = (ref, blk)
             return blk
 
-    def get_ds(self, block, serialize) -> DeviceBlock:
-        """Upload (or reuse) a host DS block, keyed like get()."""
+    def get_ds(self, block, serialize, pinned=()) -> DeviceBlock:
+        """Upload (or reuse) a host DS block, keyed like get(); blocks of the
+        current call (`pinned` ids) are never evicted to make room."""
         key = id(block)
         with self.lock:
             hit = self.lru.get(key)
@@ -264,7 +265,10 @@ class _ScratchStore:
             if hit is not None:
                 self._drop(key)
             while self.store.free_slots() == 0:
-                self._drop(next(iter(self.lru)))
+                victim = next((k for k in self.lru if k not in pinned), None)
+                if victim is None:
+                    raise CapacityError("scratch device store is full of pinned blocks")
+                self._drop(victim)
             blk = self.store.load_ds(serialize(block), block.extent, block.lod)
             try:
                 ref = weakref.ref(block)
@@ -278,12 +282,15 @@ class _ScratchStore:
         self.store.release(blk.slot)
 
 
-def scratch_store(max_ncp: int, device: int = 0) -> _ScratchStore:
-    bucket = next((b for b in _BUCKETS if b >= max_ncp), None)
+def scratch_store(max_ncp: int, device: int = 0, exact: bool = False) -> _ScratchStore:
+    """The per-process scratch store for host models of up to `max_ncp`
+    control points per axis (size buckets); `exact` sizes the slots for
+    exactly `max_ncp` (DS blocks: the ghosted sample edge)."""
+    bucket = int(max_ncp) if exact else next((b for b in _BUCKETS if b >= max_ncp), None)
     if bucket is None:
         bucket = int(max_ncp)
     with _scratch_lock:
-        key = (bucket, int(device))
+        key = (bucket, int(device), bool(exact))
         if key not in _scratch:
             _scratch[key] = _ScratchStore(bucket, device)
         return _scratch[key]
@@ -303,12 +310,13 @@ def as_device_blocks(values, device: int = 0):
 
     if hosts and all(isinstance(v, DsBlock) for v in hosts):  # DS baseline blocks
         edge = max(max(v.samples.shape) for v in hosts) if hosts else 9
-        sc = scratch_store(edge, device)
+        sc = scratch_store(edge, device, exact=True)  # DS slots sized by the sample edge, not a spline bucket
+        pinned = set(id(v) for v in values)
         slots = []
         for v in values:
             if isinstance(v, DeviceBlock):
                 raise TypeError("cannot mix resident DeviceBlocks with host DS blocks in one render")
-            slots.append(sc.get_ds(v, serialize_ds).slot)
+            slots.append(sc.get_ds(v, serialize_ds, pinned).slot)
         return sc.store, slots
     for v in hosts:
         if not (hasattr(v, "control") and hasattr(v, "knots") and hasattr(v, "degree") and hasattr(v, "extent")):

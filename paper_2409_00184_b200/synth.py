@@ -24,7 +24,7 @@ import numpy as np
 from .bspline import clamped_knots
 from .partition import BlockAddress, ManifestEntry, block_extent, skeleton
 
-__all__ = ["fit_operator", "turbulence_store", "ml_value", "field_store", "ncp_for", "pack_mfa"]
+__all__ = ["fit_operator", "turbulence_store", "ml_value", "ml_volume", "field_store", "ncp_for", "pack_mfa"]
 
 SEED = 20261017
 
@@ -141,10 +141,23 @@ def turbulence_store(levels: int = 4, coarsest: int = 2, micro: int = 65, degree
 
 
 def ml_value(x, y, z, f_m: float = 6.0, alpha: float = 0.05):
-    """Marschner-Lobb field (Marschner & Lobb 1994), normalized to [0, 1]."""
-    r = np.sqrt(x * x + y * y)
+    """Marschner-Lobb field (Marschner & Lobb 1994), normalized to [0, 1]
+    (the reference's volume.ml_value, float64, radius by np.hypot)."""
+    x, y, z = np.asarray(x, dtype=np.float64), np.asarray(y, dtype=np.float64), np.asarray(z, dtype=np.float64)
+    r = np.hypot(x, y)
     rho = np.cos(2.0 * np.pi * f_m * np.cos(np.pi * r / 2.0))
     return (1.0 - np.sin(np.pi * z / 2.0) + alpha * (1.0 + rho)) / (2.0 * (1.0 + alpha))
+
+
+def ml_volume(dims=(257, 257, 257), bounds=((0.0, 7.0),) * 3):
+    """The reference's sample_grid(marschner_lobb(), dims) (volume.py:127-139):
+    float32 samples [ix, iy, iz] over the inclusive bounds, with .bounds."""
+    from types import SimpleNamespace
+
+    b = np.asarray(bounds, dtype=np.float64)
+    axes = [np.linspace(b[a, 0], b[a, 1], int(dims[a])) for a in range(3)]
+    X, Y, Z = np.meshgrid(*axes, indexing="ij")
+    return SimpleNamespace(samples=ml_value(X, Y, Z).astype(np.float32), bounds=b)
 
 
 def field_store(levels: int, coarsest: int, micro: int, degree: int, ncp_of, fn=ml_value,

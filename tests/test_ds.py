@@ -140,3 +140,33 @@ def test_ds_point_queries_vs_reference():
         # the central-difference grids are built once at upload and held in
         # float32 (as the DS render reads them): ~1e-8 relative vs float64
         assert np.abs(g - want_g).max() <= 1e-6 * max(1.0, float(np.abs(want_g).max())), k
+
+
+@pytest.mark.gpu
+def test_ds_scratch_store_keeps_the_calls_blocks():
+    """Host DS blocks resolved in one call are pinned in the scratch store: a
+    full store evicts only blocks of earlier calls and raises CapacityError
+    when the call alone overflows it (never a slot reused within the call)."""
+    _cuda()
+    from paper_2409_00184_b200 import device, downsample
+    from paper_2409_00184_b200.errors import CapacityError
+
+    man, raw, blocks = _store(1)
+    addrs = sorted(blocks)[:5]
+    edge = max(max(blocks[a].samples.shape) for a in addrs)
+    sc = device._ScratchStore(edge, 0)
+    sc.store = device.DeviceStore(3, edge)
+    first = {id(blocks[a]) for a in addrs[:3]}
+    slots = [sc.get_ds(blocks[a], downsample.serialize_ds, first).slot for a in addrs[:3]]
+    assert len(set(slots)) == 3
+    # a new call with two other blocks evicts two of the earlier call's slots
+    second = {id(blocks[a]) for a in addrs[3:5]}
+    s2 = [sc.get_ds(blocks[a], downsample.serialize_ds, second).slot for a in addrs[3:5]]
+    assert len(set(s2)) == 2
+    # one call needing four slots of a three-slot store: CapacityError, no silent reuse
+    allp = {id(blocks[a]) for a in addrs[:4]}
+    with pytest.raises(CapacityError):
+        for a in addrs[:4]:
+            sc.get_ds(blocks[a], downsample.serialize_ds, allp)
+    # DS scratch stores are sized by the sample edge, not a spline NCP bucket
+    assert device.scratch_store(edge, 0, exact=True).store.max_ncp == edge

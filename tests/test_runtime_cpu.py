@@ -85,6 +85,22 @@ def test_evictions_release_device_slots():
     assert released == ["a", "b"]
 
 
+def test_capacity_error_releases_the_loaded_block():
+    """A block loaded for a fetch that then cannot be cached (every entry
+    pinned) is handed back to the loader's release hook: with a DeviceStore
+    loader its slot would otherwise leak."""
+    from paper_2409_00184_b200.errors import CapacityError
+    from paper_2409_00184_b200.runtime import ModelCache
+
+    released = []
+    c = ModelCache(2, load_blob, on_evict=lambda b: released.append(b.key))
+    c.fetch("a"), c.fetch("b")
+    c.begin_frame({"a", "b"})
+    with pytest.raises(CapacityError):
+        c.fetch("c")
+    assert released == ["c"] and "c" not in c and len(c) == 2
+
+
 def test_counters_and_hook():
     from paper_2409_00184_b200.runtime import ModelCache
 
