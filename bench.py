@@ -16,7 +16,9 @@ the RGBA8 tiles to rank 0 inside the timed step.
 
 --impl reference times the reference algorithm on the host CPU: the
 float64 C restatement in oracle/ (the reference itself is pure Python and
-is not on the GPU box), all host threads, on a row band of the same frames.
+is not on the GPU box), all host threads, one whole frame of the same orbit
+per step; it imports nothing from the product package (oracle/workload.py
+restates the inputs).
 """
 
 from __future__ import annotations
@@ -38,12 +40,15 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "decoded samples/s (1024^2 ray-cast, config 3)"
+DATA = ("synthetic: seeded k^-5/3 turbulence (48 Fourier modes), each block fitted by the reference encoder's "
+        "endpoint-pinned least-squares operator at an NCP hash-assigned in [40, 65] (not an adaptive search); "
+        "~120 samples per ray under o_max 0.99")
 UNIT = "samples/s"
 FLOP_PER_SAMPLE_P3 = 384  # 2*(2q^3+3q^2+4q), q=4: separable value+gradient contraction
 FLOP_VALUE_P3 = 168  # 2*(q^3+q^2+q): value only (transparent samples skip the gradient, see afam_render.cu)
 WORKLOAD = {"workload": "config3: 1024^3-equiv synthetic turbulence, 4 LODs, 4680 blocks (micro 65, degree 3, "
-                        "ncp 40-65), 1024x1024 ray-cast, sd 1e-3, ML TF + gradient shading, "
-                        "orbit_trajectory(100, r=2.0)",
+                        "ncp hash-assigned in 40-65), 1024x1024 ray-cast, sd 1e-3, o_max 0.99, ML TF + gradient "
+                        "shading, orbit_trajectory(100, r=2.0)",
             "frame": [1024, 1024], "sample_distance": 1e-3, "blocks": 4680,
             "l2": "flushed between steps (512 MiB write outside the per-step events)"}
 
@@ -58,7 +63,6 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-rows", type=int, default=24, help="rows of the frame in the CPU sample")
     ap.add_argument("--gather", default="fused", choices=["fused", "nccl"],
                     help="N > 1: band gather fused into the render kernel (peer stores) or an NCCL gather")
     return ap.parse_args()
@@ -350,7 +354,7 @@ def run_ours(args, rank, world, local_rank):
               "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
               "scaling": "strong", "vs_baseline": None, "dtype": "f32 (f64 geometry; f64 decode on "
                                                                  "ill-conditioned blocks)",
-              "data": "synthetic (seeded turbulence, fitted like the reference encoder)",
+              "data": DATA,
               "config": dict(WORKLOAD, parallelism=f"image bands x{world}", gather=gather_kind, frame_ms=step_ms,
                              kernel_ms=kern_ms, host_envelope_ms=float(np.mean(envelope)),
                              visible_blocks_mean=float(np.mean(nvis)),
@@ -461,52 +465,60 @@ def run_e2e(args, man, blobs, povs, tf, params, rank, world, local_rank):
 
 
 # ------------------------------------------------------------------ CPU
-def cpu_sample(man, blobs, povs, tf, params, rows, frame_index):
-    """Time the oracle (float64 C restatement of render.py:398-466) on a row band."""
-    from oracle import oracle
+def cpu_frame(frame_index: int, size: int, threads: int, rows=None):
+    """Render one orbit frame of the config-3 model with the float64 C
+    restatement of render.py:398-466 (oracle/), on `threads` host threads.
+    Product-free: the visible set comes from oracle.select_visible and the
+    visible blocks' .mfa images from oracle/workload.py (byte-identical to
+    the product's synthesis), so the reference arm maps no libafam code.
+    Returns (samples, seconds of the render call, description)."""
+    from oracle import oracle, workload
 
-    from paper_2409_00184_b200 import model, render
-
+    povs = workload.orbit_trajectory(100, radius=2.0)
     pov = povs[frame_index % len(povs)]
-    vis = render.select_visible(pov, man, params.aspect)
-    host = {a: model.deserialize(bytes(blobs[a]), man.entries[a].ncp, man.entries[a].extent, a.lod) for a in vis}
-    H = params.height
-    r0 = (H - rows) // 2
-    threads = len(os.sched_getaffinity(0))  # every host core (torchrun sets OMP_NUM_THREADS=1)
+    params = workload.render_params(width=size, height=size, sample_distance=1e-3)
+    tf = workload.ml_preset()
+    man = workload.skeleton(4, 2, 65)
+    vis = [workload.Addr(v[0], tuple(v[1:])) for v in oracle.select_visible(pov, man, params.aspect)]
+    man, blobs = workload.turbulence_store(addrs=vis)
+    host = {a: workload.parse_mfa(blobs[a], man.entries[a].ncp, man.entries[a].extent, a.lod) for a in vis}
     t0 = time.perf_counter()
-    _, info = oracle.render(pov, host, tf, params, rows=(r0, r0 + rows), nthreads=threads)
+    _, info = oracle.render(pov, host, tf, params, rows=rows, nthreads=threads)
     el = time.perf_counter() - t0
-    return info["samples"], el, threads, f"rows {r0}..{r0 + rows} of orbit frame {frame_index % len(povs)}"
+    what = f"orbit frame {frame_index % len(povs)}" + ("" if rows is None else f" rows {rows[0]}..{rows[1]}")
+    return info["samples"], el, what
+
+
+def host_cpu() -> tuple:
+    from oracle import workload
+
+    threads = len(os.sched_getaffinity(0))  # every host core (torchrun sets OMP_NUM_THREADS=1)
+    return threads, workload.cpu_model()
 
 
 def run_reference(args):
-    from paper_2409_00184_b200 import render, runtime
-
-    man, blobs, _ = build_model(pinned=False)
-    povs = runtime.orbit_trajectory(100, radius=2.0)
-    S = args.size
-    params = render.RenderParams(width=S, height=S, sample_distance=1e-3)
-    tf = render.TransferFunction.ml_preset()
+    """The reference algorithm on the host CPU: whole 1024^2 frames of the
+    config-3 orbit (the same frames as --impl ours: pose W + k), one frame
+    per step, the float64 C restatement on every host thread."""
+    threads, model = host_cpu()
     for k in range(min(args.warmup, 1)):
-        cpu_sample(man, blobs, povs, tf, params, 2, k)
-    tot_s, tot_t, times = 0, 0.0, []
-    threads, desc = 1, ""
-    rows = args.cpu_rows
+        cpu_frame(k, args.size, threads)
+    tot_s, tot_t = 0, 0.0
+    frames = []
     for k in range(args.steps):
-        s, t, threads, desc = cpu_sample(man, blobs, povs, tf, params, rows, args.warmup + k)
+        s, t, what = cpu_frame(args.warmup + k, args.size, threads)
         tot_s += s
         tot_t += t
-        times.append(t)
+        frames.append(what)
     value = tot_s / tot_t
-    import platform
-
+    sample = (f"whole {args.size}x{args.size} frames, one per step ({frames[0]} .. {frames[-1]}); oracle/ C float64 "
+              f"restatement of render.py:398-466, OpenMP x{threads} on {threads} host threads ({model})")
     return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (same model as --impl ours)",
-            "config": dict(WORKLOAD, l2="n/a (CPU)"), "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": f"{rows}-row band per step of the 1024^2 frames ({desc}); oracle/ C "
-                                       f"float64 restatement, OpenMP x{threads}, host {platform.processor()}"},
+            "vs_baseline": None, "dtype": "f64", "data": DATA, "config": dict(WORKLOAD, l2="n/a (CPU)"),
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "cpu": model,
+                             "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -534,14 +546,11 @@ def main():
             dist.init_process_group(backend)
     res, man, blobs = run_ours(args, rank, world, local_rank)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        from paper_2409_00184_b200 import render, runtime
-
-        povs = runtime.orbit_trajectory(100, radius=2.0)
-        params = render.RenderParams(width=args.size, height=args.size, sample_distance=1e-3)
-        s, t, threads, desc = cpu_sample(man, blobs, povs, render.TransferFunction.ml_preset(), params,
-                                         args.cpu_rows, args.warmup)
-        res["cpu_baseline"] = {"value": s / t, "unit": UNIT, "cores": threads, "kind": "port",
-                               "sample": f"{desc}: {s} samples in {t:.1f} s (oracle/ C float64, OpenMP x{threads})"}
+        threads, model = host_cpu()
+        s, t, what = cpu_frame(args.warmup, args.size, threads)
+        res["cpu_baseline"] = {"value": s / t, "unit": UNIT, "cores": threads, "kind": "port", "cpu": model,
+                               "sample": f"one whole {args.size}x{args.size} frame ({what}): {s} samples in {t:.1f} s "
+                                         f"(oracle/ C float64, OpenMP x{threads}, {model})"}
     if rank == 0:
         print(json.dumps(res), flush=True)
     if world > 1:

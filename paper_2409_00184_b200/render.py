@@ -194,23 +194,13 @@ class Frame:
         return cls(width=img.width, height=img.height, rgba=np.asarray(img, dtype=np.uint8))
 
     def to_png_bytes(self) -> bytes:
-        """PNG of the frame (render.py:216-221).  With a CUDA device the image
-        data is filtered and deflated on the GPU (png_bytes_gpu); the decoded
-        pixels are identical either way."""
+        """PNG of the frame (render.py:216-221): the image data is filtered and
+        deflated on the GPU (png_bytes_gpu).  No CPU fallback: without a CUDA
+        device this raises (the file-writing save_png is the host path)."""
         from . import _lib
 
-        if _lib.device_available():
-            return png_bytes_gpu(self.rgba)
-        return self._to_png_bytes_pil()
-
-    def _to_png_bytes_pil(self) -> bytes:
-        import io
-
-        from PIL import Image
-
-        out = io.BytesIO()
-        Image.fromarray(self.rgba, mode="RGBA").save(out, format="PNG")
-        return out.getvalue()
+        _lib.require_device()
+        return png_bytes_gpu(self.rgba)
 
 
 def png_bytes_gpu(rgba) -> bytes:

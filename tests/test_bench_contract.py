@@ -46,3 +46,52 @@ def test_reference_arm_line_contract():
     assert d["higher_is_better"] == mine["higher_is_better"]
     assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
     assert d["cpu_baseline"]["value"] == d["value"] and d["cpu_baseline"]["cores"] >= 1
+
+
+def test_reference_arm_is_product_free():
+    """bench.py --impl reference (the CPU arm) imports nothing from the
+    product package: run its input path in a fresh interpreter (a small
+    frame, one step) and check sys.modules and the mapped libraries."""
+    import subprocess
+    import sys
+
+    code = (
+        "import sys, json; sys.argv = ['bench.py', '--impl', 'reference', '--steps', '1', '--warmup', '0', "
+        "'--size', '48']\n"
+        "import bench\n"
+        "res = bench.run_reference(bench.parse())\n"
+        "maps = open('/proc/self/maps').read()\n"
+        "bad = [m for m in sys.modules if m.startswith('paper_2409_00184_b200')]\n"
+        "print(json.dumps({'bad': bad, 'libafam': 'libafam.so' in maps, 'oracle': 'libafam_oracle.so' in maps, "
+        "'value': res['value'], 'cpu': res['cpu_baseline']['cpu']}))\n")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    assert out["bad"] == [] and not out["libafam"] and out["oracle"]
+    assert out["value"] > 0 and out["cpu"]
+
+
+def test_reference_arm_inputs_match_product_synthesis():
+    """oracle/workload.py's restated config-3 inputs are byte-identical to the
+    product's synth.turbulence_store (a strided subset of blocks), and the
+    restated orbit / TF / params equal the product's."""
+    import numpy as np
+
+    from oracle import workload as W
+    from paper_2409_00184_b200 import render, runtime, synth
+
+    man, blobs = synth.turbulence_store()
+    pick = sorted(blobs)[::211]
+    m2, b2 = W.turbulence_store(addrs=[W.Addr(a.lod, a.ijk) for a in pick])
+    for a in pick:
+        assert bytes(blobs[a]) == b2[W.Addr(a.lod, a.ijk)], a
+    for a, e in man.entries.items():
+        e2 = m2.entries[W.Addr(a.lod, a.ijk)]
+        assert e.ncp == e2.ncp and np.array_equal(e.extent, e2.extent)
+    for p, q in zip(runtime.orbit_trajectory(100, radius=2.0), W.orbit_trajectory(100, radius=2.0)):
+        assert np.array_equal(p.position, q.position) and np.array_equal(p.direction, q.direction)
+    tf, tw = render.TransferFunction.ml_preset(), W.ml_preset()
+    assert np.array_equal(tf.color_points, tw.color_points) and np.array_equal(tf.opacity_points, tw.opacity_points)
+    rp, rq = render.RenderParams(width=1024, height=1024), W.render_params(width=1024, height=1024)
+    for k in ("sample_distance", "o_max", "reference_step", "near", "ambient", "diffuse", "specular", "shininess"):
+        assert getattr(rp, k) == getattr(rq, k), k
