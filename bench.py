@@ -292,6 +292,7 @@ def run_ours(args, rank, world, local_rank):
         return ev0, ev1, ev2, info, len(vis)
 
     times, ktimes, envelope, samples, fp64s, shaded, nvis = [], [], [], 0, 0, 0, []
+    exact_s, exact_c = 0, 0
     # the sampler starts before the warm-up: nvidia-smi's own start-up must not
     # overlap the timed steps; its samples cover warm-up + timed region (all under load)
     with ClockSampler(local_rank) as clk:
@@ -314,6 +315,8 @@ def run_ours(args, rank, world, local_rank):
             samples += info["samples"]
             fp64s += info["fp64_samples"]
             shaded += info["shaded_samples"]
+            exact_s += info["exact_samples"]
+            exact_c += info["exact_cells"]
             nvis.append(nv)
         torch.cuda.synchronize(dev)
         if world > 1:
@@ -358,7 +361,9 @@ def run_ours(args, rank, world, local_rank):
               "config": dict(WORKLOAD, parallelism=f"image bands x{world}", gather=gather_kind, frame_ms=step_ms,
                              kernel_ms=kern_ms, host_envelope_ms=float(np.mean(envelope)),
                              visible_blocks_mean=float(np.mean(nvis)),
-                             fp64_sample_frac=total_fp64 / max(1.0, total_samples), gen_s=round(gen_s, 1),
+                             fp64_sample_frac=total_fp64 / max(1.0, total_samples),
+                             exact_path_sample_frac=exact_s / max(1, samples),
+                             exact_geometry_per_sample=exact_c / max(1, samples), gen_s=round(gen_s, 1),
                              upload_s=round(upload_s, 2), fp64_slot_sample=int(nfp64)),
               "roofline": roofline, "clocks": clk.summary(), "gpu_launches": 3 * args.steps,
               "wall_s_timed_region": t_wall}

@@ -71,7 +71,7 @@ struct TfTable {
     int8_t lut[kTfBuckets];   // last breakpoint <= bucket start (-1: none)
     int32_t nbp;
     float lo, scale;          // bucket coordinate = (v - lo) * scale over the TF domain
-    int32_t pad;
+    float op_lo, op_hi;       // opacity support (see build_tf_table)
 };
 
 struct alignas(16) RenderArgs {
@@ -86,6 +86,8 @@ struct alignas(16) RenderArgs {
     float dom_lo, dom_hi;
     float o_max_f;      // largest float32 <= o_max: (float)A <= o_max_f iff (double)A <= o_max
     uint32_t flags;
+    float tf_lo, tf_scale;  // TfTable lo / scale, as launch arguments (constant bank, no per-sample load)
+    float op_lo, op_hi;     // TF opacity support: the kernel's alpha_tf is exactly 0 unless op_lo < v < op_hi
 };
 
 // TransferFunction.color_at / opacity_at (render.py:117-124): every
@@ -536,12 +538,31 @@ __device__ __forceinline__ bool span_interior(const BlockFast &b, int k) {
 // every block shares these polynomials (power basis, ascending; E_q is the
 // difference-form weight sum_{i>q} dN_i/df).  Checked against exact
 // rational Cox-de Boor in DESIGN.md's derivation script.
-__constant__ float kBndN[2][4][4] = {
-    {{1.f, -3.f, 3.f, -1.f}, {0.f, 3.f, -4.5f, 1.75f}, {0.f, 0.f, 1.5f, -11.f / 12.f}, {0.f, 0.f, 0.f, 1.f / 6.f}},
-    {{0.25f, -0.75f, 0.75f, -0.25f}, {7.f / 12.f, 0.25f, -1.25f, 7.f / 12.f}, {1.f / 6.f, 0.5f, 0.5f, -0.5f},
-     {0.f, 0.f, 0.f, 1.f / 6.f}}};
-__constant__ float kBndE[2][3][3] = {{{3.f, -6.f, 3.f}, {0.f, 3.f, -2.25f}, {0.f, 0.f, 0.5f}},
-                                     {{0.75f, -1.5f, 0.75f}, {0.5f, 1.f, -1.f}, {0.f, 0.f, 0.5f}}};
+// The coefficients are immediates of the FFMAs (both classes evaluated,
+// then selected): no dynamically indexed constant-bank loads per sample.
+__device__ __forceinline__ float horner3(float c0, float c1, float c2, float c3, float f) {
+    return fmaf(fmaf(fmaf(c3, f, c2), f, c1), f, c0);
+}
+
+__device__ __forceinline__ void bnd_N(int cls, float f, float (&n)[4]) {
+    const float a0 = horner3(1.f, -3.f, 3.f, -1.f, f), b0 = horner3(0.25f, -0.75f, 0.75f, -0.25f, f);
+    const float a1 = horner3(0.f, 3.f, -4.5f, 1.75f, f), b1 = horner3(7.f / 12.f, 0.25f, -1.25f, 7.f / 12.f, f);
+    const float a2 = horner3(0.f, 0.f, 1.5f, -11.f / 12.f, f), b2 = horner3(1.f / 6.f, 0.5f, 0.5f, -0.5f, f);
+    n[0] = cls ? b0 : a0;
+    n[1] = cls ? b1 : a1;
+    n[2] = cls ? b2 : a2;
+    n[3] = horner3(0.f, 0.f, 0.f, 1.f / 6.f, f);
+}
+
+__device__ __forceinline__ float horner2(float c0, float c1, float c2, float f) { return fmaf(fmaf(c2, f, c1), f, c0); }
+
+__device__ __forceinline__ void bnd_E(int cls, float f, float nsf, float (&e)[3]) {
+    const float a0 = horner2(3.f, -6.f, 3.f, f), b0 = horner2(0.75f, -1.5f, 0.75f, f);
+    const float a1 = horner2(0.f, 3.f, -2.25f, f), b1 = horner2(0.5f, 1.f, -1.f, f);
+    e[0] = nsf * (cls ? b0 : a0);
+    e[1] = nsf * (cls ? b1 : a1);
+    e[2] = nsf * horner2(0.f, 0.f, 0.5f, f);
+}
 
 // span class of a cubic boundary span k (not interior): 0/1 from the left
 // end, mirrored from the right end
@@ -561,10 +582,7 @@ __device__ __forceinline__ void axis_table_N(const BlockFast &b, const ThreadCol
             const float fr = tq - (float)k;
             const float f = mirror ? 1.f - fr : fr;
             float n[4];
-#pragma unroll
-            for (int i = 0; i < 4; i++)
-                n[i] = fmaf(fmaf(fmaf(kBndN[cls][i][3], f, kBndN[cls][i][2]), f, kBndN[cls][i][1]), f,
-                            kBndN[cls][i][0]);
+            bnd_N(cls, f, n);
 #pragma unroll
             for (int i = 0; i < 4; i++) N[i] = mirror ? n[3 - i] : n[i];
             return;
@@ -587,8 +605,7 @@ __device__ __forceinline__ void axis_fast_E(const BlockFast &b, const ThreadCold
         bnd_class(b, k, cls, mirror);
         const float f = mirror ? 1.f - fr : fr;
         float e[3];
-#pragma unroll
-        for (int q = 0; q < 3; q++) e[q] = nsf * fmaf(fmaf(kBndE[cls][q][2], f, kBndE[cls][q][1]), f, kBndE[cls][q][0]);
+        bnd_E(cls, f, nsf, e);
 #pragma unroll
         for (int q = 0; q < P; q++) E[q] = mirror ? e[2 - q] : e[q];
     } else {
@@ -601,17 +618,36 @@ __device__ __forceinline__ void axis_fast_E(const BlockFast &b, const ThreadCold
 
 // TF opacity of a decoded value from the per-bucket lines (render.py:117-124
 // np.interp); NaN-marked buckets hold a breakpoint and take the segment search.
-// The kernel's dynamic shared memory: [ThreadCold x 128 | TF opacity lines | owner grid]
-extern __shared__ __align__(16) unsigned char afam_render_smem[];
-constexpr size_t kSmemAlphaOff = 128 * sizeof(ThreadCold);
-constexpr size_t kSmemGridOff = kSmemAlphaOff + kTfBuckets * sizeof(float2);
+// Shared memory: the TF opacity lines and the per-thread cold state are
+// static arrays (fixed shared-window offsets, no per-sample base
+// arithmetic); the dynamic part holds only the owner grid.
+__shared__ float2 s_tf_alpha[kTfBuckets];
+__shared__ ThreadCold s_cold[128];
 
-__device__ __forceinline__ float tf_alpha(const TfTable &T, float v, int &bi, float &bf) {
-    const float tb = (v - T.lo) * T.scale;
+// A fresh shared-memory read at every use (volatile): the compiler would
+// otherwise hoist the loop-invariant loads into registers and keep them live
+// across the sample loop, which is exactly what keeping them in shared
+// memory is meant to avoid.
+template <typename T>
+__device__ __forceinline__ T vld(const T &x) {
+    return *(const volatile T *)&x;
+}
+
+struct FastCold {  // render2_kernel's per-thread rarely-read state
+    BlockFast b;                 // the owner block's fields read at cell changes
+    int32_t kend;                // alive samples of the ray
+    int32_t cur_own, slot, deg;  // owner index, its slot and degree
+};
+__shared__ FastCold s_fast[128];
+extern __shared__ __align__(16) unsigned char afam_render_smem[];
+constexpr size_t kSmemGridOff = 0;
+
+__device__ __forceinline__ float tf_alpha(const RenderArgs &A, const TfTable &T, float v, int &bi, float &bf) {
+    const float tb = (v - A.tf_lo) * A.tf_scale;
     bi = min(max(__float2int_rz(tb), 0), kTfBuckets - 1);
     bf = tb - (float)bi;
     // opacity lines staged in shared memory (the per-sample critical path)
-    const float2 l = reinterpret_cast<const float2 *>(afam_render_smem + kSmemAlphaOff)[bi];
+    const float2 l = s_tf_alpha[bi];
     float a = fmaf(bf, l.y, l.x);
     if (isnan(a)) a = tf_eval(T, v).w;
     return a;
@@ -752,7 +788,7 @@ __device__ __forceinline__ bool sample_fast(const RenderArgs &A, const TfTable &
     int bi;
     float bf;
     const float vc = fminf(fmaxf(v, A.dom_lo), A.dom_hi);
-    const float atf = tf_alpha(tf, vc, bi, bf);
+    const float atf = tf_alpha(A, tf, vc, bi, bf);
     if (!(atf > 0.f)) return true;  // a_s = 0: the sample changes neither C nor A
     ++M.nshade;
     float Ex[P], Ey[P], Ez[P];
@@ -849,7 +885,7 @@ __device__ __forceinline__ void sample_ds(const RenderArgs &A, const TfTable &tf
     int bi;
     float bf;
     const float vc = fminf(fmaxf(v, A.dom_lo), A.dom_hi);
-    const float atf = tf_alpha(tf, vc, bi, bf);
+    const float atf = tf_alpha(A, tf, vc, bi, bf);
     if (!(atf > 0.f)) return;
     ++M.nshade;
     const size_t plane = (size_t)dn[0] * dn[1] * dn[2];
@@ -906,10 +942,9 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
     // so L1 keeps the most room for control-point rows; GA: the launch
     // arguments in global memory, for the out-of-line exact path
     const TfTable &tf = *gtf;
-    ThreadCold &C = reinterpret_cast<ThreadCold *>(smem)[threadIdx.x];
+    ThreadCold &C = s_cold[threadIdx.x];
     int16_t *sgrid = reinterpret_cast<int16_t *>(smem + kSmemGridOff);
-    for (int i = threadIdx.x; i < kTfBuckets; i += blockDim.x)
-        reinterpret_cast<float2 *>(smem + kSmemAlphaOff)[i] = gtf->alpha[i];
+    for (int i = threadIdx.x; i < kTfBuckets; i += blockDim.x) s_tf_alpha[i] = gtf->alpha[i];
     if (SMEM_GRID)
         for (int i = threadIdx.x; i < A.cells * A.cells * A.cells; i += blockDim.x) sgrid[i] = grid[i];
     __syncthreads();
@@ -1114,6 +1149,385 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
     }
 }
 
+// ---------------------------------------------------------------------------
+// K2, restructured sample loop (render2_kernel): the same numerics as
+// render_kernel's fast path (identical span coordinates, bases, contraction
+// order and compositing, so the frames are bit-identical), with the work
+// that is constant within a knot cell hoisted out of the per-sample path:
+//  - the lane's current cell is kept as its lower corner (float span
+//    coordinates); a sample stays in the cell iff its three fractions
+//    tq - corner lie in [0, 1) (three unsigned compares on the float bits),
+//    so the span, clamp, cell key and interior test are recomputed only on
+//    a cell change (about one sample in four at LOD-2 span widths);
+//  - which axes sit on interior spans (closed-form uniform basis) is a
+//    per-cell bit mask;
+//  - the owner change, the next exact-geometry sample and the end of the
+//    ray are one per-sample compare against the segment end
+//    min(knext, kend).
+template <int P>
+struct FastCell {
+    float4 c[(P + 1) * (P + 1)];  // x-quad rows cz*Q+by of the cell (bspline.py:175-181)
+    float cx, cy, cz;             // the cell's lower corner in span coordinates
+    int32_t key;                  // x-quad row index of the (0, 0) row in the owner block; -1: none
+    uint32_t inner;               // bit a: axis a on an interior span
+};
+
+__device__ __forceinline__ bool in_unit(float f) {  // 0 <= f < 1 (also rejects -0.0 and NaN)
+    return __float_as_uint(f) < 0x3f800000u;
+}
+
+// Re-derive the cell of predicted span coordinates tq (render_kernel's
+// axis_span: floor, clamped to the block's spans) and re-gather its rows
+// when the cell key changed.
+template <int P>
+__device__ __forceinline__ BlockFast fast_block(const BlockFast &sb) {  // sb in shared memory
+    BlockFast b;
+    b.ctrl4 = vld(sb.ctrl4);
+    b.ncp = vld(sb.ncp);
+    b.nspan = vld(sb.nspan);
+    b.plane = vld(sb.plane);
+    b.nint = vld(sb.nint);
+    return b;
+}
+
+template <int P>
+__device__ __forceinline__ void fast_cell_update(const BlockFast &sb, float tqx, float tqy, float tqz, FastCell<P> &G) {
+    constexpr int Q = P + 1;
+    const BlockFast b = fast_block<P>(sb);
+    const int kx = min(max(__float2int_rd(tqx), 0), b.nspan - 1);
+    const int ky = min(max(__float2int_rd(tqy), 0), b.nspan - 1);
+    const int kz = min(max(__float2int_rd(tqz), 0), b.nspan - 1);
+    G.cx = (float)kx;
+    G.cy = (float)ky;
+    G.cz = (float)kz;
+    G.inner = (span_interior<P>(b, kx) ? 1u : 0u) | (span_interior<P>(b, ky) ? 2u : 0u) |
+              (span_interior<P>(b, kz) ? 4u : 0u);
+    const int32_t id = (kz * b.ncp + kx) * b.ncp + ky;
+    if (id != G.key) {
+        const float4 *base = b.ctrl4 + id;
+#pragma unroll
+        for (int cz = 0; cz < Q; cz++)
+#pragma unroll
+            for (int by = 0; by < Q; by++) G.c[cz * Q + by] = __ldg(base + cz * b.plane + by);
+        G.key = id;
+    }
+}
+
+// One sample of a clamped-uniform float32 block (render_kernel's
+// sample_fast, same arithmetic).  Returns false when the exact path must
+// decode it (P = 1 within 1e-4 of a knot).
+template <int P>
+__device__ __forceinline__ bool sample_fast2(const RenderArgs &A, const TfTable &tf, const BlockFast &sb, float tqx,
+                                             float tqy, float tqz, const ThreadCold &C, FastCell<P> &G, March &M) {
+    constexpr int Q = P + 1;
+    float fx = tqx - G.cx, fy = tqy - G.cy, fz = tqz - G.cz;
+    if (!(in_unit(fx) & in_unit(fy) & in_unit(fz))) {
+        fast_cell_update<P>(sb, tqx, tqy, tqz, G);
+        fx = tqx - G.cx;
+        fy = tqy - G.cy;
+        fz = tqz - G.cz;
+    }
+    if constexpr (P == 1) {
+        if (!(fabsf(fx - 0.5f) < 0.5f - 1e-4f) || !(fabsf(fy - 0.5f) < 0.5f - 1e-4f) ||
+            !(fabsf(fz - 0.5f) < 0.5f - 1e-4f))
+            return false;
+    }
+    float Nx[Q], Ny[Q], Nz[Q];
+    {
+        float2 Nxy[Q];
+        uniform_N2<P>(make_float2(fx, fy), Nxy);
+#pragma unroll
+        for (int i = 0; i < Q; i++) {
+            Nx[i] = Nxy[i].x;
+            Ny[i] = Nxy[i].y;
+        }
+        if (G.inner == 7u) {
+            uniform_N<P>(fz, Nz);
+        } else {
+            const BlockFast b = fast_block<P>(sb);
+            if (!(G.inner & 1u)) axis_table_N<P>(b, C, 0, (int)G.cx, tqx, Nx);
+            if (!(G.inner & 2u)) axis_table_N<P>(b, C, 1, (int)G.cy, tqy, Ny);
+            if (G.inner & 4u) uniform_N<P>(fz, Nz);
+            else axis_table_N<P>(b, C, 2, (int)G.cz, tqz, Nz);
+        }
+    }
+    float2 Ylo[Q], Yhi[Q], Zlo, Zhi;
+#pragma unroll
+    for (int cz = 0; cz < Q; cz++) {
+        Ylo[cz] = mul2s(Ny[0], lo2(G.c[cz * Q]));
+        Yhi[cz] = mul2s(Ny[0], hi2(G.c[cz * Q]));
+#pragma unroll
+        for (int by = 1; by < Q; by++) {
+            Ylo[cz] = fma2s(Ny[by], lo2(G.c[cz * Q + by]), Ylo[cz]);
+            Yhi[cz] = fma2s(Ny[by], hi2(G.c[cz * Q + by]), Yhi[cz]);
+        }
+    }
+    Zlo = mul2s(Nz[0], Ylo[0]);
+    Zhi = mul2s(Nz[0], Yhi[0]);
+#pragma unroll
+    for (int cz = 1; cz < Q; cz++) {
+        Zlo = fma2s(Nz[cz], Ylo[cz], Zlo);
+        Zhi = fma2s(Nz[cz], Yhi[cz], Zhi);
+    }
+    const float v = dot_x<P>(Nx, Zlo, Zhi);
+    int bi;
+    float bf;
+    const float vc = fminf(fmaxf(v, A.dom_lo), A.dom_hi);
+    // outside the TF's opacity support alpha_tf is exactly 0: no lookup
+    if (!(vc > A.op_lo) || !(vc < A.op_hi)) return true;
+    const float atf = tf_alpha(A, tf, vc, bi, bf);
+    if (!(atf > 0.f)) return true;  // a_s = 0: the sample changes neither C nor A
+    ++M.nshade;
+    float Ex[P], Ey[P], Ez[P];
+    if (G.inner == 7u) {
+        const float nsf = (float)vld(sb.nspan);
+        uniform_E<P>(fx, nsf, Ex);
+        uniform_E<P>(fy, nsf, Ey);
+        uniform_E<P>(fz, nsf, Ez);
+    } else {
+        const BlockFast b = fast_block<P>(sb);
+        axis_fast_E<P>(b, C, 0, (int)G.cx, fx, Ex);
+        axis_fast_E<P>(b, C, 1, (int)G.cy, fy, Ey);
+        axis_fast_E<P>(b, C, 2, (int)G.cz, fz, Ez);
+    }
+    const float gx = ddot_x<P>(Ex, Zlo, Zhi);
+    float2 Dlo = mul2s(Ez[0], sub2(Ylo[1], Ylo[0])), Dhi = mul2s(Ez[0], sub2(Yhi[1], Yhi[0]));
+#pragma unroll
+    for (int q = 1; q < P; q++) {
+        Dlo = fma2s(Ez[q], sub2(Ylo[q + 1], Ylo[q]), Dlo);
+        Dhi = fma2s(Ez[q], sub2(Yhi[q + 1], Yhi[q]), Dhi);
+    }
+    const float gz = dot_x<P>(Nx, Dlo, Dhi);
+    float2 Wlo[Q], Whi[Q];
+#pragma unroll
+    for (int by = 0; by < Q; by++) {
+        Wlo[by] = mul2s(Nz[0], lo2(G.c[by]));
+        Whi[by] = mul2s(Nz[0], hi2(G.c[by]));
+#pragma unroll
+        for (int cz = 1; cz < Q; cz++) {
+            Wlo[by] = fma2s(Nz[cz], lo2(G.c[cz * Q + by]), Wlo[by]);
+            Whi[by] = fma2s(Nz[cz], hi2(G.c[cz * Q + by]), Whi[by]);
+        }
+    }
+    Dlo = mul2s(Ey[0], sub2(Wlo[1], Wlo[0]));
+    Dhi = mul2s(Ey[0], sub2(Whi[1], Whi[0]));
+#pragma unroll
+    for (int q = 1; q < P; q++) {
+        Dlo = fma2s(Ey[q], sub2(Wlo[q + 1], Wlo[q]), Dlo);
+        Dhi = fma2s(Ey[q], sub2(Whi[q + 1], Whi[q]), Dhi);
+    }
+    const float gy = dot_x<P>(Nx, Dlo, Dhi);
+    const float4 gi = C.ginv;
+    const float g[3] = {gx * gi.x, gy * gi.y, gz * gi.z};
+    composite(A, C.vdir, tf_color(tf, vc, bi, bf, atf), g, M);
+    return true;
+}
+
+template <bool DEBUG, bool SMEM_GRID, int P, int MINB>
+__global__ void __launch_bounds__(128, MINB) render2_kernel(const BlockDesc *__restrict__ descs,
+                                                         const int16_t *__restrict__ grid,
+                                                         const int32_t *__restrict__ idx2slot, const RenderArgs A,
+                                                         const RenderArgs *__restrict__ GA,
+                                                         const TfTable *__restrict__ gtf, uint8_t *__restrict__ rgba,
+                                                         afam_render_stats *stats, int32_t *__restrict__ nsamp,
+                                                         uint64_t *__restrict__ ohash) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const TfTable &tf = *gtf;
+    ThreadCold &C = s_cold[threadIdx.x];
+    int16_t *sgrid = reinterpret_cast<int16_t *>(smem + kSmemGridOff);
+    for (int i = threadIdx.x; i < kTfBuckets; i += blockDim.x) s_tf_alpha[i] = gtf->alpha[i];
+    if (SMEM_GRID)
+        for (int i = threadIdx.x; i < A.cells * A.cells * A.cells; i += blockDim.x) sgrid[i] = grid[i];
+    __syncthreads();
+    const int16_t *own_grid = SMEM_GRID ? sgrid : grid;
+    RayState R;
+    // state the sample loop reads only at cell changes and segment ends
+    // (owner block fields, ray end, next exact sample) lives in shared
+    // memory, so the registers hold the cached cell and the per-sample state
+    FastCold &F = s_fast[threadIdx.x];
+
+    // this thread's pixel: column j, local row lr, frame row i (recomputed
+    // after the march instead of held in registers across it)
+    auto pixel = [&](int &j, int &lr, int &i) {
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        j = blockIdx.x * 16 + (warp & 1) * 8 + (lane & 7);
+        lr = blockIdx.y * 8 + (warp >> 1) * 4 + (lane >> 3);
+        const bool in = j < A.width && lr < A.rows;
+        i = in ? frame_row(A, lr) : 0;
+        return in;
+    };
+    int j, lr, i;
+    bool inside = pixel(j, lr, i);
+
+    // _ray_grid (render.py:332-337): exact op order, no contraction
+    const double xs = __dsub_rn(__dmul_rn(__ddiv_rn((double)j, (double)A.width), 2.0), 1.0);
+    const double ys = __dsub_rn(1.0, __dmul_rn(__ddiv_rn((double)i, (double)A.height), 2.0));
+    const double px = __dmul_rn(xs, A.tan_x), py = __dmul_rn(ys, A.tan_y);
+    double d[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) d[a] = __dadd_rn(__dadd_rn(A.f[a], __dmul_rn(px, A.r[a])), __dmul_rn(py, A.u[a]));
+    const double nrm =
+        __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])), __dmul_rn(d[2], d[2])));
+#pragma unroll
+    for (int a = 0; a < 3; a++) d[a] = __ddiv_rn(d[a], nrm);
+    // _ray_box_span (render.py:340-354)
+    double te = -INFINITY, tx = INFINITY;
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        const double inv = __drcp_rn(d[a]);
+        const double ta = __dmul_rn(__dsub_rn(-1.0, A.origin[a]), inv);
+        const double tb = __dmul_rn(__dsub_rn(1.0, A.origin[a]), inv);
+        double lo = fmin(ta, tb), hi = fmax(ta, tb);
+        if (isnan(lo)) lo = -INFINITY;
+        if (isnan(hi)) hi = INFINITY;
+        te = fmax(te, lo);
+        tx = fmin(tx, hi);
+    }
+    te = fmax(te, A.near_);
+    const bool active = inside && te < tx;
+#pragma unroll
+    for (int a = 0; a < 3; a++) R.d[a] = d[a];
+    R.te = te;
+
+    C.vdir = make_float4((float)d[0], (float)d[1], (float)d[2], 0.f);
+    C.ns64 = C.nexact = C.ncell = 0;
+    March M;
+    M.k = 0;
+    F.kend = 0;
+    M.C0 = M.C1 = M.C2 = M.Aacc = 0.f;
+    M.nshade = 0;
+    M.h = 1469598103934665603ULL;
+    M.own = -1;
+
+    if (active) {
+        // alive samples: t_k = te + (k + 0.5) sd < tx, a prefix of k (render.py:423)
+        auto tk = [&](int64_t k) { return __dadd_rn(te, __dmul_rn((double)k + 0.5, A.sd)); };
+        int64_t ke = (int64_t)fmax(ceil((tx - te) / A.sd - 0.5), 0.0);
+        while (ke > 0 && !(tk(ke - 1) < tx)) --ke;
+        while (tk(ke) < tx) ++ke;
+        F.kend = (int32_t)min(ke, (int64_t)INT32_MAX);
+        const bool k24 = ke < (1 << 24);  // the float32 sample offset dk needs k < 2^24
+        int32_t seg_end = 0;              // next sample that needs the exact geometry (or kend)
+        F.cur_own = -1;
+        F.slot = -1;
+        F.deg = 0;
+        BlockFast &b = F.b;
+        bool fast = false;
+        FastCell<P> G;
+        G.key = -1;
+        G.cx = G.cy = G.cz = -1e30f;
+        G.inner = 0;
+        float dk = 0.f;  // M.k - (sample at which tq0 was taken), exact below 2^24
+        for (;;) {
+            if (M.k >= seg_end) {  // rare: exact finest cell, owner change, end of ray
+                if (M.k >= vld(F.kend)) break;
+                double p[3];
+                ++C.ncell;
+                int32_t own, knext;
+                exact_geometry(A, R, own_grid, M.k, vld(F.kend), p, own, knext);
+                seg_end = knext;
+                M.own = own;
+                if (own < 0) break;  // render.py:430-436 (reported after the loop)
+                if (own != vld(F.cur_own)) {
+                    F.cur_own = own;
+                    const int32_t slot = __ldg(idx2slot + own);
+                    F.slot = slot;
+                    const BlockDesc *dp = descs + slot;
+                    b.ctrl4 = (const float4 *)__ldg((const unsigned long long *)&dp->ctrl4);
+                    C.tab32 = (const float *)__ldg((const unsigned long long *)&dp->tab32);
+                    b.ncp = __ldg(&dp->ncp);
+                    b.nspan = __ldg(&dp->nspan);
+                    b.plane = b.ncp * b.ncp;
+                    b.nint = (uint32_t)max(b.nspan - 2 * P + 2, 0);
+                    G.key = -1;
+                    G.cx = G.cy = G.cz = -1e30f;
+                    const int32_t deg = __ldg(&dp->deg);
+                    F.deg = deg;
+                    const uint32_t flags = __ldg(&dp->flags);
+                    fast = deg == P && (flags & kFlagUniform) && !(flags & AFAM_SLOT_FP64) &&
+                           (deg > 1 || b.nspan <= 128) && k24 && !(A.flags & kRenderForceExact);
+                    // span-coordinate prediction from the exact entry position
+#pragma unroll
+                    for (int a = 0; a < 3; a++) {
+                        const double sc = __ldg(&dp->inv_span[a]) * (double)b.nspan;
+                        M.tq0[a] = (float)((p[a] - __ldg(&dp->lo[a])) * sc);
+                        M.dtq[a] = (float)(A.sd * R.d[a] * sc);
+                    }
+                    C.ginv = make_float4(__ldg(&dp->inv_span_f[0]), __ldg(&dp->inv_span_f[1]),
+                                         __ldg(&dp->inv_span_f[2]), 0.f);
+                    dk = 0.f;
+                }
+            }
+            if (DEBUG) M.h = (M.h ^ (uint64_t)(uint32_t)vld(F.cur_own)) * 1099511628211ULL;
+            bool ok = false;
+            if (fast) {
+                const float tqx = fmaf(dk, M.dtq[0], M.tq0[0]);
+                const float tqy = fmaf(dk, M.dtq[1], M.tq0[1]);
+                const float tqz = fmaf(dk, M.dtq[2], M.tq0[2]);
+                ok = sample_fast2<P>(A, tf, b, tqx, tqy, tqz, C, G, M);
+            }
+            if (!ok) {
+                const int32_t slot = vld(F.slot), deg = vld(F.deg);
+                const BlockDesc *dpx = descs + slot;
+                int f64;
+                if (deg == 3) f64 = sample_exact<3>(GA, &tf, &R, dpx, slot, M.k);
+                else if (deg == 2) f64 = sample_exact<2>(GA, &tf, &R, dpx, slot, M.k);
+                else f64 = sample_exact<1>(GA, &tf, &R, dpx, slot, M.k);
+                C.ns64 += f64;
+                ++C.nexact;
+                const float4 tfv = R.tfv;
+                if (tfv.w > 0.f) {
+                    ++M.nshade;
+                    const float g[3] = {R.g[0], R.g[1], R.g[2]};
+                    composite(A, C.vdir, tfv, g, M);
+                }
+            }
+            // render.py:423 alive test before the next sample
+            ++M.k;
+            dk += 1.f;
+            if (!(M.Aacc <= A.o_max_f)) break;
+        }
+    }
+    const uint32_t ns = (uint32_t)M.k;
+    M.kend = F.kend;
+    inside = pixel(j, lr, i);
+    const int lane = threadIdx.x & 31;
+    if (inside) {
+        // render.py:458-461 quantise (round half to even)
+        uchar4 px4;
+        px4.x = (unsigned char)min(max(__float2int_rn(M.C0 * 255.f), 0), 255);
+        px4.y = (unsigned char)min(max(__float2int_rn(M.C1 * 255.f), 0), 255);
+        px4.z = (unsigned char)min(max(__float2int_rn(M.C2 * 255.f), 0), 255);
+        px4.w = (unsigned char)min(max(__float2int_rn(M.Aacc * 255.f), 0), 255);
+        const int64_t local = (int64_t)lr * A.width + j;
+        const int64_t dst = (A.flags & AFAM_RENDER_FULL_FRAME) ? (int64_t)i * A.width + j : local;
+        reinterpret_cast<uchar4 *>(rgba)[dst] = px4;
+        if (DEBUG) {
+            nsamp[local] = (int32_t)ns;
+            ohash[local] = M.h;
+        }
+    }
+    const uint32_t wsum = __reduce_add_sync(0xffffffffu, ns);
+    const uint32_t wsum64 = __reduce_add_sync(0xffffffffu, C.ns64);
+    const uint32_t wshade = __reduce_add_sync(0xffffffffu, M.nshade);
+    const uint32_t wexact = __reduce_add_sync(0xffffffffu, C.nexact);
+    const uint32_t wcell = __reduce_add_sync(0xffffffffu, C.ncell);
+    int64_t wmiss = M.own < 0 && M.k < M.kend ? ((int64_t)M.k << 32) | ((int64_t)i * A.width + j) : INT64_MAX;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const int64_t other = __shfl_xor_sync(0xffffffffu, wmiss, o);
+        wmiss = other < wmiss ? other : wmiss;
+    }
+    if (lane == 0) {
+        if (wsum) atomicAdd((unsigned long long *)&stats->samples, (unsigned long long)wsum);
+        if (wsum64) atomicAdd((unsigned long long *)&stats->fp64_samples, (unsigned long long)wsum64);
+        if (wshade) atomicAdd((unsigned long long *)&stats->shaded_samples, (unsigned long long)wshade);
+        if (wexact) atomicAdd((unsigned long long *)&stats->exact_samples, (unsigned long long)wexact);
+        if (wcell) atomicAdd((unsigned long long *)&stats->exact_cells, (unsigned long long)wcell);
+        if (wmiss != INT64_MAX) atomicMin((long long *)&stats->missing_key, (long long)wmiss);
+    }
+}
+
 __global__ void init_stats_kernel(afam_render_stats *s) {
     s->samples = 0;
     s->fp64_samples = 0;
@@ -1162,6 +1576,32 @@ static void build_tf_table(const afam_frame *F, TfTable &T) {
         }
         T.val[j] = make_float4(v[0], v[1], v[2], v[3]);
         T.slope[j] = make_float4(s[0], s[1], s[2], s[3]);
+    }
+    // Opacity support: below the breakpoint preceding the first nonzero
+    // opacity point (and above the one following the last) every breakpoint
+    // value and slope of the opacity channel is 0, and so is every clean
+    // bucket line there, so alpha_tf is exactly 0 for v <= op_lo and
+    // v >= op_hi (float32, the kernel's comparisons); buckets straddling
+    // them hold a breakpoint and take the exact segment search.
+    {
+        const int n = F->nopacity;
+        int k1 = -1, k2 = -1;
+        for (int k = 0; k < n; k++)
+            if (F->opacity[k][1] != 0.0) {
+                if (k1 < 0) k1 = k;
+                k2 = k;
+            }
+        const float inf = std::numeric_limits<float>::infinity();
+        if (k1 < 0) {  // fully transparent TF
+            T.op_lo = inf;
+            T.op_hi = -inf;
+        } else {
+            T.op_lo = k1 > 0 && (float)F->opacity[k1][0] > (float)F->opacity[k1 - 1][0] ? (float)F->opacity[k1 - 1][0]
+                                                                                       : -inf;
+            T.op_hi = k2 + 1 < n && (float)F->opacity[k2 + 1][0] > (float)F->opacity[k2][0]
+                          ? (float)F->opacity[k2 + 1][0]
+                          : inf;
+        }
     }
     const double lo = F->domain_lo, hi = F->domain_hi;
     const bool ok = hi > lo;
@@ -1282,11 +1722,53 @@ static void launch_render_v(const LaunchArgs &L, const RenderArgs &A) {
                                                                         L.rgba, L.stats, L.nsamp, L.ohash);
 }
 
+template <bool DEBUG, bool SMEM, int P, int MINB>
+static void launch_render2_v(const LaunchArgs &L, const RenderArgs &A) {
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(render2_kernel<DEBUG, SMEM, P, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             64 * 1024);
+        configured = true;
+    }
+    render2_kernel<DEBUG, SMEM, P, MINB><<<L.grid, 128, L.smem, L.st>>>(L.descs, L.owner, L.idx, A, L.gargs, L.gtf,
+                                                                         L.rgba, L.stats, L.nsamp, L.ohash);
+}
+
+// AFAM_RENDER_V1=1: the round-1 sample loop (render_kernel) for spline
+// blocks, for A/B checks of render2_kernel.
+static bool render_v1() {
+    static const bool v = [] {
+        const char *e = getenv("AFAM_RENDER_V1");
+        return e && atoi(e) != 0;
+    }();
+    return v;
+}
+
+// CTAs per SM of render2_kernel's cubic instantiation (AFAM_RENDER2_MINB=3|4|5 A/B).
+static int render2_minb() {
+    static int v = [] {
+        const char *e = getenv("AFAM_RENDER2_MINB");
+        const int m = e ? atoi(e) : 0;
+        return (m == 4 || m == 5) ? m : 3;
+    }();
+    return v;
+}
+
 // fd: the degree the fast path is compiled for (blocks of other degrees take
 // the exact path); debug and non-shared-grid launches use the default bounds.
 template <bool DEBUG, bool SMEM>
 static void launch_render(const LaunchArgs &L, const RenderArgs &A, int fd) {
     if (fd == 0) return launch_render_v<DEBUG, SMEM, 0, 4>(L, A);  // DS blocks
+    if (!render_v1()) {
+        if (fd == 1) return launch_render2_v<DEBUG, SMEM, 1, 4>(L, A);
+        if (fd == 2) return launch_render2_v<DEBUG, SMEM, 2, 4>(L, A);
+        if (DEBUG || !SMEM) return launch_render2_v<DEBUG, SMEM, 3, 3>(L, A);
+        switch (render2_minb()) {
+            case 4: return launch_render2_v<DEBUG, SMEM, 3, 4>(L, A);
+            case 5: return launch_render2_v<DEBUG, SMEM, 3, 5>(L, A);
+            default: return launch_render2_v<DEBUG, SMEM, 3, 3>(L, A);
+        }
+    }
     if (fd == 1) return launch_render_v<DEBUG, SMEM, 1, 4>(L, A);
     if (fd == 2) {
         if (!DEBUG && SMEM && render_minb2() == 3) return launch_render_v<DEBUG, SMEM, 2, 3>(L, A);
@@ -1385,6 +1867,8 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
         A.o_max_f = of;
     }
     A.flags = F->flags & (AFAM_RENDER_DEBUG | AFAM_RENDER_FULL_FRAME);
+    A.tf_lo = 0.f;  // set from the TF table below
+    A.tf_scale = 0.f;
     {
         static const bool force_exact = [] {
             const char *e = getenv("AFAM_RENDER_FORCE_EXACT");
@@ -1423,6 +1907,10 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
         tfc.valid = true;
     }
     const TfTable &tf = tfc.table;
+    A.tf_lo = tf.lo;
+    A.tf_scale = tf.scale;
+    A.op_lo = tf.op_lo;
+    A.op_hi = tf.op_hi;
     ht.mark();
 
     std::vector<int16_t> grid;
