@@ -664,6 +664,25 @@ __device__ __forceinline__ float4 tf_color(const TfTable &T, float v, int bi, fl
 }
 
 // Shading and compositing of one sample (render.py:383-395, :451-455).
+// MUFU approximations without the denormal-range fix-ups rsqrtf/exp2f add:
+// gn2 > 1e-24 is always normal, and ndotl^shininess below 2^-126 only ever
+// adds < 1e-38 to a colour that is quantised to 1/255.
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float lg2_ftz(float x) {
+    float r;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float ex2_ftz(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 __device__ __forceinline__ void composite(const RenderArgs &A, const float4 vdir, float4 tfv, const float (&g)[3],
                                           March &M) {
     const float atf = tfv.w;
@@ -671,12 +690,12 @@ __device__ __forceinline__ void composite(const RenderArgs &A, const float4 vdir
     const float gn2 = fmaf(g[2], g[2], fmaf(g[1], g[1], g[0] * g[0]));
     float ndotl = 0.f;
     if (gn2 > 1e-24f) {
-        const float ig = rsqrtf(gn2);
+        const float ig = rsqrt_ftz(gn2);
         ndotl = fabsf(g[0] * vdir.x + g[1] * vdir.y + g[2] * vdir.z) * ig;
     }
     const float dif = A.diffuse * ndotl;
     // ndotl**shininess via exp2(shininess * log2(ndotl)) (MUFU.LG2 + MUFU.EX2)
-    const float spec = A.specular * (ndotl > 0.f ? exp2f(A.shininess * __log2f(ndotl))
+    const float spec = A.specular * (ndotl > 0.f ? ex2_ftz(A.shininess * lg2_ftz(ndotl))
                                                  : (A.shininess == 0.f ? 1.f : 0.f));
     const float lit = A.ambient + dif;
     const float w = (1.f - M.Aacc) * as;
@@ -1262,14 +1281,25 @@ __device__ __forceinline__ bool sample_fast2(const RenderArgs &A, const TfTable 
             Yhi[cz] = fma2s(Ny[by], hi2(G.c[cz * Q + by]), Yhi[cz]);
         }
     }
-    Zlo = mul2s(Nz[0], Ylo[0]);
-    Zhi = mul2s(Nz[0], Yhi[0]);
+    if constexpr (P == 3) {  // pairwise trees: depth 3 instead of 4-long chains
+        Zlo = __fadd2_rn(fma2s(Nz[1], Ylo[1], mul2s(Nz[0], Ylo[0])), fma2s(Nz[3], Ylo[3], mul2s(Nz[2], Ylo[2])));
+        Zhi = __fadd2_rn(fma2s(Nz[1], Yhi[1], mul2s(Nz[0], Yhi[0])), fma2s(Nz[3], Yhi[3], mul2s(Nz[2], Yhi[2])));
+    } else {
+        Zlo = mul2s(Nz[0], Ylo[0]);
+        Zhi = mul2s(Nz[0], Yhi[0]);
 #pragma unroll
-    for (int cz = 1; cz < Q; cz++) {
-        Zlo = fma2s(Nz[cz], Ylo[cz], Zlo);
-        Zhi = fma2s(Nz[cz], Yhi[cz], Zhi);
+        for (int cz = 1; cz < Q; cz++) {
+            Zlo = fma2s(Nz[cz], Ylo[cz], Zlo);
+            Zhi = fma2s(Nz[cz], Yhi[cz], Zhi);
+        }
     }
-    const float v = dot_x<P>(Nx, Zlo, Zhi);
+    float v;
+    if constexpr (P == 3) {
+        const float2 t = __ffma2_rn(Zhi, make_float2(Nx[2], Nx[3]), __fmul2_rn(Zlo, make_float2(Nx[0], Nx[1])));
+        v = t.x + t.y;
+    } else {
+        v = dot_x<P>(Nx, Zlo, Zhi);
+    }
     int bi;
     float bf;
     const float vc = fminf(fmaxf(v, A.dom_lo), A.dom_hi);
