@@ -63,6 +63,10 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="config3", choices=["config3", "config2", "config5"],
+                    help="the headline workload; the default config-3 line also carries config 2 and config 5 "
+                         "under 'workloads' (unless --no-extra)")
+    ap.add_argument("--no-extra", action="store_true", help="config 3 only (no config-2 / config-5 lines)")
     ap.add_argument("--gather", default="fused", choices=["fused", "nccl"],
                     help="N > 1: band gather fused into the render kernel (peer stores) or an NCCL gather")
     return ap.parse_args()
@@ -374,8 +378,48 @@ def run_ours(args, rank, world, local_rank):
     if peer is not None:
         dist.barrier()
         peer.close()
-    del resident_all, ds
+    del flush
+    # -- the other BASELINE configs on the same box (own metric, value and roofline each)
+    if not args.no_extra:
+        result["workloads"] = {
+            "config5": run_config5(ds, resident_all, man, blobs, rank, world, dev, max(3, args.steps // 4),
+                                   args.warmup),
+        }
+        del resident_all, ds
+        torch.cuda.empty_cache()
+        result["workloads"]["config2"] = run_config2(rank, world, dev, args.steps, args.warmup, fma_peak)
+    else:
+        del resident_all, ds
     return result, man, blobs
+
+
+def run_headline(args, rank, world, local_rank):
+    """--workload config5 / config2: that config's line (value, roofline, e2e)."""
+    import torch
+
+    from paper_2409_00184_b200.device import DeviceStore
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    with ClockSampler(local_rank) as clk:
+        time.sleep(1.0)
+        if args.workload == "config5":
+            man, blobs, _ = build_model(pinned=True) if world == 1 else build_model_distributed(rank, dev)
+            ds = DeviceStore(len(blobs) + 1, 65, device=local_rank)
+            resident_all = {a: ds.load_mfa(b, man.entries[a].ncp, man.entries[a].extent, a.lod)
+                            for a, b in blobs.items()}
+            torch.cuda.synchronize(dev)
+            res = run_config5(ds, resident_all, man, blobs, rank, world, dev, args.steps, args.warmup,
+                              e2e=not args.no_e2e)
+            res["dtype"] = "f32 (f64 on ill-conditioned blocks)"
+        else:
+            res = run_config2(rank, world, dev, args.steps, args.warmup, measure_fma_peak(dev),
+                              e2e=not args.no_e2e and rank == 0)
+            res["dtype"] = "f32 + f64 (ill-conditioned ncp 64/65 blocks decode in float64)"
+    res.update({"warmup": args.warmup, "vs_baseline": None, "data": "synthetic (see config.workload)",
+                "clocks": clk.summary(), "gpu_launches": None})
+    res["gpu_launches"] = args.steps if args.workload == "config5" else 3 * args.steps
+    return res
 
 
 def run_e2e(args, man, blobs, povs, tf, params, rank, world, local_rank):
@@ -469,6 +513,294 @@ def run_e2e(args, man, blobs, povs, tf, params, rank, world, local_rank):
             "prefetch_models_loaded": agg["prefetch_models_loaded"]}
 
 
+# ------------------------------------------------------------------ config 5 / config 2
+def measured_peaks():
+    """(HBM GB/s, source) from MEASURED_PEAKS.json (driver-written), else the
+    profiling guide's fallback."""
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        return float(json.loads(p.read_text())["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)"
+
+
+def measure_dfma_peak(dev):
+    """FP64 FMA peak of this GPU (afam_bench_dfma)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2409_00184_b200 import _lib
+
+    out = torch.empty(148 * 8 * 256, dtype=torch.float64, device=dev)
+    s = torch.cuda.current_stream(dev)
+    flops = C.c_double()
+    best = 0.0
+    for _ in range(3):
+        ms = C.c_float()
+        _lib.check(_lib.lib().afam_bench_dfma(C.c_void_p(out.data_ptr()), 512, C.byref(ms), C.byref(flops),
+                                              C.c_void_p(s.cuda_stream)))
+        best = max(best, flops.value / (ms.value * 1e-3))
+    return best / 1e12
+
+
+C5_METRIC = "decoded samples/s (decode_grid 65^3 of all 4,680 blocks, config 5)"
+
+
+def run_config5(ds, resident_all, man, blobs, rank, world, dev, steps, warmup, e2e=False):
+    """BASELINE config 5: decode_grid((65,)*3) of every block of the config-3
+    model (model.py:89-93 -> bspline.py:162-172), blocks round-robin over the
+    ranks (block i on rank i % N: no exchange, the decoded
+    grids stay on their rank).  One step = one afam_decode_grid launch over
+    this rank's blocks; inputs (2.9 GB of control points) and outputs (5.1 GB
+    at N = 1) exceed L2, so no flush is needed.  value = all ranks' samples /
+    the max over ranks of the summed device time."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2409_00184_b200 import _lib
+
+    m = 65
+    addrs = sorted(resident_all)[rank::world]
+    slots = np.array([resident_all[a].slot for a in addrs], dtype=np.int32)
+    ncps = np.array([resident_all[a].ncp for a in addrs], dtype=np.int64)
+    out = torch.empty(len(slots) * m ** 3, dtype=torch.float32, device=dev)
+    st = torch.cuda.current_stream(dev)
+    lib = _lib.lib()
+
+    def launch():
+        _lib.check(lib.afam_decode_grid(ds.handle, slots.ctypes.data_as(C.c_void_p), len(slots), m,
+                                        C.c_void_p(out.data_ptr()), C.c_void_p(st.cuda_stream)))
+
+    for _ in range(warmup):
+        launch()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for e0, e1 in evs:
+        e0.record(st)
+        launch()
+        e1.record(st)
+    torch.cuda.synchronize(dev)
+    ms = [e0.elapsed_time(e1) for e0, e1 in evs]
+    t = torch.tensor([sum(ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_blocks = len(resident_all)
+    value = total_blocks * m ** 3 * steps / (float(t[0]) / 1e3)
+    nbytes = float((4 * ncps ** 3).sum() + 4 * m ** 3 * len(slots))  # this rank's algorithmic bytes per launch
+    hbm, src = measured_peaks()
+    achieved = nbytes / (float(np.mean(ms)) * 1e-3) / 1e9
+    res = {"metric": C5_METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+           "ms_per_step": float(t[0]) / steps, "higher_is_better": True, "scaling": "strong",
+           "config": {"workload": "config5: decode_grid((65,65,65)) of all 4,680 blocks of the config-3 model "
+                                  "(ncp hash-assigned in 40-65, degree 3), float32 out",
+                      "parallelism": f"blocks round-robin over {world} rank(s), no collective",
+                      "blocks_per_rank": len(slots), "l2": "inputs and outputs exceed L2 (2.9 GB in, 5.1 GB out)"},
+           "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                        "frac": achieved / hbm, "traffic": None, "kernel": "decode_grid_kernel (K3)",
+                        "note": "algorithmic bytes = 4 ncp^3 (control points read) + 4 m^3 (grid written) per "
+                                f"block, this rank's blocks per launch; peak = {src}"}}
+    if e2e:
+        res["e2e"] = config5_e2e(man, blobs, addrs, rank, world, dev, steps)
+    del out
+    return res
+
+
+def config5_e2e(man, blobs, addrs, rank, world, dev, steps):
+    """Config 5 through the C-ABI with host buffers: every step copies this
+    rank's .mfa images from pinned host memory (afam_store_put_mfa: H2D +
+    realignment on the device), decodes them, and reads the 65^3 grids back
+    into pinned host memory; max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2409_00184_b200 import _lib
+    from paper_2409_00184_b200.device import DeviceStore
+    import ctypes as C
+
+    m = 65
+    chunk = 256  # blocks per upload/decode round (device slots reused)
+    ds = DeviceStore(chunk, 65, device=dev.index)
+    slots = np.array([ds.alloc() for _ in range(chunk)], dtype=np.int32)
+    dout = torch.empty(chunk * m ** 3, dtype=torch.float32, device=dev)
+    hout = torch.empty(chunk * m ** 3, dtype=torch.float32, pin_memory=True)
+    st = torch.cuda.current_stream(dev)
+    lib = _lib.lib()
+
+    def one_pass():
+        h2d = 0
+        for c0 in range(0, len(addrs), chunk):
+            part = addrs[c0:c0 + chunk]
+            for i, a in enumerate(part):
+                ds.put_mfa(int(slots[i]), blobs[a], man.entries[a].ncp, man.entries[a].extent, stream=st)
+                h2d += len(blobs[a])
+            _lib.check(lib.afam_decode_grid(ds.handle, slots.ctypes.data_as(C.c_void_p), len(part), m,
+                                            C.c_void_p(dout.data_ptr()), C.c_void_p(st.cuda_stream)))
+            n = len(part) * m ** 3
+            hout[:n].copy_(dout[:n], non_blocking=True)
+        st.synchronize()
+        return h2d
+
+    one_pass()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    nst = max(1, min(steps, 3))
+    h2d = 0
+    for _ in range(nst):
+        h2d += one_pass()
+    el = time.perf_counter() - t0
+    t = torch.tensor([el], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total = len(man.entries) * m ** 3 * nst
+    return {"value": total / float(t[0]), "unit": UNIT, "h2d_bytes_per_step": h2d / nst,
+            "d2h_bytes_per_step": 4 * m ** 3 * len(addrs), "steps": nst,
+            "api": "afam_store_put_mfa (pinned .mfa images -> device slots) + afam_decode_grid + D2H of the grids, "
+                   f"{chunk}-block rounds, wall clock with a stream sync per step"}
+
+
+C2_METRIC = "decoded samples/s (512^2 ray-cast, config 2)"
+C2_VIEWS = [(0.6, 0.5, 1.2), (2.0, 1.6, 2.6)]
+
+
+def build_config2():
+    from paper_2409_00184_b200 import encoder, synth
+
+    t0 = time.time()
+    vol = synth.ml_volume((257, 257, 257))
+    man, models, _ = encoder.encode_volume(vol, levels=2, micro_dims=65, degree=3, error_bound=1e-3, coarsest=2,
+                                           mode="adaptive")
+    return man, models, time.time() - t0
+
+
+def run_config2(rank, world, dev, steps, warmup, fma_peak, e2e=False):
+    """BASELINE config 2: the 257^3 Marschner-Lobb volume encoded adaptively
+    (2 LODs, micro 65, degree 3, error bound 1e-3) by the B200 encoder
+    (pinned to the reference encoder's decisions, tests/golden/config2.npz),
+    512^2 frames at sd 1e-3 alternating between SURVEY.md 8d's two views:
+    (0.6, 0.5, 1.2) shows LODs 1 + 2, the three-quarter view (2.0, 1.6, 2.6)
+    only LOD-2 blocks, all of them ill-conditioned (ncp 64/65, decoded on the
+    float64 path).  N > 1: interleaved 8-row bands per rank, bands stay on
+    their rank (no gather)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2409_00184_b200 import render
+    from paper_2409_00184_b200.device import DeviceStore
+
+    man, models, enc_s = build_config2()
+    params = render.RenderParams(width=512, height=512, sample_distance=1e-3)
+    tf = render.TransferFunction.ml_preset()
+    ds = DeviceStore(len(models), 65, device=dev.index)
+    resident = {a: ds.load_model(mm) for a, mm in models.items()}
+    nfp64 = sum(ds.info(b.slot)["fp64"] for b in resident.values())
+    povs = [render.PointOfView(np.asarray(p), -np.asarray(p), [0.0, 1.0, 0.0]) for p in C2_VIEWS]
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    out = torch.empty((render._lib.lib().afam_frame_rows(512, 8, world, rank), 512, 4), dtype=torch.uint8,
+                      device=dev)
+
+    def frame(k):
+        pov = povs[k % 2]
+        vis = render.select_visible(pov, man, params.aspect)
+        _, info, _ = render.render_part(pov, {a: resident[a] for a in vis}, tf, params, band_rows=8, nparts=world,
+                                        part=rank, device=dev.index, out=out)
+        return info
+
+    for k in range(warmup):
+        frame(k)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    kms, samples, s64, shaded, shaded64 = [], 0, 0, 0, 0
+    for k in range(steps):
+        flush.zero_()
+        info = frame(warmup + k)
+        kms.append(info["kernel_ms"])
+        samples += info["samples"]
+        s64 += info["fp64_samples"]
+        shaded += info["shaded_samples"]
+    tot = torch.tensor([samples, s64, sum(kms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        t = tot[2:].clone()
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot[2] = t[0]
+    value = float(tot[0]) / (float(tot[2]) / 1e3)
+    dfma = measure_dfma_peak(dev)
+    # roofline: time the FMA pipes would need for the algorithmic FLOP (value
+    # contraction for every sample, + the gradient for shaded ones), float64
+    # samples at the FP64 peak and the rest at the FP32 peak, over the
+    # measured kernel time (shaded fraction applied uniformly to both kinds)
+    f64frac = s64 / max(1, samples)
+    flop = samples * FLOP_VALUE_P3 + shaded * (FLOP_PER_SAMPLE_P3 - FLOP_VALUE_P3)
+    t_ideal = flop * f64frac / (dfma * 1e12) + flop * (1 - f64frac) / (fma_peak * 1e12)
+    t_meas = sum(kms) / 1e3
+    res = {"metric": C2_METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+           "ms_per_step": float(tot[2]) / steps, "higher_is_better": True, "scaling": "strong",
+           "config": {"workload": "config2: 257^3 Marschner-Lobb, encoded adaptively by the B200 encoder "
+                                  "(levels 2, micro 65, degree 3, error bound 1e-3; reference decisions), 512x512 "
+                                  "ray-cast, sd 1e-3, o_max 0.99, ML TF + shading, views (0.6,0.5,1.2) / "
+                                  "(2.0,1.6,2.6) alternating",
+                      "blocks": len(models), "fp64_slots": int(nfp64), "encode_s": round(enc_s, 1),
+                      "fp64_sample_frac": float(tot[1]) / max(1.0, float(tot[0])),
+                      "parallelism": f"image bands x{world} (bands stay on their rank)",
+                      "l2": "flushed between steps (512 MiB write outside the per-step events)"},
+           "roofline": {"bound": "fp64+fp32", "achieved": flop / t_meas / 1e12, "peak": dfma, "unit": "TFLOP/s",
+                        "frac": t_ideal / t_meas, "traffic": None, "kernel": "render kernels (K2, float64 path)",
+                        "note": f"frac = (float64 samples' algorithmic FLOP at the measured FP64 FMA peak {dfma:.1f} "
+                                f"TFLOP/s + float32 samples' at the FP32 peak {fma_peak:.1f}) / kernel time; "
+                                "FLOP per sample as config 3 (168 value + 216 gradient when shaded)"}}
+    if e2e:
+        res["e2e"] = config2_e2e(man, models, povs, tf, params, rank, world, dev, steps)
+    return res
+
+
+def config2_e2e(man, models, povs, tf, params, rank, world, dev, steps):
+    """Config 2 through the public API with host models (the reference CLI's
+    call, cli.py:153-164): render.render(pov, {addr: MicroModel}, tf, params)
+    uploads the visible blocks (H2D + realignment on the device) and returns
+    the host Frame.  Every step gets fresh model objects (shallow copies made
+    before the timed region), so every step uploads its whole visible set.
+    Rank 0 only at N > 1 (render.render draws whole frames)."""
+    import copy
+
+    import torch
+
+    from paper_2409_00184_b200 import model as mmod
+    from paper_2409_00184_b200 import render
+
+    sets = []
+    for k in range(steps + 1):
+        pov = povs[k % 2]
+        vis = render.select_visible(pov, man, params.aspect)
+        sets.append((pov, {a: copy.copy(models[a]) for a in vis}))
+
+    def one(k):
+        pov, blocks = sets[k]
+        fr = render.render(pov, blocks, tf, params)
+        h2d = sum(mmod.serialized_size(b.ncp, b.degree) for b in blocks.values())
+        return render.render.last_stats["samples"], fr.rgba.nbytes, h2d
+
+    one(0)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    tot, d2h, h2d = 0, 0, 0
+    for k in range(1, steps + 1):
+        s, o, i = one(k)
+        tot += s
+        d2h += o
+        h2d += i
+    el = time.perf_counter() - t0
+    return {"value": tot / el, "unit": UNIT, "h2d_bytes_per_step": h2d / steps, "d2h_bytes_per_step": d2h / steps,
+            "steps": steps, "api": "render.render(pov, {addr: MicroModel}, tf, params) -> Frame (host RGBA8); "
+                                   "fresh host models every step, so every visible block is uploaded per frame"}
+
+
 # ------------------------------------------------------------------ CPU
 def cpu_frame(frame_index: int, size: int, threads: int, rows=None):
     """Render one orbit frame of the config-3 model with the float64 C
@@ -494,6 +826,43 @@ def cpu_frame(frame_index: int, size: int, threads: int, rows=None):
     return info["samples"], el, what
 
 
+def cpu_baseline_other(workload: str) -> dict:
+    """The oracle on the host cores for --workload config5 (decode_grid of a
+    sample of blocks, one block per thread) / config2 (a 64-row band of the
+    first view)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle, workload as wl
+
+    threads, model = host_cpu()
+    if workload == "config5":
+        man = wl.skeleton(4, 2, 65)
+        addrs = sorted(man.entries)[:: 4680 // (2 * threads)][: 2 * threads]
+        man, blobs = wl.turbulence_store(addrs=addrs)
+        ctrls = [wl.parse_mfa(blobs[a], man.entries[a].ncp, man.entries[a].extent, a.lod).control for a in addrs]
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(lambda c: oracle.decode_grid(c, 3, 65), ctrls))
+        el = time.perf_counter() - t0
+        return {"value": len(ctrls) * 65 ** 3 / el, "unit": UNIT, "cores": threads, "kind": "port", "cpu": model,
+                "sample": f"decode_grid((65,)*3) of {len(ctrls)} config-5 blocks in {el:.1f} s (oracle/ C float64, "
+                          f"one block per thread, {threads} threads, {model})"}
+    from paper_2409_00184_b200 import render
+
+    man, models, _ = build_config2()
+    p = np.asarray(C2_VIEWS[0])
+    pov = render.PointOfView(p, -p, [0.0, 1.0, 0.0])
+    params = render.RenderParams(width=512, height=512, sample_distance=1e-3)
+    vis = render.select_visible(pov, man, params.aspect)
+    t0 = time.perf_counter()
+    _, info = oracle.render(pov, {a: models[a] for a in vis}, render.TransferFunction.ml_preset(), params,
+                            rows=(224, 288), nthreads=threads)
+    el = time.perf_counter() - t0
+    return {"value": info["samples"] / el, "unit": UNIT, "cores": threads, "kind": "port", "cpu": model,
+            "sample": f"rows 224..288 of the (0.6,0.5,1.2) 512^2 frame: {info['samples']} samples in {el:.1f} s "
+                      f"(oracle/ C float64, OpenMP x{threads}, {model})"}
+
+
 def host_cpu() -> tuple:
     from oracle import workload
 
@@ -505,6 +874,17 @@ def run_reference(args):
     """The reference algorithm on the host CPU: whole 1024^2 frames of the
     config-3 orbit (the same frames as --impl ours: pose W + k), one frame
     per step, the float64 C restatement on every host thread."""
+    if args.workload == "config5":
+        cb = cpu_baseline_other("config5")
+        return {"metric": C5_METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": 0, "steps": 1,
+                "warmup": 0, "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (config-3 model)",
+                "config": {"workload": "config5: decode_grid((65,65,65)) of a sample of the 4,680 config-3 blocks"},
+                "impl": "reference", "cpu_baseline": cb,
+                "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if args.workload == "config2":
+        return {"impl": "reference", "unavailable": "config 2's encoded store comes from the B200 encoder; "
+                                                    "the reference arm is timed on config 3 / config 5"}
     threads, model = host_cpu()
     for k in range(min(args.warmup, 1)):
         cpu_frame(k, args.size, threads)
@@ -549,6 +929,16 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         else:
             dist.init_process_group(backend)
+    if args.workload != "config3":
+        res = run_headline(args, rank, world, local_rank)
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            res["cpu_baseline"] = cpu_baseline_other(args.workload)
+        if rank == 0:
+            print(json.dumps(res), flush=True)
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
     res, man, blobs = run_ours(args, rank, world, local_rank)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads, model = host_cpu()

@@ -297,6 +297,9 @@ int afam_owner_grid(afam_store *s, const int32_t *slots, int32_t nblocks, int32_
  * has no FP32 figure): independent FFMA chains on every SM; writes the
  * elapsed ms and the FLOPs executed.  out: device float[148*8*256]. */
 int afam_bench_fma(float *out, int32_t iters, float *ms, double *flops, void *stream);
+/* FP64 twin (the roofline denominator of the float64 decode path of
+ * ill-conditioned blocks).  out: device double[148*8*256]. */
+int afam_bench_dfma(double *out, int32_t iters, float *ms, double *flops, void *stream);
 
 #ifdef __cplusplus
 }

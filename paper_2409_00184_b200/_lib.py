@@ -119,6 +119,7 @@ SIGNATURES = [
     ("afam_owner_grid", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.c_void_p,
                                   C.c_int32]),
     ("afam_bench_fma", C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_float), C.POINTER(C.c_double), C.c_void_p]),
+    ("afam_bench_dfma", C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_float), C.POINTER(C.c_double), C.c_void_p]),
 ]
 
 

@@ -1,5 +1,6 @@
-// FP32 FMA throughput probe: the denominator of the K2 roofline (the ray
-// march is FMA-issue bound; MEASURED_PEAKS.json carries only
+// FP32 / FP64 FMA throughput probes: the denominators of the K2 rooflines
+// (the ray march is FMA-issue bound; the float64 path of
+// ill-conditioned blocks is FP64-bound; MEASURED_PEAKS.json carries only
 // HBM and bf16 tensor peaks).
 #include <algorithm>
 
@@ -7,18 +8,19 @@
 
 namespace afam {
 
-__global__ void __launch_bounds__(256) fma_probe_kernel(float *out, int iters) {
-    float a[8];
+template <typename T>
+__global__ void __launch_bounds__(256) fma_probe_kernel(T *out, int iters) {
+    T a[8];
 #pragma unroll
-    for (int k = 0; k < 8; k++) a[k] = threadIdx.x * 1e-3f + k;
-    const float b = 0.999999f, c = 1e-7f;
+    for (int k = 0; k < 8; k++) a[k] = threadIdx.x * T(1e-3) + k;
+    const T b = T(0.999999), c = T(1e-7);
     for (int i = 0; i < iters; i++) {
 #pragma unroll
         for (int r = 0; r < 16; r++)
 #pragma unroll
-            for (int k = 0; k < 8; k++) a[k] = fmaf(a[k], b, c);
+            for (int k = 0; k < 8; k++) a[k] = fma(a[k], b, c);
     }
-    float s = 0.f;
+    T s = 0;
 #pragma unroll
     for (int k = 0; k < 8; k++) s += a[k];
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
@@ -26,7 +28,8 @@ __global__ void __launch_bounds__(256) fma_probe_kernel(float *out, int iters) {
 
 }  // namespace afam
 
-extern "C" int afam_bench_fma(float *out, int32_t iters, float *ms, double *flops, void *stream) {
+template <typename T>
+static int bench_fma(T *out, int32_t iters, float *ms, double *flops, void *stream) {
     AFAM_CHECK(out && ms && flops && iters > 0, AFAM_E_VALUE, "bad afam_bench_fma arguments");
     cudaStream_t st = (cudaStream_t)stream;
     int dev = 0, sms = 148;
@@ -46,4 +49,12 @@ extern "C" int afam_bench_fma(float *out, int32_t iters, float *ms, double *flop
     cudaEventDestroy(e1);
     *flops = 2.0 * 16 * 8 * (double)iters * blocks * 256;
     return AFAM_OK;
+}
+
+extern "C" int afam_bench_fma(float *out, int32_t iters, float *ms, double *flops, void *stream) {
+    return bench_fma<float>(out, iters, ms, flops, stream);
+}
+
+extern "C" int afam_bench_dfma(double *out, int32_t iters, float *ms, double *flops, void *stream) {
+    return bench_fma<double>(out, iters, ms, flops, stream);
 }
