@@ -23,6 +23,8 @@ namespace afam {
 struct DecodeJob {
     int32_t slot;
     int32_t tc_kp;  // tensor-core path: K extent (ncp rounded up to 8); 0 = CUDA-core path
+    int32_t fx;     // 1: float32 slots take decode_fx_kernel (register-tiled, m == 65)
+    int32_t pad_;
     const int32_t *col0;
     const float *b32;
     const double *b64;
@@ -273,6 +275,7 @@ __global__ void __launch_bounds__(kDecodeThreads) decode_grid_kernel(const Block
     constexpr bool kF64 = sizeof(T) == 8;
     if (((d.flags & AFAM_SLOT_FP64) != 0) != kF64) return;
     if (!kF64 && jb.tc_kp > 0) return;  // decoded by decode_tc_kernel
+    if (!kF64 && jb.fx) return;         // decoded by decode_fx_kernel
     const int k0 = blockIdx.x * kDecodeChunk;
     const int k1 = min(m, k0 + kDecodeChunk);
     float *o = out + (size_t)blockIdx.y * m * m * m;
@@ -282,6 +285,215 @@ __global__ void __launch_bounds__(kDecodeThreads) decode_grid_kernel(const Block
         case 1: decode_planes<1, T>(d, jb.col0, b, m, k0, k1, o, smem); break;
         case 2: decode_planes<2, T>(d, jb.col0, b, m, k0, k1, o, smem); break;
         default: decode_planes<3, T>(d, jb.col0, b, m, k0, k1, o, smem); break;
+    }
+}
+
+
+// ---------------------------------------------------------------------------
+// Register-tiled grid decode (float32 slots, m == 65, ncp <= 65): the
+// default CUDA-core path.  One CTA per block, the control-point z-planes
+// streaming through a ring of kFxRing shared slots by TMA bulk copies;
+// per input plane zc, in one pass and with one CTA barrier:
+//   x stage: X[r][x] = sum_a Bx[x][a] C[zc][r][x0(x)+a] for every control row
+//     r and lattice column x < 64 -- thread (row set, x quad q) reads the
+//     12-float aligned window of its quad (3 LDS.128) and applies a dense
+//     4 x 12 weight block held in registers (zeros off the band), one
+//     16-byte store into the double-buffered X plane;
+//   y stage: Y[y][x] = sum_b By[y][b] X[y0(y)+b][x] -- thread (q, g) owns
+//     lattice rows y = 4g..4g+3 and columns x = q, q+16, q+32, q+48 (lanes
+//     read consecutive words: conflict-free), a dense 4 x 7 window of By in
+//     registers; the 16 results go into a register ring of the last 4 planes;
+//   z stage: every output plane k whose last support plane is zc
+//     (col0[k] + p == zc) is sum_c Bz[k][c] Y_{col0[k]+c}, read from the
+//     register ring, and stored (16 lanes write 16 consecutive x).
+// The lattice's last row/column (u = 1) selects the last control index
+// exactly (checked on the host), so X[.][64] is the control column ncp-1 and
+// Y[64][.] the X row ncp-1: threads 0..128 carry one such value each
+// (threads 0..15 also take the x stage's control row 64).  Control points are read once from HBM (TMA), the
+// output written once; x and y run out of registers and one X plane.
+constexpr int kFxThreads = 256;  // 8 warps: 16 x lanes x 16 row groups
+constexpr int kFxRing = 4;       // TMA plane slots
+constexpr int kFxXPitch = 68;    // X plane row pitch (floats)
+constexpr int kFxXRows = 72;     // X plane rows (the y windows over-read up to row ncp + 4, zeros)
+constexpr int kFxPad = 16;       // zero floats after each ring slot (x windows over-read the last row)
+
+
+template <int P>
+__device__ __forceinline__ void fx_decode_block(const BlockDesc &d, const int32_t *__restrict__ c0g,
+                                                const float *__restrict__ Bg, float *__restrict__ out,
+                                                unsigned char *smem) {
+    constexpr int Q = P + 1;
+    constexpr int M = 65;
+    const int n = d.ncp, pitch = d.pitch;
+    const int sstride = n * pitch + kFxPad;
+    float *ring = reinterpret_cast<float *>(smem);
+    float *xb = ring + kFxRing * sstride;
+    float *Bs = xb + 2 * kFxXRows * kFxXPitch;
+    int *c0 = reinterpret_cast<int *>(Bs + M * 4);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(c0 + 68);
+    const int tid = threadIdx.x;
+
+    for (int i = tid; i < M * 4; i += blockDim.x) Bs[i] = Bg[i];
+    for (int i = tid; i < M; i += blockDim.x) c0[i] = c0g[i];
+    for (int i = tid; i < kFxRing * kFxPad; i += blockDim.x)
+        ring[(i / kFxPad) * sstride + n * pitch + (i % kFxPad)] = 0.f;
+    for (int i = tid; i < 2 * (kFxXRows - n) * kFxXPitch; i += blockDim.x) {
+        const int b = i / ((kFxXRows - n) * kFxXPitch), o = i % ((kFxXRows - n) * kFxXPitch);
+        xb[b * kFxXRows * kFxXPitch + n * kFxXPitch + o] = 0.f;
+    }
+    if (tid == 0) {
+        for (int r = 0; r < kFxRing; r++) mbar_init(bar + r, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const float *__restrict__ C = d.ctrl;
+    const uint32_t plane_bytes = (uint32_t)((size_t)n * pitch * sizeof(float));
+    if (tid == 0) {
+        fence_proxy_async();
+        for (int z = 0; z < min(n, kFxRing); z++) {
+            mbar_arrive_expect_tx(bar + z, plane_bytes);
+            tma_load_1d(ring + (size_t)z * sstride, C + (size_t)z * n * pitch, plane_bytes, bar + z);
+        }
+    }
+
+    // x stage weights: quad q (lattice columns 4q..4q+3) over the aligned
+    // 12-float window starting at cw (dense, zeros off the band)
+    const int q = tid & 15, g = tid >> 4;
+    const int cw = c0[4 * q] & ~3;
+    float wx[4][12];
+#pragma unroll
+    for (int xi = 0; xi < 4; xi++) {
+        const int x = 4 * q + xi, off = c0[x] - cw;
+#pragma unroll
+        for (int e = 0; e < 12; e++) {
+            const int a = e - off;
+            wx[xi][e] = (a >= 0 && a < Q) ? Bs[x * 4 + a] : 0.f;
+        }
+    }
+    // y stage weights: rows 4g..4g+3 over the 7-row window starting at r0
+    const int r0 = c0[4 * g];
+    float wy[4][7];
+#pragma unroll
+    for (int yi = 0; yi < 4; yi++) {
+        const int y = 4 * g + yi, off = c0[y] - r0;
+#pragma unroll
+        for (int e = 0; e < 7; e++) {
+            const int b = e - off;
+            wy[yi][e] = (b >= 0 && b < Q) ? Bs[y * 4 + b] : 0.f;
+        }
+    }
+    float yr[4][4][4];  // [plane slot][yi][s]: Y of the last 4 planes, columns q + 16 s
+    float er[4];        // threads 0..128: the lattice column x = 64 / row y = 64 value of the last 4 planes
+    int knext = 0;
+
+    for (int z0 = 0; z0 < n; z0 += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int zc = z0 + u;
+            if (zc >= n) break;
+            mbar_wait(bar + u, (uint32_t)((zc >> 2) & 1));
+            const float *Cp = ring + u * sstride;
+            float *X = xb + (u & 1) * kFxXRows * kFxXPitch;
+            // ---- x stage (threads 0..15 also take control row 64)
+#pragma unroll
+            for (int i = 0; i < 5; i++) {
+                const int r = i < 4 ? g + 16 * i : 64;
+                if (r < n && (i < 4 || g == 0)) {
+                    const float4 *src = reinterpret_cast<const float4 *>(Cp + r * pitch + cw);
+                    const float4 v0 = src[0], v1 = src[1], v2 = src[2];
+                    const float w[12] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, v2.x, v2.y, v2.z, v2.w};
+                    float2 a01 = make_float2(0.f, 0.f), a23 = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int e = 0; e < 12; e++) {
+                        a01 = __ffma2_rn(make_float2(wx[0][e], wx[1][e]), make_float2(w[e], w[e]), a01);
+                        a23 = __ffma2_rn(make_float2(wx[2][e], wx[3][e]), make_float2(w[e], w[e]), a23);
+                    }
+                    *reinterpret_cast<float4 *>(X + r * kFxXPitch + 4 * q) = make_float4(a01.x, a01.y, a23.x, a23.y);
+                }
+            }
+            if (tid < n) X[tid * kFxXPitch + 64] = Cp[tid * pitch + n - 1];  // u = 1 column: control column n-1
+            __syncthreads();
+            if (tid == 0 && zc + kFxRing < n) {  // ring slot u is free: every thread passed its x stage
+                fence_proxy_async();
+                mbar_arrive_expect_tx(bar + u, plane_bytes);
+                tma_load_1d(ring + (size_t)u * sstride, C + (size_t)(zc + kFxRing) * n * pitch, plane_bytes, bar + u);
+            }
+            // ---- y stage (into the register ring)
+#pragma unroll
+            for (int yi = 0; yi < 4; yi++)
+#pragma unroll
+                for (int s = 0; s < 4; s++) yr[u][yi][s] = 0.f;
+#pragma unroll
+            for (int e = 0; e < 7; e++) {
+                const float *xr = X + (r0 + e) * kFxXPitch + q;
+                const float v[4] = {xr[0], xr[16], xr[32], xr[48]};
+#pragma unroll
+                for (int yi = 0; yi < 4; yi++) {
+                    float2 lo = make_float2(yr[u][yi][0], yr[u][yi][1]), hi = make_float2(yr[u][yi][2], yr[u][yi][3]);
+                    lo = __ffma2_rn(make_float2(wy[yi][e], wy[yi][e]), make_float2(v[0], v[1]), lo);
+                    hi = __ffma2_rn(make_float2(wy[yi][e], wy[yi][e]), make_float2(v[2], v[3]), hi);
+                    yr[u][yi][0] = lo.x; yr[u][yi][1] = lo.y; yr[u][yi][2] = hi.x; yr[u][yi][3] = hi.y;
+                }
+            }
+            // lattice column x = 64 (threads 0..64: y = tid) and row y = 64 (threads 65..128: x = tid - 65)
+            if (tid <= 64) {
+                float acc = 0.f;
+                if (tid == 64) {
+                    acc = X[(n - 1) * kFxXPitch + 64];
+                } else {
+#pragma unroll
+                    for (int b = 0; b < Q; b++) acc = fmaf(Bs[tid * 4 + b], X[(c0[tid] + b) * kFxXPitch + 64], acc);
+                }
+                er[u] = acc;
+            } else if (tid < 129) {
+                er[u] = X[(n - 1) * kFxXPitch + tid - 65];
+            }
+            // ---- z stage: output planes whose support ends at zc
+            while (knext < M && c0[knext] + P == zc) {
+                const int k = knext++;
+                float wz[Q];
+#pragma unroll
+                for (int c = 0; c < Q; c++) wz[c] = Bs[k * 4 + c];
+                float *ok = out + (size_t)k * M * M;
+#pragma unroll
+                for (int yi = 0; yi < 4; yi++) {
+                    float2 lo = make_float2(0.f, 0.f), hi = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int c = 0; c < Q; c++) {
+                        const int sl = (u - P + c) & 3;
+                        lo = __ffma2_rn(make_float2(wz[c], wz[c]), make_float2(yr[sl][yi][0], yr[sl][yi][1]), lo);
+                        hi = __ffma2_rn(make_float2(wz[c], wz[c]), make_float2(yr[sl][yi][2], yr[sl][yi][3]), hi);
+                    }
+                    float *orow = ok + (4 * g + yi) * M + q;
+                    orow[0] = lo.x;
+                    orow[16] = lo.y;
+                    orow[32] = hi.x;
+                    orow[48] = hi.y;
+                }
+                if (tid < 129) {
+                    float acc = 0.f;
+#pragma unroll
+                    for (int c = 0; c < Q; c++) acc = fmaf(wz[c], er[(u - P + c) & 3], acc);
+                    ok[tid <= 64 ? tid * M + 64 : 64 * M + tid - 65] = acc;
+                }
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kFxThreads, 1) decode_fx_kernel(const BlockDesc *__restrict__ descs,
+                                                                   const DecodeJob *__restrict__ jobs,
+                                                                   float *__restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const DecodeJob jb = jobs[blockIdx.x];
+    if (!jb.fx) return;
+    const BlockDesc d = descs[jb.slot];
+    if (d.flags & AFAM_SLOT_FP64) return;  // float64 slots: decode_grid_kernel<double>
+    float *o = out + (size_t)blockIdx.x * 65 * 65 * 65;
+    switch (d.deg) {
+        case 1: fx_decode_block<1>(d, jb.col0, jb.b32, o, smem); break;
+        case 2: fx_decode_block<2>(d, jb.col0, jb.b32, o, smem); break;
+        default: fx_decode_block<3>(d, jb.col0, jb.b32, o, smem); break;
     }
 }
 
@@ -600,6 +812,16 @@ static bool tc_default() {
     return v;
 }
 
+// AFAM_DECODE_FX=0: the banded smem-staged kernel for float32 slots instead
+// of the register-tiled one (A/B checks)
+static bool fx_disabled() {
+    static const bool v = [] {
+        const char *e = getenv("AFAM_DECODE_FX");
+        return e && atoi(e) == 0;
+    }();
+    return v;
+}
+
 static int get_op(afam_store *s, int ncp, int deg, int m, DecodeOp **op) {
     auto key = std::make_tuple(ncp, deg, m);
     auto it = s->ops.find(key);
@@ -639,6 +861,13 @@ static int get_op(afam_store *s, int ncp, int deg, int m, DecodeOp **op) {
                 o.tc_kp = kp;
             }
         }
+        {  // register-tiled decode: m == 65, deg + 1 <= ncp <= 65 (lattice steps advance the span by <= 1),
+           // the u = 1 row e_{ncp-1} in float32
+            bool ok = m == 65 && ncp <= 65 && ncp >= deg + 1 && c0[m - 1] + deg == ncp - 1 &&
+                      (float)b[(size_t)(m - 1) * 4 + deg] == 1.0f;
+            for (int a = 0; a < deg; a++) ok = ok && (float)b[(size_t)(m - 1) * 4 + a] == 0.0f;
+            o.fx_ok = ok;
+        }
         AFAM_CUDA(cudaMalloc(&o.b32, b32.size() * sizeof(float)));
         AFAM_CUDA(cudaMalloc(&o.b64, b.size() * sizeof(double)));
         AFAM_CUDA(cudaMalloc(&o.col0, c0.size() * sizeof(int32_t)));
@@ -671,7 +900,8 @@ extern "C" int afam_decode_grid_ex(afam_store *s, const int32_t *slots, int32_t 
     cudaStream_t st = (cudaStream_t)stream;
     AFAM_CUDA(cudaSetDevice(s->device));
     std::vector<DecodeJob> jobs(nblk);
-    int maxn = 0, ntc = 0, maxkp = 0, maxn_tc = 0;
+    int maxn = 0, ntc = 0, maxkp = 0, maxn_tc = 0, nfx = 0;
+    size_t maxfx = 0;  // largest ncp * pitch among the register-tiled jobs
     {
         std::lock_guard<std::mutex> lk(s->mu);
         for (int b = 0; b < nblk; b++) {
@@ -688,6 +918,12 @@ extern "C" int afam_decode_grid_ex(afam_store *s, const int32_t *slots, int32_t 
             jobs[b].b64 = op->b64;
             jobs[b].tc_b = op->tc_b;
             jobs[b].tc_kp = use_tc ? op->tc_kp : 0;  // float64 slots (device flag) stay on the CUDA-core kernel
+            jobs[b].fx = (!jobs[b].tc_kp && op->fx_ok && !fx_disabled()) ? 1 : 0;
+            jobs[b].pad_ = 0;
+            if (jobs[b].fx) {
+                nfx++;
+                maxfx = std::max(maxfx, (size_t)h.ncp * (size_t)((h.ncp + 3) & ~3));
+            }
             if (jobs[b].tc_kp) {
                 ntc++;
                 maxkp = std::max(maxkp, (int)jobs[b].tc_kp);
@@ -714,7 +950,14 @@ extern "C" int afam_decode_grid_ex(afam_store *s, const int32_t *slots, int32_t 
         AFAM_CUDA(cudaFuncSetAttribute(decode_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         decode_tc_kernel<<<nblk, kTcThreads, smem, st>>>(s->d_desc, d_jobs, m, out);
     }
-    if (ntc < nblk) {
+    if (nfx > 0) {
+        const size_t smem = ((size_t)kFxRing * (maxfx + kFxPad) + 2 * (size_t)kFxXRows * kFxXPitch + 65 * 4 + 68) * 4 +
+                            kFxRing * 8;
+        AFAM_CHECK(smem <= 227 * 1024, AFAM_E_VALUE, "register-tiled decode needs %zu B of shared memory", smem);
+        AFAM_CUDA(cudaFuncSetAttribute(decode_fx_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        decode_fx_kernel<<<nblk, kFxThreads, smem, st>>>(s->d_desc, d_jobs, out);
+    }
+    if (ntc + nfx < nblk) {
         const size_t smem = smem_for(sizeof(float));
         AFAM_CHECK(smem <= 227 * 1024, AFAM_E_VALUE, "decode of ncp=%d onto m=%d needs %zu B of shared memory", maxn,
                    m, smem);

@@ -85,6 +85,10 @@ struct DecodeOp {  // banded collocation matrix of bspline.py:98-125 for (ncp, d
     // into tf32 hi and lo parts, in the K-major no-swizzle operand layout
     float *tc_b = nullptr;  // [2][kp/4][m-1][4]: hi panels, then lo panels
     int32_t tc_kp = 0;      // 0: the tensor-core path does not apply
+    // register-tiled decode (afam_decode.cu, decode_fx_kernel): m == 65,
+    // deg + 1 <= ncp <= 65 and the u = 1 row selecting the last control
+    // point exactly
+    bool fx_ok = false;
 };
 
 // Banded rows of the collocation matrix of bspline.py:98-125 for (ncp, deg,
