@@ -311,14 +311,13 @@ __global__ void __launch_bounds__(kDecodeThreads) decode_grid_kernel(const Block
 // Y[64][.] the X row ncp-1: threads 0..128 carry one such value each
 // (threads 0..15 also take the x stage's control row 64).  Control points are read once from HBM (TMA), the
 // output written once; x and y run out of registers and one X plane.
-constexpr int kFxThreads = 256;  // 8 warps: 16 x lanes x 16 row groups
 constexpr int kFxRing = 4;       // TMA plane slots
 constexpr int kFxXPitch = 68;    // X plane row pitch (floats)
 constexpr int kFxXRows = 72;     // X plane rows (the y windows over-read up to row ncp + 4, zeros)
 constexpr int kFxPad = 16;       // zero floats after each ring slot (x windows over-read the last row)
 
 
-template <int P>
+template <int P, int YPT>
 __device__ __forceinline__ void fx_decode_block(const BlockDesc &d, const int32_t *__restrict__ c0g,
                                                 const float *__restrict__ Bg, float *__restrict__ out,
                                                 unsigned char *smem) {
@@ -330,7 +329,8 @@ __device__ __forceinline__ void fx_decode_block(const BlockDesc &d, const int32_
     float *xb = ring + kFxRing * sstride;
     float *Bs = xb + 2 * kFxXRows * kFxXPitch;
     int *c0 = reinterpret_cast<int *>(Bs + M * 4);
-    uint64_t *bar = reinterpret_cast<uint64_t *>(c0 + 68);
+    float *xcol = reinterpret_cast<float *>(c0 + 68);  // 2 x 72: X[.][64] = control column n-1, contiguous
+    uint64_t *bar = reinterpret_cast<uint64_t *>(xcol + 2 * 72);
     const int tid = threadIdx.x;
 
     for (int i = tid; i < M * 4; i += blockDim.x) Bs[i] = Bg[i];
@@ -358,31 +358,33 @@ __device__ __forceinline__ void fx_decode_block(const BlockDesc &d, const int32_
 
     // x stage weights: quad q (lattice columns 4q..4q+3) over the aligned
     // 12-float window starting at cw (dense, zeros off the band)
+    // YPT lattice rows per thread: 16 x lanes x (64 / YPT) row groups
+    constexpr int NT = 16 * 64 / YPT, NG = NT / 16, YW = YPT + 3;
     const int q = tid & 15, g = tid >> 4;
     const int cw = c0[4 * q] & ~3;
-    float wx[4][12];
+    float wx[4][10];
 #pragma unroll
     for (int xi = 0; xi < 4; xi++) {
         const int x = 4 * q + xi, off = c0[x] - cw;
 #pragma unroll
-        for (int e = 0; e < 12; e++) {
+        for (int e = 0; e < 10; e++) {
             const int a = e - off;
             wx[xi][e] = (a >= 0 && a < Q) ? Bs[x * 4 + a] : 0.f;
         }
     }
     // y stage weights: rows 4g..4g+3 over the 7-row window starting at r0
-    const int r0 = c0[4 * g];
-    float wy[4][7];
+    const int r0 = c0[YPT * g];
+    float wy[YPT][YW];
 #pragma unroll
-    for (int yi = 0; yi < 4; yi++) {
-        const int y = 4 * g + yi, off = c0[y] - r0;
+    for (int yi = 0; yi < YPT; yi++) {
+        const int y = YPT * g + yi, off = c0[y] - r0;
 #pragma unroll
-        for (int e = 0; e < 7; e++) {
+        for (int e = 0; e < YW; e++) {
             const int b = e - off;
             wy[yi][e] = (b >= 0 && b < Q) ? Bs[y * 4 + b] : 0.f;
         }
     }
-    float yr[4][4][4];  // [plane slot][yi][s]: Y of the last 4 planes, columns q + 16 s
+    float yr[4][YPT][4];  // [plane slot][yi][s]: Y of the last 4 planes, columns q + 16 s
     float er[4];        // threads 0..128: the lattice column x = 64 / row y = 64 value of the last 4 planes
     int knext = 0;
 
@@ -394,24 +396,51 @@ __device__ __forceinline__ void fx_decode_block(const BlockDesc &d, const int32_
             mbar_wait(bar + u, (uint32_t)((zc >> 2) & 1));
             const float *Cp = ring + u * sstride;
             float *X = xb + (u & 1) * kFxXRows * kFxXPitch;
-            // ---- x stage (threads 0..15 also take control row 64)
+            // ---- x stage: rows g + 16 i two at a time (four independent FFMA2
+            // chains), threads 0..15 also take control row 64; window
+            // entries 10, 11 never carry weight (offsets <= 3 + 3, p <= 3)
 #pragma unroll
-            for (int i = 0; i < 5; i++) {
-                const int r = i < 4 ? g + 16 * i : 64;
-                if (r < n && (i < 4 || g == 0)) {
-                    const float4 *src = reinterpret_cast<const float4 *>(Cp + r * pitch + cw);
-                    const float4 v0 = src[0], v1 = src[1], v2 = src[2];
-                    const float w[12] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, v2.x, v2.y, v2.z, v2.w};
-                    float2 a01 = make_float2(0.f, 0.f), a23 = make_float2(0.f, 0.f);
+            for (int i = 0; i < 64 / NG; i += 2) {
+                const int ra = g + NG * i, rb = ra + NG;
+                const float4 *sa = reinterpret_cast<const float4 *>(Cp + min(ra, n - 1) * pitch + cw);
+                const float4 *sb = reinterpret_cast<const float4 *>(Cp + min(rb, n - 1) * pitch + cw);
+                const float4 a0 = sa[0], a1 = sa[1], a2 = sa[2], b0 = sb[0], b1 = sb[1], b2 = sb[2];
+                const float va[10] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y};
+                const float vb[10] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x, b2.y};
+                // even / odd taps in separate chains: eight independent FFMA2 chains of 5
+                float2 pa01 = make_float2(0.f, 0.f), pa23 = pa01, pb01 = pa01, pb23 = pa01;
+                float2 qa01 = pa01, qa23 = pa01, qb01 = pa01, qb23 = pa01;
 #pragma unroll
-                    for (int e = 0; e < 12; e++) {
-                        a01 = __ffma2_rn(make_float2(wx[0][e], wx[1][e]), make_float2(w[e], w[e]), a01);
-                        a23 = __ffma2_rn(make_float2(wx[2][e], wx[3][e]), make_float2(w[e], w[e]), a23);
-                    }
-                    *reinterpret_cast<float4 *>(X + r * kFxXPitch + 4 * q) = make_float4(a01.x, a01.y, a23.x, a23.y);
+                for (int e = 0; e < 10; e += 2) {
+                    pa01 = __ffma2_rn(make_float2(wx[0][e], wx[1][e]), make_float2(va[e], va[e]), pa01);
+                    pa23 = __ffma2_rn(make_float2(wx[2][e], wx[3][e]), make_float2(va[e], va[e]), pa23);
+                    pb01 = __ffma2_rn(make_float2(wx[0][e], wx[1][e]), make_float2(vb[e], vb[e]), pb01);
+                    pb23 = __ffma2_rn(make_float2(wx[2][e], wx[3][e]), make_float2(vb[e], vb[e]), pb23);
+                    qa01 = __ffma2_rn(make_float2(wx[0][e + 1], wx[1][e + 1]), make_float2(va[e + 1], va[e + 1]), qa01);
+                    qa23 = __ffma2_rn(make_float2(wx[2][e + 1], wx[3][e + 1]), make_float2(va[e + 1], va[e + 1]), qa23);
+                    qb01 = __ffma2_rn(make_float2(wx[0][e + 1], wx[1][e + 1]), make_float2(vb[e + 1], vb[e + 1]), qb01);
+                    qb23 = __ffma2_rn(make_float2(wx[2][e + 1], wx[3][e + 1]), make_float2(vb[e + 1], vb[e + 1]), qb23);
                 }
+                pa01 = __fadd2_rn(pa01, qa01);
+                pa23 = __fadd2_rn(pa23, qa23);
+                pb01 = __fadd2_rn(pb01, qb01);
+                pb23 = __fadd2_rn(pb23, qb23);
+                if (ra < n) *reinterpret_cast<float4 *>(X + ra * kFxXPitch + 4 * q) = make_float4(pa01.x, pa01.y, pa23.x, pa23.y);
+                if (rb < n) *reinterpret_cast<float4 *>(X + rb * kFxXPitch + 4 * q) = make_float4(pb01.x, pb01.y, pb23.x, pb23.y);
             }
-            if (tid < n) X[tid * kFxXPitch + 64] = Cp[tid * pitch + n - 1];  // u = 1 column: control column n-1
+            if (g == NG - 1 && n > 64) {  // control row 64 (the last row group: the edge values sit on warps 0..4)
+                const float4 *src = reinterpret_cast<const float4 *>(Cp + 64 * pitch + cw);
+                const float4 v0 = src[0], v1 = src[1], v2 = src[2];
+                const float w[10] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, v2.x, v2.y};
+                float2 a01 = make_float2(0.f, 0.f), a23 = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int e = 0; e < 10; e++) {
+                    a01 = __ffma2_rn(make_float2(wx[0][e], wx[1][e]), make_float2(w[e], w[e]), a01);
+                    a23 = __ffma2_rn(make_float2(wx[2][e], wx[3][e]), make_float2(w[e], w[e]), a23);
+                }
+                *reinterpret_cast<float4 *>(X + 64 * kFxXPitch + 4 * q) = make_float4(a01.x, a01.y, a23.x, a23.y);
+            }
+            if (tid < n) xcol[(u & 1) * 72 + tid] = Cp[tid * pitch + n - 1];  // u = 1 column: control column n-1
             __syncthreads();
             if (tid == 0 && zc + kFxRing < n) {  // ring slot u is free: every thread passed its x stage
                 fence_proxy_async();
@@ -420,15 +449,15 @@ __device__ __forceinline__ void fx_decode_block(const BlockDesc &d, const int32_
             }
             // ---- y stage (into the register ring)
 #pragma unroll
-            for (int yi = 0; yi < 4; yi++)
+            for (int yi = 0; yi < YPT; yi++)
 #pragma unroll
                 for (int s = 0; s < 4; s++) yr[u][yi][s] = 0.f;
 #pragma unroll
-            for (int e = 0; e < 7; e++) {
+            for (int e = 0; e < YW; e++) {
                 const float *xr = X + (r0 + e) * kFxXPitch + q;
                 const float v[4] = {xr[0], xr[16], xr[32], xr[48]};
 #pragma unroll
-                for (int yi = 0; yi < 4; yi++) {
+                for (int yi = 0; yi < YPT; yi++) {
                     float2 lo = make_float2(yr[u][yi][0], yr[u][yi][1]), hi = make_float2(yr[u][yi][2], yr[u][yi][3]);
                     lo = __ffma2_rn(make_float2(wy[yi][e], wy[yi][e]), make_float2(v[0], v[1]), lo);
                     hi = __ffma2_rn(make_float2(wy[yi][e], wy[yi][e]), make_float2(v[2], v[3]), hi);
@@ -439,10 +468,10 @@ __device__ __forceinline__ void fx_decode_block(const BlockDesc &d, const int32_
             if (tid <= 64) {
                 float acc = 0.f;
                 if (tid == 64) {
-                    acc = X[(n - 1) * kFxXPitch + 64];
+                    acc = xcol[(u & 1) * 72 + n - 1];
                 } else {
 #pragma unroll
-                    for (int b = 0; b < Q; b++) acc = fmaf(Bs[tid * 4 + b], X[(c0[tid] + b) * kFxXPitch + 64], acc);
+                    for (int b = 0; b < Q; b++) acc = fmaf(Bs[tid * 4 + b], xcol[(u & 1) * 72 + c0[tid] + b], acc);
                 }
                 er[u] = acc;
             } else if (tid < 129) {
@@ -456,7 +485,7 @@ __device__ __forceinline__ void fx_decode_block(const BlockDesc &d, const int32_
                 for (int c = 0; c < Q; c++) wz[c] = Bs[k * 4 + c];
                 float *ok = out + (size_t)k * M * M;
 #pragma unroll
-                for (int yi = 0; yi < 4; yi++) {
+                for (int yi = 0; yi < YPT; yi++) {
                     float2 lo = make_float2(0.f, 0.f), hi = make_float2(0.f, 0.f);
 #pragma unroll
                     for (int c = 0; c < Q; c++) {
@@ -464,7 +493,7 @@ __device__ __forceinline__ void fx_decode_block(const BlockDesc &d, const int32_
                         lo = __ffma2_rn(make_float2(wz[c], wz[c]), make_float2(yr[sl][yi][0], yr[sl][yi][1]), lo);
                         hi = __ffma2_rn(make_float2(wz[c], wz[c]), make_float2(yr[sl][yi][2], yr[sl][yi][3]), hi);
                     }
-                    float *orow = ok + (4 * g + yi) * M + q;
+                    float *orow = ok + (YPT * g + yi) * M + q;
                     orow[0] = lo.x;
                     orow[16] = lo.y;
                     orow[32] = hi.x;
@@ -481,9 +510,10 @@ __device__ __forceinline__ void fx_decode_block(const BlockDesc &d, const int32_
     }
 }
 
-__global__ void __launch_bounds__(kFxThreads, 1) decode_fx_kernel(const BlockDesc *__restrict__ descs,
-                                                                   const DecodeJob *__restrict__ jobs,
-                                                                   float *__restrict__ out) {
+template <int YPT>
+__global__ void __launch_bounds__(16 * 64 / YPT, 1) decode_fx_kernel(const BlockDesc *__restrict__ descs,
+                                                                      const DecodeJob *__restrict__ jobs,
+                                                                      float *__restrict__ out) {
     extern __shared__ __align__(16) unsigned char smem[];
     const DecodeJob jb = jobs[blockIdx.x];
     if (!jb.fx) return;
@@ -491,9 +521,9 @@ __global__ void __launch_bounds__(kFxThreads, 1) decode_fx_kernel(const BlockDes
     if (d.flags & AFAM_SLOT_FP64) return;  // float64 slots: decode_grid_kernel<double>
     float *o = out + (size_t)blockIdx.x * 65 * 65 * 65;
     switch (d.deg) {
-        case 1: fx_decode_block<1>(d, jb.col0, jb.b32, o, smem); break;
-        case 2: fx_decode_block<2>(d, jb.col0, jb.b32, o, smem); break;
-        default: fx_decode_block<3>(d, jb.col0, jb.b32, o, smem); break;
+        case 1: fx_decode_block<1, YPT>(d, jb.col0, jb.b32, o, smem); break;
+        case 2: fx_decode_block<2, YPT>(d, jb.col0, jb.b32, o, smem); break;
+        default: fx_decode_block<3, YPT>(d, jb.col0, jb.b32, o, smem); break;
     }
 }
 
@@ -822,6 +852,15 @@ static bool fx_disabled() {
     return v;
 }
 
+// lattice rows per thread of the register-tiled decode (AFAM_DECODE_FX_YPT=2|4 A/B)
+static int fx_ypt() {
+    static const int v = [] {
+        const char *e = getenv("AFAM_DECODE_FX_YPT");
+        return (e && atoi(e) == 2) ? 2 : 4;
+    }();
+    return v;
+}
+
 static int get_op(afam_store *s, int ncp, int deg, int m, DecodeOp **op) {
     auto key = std::make_tuple(ncp, deg, m);
     auto it = s->ops.find(key);
@@ -951,11 +990,17 @@ extern "C" int afam_decode_grid_ex(afam_store *s, const int32_t *slots, int32_t 
         decode_tc_kernel<<<nblk, kTcThreads, smem, st>>>(s->d_desc, d_jobs, m, out);
     }
     if (nfx > 0) {
-        const size_t smem = ((size_t)kFxRing * (maxfx + kFxPad) + 2 * (size_t)kFxXRows * kFxXPitch + 65 * 4 + 68) * 4 +
-                            kFxRing * 8;
+        const size_t smem =
+            ((size_t)kFxRing * (maxfx + kFxPad) + 2 * (size_t)kFxXRows * kFxXPitch + 65 * 4 + 68 + 2 * 72) * 4 +
+            kFxRing * 8;
         AFAM_CHECK(smem <= 227 * 1024, AFAM_E_VALUE, "register-tiled decode needs %zu B of shared memory", smem);
-        AFAM_CUDA(cudaFuncSetAttribute(decode_fx_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        decode_fx_kernel<<<nblk, kFxThreads, smem, st>>>(s->d_desc, d_jobs, out);
+        if (fx_ypt() == 4) {
+            AFAM_CUDA(cudaFuncSetAttribute(decode_fx_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            decode_fx_kernel<4><<<nblk, 256, smem, st>>>(s->d_desc, d_jobs, out);
+        } else {
+            AFAM_CUDA(cudaFuncSetAttribute(decode_fx_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            decode_fx_kernel<2><<<nblk, 512, smem, st>>>(s->d_desc, d_jobs, out);
+        }
     }
     if (ntc + nfx < nblk) {
         const size_t smem = smem_for(sizeof(float));

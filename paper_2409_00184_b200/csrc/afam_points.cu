@@ -78,9 +78,12 @@ __global__ void __launch_bounds__(256) eval_points_kernel(const BlockDesc *__res
                                                           const int32_t *__restrict__ slots, int32_t slot,
                                                           const double *__restrict__ pts, int64_t n,
                                                           OT *__restrict__ val, OT *__restrict__ grad,
-                                                          uint32_t flags) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
+                                                          uint32_t flags, const int32_t *__restrict__ order) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    // order: the batch bucketed by slot (slot_scatter_kernel), so the lanes
+    // of a warp gather from one block's control points (L1/L2 reuse)
+    const int64_t i = order ? (int64_t)__ldg(order + j) : j;
     const int32_t sl = slots ? __ldg(slots + i) : slot;
     const BlockDesc d = load_desc(descs + sl);
     if (d.flags & AFAM_SLOT_DS) {  // world points only (DS blocks have no parameter space)
@@ -114,15 +117,104 @@ __global__ void __launch_bounds__(256) eval_points_kernel(const BlockDesc *__res
 
 template <typename OT>
 static void launch(const BlockDesc *descs, const int32_t *slots, int32_t slot, const double *pts, int64_t n,
-                   void *val, void *grad, uint32_t flags, cudaStream_t st) {
+                   void *val, void *grad, uint32_t flags, const int32_t *order, cudaStream_t st) {
     const int threads = 256;
     const unsigned blocks = (unsigned)((n + threads - 1) / threads);
     if (grad)
         eval_points_kernel<true, OT><<<blocks, threads, 0, st>>>(descs, slots, slot, pts, n, (OT *)val, (OT *)grad,
-                                                                 flags);
+                                                                 flags, order);
     else
         eval_points_kernel<false, OT><<<blocks, threads, 0, st>>>(descs, slots, slot, pts, n, (OT *)val, nullptr,
-                                                                  flags);
+                                                                  flags, order);
+}
+
+// ---- bucketing a per-point slot batch by slot (counting sort, three passes)
+// A random batch (points of many blocks interleaved) gathers each point's
+// (p+1)^3 control points from a different block: 4 x 64-byte x-quad runs
+// per point, each straddling DRAM bursts.  Bucketed, the lanes of a warp
+// read one block's control points and L1/L2 serve the overlap.
+constexpr int kBucketChunk = 8192;  // points per CTA (count and scatter passes)
+constexpr int kBucketThreads = 512;
+constexpr int kBucketMaxSlots = 16383;  // per-CTA shared histogram: nslots + 1 int32
+
+__device__ __forceinline__ int bucket_of(int32_t sl, int nslots) { return (sl >= 0 && sl < nslots) ? sl : nslots; }
+
+__global__ void __launch_bounds__(kBucketThreads) slot_count_kernel(const int32_t *__restrict__ slots, int64_t n,
+                                                                    int nslots, int32_t *__restrict__ count) {
+    extern __shared__ int32_t h[];
+    for (int i = threadIdx.x; i <= nslots; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    const int64_t b = (int64_t)blockIdx.x * kBucketChunk, e = min(n, b + kBucketChunk);
+    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) atomicAdd(&h[bucket_of(__ldg(slots + i), nslots)], 1);
+    __syncthreads();
+    for (int i = threadIdx.x; i <= nslots; i += blockDim.x)
+        if (h[i]) atomicAdd(&count[i], h[i]);
+}
+
+// exclusive scan of count[0..nb) into offs (one CTA of 1024 threads, tiles with a carry)
+__global__ void __launch_bounds__(1024) slot_scan_kernel(const int32_t *__restrict__ count, int nb,
+                                                         int32_t *__restrict__ offs) {
+    __shared__ int32_t wsum[32];
+    __shared__ int32_t carry;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < nb; base += 1024) {
+        const int i = base + threadIdx.x;
+        const int32_t v = i < nb ? count[i] : 0;
+        int32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            int32_t w = wsum[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int32_t y = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += y;
+            }
+            wsum[lane] = w;
+        }
+        __syncthreads();
+        const int32_t incl = x + (warp ? wsum[warp - 1] : 0);
+        if (i < nb) offs[i] = carry + incl - v;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry += incl;
+        __syncthreads();
+    }
+}
+
+// order[pos] = i with pos in slot i's bucket: per CTA a shared histogram,
+// one global reservation per (CTA, slot), then shared cursors
+__global__ void __launch_bounds__(kBucketThreads) slot_scatter_kernel(const int32_t *__restrict__ slots, int64_t n,
+                                                                      int nslots, int32_t *__restrict__ cursor,
+                                                                      int32_t *__restrict__ order) {
+    extern __shared__ int32_t h[];
+    for (int i = threadIdx.x; i <= nslots; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    const int64_t b = (int64_t)blockIdx.x * kBucketChunk, e = min(n, b + kBucketChunk);
+    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) atomicAdd(&h[bucket_of(__ldg(slots + i), nslots)], 1);
+    __syncthreads();
+    for (int i = threadIdx.x; i <= nslots; i += blockDim.x)
+        if (h[i]) h[i] = atomicAdd(&cursor[i], h[i]);
+    __syncthreads();
+    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+        const int pos = atomicAdd(&h[bucket_of(__ldg(slots + i), nslots)], 1);
+        order[pos] = (int32_t)i;
+    }
+}
+
+// AFAM_EVAL_BUCKET=0 disables the bucketing (A/B)
+static bool bucket_enabled() {
+    static const bool v = [] {
+        const char *e = getenv("AFAM_EVAL_BUCKET");
+        return !(e && atoi(e) == 0);
+    }();
+    return v;
 }
 
 }  // namespace afam
@@ -154,9 +246,31 @@ extern "C" int afam_eval_points(afam_store *s, const int32_t *slots, int32_t slo
             }
         }
     }
-    if (flags & AFAM_EVAL_OUT_F64) launch<double>(s->d_desc, slots, slot, pts, n, val, grad, flags, st);
-    else launch<float>(s->d_desc, slots, slot, pts, n, val, grad, flags, st);
+    int32_t *order = nullptr, *count = nullptr;
+    if (slots && n >= (1 << 16) && n < INT32_MAX && s->nslots <= kBucketMaxSlots && bucket_enabled()) {
+        const int nb = s->nslots + 1;
+        const size_t hsm = (size_t)nb * sizeof(int32_t);
+        const unsigned grid = (unsigned)((n + kBucketChunk - 1) / kBucketChunk);
+        AFAM_CUDA(cudaMallocAsync(&order, (size_t)n * sizeof(int32_t), st));
+        AFAM_CUDA(cudaMallocAsync(&count, 2 * hsm, st));
+        AFAM_CUDA(cudaMemsetAsync(count, 0, hsm, st));
+        static bool configured = false;
+        if (!configured) {
+            AFAM_CUDA(cudaFuncSetAttribute(slot_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+            AFAM_CUDA(cudaFuncSetAttribute(slot_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+            configured = true;
+        }
+        slot_count_kernel<<<grid, kBucketThreads, hsm, st>>>(slots, n, s->nslots, count);
+        slot_scan_kernel<<<1, 1024, 0, st>>>(count, nb, count + nb);
+        slot_scatter_kernel<<<grid, kBucketThreads, hsm, st>>>(slots, n, s->nslots, count + nb, order);
+    }
+    if (flags & AFAM_EVAL_OUT_F64) launch<double>(s->d_desc, slots, slot, pts, n, val, grad, flags, order, st);
+    else launch<float>(s->d_desc, slots, slot, pts, n, val, grad, flags, order, st);
     AFAM_CUDA(cudaGetLastError());
+    if (order) {
+        AFAM_CUDA(cudaFreeAsync(order, st));
+        AFAM_CUDA(cudaFreeAsync(count, st));
+    }
     // later uploads into the slots read here wait for this launch (the
     // per-point slot ids are device data: every valid slot is marked)
     ThreadCtx *tc = thread_ctx(s->device);
