@@ -81,6 +81,21 @@ int afam_store_slots(const afam_store *s, int32_t *slots, int32_t *max_ncp);
 int afam_store_put_mfa(afam_store *s, int32_t slot, const uint8_t *bytes, uint64_t nbytes, int32_t ncp,
                        const double extent[6], void *stream);
 
+/* Validate one host .mfa image without uploading it (the checks of
+ * afam_store_put_mfa: length / degree byte -> AFAM_E_FORMAT, non-finite
+ * control points -> AFAM_E_VALUE); *degree (nullable) receives the degree
+ * byte.  Replaces the validation half of model.deserialize
+ * (model.py:121-148) for loaders that move the bytes by other means. */
+int afam_mfa_check(const uint8_t *bytes, uint64_t nbytes, int32_t ncp, int32_t *degree);
+
+/* afam_store_put_mfa from a DEVICE copy of an image already validated by
+ * afam_mfa_check (e.g. received over NVLink from the rank that read it from
+ * the host: one H2D per cache miss for all ranks): D2D copy
+ * into the slot and the same realignment.  Replaces store.load_model +
+ * model.deserialize (store.py:43-47, model.py:121-148) on the receiving ranks. */
+int afam_store_put_mfa_device(afam_store *s, int32_t slot, const uint8_t *dbytes, uint64_t nbytes, int32_t degree,
+                              int32_t ncp, const double extent[6], void *stream);
+
 /* Upload one down-sampled (DS) block file image (reference downsample.py:
  * 16-byte header of uint32 (nx, ny, nz, ghost) then nx*ny*nz float32 LE,
  * x fastest; serialize_ds / deserialize_ds, downsample.py:140-161) into

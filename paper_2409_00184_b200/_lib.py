@@ -83,6 +83,9 @@ SIGNATURES = [
                                       C.c_void_p]),
     ("afam_store_put_mfa", C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_uint64, C.c_int32, C.c_void_p,
                                      C.c_void_p]),
+    ("afam_mfa_check", C.c_int, [C.c_void_p, C.c_uint64, C.c_int32, C.POINTER(C.c_int32)]),
+    ("afam_store_put_mfa_device", C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_uint64, C.c_int32, C.c_int32,
+                                            C.c_void_p, C.c_void_p]),
     ("afam_store_put", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_void_p]),
     ("afam_store_evict", C.c_int, [C.c_void_p, C.c_int32]),

@@ -51,8 +51,8 @@ __device__ __forceinline__ double ds_trilinear(const float *__restrict__ g, cons
 }
 
 template <bool GRAD, typename OT>
-__device__ __forceinline__ void eval_ds(const BlockDesc &d, const double *__restrict__ pts, int64_t i, OT *val,
-                                        OT *grad) {
+__device__ __forceinline__ void eval_ds(const BlockDesc &d, const double *__restrict__ pts, int64_t i, int64_t o,
+                                        OT *val, OT *grad) {
     const int g = d.deg;  // ghost width
     const int n[3] = {d.ds_n[0], d.ds_n[1], d.ds_n[2]};
     const int nr[3] = {n[0] + 2 * g, n[1] + 2 * g, n[2] + 2 * g};
@@ -63,13 +63,13 @@ __device__ __forceinline__ void eval_ds(const BlockDesc &d, const double *__rest
         x[a] = clamp01(__ddiv_rn(__dsub_rn(p, d.lo[a]), d.span[a])) * (double)(n[a] - 1);
         xg[a] = x[a] + (double)g;
     }
-    val[i] = (OT)ds_trilinear(d.ctrl, nr, xg);
+    val[o] = (OT)ds_trilinear(d.ctrl, nr, xg);
     if (GRAD) {
         const size_t plane = (size_t)n[0] * n[1] * n[2];
         const float *grids = reinterpret_cast<const float *>(d.ctrl4);
 #pragma unroll
         for (int a = 0; a < 3; a++)  // central-difference grids x (n - 1) / span (downsample.py:118-128)
-            grad[3 * i + a] = (OT)(ds_trilinear(grids + a * plane, n, x) * ((double)(n[a] - 1) / d.span[a]));
+            grad[3 * o + a] = (OT)(ds_trilinear(grids + a * plane, n, x) * ((double)(n[a] - 1) / d.span[a]));
     }
 }
 
@@ -78,16 +78,27 @@ __global__ void __launch_bounds__(256) eval_points_kernel(const BlockDesc *__res
                                                           const int32_t *__restrict__ slots, int32_t slot,
                                                           const double *__restrict__ pts, int64_t n,
                                                           OT *__restrict__ val, OT *__restrict__ grad,
-                                                          uint32_t flags, const int32_t *__restrict__ order) {
+                                                          uint32_t flags, const int32_t *__restrict__ order,
+                                                          const int32_t *__restrict__ keep, OT *__restrict__ tval,
+                                                          OT *__restrict__ tgrad) {
     const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (j >= n) return;
     // order: the batch bucketed by slot (slot_scatter_kernel), so the lanes
-    // of a warp gather from one block's control points (L1/L2 reuse)
-    const int64_t i = order ? (int64_t)__ldg(order + j) : j;
+    // of a warp gather from one block's control points (L1/L2 reuse); a
+    // batch that already comes in runs of one slot keeps its order (*keep)
+    const bool bucketed = order && !*keep;
+    const int64_t i = bucketed ? (int64_t)__ldg(order + j) : j;
+    // bucketed batches write their results in bucket order (coalesced);
+    // unpermute_kernel moves them to the caller's order
+    const int64_t o = bucketed ? j : i;
+    if (bucketed) {
+        val = tval;
+        grad = tgrad;
+    }
     const int32_t sl = slots ? __ldg(slots + i) : slot;
     const BlockDesc d = load_desc(descs + sl);
     if (d.flags & AFAM_SLOT_DS) {  // world points only (DS blocks have no parameter space)
-        eval_ds<GRAD, OT>(d, pts, i, val, grad);
+        eval_ds<GRAD, OT>(d, pts, i, o, val, grad);
         return;
     }
     const bool param = flags & AFAM_EVAL_PARAM;
@@ -108,24 +119,25 @@ __global__ void __launch_bounds__(256) eval_points_kernel(const BlockDesc *__res
 #pragma unroll
             for (int a = 0; a < 3; a++) g[a] = gf[a];
     }
-    val[i] = (OT)v;
+    val[o] = (OT)v;
     if (GRAD) {
 #pragma unroll
-        for (int a = 0; a < 3; a++) grad[3 * i + a] = (OT)(param ? g[a] : g[a] / d.span[a]);  // model.py:79
+        for (int a = 0; a < 3; a++) grad[3 * o + a] = (OT)(param ? g[a] : g[a] / d.span[a]);  // model.py:79
     }
 }
 
 template <typename OT>
 static void launch(const BlockDesc *descs, const int32_t *slots, int32_t slot, const double *pts, int64_t n,
-                   void *val, void *grad, uint32_t flags, const int32_t *order, cudaStream_t st) {
+                   void *val, void *grad, uint32_t flags, const int32_t *order, const int32_t *keep, void *tval,
+                   void *tgrad, cudaStream_t st) {
     const int threads = 256;
     const unsigned blocks = (unsigned)((n + threads - 1) / threads);
     if (grad)
         eval_points_kernel<true, OT><<<blocks, threads, 0, st>>>(descs, slots, slot, pts, n, (OT *)val, (OT *)grad,
-                                                                 flags, order);
+                                                                 flags, order, keep, (OT *)tval, (OT *)tgrad);
     else
         eval_points_kernel<false, OT><<<blocks, threads, 0, st>>>(descs, slots, slot, pts, n, (OT *)val, nullptr,
-                                                                  flags, order);
+                                                                  flags, order, keep, (OT *)tval, nullptr);
 }
 
 // ---- bucketing a per-point slot batch by slot (counting sort, three passes)
@@ -140,12 +152,20 @@ constexpr int kBucketMaxSlots = 16383;  // per-CTA shared histogram: nslots + 1 
 __device__ __forceinline__ int bucket_of(int32_t sl, int nslots) { return (sl >= 0 && sl < nslots) ? sl : nslots; }
 
 __global__ void __launch_bounds__(kBucketThreads) slot_count_kernel(const int32_t *__restrict__ slots, int64_t n,
-                                                                    int nslots, int32_t *__restrict__ count) {
+                                                                    int nslots, int32_t *__restrict__ count,
+                                                                    unsigned long long *__restrict__ runs) {
     extern __shared__ int32_t h[];
     for (int i = threadIdx.x; i <= nslots; i += blockDim.x) h[i] = 0;
     __syncthreads();
     const int64_t b = (int64_t)blockIdx.x * kBucketChunk, e = min(n, b + kBucketChunk);
-    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) atomicAdd(&h[bucket_of(__ldg(slots + i), nslots)], 1);
+    unsigned breaks = 0;  // i with slots[i] != slots[i-1]: how far the batch already is from bucketed
+    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+        const int32_t sl = __ldg(slots + i);
+        atomicAdd(&h[bucket_of(sl, nslots)], 1);
+        breaks += (i > 0 && __ldg(slots + i - 1) != sl) ? 1u : 0u;
+    }
+    breaks = __reduce_add_sync(0xffffffffu, breaks);
+    if ((threadIdx.x & 31) == 0 && breaks) atomicAdd(runs, (unsigned long long)breaks);
     __syncthreads();
     for (int i = threadIdx.x; i <= nslots; i += blockDim.x)
         if (h[i]) atomicAdd(&count[i], h[i]);
@@ -153,10 +173,15 @@ __global__ void __launch_bounds__(kBucketThreads) slot_count_kernel(const int32_
 
 // exclusive scan of count[0..nb) into offs (one CTA of 1024 threads, tiles with a carry)
 __global__ void __launch_bounds__(1024) slot_scan_kernel(const int32_t *__restrict__ count, int nb,
-                                                         int32_t *__restrict__ offs) {
+                                                         int32_t *__restrict__ offs,
+                                                         const unsigned long long *__restrict__ runs, int64_t n,
+                                                         int32_t *__restrict__ keep) {
     __shared__ int32_t wsum[32];
     __shared__ int32_t carry;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // runs of one slot averaging >= 256 points (8 warps): gathers are
+    // already coherent, keep the caller's order (no scatter, no unpermute)
+    if (threadIdx.x == 0) *keep = (*runs + 1) * 256 <= (unsigned long long)n ? 1 : 0;
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
     for (int base = 0; base < nb; base += 1024) {
@@ -192,7 +217,10 @@ __global__ void __launch_bounds__(1024) slot_scan_kernel(const int32_t *__restri
 // one global reservation per (CTA, slot), then shared cursors
 __global__ void __launch_bounds__(kBucketThreads) slot_scatter_kernel(const int32_t *__restrict__ slots, int64_t n,
                                                                       int nslots, int32_t *__restrict__ cursor,
-                                                                      int32_t *__restrict__ order) {
+                                                                      int32_t *__restrict__ order,
+                                                                      int32_t *__restrict__ inv,
+                                                                      const int32_t *__restrict__ keep) {
+    if (*keep) return;
     extern __shared__ int32_t h[];
     for (int i = threadIdx.x; i <= nslots; i += blockDim.x) h[i] = 0;
     __syncthreads();
@@ -205,6 +233,25 @@ __global__ void __launch_bounds__(kBucketThreads) slot_scatter_kernel(const int3
     for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
         const int pos = atomicAdd(&h[bucket_of(__ldg(slots + i), nslots)], 1);
         order[pos] = (int32_t)i;
+        inv[i] = pos;
+    }
+}
+
+// out[i] = tmp[inv[i]]: results back to the caller's order (coalesced
+// writes, 16-byte random reads instead of scattered partial-sector writes)
+template <typename OT>
+__global__ void __launch_bounds__(256) unpermute_kernel(const int32_t *__restrict__ inv, int64_t n,
+                                                        const OT *__restrict__ tval, const OT *__restrict__ tgrad,
+                                                        OT *__restrict__ val, OT *__restrict__ grad,
+                                                        const int32_t *__restrict__ keep) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n || *keep) return;
+    const int64_t j = __ldg(inv + i);
+    val[i] = tval[j];
+    if (grad) {
+        grad[3 * i] = tgrad[3 * j];
+        grad[3 * i + 1] = tgrad[3 * j + 1];
+        grad[3 * i + 2] = tgrad[3 * j + 2];
     }
 }
 
@@ -246,29 +293,51 @@ extern "C" int afam_eval_points(afam_store *s, const int32_t *slots, int32_t slo
             }
         }
     }
-    int32_t *order = nullptr, *count = nullptr;
+    int32_t *order = nullptr, *count = nullptr, *inv = nullptr, *keep = nullptr;
+    unsigned long long *runs = nullptr;
+    void *tmp = nullptr;
+    const size_t osz = (flags & AFAM_EVAL_OUT_F64) ? sizeof(double) : sizeof(float);
     if (slots && n >= (1 << 16) && n < INT32_MAX && s->nslots <= kBucketMaxSlots && bucket_enabled()) {
         const int nb = s->nslots + 1;
         const size_t hsm = (size_t)nb * sizeof(int32_t);
         const unsigned grid = (unsigned)((n + kBucketChunk - 1) / kBucketChunk);
         AFAM_CUDA(cudaMallocAsync(&order, (size_t)n * sizeof(int32_t), st));
-        AFAM_CUDA(cudaMallocAsync(&count, 2 * hsm, st));
-        AFAM_CUDA(cudaMemsetAsync(count, 0, hsm, st));
+        AFAM_CUDA(cudaMallocAsync(&inv, (size_t)n * sizeof(int32_t), st));
+        AFAM_CUDA(cudaMallocAsync(&tmp, (size_t)n * osz * (grad ? 4 : 1), st));
+        // count[nb] | offsets[nb] | keep (int32, padded) | runs (u64)
+        AFAM_CUDA(cudaMallocAsync(&count, 2 * hsm + 32, st));
+        AFAM_CUDA(cudaMemsetAsync(count, 0, 2 * hsm + 32, st));
+        keep = count + 2 * nb;
+        runs = reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(count) + ((2 * hsm + 8 + 7) & ~7ull));
         static bool configured = false;
         if (!configured) {
             AFAM_CUDA(cudaFuncSetAttribute(slot_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
             AFAM_CUDA(cudaFuncSetAttribute(slot_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
             configured = true;
         }
-        slot_count_kernel<<<grid, kBucketThreads, hsm, st>>>(slots, n, s->nslots, count);
-        slot_scan_kernel<<<1, 1024, 0, st>>>(count, nb, count + nb);
-        slot_scatter_kernel<<<grid, kBucketThreads, hsm, st>>>(slots, n, s->nslots, count + nb, order);
+        slot_count_kernel<<<grid, kBucketThreads, hsm, st>>>(slots, n, s->nslots, count, runs);
+        slot_scan_kernel<<<1, 1024, 0, st>>>(count, nb, count + nb, runs, n, keep);
+        slot_scatter_kernel<<<grid, kBucketThreads, hsm, st>>>(slots, n, s->nslots, count + nb, order, inv, keep);
     }
-    if (flags & AFAM_EVAL_OUT_F64) launch<double>(s->d_desc, slots, slot, pts, n, val, grad, flags, order, st);
-    else launch<float>(s->d_desc, slots, slot, pts, n, val, grad, flags, order, st);
+    void *ev = order ? tmp : nullptr;
+    void *eg = order && grad ? (void *)((char *)tmp + (size_t)n * osz) : nullptr;
+    if (flags & AFAM_EVAL_OUT_F64)
+        launch<double>(s->d_desc, slots, slot, pts, n, val, grad, flags, order, keep, ev, eg, st);
+    else
+        launch<float>(s->d_desc, slots, slot, pts, n, val, grad, flags, order, keep, ev, eg, st);
     AFAM_CUDA(cudaGetLastError());
     if (order) {
+        const unsigned g2 = (unsigned)((n + 255) / 256);
+        if (flags & AFAM_EVAL_OUT_F64)
+            unpermute_kernel<double><<<g2, 256, 0, st>>>(inv, n, (const double *)ev, (const double *)eg,
+                                                         (double *)val, (double *)grad, keep);
+        else
+            unpermute_kernel<float><<<g2, 256, 0, st>>>(inv, n, (const float *)ev, (const float *)eg, (float *)val,
+                                                        (float *)grad, keep);
+        AFAM_CUDA(cudaGetLastError());
         AFAM_CUDA(cudaFreeAsync(order, st));
+        AFAM_CUDA(cudaFreeAsync(inv, st));
+        AFAM_CUDA(cudaFreeAsync(tmp, st));
         AFAM_CUDA(cudaFreeAsync(count, st));
     }
     // later uploads into the slots read here wait for this launch (the

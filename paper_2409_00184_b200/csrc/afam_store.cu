@@ -366,6 +366,36 @@ int afam_store_put_mfa(afam_store *s, int32_t slot, const uint8_t *bytes, uint64
 }
 
 
+int afam_mfa_check(const uint8_t *bytes, uint64_t nbytes, int32_t ncp, int32_t *degree) {
+    AFAM_CHECK(bytes && nbytes >= 1, AFAM_E_FORMAT, "empty micro-model byte string");
+    const int deg = bytes[0];
+    AFAM_CHECK(deg < ncp, AFAM_E_FORMAT, "degree byte %d >= ncp %d", deg, ncp);
+    const size_t expected = serialized_size(ncp, deg);
+    AFAM_CHECK(nbytes == expected, AFAM_E_FORMAT,
+               "micro-model length mismatch: expected %zu bytes for ncp=%d, degree=%d, found %llu", expected,
+               ncp, deg, (unsigned long long)nbytes);
+    AFAM_CHECK(all_finite_le_f32(bytes + 1 + 12ull * (ncp + deg), (size_t)ncp * ncp * ncp), AFAM_E_VALUE,
+               "non-finite control points");
+    if (degree) *degree = deg;
+    return AFAM_OK;
+}
+
+int afam_store_put_mfa_device(afam_store *s, int32_t slot, const uint8_t *dbytes, uint64_t nbytes, int32_t degree,
+                              int32_t ncp, const double extent[6], void *stream) {
+    AFAM_CHECK(dbytes, AFAM_E_VALUE, "NULL device image");
+    AFAM_CHECK(degree >= 1 && degree < ncp && nbytes == serialized_size(ncp, degree), AFAM_E_FORMAT,
+               "device .mfa image: %llu bytes for ncp=%d, degree=%d", (unsigned long long)nbytes, ncp, degree);
+    int rc = check_put(s, slot, degree, ncp, extent);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    std::lock_guard<std::mutex> lk(s->mu);
+    AFAM_CUDA(cudaSetDevice(s->device));
+    AFAM_CUDA(cudaStreamWaitEvent(st, s->host[slot].ready, 0));
+    AFAM_CUDA(wait_readers(s, slot, st));
+    AFAM_CUDA(cudaMemcpyAsync(s->raw_ptr(slot), dbytes, nbytes, cudaMemcpyDeviceToDevice, st));
+    return launch_unpack(s, slot, degree, ncp, 1, 0, 1 + 12ull * (ncp + degree), extent, st);
+}
+
 int afam_store_put_file(afam_store *s, int32_t slot, const char *path, int32_t ncp, const double extent[6],
                         int32_t *degree, void *stream) {
     AFAM_CHECK(s && path, AFAM_E_VALUE, "NULL argument to afam_store_put_file");

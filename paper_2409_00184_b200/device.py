@@ -32,6 +32,15 @@ def serialized_size(ncp: int, degree: int) -> int:
     return 1 + ((ncp + degree) * 3 + ncp ** 3) * 4
 
 
+def check_mfa(data, ncp: int) -> int:
+    """Validate a host .mfa image like afam_store_put_mfa (FormatError /
+    ValueError); returns its degree byte."""
+    buf = np.frombuffer(data, dtype=np.uint8) if not isinstance(data, np.ndarray) else data
+    deg = C.c_int32(0)
+    _lib.check(_lib.lib().afam_mfa_check(buf.ctypes.data_as(C.c_void_p), buf.size, int(ncp), C.byref(deg)))
+    return int(deg.value)
+
+
 def stream_handle(stream=None, device=None) -> int:
     """cudaStream_t (as int) of a torch stream, or torch's current stream."""
     import torch
@@ -124,6 +133,14 @@ class DeviceStore:
         _lib.check(_lib.lib().afam_store_put_mfa(self._h, int(slot), buf.ctypes.data_as(C.c_void_p), buf.size,
                                                  int(ncp), ext.ctypes.data_as(C.c_void_p),
                                                  C.c_void_p(stream_handle(stream, self.device))))
+
+    def put_mfa_device(self, slot: int, dptr: int, nbytes: int, degree: int, ncp: int, extent, stream=None) -> None:
+        """Upload a .mfa image that already sits in device memory (validated
+        on the host by check_mfa): D2D copy + realignment."""
+        ext = _extent6(extent)
+        _lib.check(_lib.lib().afam_store_put_mfa_device(self._h, int(slot), C.c_void_p(int(dptr)), int(nbytes),
+                                                        int(degree), int(ncp), ext.ctypes.data_as(C.c_void_p),
+                                                        C.c_void_p(stream_handle(stream, self.device))))
 
     def put_file(self, slot: int, path, ncp: int, extent, stream=None) -> int:
         """Upload one .mfa file from disk through the native pinned staging

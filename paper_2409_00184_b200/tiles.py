@@ -12,7 +12,8 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["part_rows", "assemble", "gather_bands", "render_tiles", "PeerFrame", "render_tiles_fused"]
+__all__ = ["part_rows", "assemble", "gather_bands", "render_tiles", "PeerFrame", "render_tiles_fused",
+           "BroadcastLoader", "LockstepDone"]
 
 
 def part_rows(height: int, band_rows: int, nparts: int, part: int) -> np.ndarray:
@@ -207,3 +208,125 @@ def submit_tiles_fused(pov, blocks: dict, tf, params, peer: PeerFrame, *, group=
 
 render_tiles_fused.submit = submit_tiles_fused
 render_tiles_fused.last_stats = None
+
+
+# ------------------------------------------------------------ shared misses
+_STATUS = {0: None, 2: "FormatError", 4: "ValueError"}
+
+
+class LockstepDone:
+    """`rendering_done` for a prefetch loop that runs in lockstep on every
+    rank: rank 0's answer is broadcast, so every rank stops prefetching
+    before the same block (reference runtime.py:183-188 checks
+    rendering_done before each load)."""
+
+    def __init__(self, inner, group=None, device=None):
+        import torch
+
+        self.inner, self.group = inner, group
+        self.flag = torch.zeros(1, dtype=torch.int32, device=device)
+
+    def is_set(self) -> bool:
+        import torch.distributed as dist
+
+        if dist.get_rank(self.group) == 0:
+            self.flag.fill_(1 if self.inner.is_set() else 0)
+        dist.broadcast(self.flag, src=dist.get_global_rank(self.group, 0) if self.group is not None else 0,
+                       group=self.group)
+        return bool(self.flag.item())
+
+
+class BroadcastLoader:
+    """ModelCache loader for N ranks that share one host store (SURVEY.md
+    8e): each cache miss is read from host memory and copied H2D by ONE rank
+    (the i-th miss by rank i % N, spreading the PCIe links), then broadcast
+    over NVLink (NCCL) into every rank's staging buffer, where
+    afam_store_put_mfa_device realigns it into that rank's slot.  The
+    reference loads each miss from disk per process (runtime.py:112-133,
+    cache_frame :154-166); per-rank H2D (make_loader) stays the default.
+
+    Every rank must issue the same misses in the same order: the cache
+    decisions are deterministic given identical histories (select_visible
+    is), and replay() wraps the prefetch's rendering_done in LockstepDone
+    (`lockstep`) so all ranks stop prefetching at the same block.  Needs a
+    render function with `submit` (prefetch on the frame thread)."""
+
+    def __init__(self, manifest, dstore, source, group=None, device=None, max_bytes=None):
+        import torch
+        import torch.distributed as dist
+
+        from .model import serialized_size
+
+        self.manifest, self.dstore, self.source, self.group = manifest, dstore, source, group
+        self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        self.device = torch.device("cuda", dstore.device) if device is None else torch.device(device)
+        cap = max_bytes if max_bytes is not None else serialized_size(dstore.max_ncp, 3)
+        self.staging = torch.empty(int(cap), dtype=torch.uint8, device=self.device)
+        self.hdr = torch.zeros(3, dtype=torch.int64, device=self.device)
+        self.misses = 0
+        self.h2d_bytes = 0  # bytes this rank copied from the host
+        self.recv_bytes = 0  # bytes this rank received over the interconnect
+
+    def _src(self, r):
+        import torch.distributed as dist
+
+        return dist.get_global_rank(self.group, r) if self.group is not None else r
+
+    def __call__(self, addr):
+        import torch
+        import torch.distributed as dist
+
+        from .device import DeviceBlock, check_mfa
+        from .errors import FormatError
+
+        ent = self.manifest.entries.get(addr)
+        if ent is None:
+            raise FormatError(f"manifest has no model file for block {addr.key}")
+        root = self.misses % self.world
+        self.misses += 1
+        buf, msg = None, ""
+        if self.rank == root:
+            data = self.source(addr)
+            buf = np.frombuffer(data, dtype=np.uint8) if not isinstance(data, np.ndarray) else data
+            status, deg = 0, 0
+            try:
+                deg = check_mfa(buf, ent.ncp)
+            except FormatError as exc:
+                status, msg = 2, str(exc)
+            except ValueError as exc:
+                status, msg = 4, str(exc)
+            self.hdr.copy_(torch.tensor([status, deg, buf.size], dtype=torch.int64))
+        dist.broadcast(self.hdr, src=self._src(root), group=self.group)
+        status, deg, nbytes = (int(v) for v in self.hdr.tolist())
+        if status:
+            text = msg or f"block {addr.key}: invalid .mfa image (rank {root})"
+            raise FormatError(text) if status == 2 else ValueError(text)
+        if nbytes > self.staging.numel():
+            raise FormatError(f"block {addr.key}: {nbytes} bytes exceed the staging buffer")
+        view = self.staging[:nbytes]
+        if self.rank == root:
+            view.copy_(torch.from_numpy(np.ascontiguousarray(buf)), non_blocking=True)
+            self.h2d_bytes += nbytes
+        else:
+            self.recv_bytes += nbytes
+        dist.broadcast(view, src=self._src(root), group=self.group)
+        slot = self.dstore.alloc()
+        try:
+            st = torch.cuda.current_stream(self.device) if self.device.type == "cuda" else None
+            self.dstore.put_mfa_device(slot, view.data_ptr(), nbytes, deg, ent.ncp, ent.extent, stream=st)
+        except Exception:
+            self.dstore.release(slot)
+            raise
+        return DeviceBlock(self.dstore, slot, ent.extent, addr.lod, deg, ent.ncp)
+
+    def release(self, block):
+        self.dstore.release(block.slot)
+
+    def sync(self):
+        import torch
+
+        if self.device.type == "cuda":
+            torch.cuda.current_stream(self.device).synchronize()
+
+    def lockstep(self, done):
+        return LockstepDone(done, self.group, self.device)
