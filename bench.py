@@ -67,6 +67,9 @@ def parse():
                     help="the headline workload; the default config-3 line also carries config 2 and config 5 "
                          "under 'workloads' (unless --no-extra)")
     ap.add_argument("--no-extra", action="store_true", help="config 3 only (no config-2 / config-5 lines)")
+    ap.add_argument("--miss-load", default="per-rank", choices=["per-rank", "broadcast"],
+                    help="N > 1 e2e: every rank copies its cache misses H2D, or one rank per miss + a broadcast "
+                         "over NVLink (tiles.BroadcastLoader)")
     ap.add_argument("--gather", default="fused", choices=["fused", "nccl"],
                     help="N > 1: band gather fused into the render kernel (peer stores) or an NCCL gather")
     return ap.parse_args()
@@ -422,6 +425,12 @@ def run_headline(args, rank, world, local_rank):
     return res
 
 
+def tiles_mod():
+    from paper_2409_00184_b200 import tiles
+
+    return tiles
+
+
 def run_e2e(args, man, blobs, povs, tf, params, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -431,7 +440,10 @@ def run_e2e(args, man, blobs, povs, tf, params, rank, world, local_rank):
 
     cap = 200
     ds = DeviceStore(cap + 1, 65, device=local_rank)
-    loader = runtime.make_loader(None, man, ds, source=lambda a: blobs[a])
+    if world > 1 and args.miss_load == "broadcast":
+        loader = tiles_mod().BroadcastLoader(man, ds, lambda a: blobs[a])
+    else:
+        loader = runtime.make_loader(None, man, ds, source=lambda a: blobs[a])
     cache = runtime.ModelCache(cap, loader)
     band = 8
     S = params.width
@@ -505,7 +517,10 @@ def run_e2e(args, man, blobs, povs, tf, params, rank, world, local_rank):
     if peer is not None:
         dist.barrier()
         peer.close()
-    return {"value": float(tot[0]) / float(tot[1]), "unit": UNIT, "h2d_bytes_per_step": h2d,
+    extra = {"miss_load": args.miss_load if world > 1 else "single GPU"}
+    if hasattr(loader, "h2d_bytes"):
+        extra.update(rank_h2d_bytes=loader.h2d_bytes, rank_recv_bytes=loader.recv_bytes)
+    return {**extra, "value": float(tot[0]) / float(tot[1]), "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": draw.d2h / nsteps, "steps": nsteps,
             "api": "runtime.replay(ModelCache(200), prefetch='linear' on the frame thread while the GPU marches) -> tiles.render_tiles -> Frame bytes on host",
             "mean_caching_ms": agg["mean_caching_ms"], "mean_rendering_ms": agg["mean_rendering_ms"],

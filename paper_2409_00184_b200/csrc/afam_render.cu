@@ -1183,12 +1183,22 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
 //  - the owner change, the next exact-geometry sample and the end of the
 //    ray are one per-sample compare against the segment end
 //    min(knext, kend).
-template <int P>
+// The cell's x-quad rows cz*Q+by (bspline.py:175-181): the first NR in
+// registers, the last SR in this thread's column of a shared array
+// (s[k * 128]), so SR trades registers (occupancy) for LDS traffic.
+template <int P, int SR>
 struct FastCell {
-    float4 c[(P + 1) * (P + 1)];  // x-quad rows cz*Q+by of the cell (bspline.py:175-181)
+    static constexpr int NR = (P + 1) * (P + 1) - SR;
+    float4 c[NR > 0 ? NR : 1];
+    float4 *s;                    // this thread's shared rows (stride 128)
     float cx, cy, cz;             // the cell's lower corner in span coordinates
     int32_t key;                  // x-quad row index of the (0, 0) row in the owner block; -1: none
     uint32_t inner;               // bit a: axis a on an interior span
+    __device__ __forceinline__ float4 get(int i) const { return i < NR ? c[i] : s[(i - NR) * 128]; }
+    __device__ __forceinline__ void set(int i, float4 v) {
+        if (i < NR) c[i] = v;
+        else s[(i - NR) * 128] = v;
+    }
 };
 
 __device__ __forceinline__ bool in_unit(float f) {  // 0 <= f < 1 (also rejects -0.0 and NaN)
@@ -1209,8 +1219,9 @@ __device__ __forceinline__ BlockFast fast_block(const BlockFast &sb) {  // sb in
     return b;
 }
 
-template <int P>
-__device__ __forceinline__ void fast_cell_update(const BlockFast &sb, float tqx, float tqy, float tqz, FastCell<P> &G) {
+template <int P, int SR>
+__device__ __forceinline__ void fast_cell_update(const BlockFast &sb, float tqx, float tqy, float tqz,
+                                                 FastCell<P, SR> &G) {
     constexpr int Q = P + 1;
     const BlockFast b = fast_block<P>(sb);
     const int kx = min(max(__float2int_rd(tqx), 0), b.nspan - 1);
@@ -1227,7 +1238,7 @@ __device__ __forceinline__ void fast_cell_update(const BlockFast &sb, float tqx,
 #pragma unroll
         for (int cz = 0; cz < Q; cz++)
 #pragma unroll
-            for (int by = 0; by < Q; by++) G.c[cz * Q + by] = __ldg(base + cz * b.plane + by);
+            for (int by = 0; by < Q; by++) G.set(cz * Q + by, __ldg(base + cz * b.plane + by));
         G.key = id;
     }
 }
@@ -1235,13 +1246,14 @@ __device__ __forceinline__ void fast_cell_update(const BlockFast &sb, float tqx,
 // One sample of a clamped-uniform float32 block (render_kernel's
 // sample_fast, same arithmetic).  Returns false when the exact path must
 // decode it (P = 1 within 1e-4 of a knot).
-template <int P>
+template <int P, int SR>
 __device__ __forceinline__ bool sample_fast2(const RenderArgs &A, const TfTable &tf, const BlockFast &sb, float tqx,
-                                             float tqy, float tqz, const ThreadCold &C, FastCell<P> &G, March &M) {
+                                             float tqy, float tqz, const ThreadCold &C, FastCell<P, SR> &G,
+                                             March &M) {
     constexpr int Q = P + 1;
     float fx = tqx - G.cx, fy = tqy - G.cy, fz = tqz - G.cz;
     if (!(in_unit(fx) & in_unit(fy) & in_unit(fz))) {
-        fast_cell_update<P>(sb, tqx, tqy, tqz, G);
+        fast_cell_update<P, SR>(sb, tqx, tqy, tqz, G);
         fx = tqx - G.cx;
         fy = tqy - G.cy;
         fz = tqz - G.cz;
@@ -1273,12 +1285,12 @@ __device__ __forceinline__ bool sample_fast2(const RenderArgs &A, const TfTable 
     float2 Ylo[Q], Yhi[Q], Zlo, Zhi;
 #pragma unroll
     for (int cz = 0; cz < Q; cz++) {
-        Ylo[cz] = mul2s(Ny[0], lo2(G.c[cz * Q]));
-        Yhi[cz] = mul2s(Ny[0], hi2(G.c[cz * Q]));
+        Ylo[cz] = mul2s(Ny[0], lo2(G.get(cz * Q)));
+        Yhi[cz] = mul2s(Ny[0], hi2(G.get(cz * Q)));
 #pragma unroll
         for (int by = 1; by < Q; by++) {
-            Ylo[cz] = fma2s(Ny[by], lo2(G.c[cz * Q + by]), Ylo[cz]);
-            Yhi[cz] = fma2s(Ny[by], hi2(G.c[cz * Q + by]), Yhi[cz]);
+            Ylo[cz] = fma2s(Ny[by], lo2(G.get(cz * Q + by)), Ylo[cz]);
+            Yhi[cz] = fma2s(Ny[by], hi2(G.get(cz * Q + by)), Yhi[cz]);
         }
     }
     if constexpr (P == 3) {  // pairwise trees: depth 3 instead of 4-long chains
@@ -1331,12 +1343,12 @@ __device__ __forceinline__ bool sample_fast2(const RenderArgs &A, const TfTable 
     float2 Wlo[Q], Whi[Q];
 #pragma unroll
     for (int by = 0; by < Q; by++) {
-        Wlo[by] = mul2s(Nz[0], lo2(G.c[by]));
-        Whi[by] = mul2s(Nz[0], hi2(G.c[by]));
+        Wlo[by] = mul2s(Nz[0], lo2(G.get(by)));
+        Whi[by] = mul2s(Nz[0], hi2(G.get(by)));
 #pragma unroll
         for (int cz = 1; cz < Q; cz++) {
-            Wlo[by] = fma2s(Nz[cz], lo2(G.c[cz * Q + by]), Wlo[by]);
-            Whi[by] = fma2s(Nz[cz], hi2(G.c[cz * Q + by]), Whi[by]);
+            Wlo[by] = fma2s(Nz[cz], lo2(G.get(cz * Q + by)), Wlo[by]);
+            Whi[by] = fma2s(Nz[cz], hi2(G.get(cz * Q + by)), Whi[by]);
         }
     }
     Dlo = mul2s(Ey[0], sub2(Wlo[1], Wlo[0]));
@@ -1353,7 +1365,7 @@ __device__ __forceinline__ bool sample_fast2(const RenderArgs &A, const TfTable 
     return true;
 }
 
-template <bool DEBUG, bool SMEM_GRID, int P, int MINB>
+template <bool DEBUG, bool SMEM_GRID, int P, int MINB, int SR>
 __global__ void __launch_bounds__(128, MINB) render2_kernel(const BlockDesc *__restrict__ descs,
                                                          const int16_t *__restrict__ grid,
                                                          const int32_t *__restrict__ idx2slot, const RenderArgs A,
@@ -1443,7 +1455,9 @@ __global__ void __launch_bounds__(128, MINB) render2_kernel(const BlockDesc *__r
         F.deg = 0;
         BlockFast &b = F.b;
         bool fast = false;
-        FastCell<P> G;
+        __shared__ float4 s_cellrows[SR > 0 ? SR : 1][128];
+        FastCell<P, SR> G;
+        G.s = &s_cellrows[0][threadIdx.x];
         G.key = -1;
         G.cx = G.cy = G.cz = -1e30f;
         G.inner = 0;
@@ -1494,7 +1508,7 @@ __global__ void __launch_bounds__(128, MINB) render2_kernel(const BlockDesc *__r
                 const float tqx = fmaf(dk, M.dtq[0], M.tq0[0]);
                 const float tqy = fmaf(dk, M.dtq[1], M.tq0[1]);
                 const float tqz = fmaf(dk, M.dtq[2], M.tq0[2]);
-                ok = sample_fast2<P>(A, tf, b, tqx, tqy, tqz, C, G, M);
+                ok = sample_fast2<P, SR>(A, tf, b, tqx, tqy, tqz, C, G, M);
             }
             if (!ok) {
                 const int32_t slot = vld(F.slot), deg = vld(F.deg);
@@ -1752,16 +1766,17 @@ static void launch_render_v(const LaunchArgs &L, const RenderArgs &A) {
                                                                         L.rgba, L.stats, L.nsamp, L.ohash);
 }
 
-template <bool DEBUG, bool SMEM, int P, int MINB>
+template <bool DEBUG, bool SMEM, int P, int MINB, int SR = 0>
 static void launch_render2_v(const LaunchArgs &L, const RenderArgs &A) {
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(render2_kernel<DEBUG, SMEM, P, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(render2_kernel<DEBUG, SMEM, P, MINB, SR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              64 * 1024);
         configured = true;
     }
-    render2_kernel<DEBUG, SMEM, P, MINB><<<L.grid, 128, L.smem, L.st>>>(L.descs, L.owner, L.idx, A, L.gargs, L.gtf,
-                                                                         L.rgba, L.stats, L.nsamp, L.ohash);
+    render2_kernel<DEBUG, SMEM, P, MINB, SR><<<L.grid, 128, L.smem, L.st>>>(L.descs, L.owner, L.idx, A, L.gargs,
+                                                                             L.gtf, L.rgba, L.stats, L.nsamp,
+                                                                             L.ohash);
 }
 
 // AFAM_RENDER_V1=1: the round-1 sample loop (render_kernel) for spline
@@ -1779,7 +1794,7 @@ static int render2_minb() {
     static int v = [] {
         const char *e = getenv("AFAM_RENDER2_MINB");
         const int m = e ? atoi(e) : 0;
-        return (m == 4 || m == 5) ? m : 3;
+        return (m == 4 || m == 5 || m == 48 || m == 44) ? m : 3;
     }();
     return v;
 }
@@ -1796,6 +1811,8 @@ static void launch_render(const LaunchArgs &L, const RenderArgs &A, int fd) {
         switch (render2_minb()) {
             case 4: return launch_render2_v<DEBUG, SMEM, 3, 4>(L, A);
             case 5: return launch_render2_v<DEBUG, SMEM, 3, 5>(L, A);
+            case 48: return launch_render2_v<DEBUG, SMEM, 3, 4, 8>(L, A);   // 8 rows in shared memory
+            case 44: return launch_render2_v<DEBUG, SMEM, 3, 4, 4>(L, A);   // 4 rows in shared memory
             default: return launch_render2_v<DEBUG, SMEM, 3, 3>(L, A);
         }
     }
