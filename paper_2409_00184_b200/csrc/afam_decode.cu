@@ -388,65 +388,74 @@ __device__ __forceinline__ void fx_decode_block(const BlockDesc &d, const int32_
     float er[4];        // threads 0..128: the lattice column x = 64 / row y = 64 value of the last 4 planes
     int knext = 0;
 
+    // x stage of plane z into X plane z & 1 (ring slot z & 3)
+    auto xstage = [&](int z) {
+        mbar_wait(bar + (z & 3), (uint32_t)((z >> 2) & 1));
+        const float *Cp = ring + (z & 3) * sstride;
+        float *X = xb + (z & 1) * kFxXRows * kFxXPitch;
+                // ---- x stage: rows g + 16 i two at a time (four independent FFMA2
+                // chains), threads 0..15 also take control row 64; window
+                // entries 10, 11 never carry weight (offsets <= 3 + 3, p <= 3)
+#pragma unroll
+                for (int i = 0; i < 64 / NG; i += 2) {
+                    const int ra = g + NG * i, rb = ra + NG;
+                    const float4 *sa = reinterpret_cast<const float4 *>(Cp + min(ra, n - 1) * pitch + cw);
+                    const float4 *sb = reinterpret_cast<const float4 *>(Cp + min(rb, n - 1) * pitch + cw);
+                    const float4 a0 = sa[0], a1 = sa[1], a2 = sa[2], b0 = sb[0], b1 = sb[1], b2 = sb[2];
+                    const float va[10] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y};
+                    const float vb[10] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x, b2.y};
+                    // even / odd taps in separate chains: eight independent FFMA2 chains of 5
+                    float2 pa01 = make_float2(0.f, 0.f), pa23 = pa01, pb01 = pa01, pb23 = pa01;
+                    float2 qa01 = pa01, qa23 = pa01, qb01 = pa01, qb23 = pa01;
+#pragma unroll
+                    for (int e = 0; e < 10; e += 2) {
+                        pa01 = __ffma2_rn(make_float2(wx[0][e], wx[1][e]), make_float2(va[e], va[e]), pa01);
+                        pa23 = __ffma2_rn(make_float2(wx[2][e], wx[3][e]), make_float2(va[e], va[e]), pa23);
+                        pb01 = __ffma2_rn(make_float2(wx[0][e], wx[1][e]), make_float2(vb[e], vb[e]), pb01);
+                        pb23 = __ffma2_rn(make_float2(wx[2][e], wx[3][e]), make_float2(vb[e], vb[e]), pb23);
+                        qa01 = __ffma2_rn(make_float2(wx[0][e + 1], wx[1][e + 1]), make_float2(va[e + 1], va[e + 1]), qa01);
+                        qa23 = __ffma2_rn(make_float2(wx[2][e + 1], wx[3][e + 1]), make_float2(va[e + 1], va[e + 1]), qa23);
+                        qb01 = __ffma2_rn(make_float2(wx[0][e + 1], wx[1][e + 1]), make_float2(vb[e + 1], vb[e + 1]), qb01);
+                        qb23 = __ffma2_rn(make_float2(wx[2][e + 1], wx[3][e + 1]), make_float2(vb[e + 1], vb[e + 1]), qb23);
+                    }
+                    pa01 = __fadd2_rn(pa01, qa01);
+                    pa23 = __fadd2_rn(pa23, qa23);
+                    pb01 = __fadd2_rn(pb01, qb01);
+                    pb23 = __fadd2_rn(pb23, qb23);
+                    if (ra < n) *reinterpret_cast<float4 *>(X + ra * kFxXPitch + 4 * q) = make_float4(pa01.x, pa01.y, pa23.x, pa23.y);
+                    if (rb < n) *reinterpret_cast<float4 *>(X + rb * kFxXPitch + 4 * q) = make_float4(pb01.x, pb01.y, pb23.x, pb23.y);
+                }
+                if (g == NG - 1 && n > 64) {  // control row 64 (the last row group: the edge values sit on warps 0..4)
+                    const float4 *src = reinterpret_cast<const float4 *>(Cp + 64 * pitch + cw);
+                    const float4 v0 = src[0], v1 = src[1], v2 = src[2];
+                    const float w[10] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, v2.x, v2.y};
+                    float2 a01 = make_float2(0.f, 0.f), a23 = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int e = 0; e < 10; e++) {
+                        a01 = __ffma2_rn(make_float2(wx[0][e], wx[1][e]), make_float2(w[e], w[e]), a01);
+                        a23 = __ffma2_rn(make_float2(wx[2][e], wx[3][e]), make_float2(w[e], w[e]), a23);
+                    }
+                    *reinterpret_cast<float4 *>(X + 64 * kFxXPitch + 4 * q) = make_float4(a01.x, a01.y, a23.x, a23.y);
+                }
+                if (tid < n) xcol[(z & 1) * 72 + tid] = Cp[tid * pitch + n - 1];  // u = 1 column: control column n-1
+    };
+    // software pipeline over the planes, one barrier per plane: the x stage
+    // of plane zc + 1 runs beside the y / z stages of plane zc (different X
+    // buffers), so each warp has two independent instruction streams
+    xstage(0);
+    __syncthreads();
+    if (tid == 0 && kFxRing < n) {  // slot 0 is free: plane 0's x stage is done
+        fence_proxy_async();
+        mbar_arrive_expect_tx(bar, plane_bytes);
+        tma_load_1d(ring, C + (size_t)kFxRing * n * pitch, plane_bytes, bar);
+    }
     for (int z0 = 0; z0 < n; z0 += 4) {
 #pragma unroll
         for (int u = 0; u < 4; u++) {
             const int zc = z0 + u;
             if (zc >= n) break;
-            mbar_wait(bar + u, (uint32_t)((zc >> 2) & 1));
-            const float *Cp = ring + u * sstride;
-            float *X = xb + (u & 1) * kFxXRows * kFxXPitch;
-            // ---- x stage: rows g + 16 i two at a time (four independent FFMA2
-            // chains), threads 0..15 also take control row 64; window
-            // entries 10, 11 never carry weight (offsets <= 3 + 3, p <= 3)
-#pragma unroll
-            for (int i = 0; i < 64 / NG; i += 2) {
-                const int ra = g + NG * i, rb = ra + NG;
-                const float4 *sa = reinterpret_cast<const float4 *>(Cp + min(ra, n - 1) * pitch + cw);
-                const float4 *sb = reinterpret_cast<const float4 *>(Cp + min(rb, n - 1) * pitch + cw);
-                const float4 a0 = sa[0], a1 = sa[1], a2 = sa[2], b0 = sb[0], b1 = sb[1], b2 = sb[2];
-                const float va[10] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y};
-                const float vb[10] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x, b2.y};
-                // even / odd taps in separate chains: eight independent FFMA2 chains of 5
-                float2 pa01 = make_float2(0.f, 0.f), pa23 = pa01, pb01 = pa01, pb23 = pa01;
-                float2 qa01 = pa01, qa23 = pa01, qb01 = pa01, qb23 = pa01;
-#pragma unroll
-                for (int e = 0; e < 10; e += 2) {
-                    pa01 = __ffma2_rn(make_float2(wx[0][e], wx[1][e]), make_float2(va[e], va[e]), pa01);
-                    pa23 = __ffma2_rn(make_float2(wx[2][e], wx[3][e]), make_float2(va[e], va[e]), pa23);
-                    pb01 = __ffma2_rn(make_float2(wx[0][e], wx[1][e]), make_float2(vb[e], vb[e]), pb01);
-                    pb23 = __ffma2_rn(make_float2(wx[2][e], wx[3][e]), make_float2(vb[e], vb[e]), pb23);
-                    qa01 = __ffma2_rn(make_float2(wx[0][e + 1], wx[1][e + 1]), make_float2(va[e + 1], va[e + 1]), qa01);
-                    qa23 = __ffma2_rn(make_float2(wx[2][e + 1], wx[3][e + 1]), make_float2(va[e + 1], va[e + 1]), qa23);
-                    qb01 = __ffma2_rn(make_float2(wx[0][e + 1], wx[1][e + 1]), make_float2(vb[e + 1], vb[e + 1]), qb01);
-                    qb23 = __ffma2_rn(make_float2(wx[2][e + 1], wx[3][e + 1]), make_float2(vb[e + 1], vb[e + 1]), qb23);
-                }
-                pa01 = __fadd2_rn(pa01, qa01);
-                pa23 = __fadd2_rn(pa23, qa23);
-                pb01 = __fadd2_rn(pb01, qb01);
-                pb23 = __fadd2_rn(pb23, qb23);
-                if (ra < n) *reinterpret_cast<float4 *>(X + ra * kFxXPitch + 4 * q) = make_float4(pa01.x, pa01.y, pa23.x, pa23.y);
-                if (rb < n) *reinterpret_cast<float4 *>(X + rb * kFxXPitch + 4 * q) = make_float4(pb01.x, pb01.y, pb23.x, pb23.y);
-            }
-            if (g == NG - 1 && n > 64) {  // control row 64 (the last row group: the edge values sit on warps 0..4)
-                const float4 *src = reinterpret_cast<const float4 *>(Cp + 64 * pitch + cw);
-                const float4 v0 = src[0], v1 = src[1], v2 = src[2];
-                const float w[10] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, v2.x, v2.y};
-                float2 a01 = make_float2(0.f, 0.f), a23 = make_float2(0.f, 0.f);
-#pragma unroll
-                for (int e = 0; e < 10; e++) {
-                    a01 = __ffma2_rn(make_float2(wx[0][e], wx[1][e]), make_float2(w[e], w[e]), a01);
-                    a23 = __ffma2_rn(make_float2(wx[2][e], wx[3][e]), make_float2(w[e], w[e]), a23);
-                }
-                *reinterpret_cast<float4 *>(X + 64 * kFxXPitch + 4 * q) = make_float4(a01.x, a01.y, a23.x, a23.y);
-            }
-            if (tid < n) xcol[(u & 1) * 72 + tid] = Cp[tid * pitch + n - 1];  // u = 1 column: control column n-1
-            __syncthreads();
-            if (tid == 0 && zc + kFxRing < n) {  // ring slot u is free: every thread passed its x stage
-                fence_proxy_async();
-                mbar_arrive_expect_tx(bar + u, plane_bytes);
-                tma_load_1d(ring + (size_t)u * sstride, C + (size_t)(zc + kFxRing) * n * pitch, plane_bytes, bar + u);
-            }
+            if (zc + 1 < n) xstage(zc + 1);
+            const float *X = xb + (u & 1) * kFxXRows * kFxXPitch;
             // ---- y stage (into the register ring)
 #pragma unroll
             for (int yi = 0; yi < YPT; yi++)
@@ -505,6 +514,15 @@ __device__ __forceinline__ void fx_decode_block(const BlockDesc &d, const int32_
                     for (int c = 0; c < Q; c++) acc = fmaf(wz[c], er[(u - P + c) & 3], acc);
                     ok[tid <= 64 ? tid * M + 64 : 64 * M + tid - 65] = acc;
                 }
+            }
+            __syncthreads();
+            // plane zc + 1's slot is free (its x stage is done): fetch plane zc + 1 + kFxRing
+            if (tid == 0 && zc + 1 + kFxRing < n) {
+                const int sl = (zc + 1) & 3;
+                fence_proxy_async();
+                mbar_arrive_expect_tx(bar + sl, plane_bytes);
+                tma_load_1d(ring + (size_t)sl * sstride, C + (size_t)(zc + 1 + kFxRing) * n * pitch, plane_bytes,
+                            bar + sl);
             }
         }
     }

@@ -356,7 +356,8 @@ __device__ __forceinline__ void decode_f32(const BlockLite &b, const BlockDesc *
 // are shared with the float32 path.
 template <int P>
 __device__ __forceinline__ void decode_f64(const BlockLite &b, const BlockDesc *__restrict__ dp, int32_t slot,
-                                           GatherCache &G, const double (&pos)[3], float &v, float (&g)[3]) {
+                                           GatherCache &G, const double (&pos)[3], const TfTable &tf, float dom_lo,
+                                           float dom_hi, float &v, float4 &tfv, float (&g)[3]) {
     constexpr int Q = P + 1;
     double N[3][Q], E[3][P], span[3];
     int s[3];
@@ -371,9 +372,29 @@ __device__ __forceinline__ void decode_f64(const BlockLite &b, const BlockDesc *
         basis_eval<P, double>(t, u, N[a], E[a]);
     }
     gather_quad<P>(b, slot, G, s[0] - P, s[1] - P, s[2] - P);
-    double vv, gg[3];
-    contract_quad<P, double>(G.c4, N[0], E[0], N[1], E[1], N[2], E[2], vv, gg);
+    // value pass in float64 (x -> y -> z), then the TF: the gradient only
+    // for samples it makes visible (alpha_tf = 0 adds nothing to C or A,
+    // render.py:451-455, so the frame is unchanged)
+    double vv = 0.0;
+#pragma unroll
+    for (int cz = 0; cz < Q; cz++) {
+        double ay = 0.0;
+#pragma unroll
+        for (int by = 0; by < Q; by++) {
+            double acc = 0.0, dacc = 0.0;
+            row_contract<P, 0, double>(G.c4[cz * Q + by], N[0], E[0], acc, dacc);
+            ay = fma(N[1][by], acc, ay);
+        }
+        vv = fma(N[2][cz], ay, vv);
+    }
     v = (float)vv;
+    tfv = tf_eval(tf, fminf(fmaxf(v, dom_lo), dom_hi));
+    if (!(tfv.w > 0.f)) {
+        g[0] = g[1] = g[2] = 0.f;
+        return;
+    }
+    double gg[3];
+    contract_quad<P, double>(G.c4, N[0], E[0], N[1], E[1], N[2], E[2], vv, gg);
 #pragma unroll
     for (int a = 0; a < 3; a++) g[a] = (float)(gg[a] / span[a]);
 }
@@ -935,8 +956,7 @@ __device__ __noinline__ int sample_exact(const RenderArgs *GA, const TfTable *tf
     float4 tfv;
     const bool f64 = b.flags & AFAM_SLOT_FP64;
     if (f64) {
-        decode_f64<P>(b, dp, slot, G, pos, v, g);
-        tfv = tf_eval(*tf, fminf(fmaxf(v, GA->dom_lo), GA->dom_hi));
+        decode_f64<P>(b, dp, slot, G, pos, *tf, GA->dom_lo, GA->dom_hi, v, tfv, g);
     } else {
         decode_f32<P>(b, dp, slot, G, pos, *tf, GA->dom_lo, GA->dom_hi, v, tfv, g);
     }
