@@ -355,6 +355,19 @@ __device__ __forceinline__ void decode_f32(const BlockLite &b, const BlockDesc *
 // accumulation; control points are float32 in the file, so the float4 rows
 // are shared with the float32 path.
 template <int P>
+__device__ __noinline__ void grad_f64(const float4 *__restrict__ base, size_t plane, const double (&N)[3][P + 1],
+                                      const double (&E)[3][P], double (&gg)[3]) {
+    constexpr int Q = P + 1;
+    float4 c4[16];
+#pragma unroll
+    for (int cz = 0; cz < Q; cz++)
+#pragma unroll
+        for (int by = 0; by < Q; by++) c4[cz * Q + by] = __ldg(base + cz * plane + by);
+    double vv;
+    contract_quad<P, double>(c4, N[0], E[0], N[1], E[1], N[2], E[2], vv, gg);
+}
+
+template <int P>
 __device__ __forceinline__ void decode_f64(const BlockLite &b, const BlockDesc *__restrict__ dp, int32_t slot,
                                            GatherCache &G, const double (&pos)[3], const TfTable &tf, float dom_lo,
                                            float dom_hi, float &v, float4 &tfv, float (&g)[3]) {
@@ -393,8 +406,12 @@ __device__ __forceinline__ void decode_f64(const BlockLite &b, const BlockDesc *
         g[0] = g[1] = g[2] = 0.f;
         return;
     }
+    // the gradient in its own frame (re-reading the rows through L1): kept
+    // out of line so the value pass's float64 conversions are not held live
+    // across it (a fused value + gradient pass spilled ~1 KB per thread)
     double gg[3];
-    contract_quad<P, double>(G.c4, N[0], E[0], N[1], E[1], N[2], E[2], vv, gg);
+    grad_f64<P>(b.ctrl4 + ((size_t)(s[2] - P) * b.ncp + (s[0] - P)) * b.ncp + (s[1] - P), (size_t)b.ncp * b.ncp,
+                N, E, gg);
 #pragma unroll
     for (int a = 0; a < 3; a++) g[a] = (float)(gg[a] / span[a]);
 }
