@@ -44,7 +44,7 @@ extern "C" {
 #define AFAM_E_CUDA 5
 
 #define AFAM_MAX_DEGREE 3     /* degrees 1..3 are evaluated on device */
-#define AFAM_MAX_TF_POINTS 32
+#define AFAM_MAX_TF_POINTS 32  /* inline TF control points in afam_frame; more via color_pts / opacity_pts */
 
 /* Per-slot flags (afam_store_info). */
 #define AFAM_SLOT_VALID 1u
@@ -253,6 +253,13 @@ typedef struct {
     double color[AFAM_MAX_TF_POINTS][4];  /* scalar, r, g, b */
     double opacity[AFAM_MAX_TF_POINTS][2];/* scalar, alpha */
     uint32_t flags;                       /* AFAM_RENDER_* */
+    /* Optional: when non-NULL, the control points are read from these
+     * row-major arrays (ncolor x 4, nopacity x 2) instead of the inline ones,
+     * and ncolor / nopacity are unbounded (the reference's TransferFunction
+     * takes any number of points, render.py:93-115).  Read only during the
+     * afam_render call. */
+    const double *color_pts;
+    const double *opacity_pts;
 } afam_frame;
 
 #define AFAM_RENDER_DEBUG 1u   /* write per-ray sample counts + owner hashes */

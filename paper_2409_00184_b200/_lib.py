@@ -61,6 +61,8 @@ class AfamFrame(C.Structure):
         ("color", (C.c_double * 4) * AFAM_MAX_TF_POINTS),
         ("opacity", (C.c_double * 2) * AFAM_MAX_TF_POINTS),
         ("flags", C.c_uint32),
+        ("color_pts", C.c_void_p),
+        ("opacity_pts", C.c_void_p),
     ]
 
 

@@ -58,17 +58,19 @@ struct HostTimer {
 
 namespace afam {
 
-constexpr int kTfMaxBp = 2 * AFAM_MAX_TF_POINTS;
 constexpr int kTfBuckets = 512;
 
+// The breakpoint arrays (val, slope, bp: nbp entries each, any number of TF
+// control points) follow the table in the frame's argument upload; the
+// pointers are set to their device copies when the upload is packed.
 struct TfTable {
-    float4 val[kTfMaxBp];     // (r, g, b, alpha) at breakpoint j
-    float4 slope[kTfMaxBp];   // d/dv on [bp[j], bp[j+1]); 0 past the last breakpoint
     float4 c0[kTfBuckets];    // rgb at the bucket start; .w NaN: a color breakpoint lies in the bucket
     float4 dc[kTfBuckets];    // rgb increment across the bucket
     float2 alpha[kTfBuckets]; // (alpha at the bucket start, increment); .y NaN: an opacity breakpoint lies in it
-    float bp[kTfMaxBp];       // sorted union of color and opacity control scalars
-    int8_t lut[kTfBuckets];   // last breakpoint <= bucket start (-1: none)
+    int32_t lut[kTfBuckets];  // last breakpoint <= bucket start (-1: none)
+    const float4 *val;        // (r, g, b, alpha) at breakpoint j
+    const float4 *slope;      // d/dv on [bp[j], bp[j+1]); 0 past the last breakpoint
+    const float *bp;          // sorted union of color and opacity control scalars
     int32_t nbp;
     float lo, scale;          // bucket coordinate = (v - lo) * scale over the TF domain
     float op_lo, op_hi;       // opacity support (see build_tf_table)
@@ -1622,41 +1624,67 @@ __global__ void finish_stats_kernel(afam_render_stats *s) {
     if (s->missing_key == INT64_MAX) s->missing_key = -1;
 }
 
-// np.interp(x, xs, ys) (numpy compiled_base.c) in float64 on the host.
-static double host_interp(double x, const double (*pts)[4], const double (*opts)[2], int n, int col, bool color) {
-    auto X = [&](int k) { return color ? pts[k][0] : opts[k][0]; };
-    auto Y = [&](int k) { return color ? pts[k][col] : opts[k][1]; };
+// np.interp(x, xs, ys) (numpy compiled_base.c) in float64 on the host, over
+// n points of `stride` doubles (scalar first), value column `col`.
+static double host_interp(double x, const double *pts, int n, int stride, int col) {
+    auto X = [&](int k) { return pts[(size_t)k * stride]; };
+    auto Y = [&](int k) { return pts[(size_t)k * stride + col]; };
     if (n == 1 || x <= X(0)) return Y(0);
     if (x >= X(n - 1)) return Y(n - 1);
-    int j = 0;
-    while (j + 1 < n && X(j + 1) <= x) ++j;
+    int j;  // the last k with X(k) <= x (binary search)
+    {
+        int lo = 0, hi = n - 1;  // X(lo) <= x < X(hi)
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) / 2;
+            if (X(mid) <= x) lo = mid;
+            else hi = mid;
+        }
+        j = lo;
+    }
     if (X(j) == x) return Y(j);
     const double slope = (Y(j + 1) - Y(j)) / (X(j + 1) - X(j));
     return slope * (x - X(j)) + Y(j);
 }
 
-static void build_tf_table(const afam_frame *F, TfTable &T) {
+// The TF's control points: the inline arrays, or the caller's when given.
+static const double *tf_color_pts(const afam_frame *F) { return F->color_pts ? F->color_pts : &F->color[0][0]; }
+static const double *tf_opacity_pts(const afam_frame *F) {
+    return F->opacity_pts ? F->opacity_pts : &F->opacity[0][0];
+}
+
+// Host half of the TF table: the device table plus its breakpoint arrays.
+struct TfHost {
+    TfTable T;
+    std::vector<float4> val, slope;
+    std::vector<float> bp;
+};
+
+static void build_tf_table(const afam_frame *F, TfHost &H) {
+    TfTable &T = H.T;
+    const double *cp = tf_color_pts(F), *op = tf_opacity_pts(F);
     std::vector<double> xs, xc, xo;
-    for (int k = 0; k < F->ncolor; k++) xc.push_back(F->color[k][0]);
-    for (int k = 0; k < F->nopacity; k++) xo.push_back(F->opacity[k][0]);
+    for (int k = 0; k < F->ncolor; k++) xc.push_back(cp[4 * k]);
+    for (int k = 0; k < F->nopacity; k++) xo.push_back(op[2 * k]);
     xs = xc;
     xs.insert(xs.end(), xo.begin(), xo.end());
     std::sort(xs.begin(), xs.end());
     xs.erase(std::unique(xs.begin(), xs.end()), xs.end());
     T.nbp = (int)xs.size();
     auto eval = [&](double x, int c) {
-        return c < 3 ? host_interp(x, F->color, F->opacity, F->ncolor, 1 + c, true)
-                     : host_interp(x, F->color, F->opacity, F->nopacity, 1, false);
+        return c < 3 ? host_interp(x, cp, F->ncolor, 4, 1 + c) : host_interp(x, op, F->nopacity, 2, 1);
     };
+    H.val.assign(T.nbp, make_float4(0.f, 0.f, 0.f, 0.f));
+    H.slope.assign(T.nbp, make_float4(0.f, 0.f, 0.f, 0.f));
+    H.bp.assign(T.nbp, 0.f);
     for (int j = 0; j < T.nbp; j++) {
-        T.bp[j] = (float)xs[j];
+        H.bp[j] = (float)xs[j];
         float v[4], s[4];
         for (int c = 0; c < 4; c++) {
             v[c] = (float)eval(xs[j], c);
             s[c] = j + 1 < T.nbp ? (float)((eval(xs[j + 1], c) - eval(xs[j], c)) / (xs[j + 1] - xs[j])) : 0.f;
         }
-        T.val[j] = make_float4(v[0], v[1], v[2], v[3]);
-        T.slope[j] = make_float4(s[0], s[1], s[2], s[3]);
+        H.val[j] = make_float4(v[0], v[1], v[2], v[3]);
+        H.slope[j] = make_float4(s[0], s[1], s[2], s[3]);
     }
     // Opacity support: below the breakpoint preceding the first nonzero
     // opacity point (and above the one following the last) every breakpoint
@@ -1668,7 +1696,7 @@ static void build_tf_table(const afam_frame *F, TfTable &T) {
         const int n = F->nopacity;
         int k1 = -1, k2 = -1;
         for (int k = 0; k < n; k++)
-            if (F->opacity[k][1] != 0.0) {
+            if (op[2 * k + 1] != 0.0) {
                 if (k1 < 0) k1 = k;
                 k2 = k;
             }
@@ -1677,11 +1705,8 @@ static void build_tf_table(const afam_frame *F, TfTable &T) {
             T.op_lo = inf;
             T.op_hi = -inf;
         } else {
-            T.op_lo = k1 > 0 && (float)F->opacity[k1][0] > (float)F->opacity[k1 - 1][0] ? (float)F->opacity[k1 - 1][0]
-                                                                                       : -inf;
-            T.op_hi = k2 + 1 < n && (float)F->opacity[k2 + 1][0] > (float)F->opacity[k2][0]
-                          ? (float)F->opacity[k2 + 1][0]
-                          : inf;
+            T.op_lo = k1 > 0 && (float)op[2 * k1] > (float)op[2 * (k1 - 1)] ? (float)op[2 * (k1 - 1)] : -inf;
+            T.op_hi = k2 + 1 < n && (float)op[2 * (k2 + 1)] > (float)op[2 * k2] ? (float)op[2 * (k2 + 1)] : inf;
         }
     }
     const double lo = F->domain_lo, hi = F->domain_hi;
@@ -1702,7 +1727,7 @@ static void build_tf_table(const afam_frame *F, TfTable &T) {
         const double x0 = lo + w * i, x1 = lo + w * (i + 1);
         int j = -1;
         while (j + 1 < T.nbp && xs[j + 1] <= x0) ++j;
-        T.lut[i] = (int8_t)j;
+        T.lut[i] = j;
         if (clean(xo, x0, x1)) {
             const double a0 = eval(x0, 3), a1 = eval(x1, 3);
             T.alpha[i] = make_float2((float)a0, (float)(a1 - a0));
@@ -1904,9 +1929,11 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
     AFAM_CHECK(F->width >= 1 && F->height >= 1, AFAM_E_VALUE, "frame dimensions must be positive");
     AFAM_CHECK(F->sample_distance > 0, AFAM_E_VALUE, "sample distance must be positive");
     AFAM_CHECK(F->o_max > 0 && F->o_max <= 1, AFAM_E_VALUE, "o_max must be in (0, 1]");
-    AFAM_CHECK(F->ncolor >= 1 && F->ncolor <= AFAM_MAX_TF_POINTS && F->nopacity >= 1 &&
-                   F->nopacity <= AFAM_MAX_TF_POINTS,
-               AFAM_E_VALUE, "transfer function needs 1..%d control points", AFAM_MAX_TF_POINTS);
+    AFAM_CHECK(F->ncolor >= 1 && F->nopacity >= 1, AFAM_E_VALUE, "transfer function needs control points");
+    AFAM_CHECK((F->ncolor <= AFAM_MAX_TF_POINTS || F->color_pts) &&
+                   (F->nopacity <= AFAM_MAX_TF_POINTS || F->opacity_pts),
+               AFAM_E_VALUE, "more than %d inline transfer-function points (pass color_pts / opacity_pts)",
+               AFAM_MAX_TF_POINTS);
     AFAM_CHECK(nblocks >= 0 && nblocks < 32768, AFAM_E_VALUE, "too many resident blocks (%d)", nblocks);
     const bool debug = F->flags & AFAM_RENDER_DEBUG;
     AFAM_CHECK(!debug || (nsamp && ohash), AFAM_E_VALUE, "debug buffers missing");
@@ -1965,32 +1992,30 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
     // frame with the same TF)
     struct TfCache {
         bool valid = false;
-        double key[2 + 4 * AFAM_MAX_TF_POINTS + 2 * AFAM_MAX_TF_POINTS + 2];
-        TfTable table;
+        std::vector<double> key;
+        TfHost table;
     };
     static thread_local TfCache tfc;
-    double key[sizeof(tfc.key) / sizeof(double)];
+    std::vector<double> key;
     {
-        memset(key, 0, sizeof(key));
-        int o = 0;
-        key[o++] = F->ncolor;
-        key[o++] = F->nopacity;
-        for (int k = 0; k < F->ncolor; k++)
-            for (int c = 0; c < 4; c++) key[o + 4 * k + c] = F->color[k][c];
-        o += 4 * AFAM_MAX_TF_POINTS;
-        for (int k = 0; k < F->nopacity; k++)
-            for (int c = 0; c < 2; c++) key[o + 2 * k + c] = F->opacity[k][c];
-        o += 2 * AFAM_MAX_TF_POINTS;
-        key[o++] = F->domain_lo;
-        key[o++] = F->domain_hi;
+        const double *cp = tf_color_pts(F), *op = tf_opacity_pts(F);
+        key.reserve(4 + 4 * (size_t)F->ncolor + 2 * (size_t)F->nopacity);
+        key.push_back(F->ncolor);
+        key.push_back(F->nopacity);
+        key.insert(key.end(), cp, cp + 4 * (size_t)F->ncolor);
+        key.insert(key.end(), op, op + 2 * (size_t)F->nopacity);
+        key.push_back(F->domain_lo);
+        key.push_back(F->domain_hi);
     }
-    if (!tfc.valid || memcmp(key, tfc.key, sizeof(key)) != 0) {
-        memset(&tfc.table, 0, sizeof(tfc.table));
+    if (!tfc.valid || key.size() != tfc.key.size() ||
+        memcmp(key.data(), tfc.key.data(), key.size() * sizeof(double)) != 0) {
+        memset(&tfc.table.T, 0, sizeof(tfc.table.T));
         build_tf_table(F, tfc.table);
-        memcpy(tfc.key, key, sizeof(key));
+        tfc.key.swap(key);
         tfc.valid = true;
     }
-    const TfTable &tf = tfc.table;
+    const TfHost &tfh = tfc.table;
+    const TfTable &tf = tfh.T;
     A.tf_lo = tf.lo;
     A.tf_scale = tf.scale;
     A.op_lo = tf.op_lo;
@@ -2020,10 +2045,13 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
     ht.mark();
     A.cells = cells;
     A.nb = nblocks;
-    // one upload: [RenderArgs | TfTable | owner grid | slot of each owner index]
+    // one upload: [RenderArgs | TfTable | TF breakpoints (val, slope, bp) |
+    // owner grid | slot of each owner index]
     auto al = [](size_t v) { return (v + 255) & ~(size_t)255; };
     const size_t gbytes = grid.size() * sizeof(int16_t);
-    const size_t off_tf = al(sizeof(RenderArgs)), off_grid = off_tf + al(sizeof(TfTable));
+    const size_t nbp = (size_t)std::max(tf.nbp, 1);
+    const size_t off_tf = al(sizeof(RenderArgs)), off_bp = off_tf + al(sizeof(TfTable));
+    const size_t off_grid = off_bp + al(nbp * (2 * sizeof(float4) + sizeof(float)));
     const size_t off_idx = off_grid + al(gbytes);
     const size_t total = off_idx + std::max<size_t>(1, (size_t)nblocks) * sizeof(int32_t);
     // staged in this thread's pinned buffer, so the H2D copy is asynchronous
@@ -2043,13 +2071,23 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
         AFAM_CUDA(cudaEventSynchronize(tc->ev_pack));
     }
     unsigned char *pack = tc->pack;
-    memset(pack, 0, total);
-    memcpy(pack, &A, sizeof(A));
-    memcpy(pack + off_tf, &tf, sizeof(tf));
-    memcpy(pack + off_grid, grid.data(), gbytes);
-    if (nblocks) memcpy(pack + off_idx, slots, (size_t)nblocks * sizeof(int32_t));
     unsigned char *d_pack = nullptr;
     AFAM_CUDA(cudaMallocAsync(&d_pack, total, st));
+    memset(pack, 0, total);
+    memcpy(pack, &A, sizeof(A));
+    {
+        TfTable t = tf;
+        t.val = (const float4 *)(d_pack + off_bp);
+        t.slope = t.val + nbp;
+        t.bp = (const float *)(t.slope + nbp);
+        memcpy(pack + off_tf, &t, sizeof(t));
+        const size_t n = tfh.bp.size();
+        memcpy(pack + off_bp, tfh.val.data(), n * sizeof(float4));
+        memcpy(pack + off_bp + nbp * sizeof(float4), tfh.slope.data(), n * sizeof(float4));
+        memcpy(pack + off_bp + 2 * nbp * sizeof(float4), tfh.bp.data(), n * sizeof(float));
+    }
+    memcpy(pack + off_grid, grid.data(), gbytes);
+    if (nblocks) memcpy(pack + off_idx, slots, (size_t)nblocks * sizeof(int32_t));
     AFAM_CUDA(cudaMemcpyAsync(d_pack, pack, total, cudaMemcpyHostToDevice, st));
     AFAM_CUDA(cudaEventRecord(tc->ev_pack, st));
     ht.mark();

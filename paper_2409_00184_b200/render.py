@@ -95,8 +95,6 @@ class TransferFunction:
         for pts, what in ((cp, "color"), (op, "opacity")):
             if pts.shape[0] < 1:
                 raise ValueError(f"need at least one {what} control point")
-            if pts.shape[0] > _lib.AFAM_MAX_TF_POINTS:
-                raise ValueError(f"at most {_lib.AFAM_MAX_TF_POINTS} {what} control points")
             if (np.diff(pts[:, 0]) <= 0).any():
                 raise ValueError(f"{what} control scalars must strictly increase")
             if pts[:, 1:].min() < 0 or pts[:, 1:].max() > 1:
@@ -328,9 +326,15 @@ def _frame_struct(pov, tf, params, band_rows, nparts, part, debug, full_frame=Fa
            float(params.ambient), float(params.diffuse), float(params.specular), float(params.shininess))
     cache = getattr(_tls, "frame_tmpl", None)
     if cache is None or cache[0] != key:
-        cache = (key, _frame_struct_full(pov, tf, params, band_rows, nparts, part, debug, full_frame))
+        # TFs with more control points than the struct holds inline pass them
+        # by pointer (afam_frame.color_pts / opacity_pts); the arrays live in
+        # this cache entry, and libafam reads them only inside afam_render
+        cpc, opc = np.ascontiguousarray(cp), np.ascontiguousarray(op)
+        cache = (key, _frame_struct_full(pov, tf, params, band_rows, nparts, part, debug, full_frame), cpc, opc)
         _tls.frame_tmpl = cache
     fr = _lib.AfamFrame.from_buffer_copy(cache[1])
+    if cache[2].shape[0] > _lib.AFAM_MAX_TF_POINTS or cache[3].shape[0] > _lib.AFAM_MAX_TF_POINTS:
+        fr.color_pts, fr.opacity_pts = cache[2].ctypes.data, cache[3].ctypes.data
     cam = camera_setup(pov, params)
     for a in range(3):
         fr.origin[a] = float(pov.position[a])
@@ -358,10 +362,10 @@ def _frame_struct_full(pov, tf, params, band_rows, nparts, part, debug, full_fra
     fr.specular, fr.shininess = float(params.specular), float(params.shininess)
     cp, op = np.asarray(tf.color_points, np.float64), np.asarray(tf.opacity_points, np.float64)
     fr.ncolor, fr.nopacity = cp.shape[0], op.shape[0]
-    for k in range(cp.shape[0]):
+    for k in range(min(cp.shape[0], _lib.AFAM_MAX_TF_POINTS)):
         for c in range(4):
             fr.color[k][c] = float(cp[k, c])
-    for k in range(op.shape[0]):
+    for k in range(min(op.shape[0], _lib.AFAM_MAX_TF_POINTS)):
         fr.opacity[k][0], fr.opacity[k][1] = float(op[k, 0]), float(op[k, 1])
     fr.domain_lo, fr.domain_hi = float(tf.domain[0]), float(tf.domain[1])
     fr.flags = (_lib.AFAM_RENDER_DEBUG if debug else 0) | (_lib.AFAM_RENDER_FULL_FRAME if full_frame else 0)

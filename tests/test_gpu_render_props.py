@@ -143,3 +143,37 @@ def test_determinism_and_resolution_doubling(ml_store):
     np.testing.assert_array_equal(a.rgba, b.rgba)
     hi = _render(man, models, pov, tf, render.RenderParams(width=32, height=32, sample_distance=0.02))
     np.testing.assert_array_equal(hi.rgba[::2, ::2], a.rgba)
+
+
+def test_large_transfer_function_vs_oracle(ml_store, oracle):
+    """A TF with more control points than afam_frame holds inline (passed by
+    pointer, any count, as the reference's TransferFunction allows,
+    render.py:93-124): 300 colour and 170 opacity points, breakpoints packed
+    several to a bucket, against the float64 oracle (PSNR >= 60 dB, sample
+    counts identical at o_max = 1)."""
+    from paper_2409_00184_b200 import _lib, render
+
+    man, models = ml_store
+    rng = np.random.default_rng(7)
+    xc = np.sort(rng.uniform(0.0, 1.0, 300))
+    xo = np.sort(rng.uniform(0.0, 1.0, 170))
+    cp = np.column_stack([xc, rng.uniform(0, 1, (300, 3))])
+    op = np.column_stack([xo, rng.uniform(0, 0.08, 170)])
+    assert cp.shape[0] > _lib.AFAM_MAX_TF_POINTS and op.shape[0] > _lib.AFAM_MAX_TF_POINTS
+    tf = render.TransferFunction(color_points=cp, opacity_points=op, domain=(-0.2, 1.2))
+    pov = render.PointOfView([0.4, 0.3, 2.0], [-0.1, -0.1, -1.0], [0, 1, 0])
+    for o_max in (1.0, 0.99):
+        params = render.RenderParams(width=48, height=48, sample_distance=0.01, o_max=o_max)
+        vis = render.select_visible(pov, man, params.aspect)
+        resident = {a: models[a] for a in vis}
+        fr = render.render(pov, resident, tf, params)
+        want, info = oracle.render(pov, resident, tf, params)
+        assert oracle.psnr(fr.rgba, want) >= 60.0
+        if o_max == 1.0:
+            assert render.render.last_stats["samples"] == info["samples"]
+    # the same TF again (cached table) and a small one after it
+    again = render.render(pov, resident, tf, params)
+    np.testing.assert_array_equal(again.rgba, fr.rgba)
+    small = render.render(pov, resident, render.TransferFunction.ml_preset(), params)
+    want, _ = oracle.render(pov, resident, render.TransferFunction.ml_preset(), params)
+    assert oracle.psnr(small.rgba, want) >= 60.0
