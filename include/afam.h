@@ -43,7 +43,9 @@ extern "C" {
 #define AFAM_E_VALUE 4
 #define AFAM_E_CUDA 5
 
-#define AFAM_MAX_DEGREE 3     /* degrees 1..3 are evaluated on device */
+#define AFAM_MAX_DEGREE 15    /* degrees 1..15 are evaluated on device */
+#define AFAM_FAST_DEGREE 3    /* degrees 1..3: per-span tables and the float32 kernels;
+                                 higher degrees: float64 Cox-de Boor from the knots */
 #define AFAM_MAX_TF_POINTS 32  /* inline TF control points in afam_frame; more via color_pts / opacity_pts */
 
 /* Per-slot flags (afam_store_info). */

@@ -21,7 +21,8 @@ CSRC = PKG / "csrc"
 AFAM_OK = 0
 _ERRORS = {1: MissingBlockError, 2: FormatError, 3: CapacityError, 4: ValueError, 5: RuntimeError}
 
-AFAM_MAX_DEGREE = 3
+AFAM_MAX_DEGREE = 15
+AFAM_FAST_DEGREE = 3
 AFAM_MAX_TF_POINTS = 32
 AFAM_SLOT_VALID = 1
 AFAM_SLOT_FP64 = 2

@@ -24,7 +24,7 @@ struct DecodeJob {
     int32_t slot;
     int32_t tc_kp;  // tensor-core path: K extent (ncp rounded up to 8); 0 = CUDA-core path
     int32_t fx;     // 1: float32 slots take decode_fx_kernel (register-tiled, m == 65)
-    int32_t pad_;
+    int32_t any;    // 1: degree above AFAM_FAST_DEGREE -> decode_any_kernel (b64: [m][deg+1] band)
     const int32_t *col0;
     const float *b32;
     const double *b64;
@@ -33,7 +33,7 @@ struct DecodeJob {
 
 constexpr int kDecodeChunk = 65;     // output planes per CTA (a whole 65^3 block)
 constexpr int kDecodeThreads = 416;  // 13 warps: 65 rows = 5 per warp
-constexpr int kRing = AFAM_MAX_DEGREE + 1;  // plane slots: one window of p+1 planes
+constexpr int kRing = AFAM_FAST_DEGREE + 1;  // plane slots: one window of p+1 planes
 
 // ---- TMA bulk copy + mbarrier (PTX; SASS UBLKCP / SYNCS) ----
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -273,6 +273,7 @@ __global__ void __launch_bounds__(kDecodeThreads) decode_grid_kernel(const Block
     const DecodeJob jb = jobs[blockIdx.y];
     const BlockDesc d = descs[jb.slot];
     constexpr bool kF64 = sizeof(T) == 8;
+    if (jb.any) return;  // decode_any_kernel
     if (((d.flags & AFAM_SLOT_FP64) != 0) != kF64) return;
     if (!kF64 && jb.tc_kp > 0) return;  // decoded by decode_tc_kernel
     if (!kF64 && jb.fx) return;         // decoded by decode_fx_kernel
@@ -809,6 +810,38 @@ __global__ void __launch_bounds__(kTcThreads, 1) decode_tc_kernel(const BlockDes
     }
 }
 
+// Degrees above AFAM_FAST_DEGREE (any slot flags): the separable decode of
+// bspline.py:162-172 evaluated per lattice point in float64, out[k][j][i] =
+// sum_c Bz[k][c] sum_b By[j][b] sum_a Bx[i][a] C[x0+a][y0+b][z0+c] with the
+// banded float64 collocation rows of host_band (stride deg + 1).  One thread
+// per output; a correctness path (such degrees are rare), not a tuned one.
+__global__ void decode_any_kernel(const BlockDesc *__restrict__ descs, const DecodeJob *__restrict__ jobs, int m,
+                                  float *__restrict__ out) {
+    const DecodeJob jb = jobs[blockIdx.y];
+    if (!jb.any) return;
+    const BlockDesc d = descs[jb.slot];
+    const int p = d.deg, Q = p + 1;
+    const int64_t mm = (int64_t)m * m, total = mm * m;
+    float *o = out + (size_t)blockIdx.y * total;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(e % m), j = (int)((e / m) % m), k = (int)(e / mm);
+        const double *bx = jb.b64 + (size_t)i * Q, *by = jb.b64 + (size_t)j * Q, *bz = jb.b64 + (size_t)k * Q;
+        const int x0 = __ldg(jb.col0 + i), y0 = __ldg(jb.col0 + j), z0 = __ldg(jb.col0 + k);
+        double v = 0.0;
+        for (int c = 0; c < Q; c++) {
+            double ay = 0.0;
+            for (int b = 0; b < Q; b++) {
+                const float *row = d.ctrl + ((size_t)(z0 + c) * d.ncp + (y0 + b)) * d.pitch + x0;
+                double ax = 0.0;
+                for (int a = 0; a < Q; a++) ax = fma(__ldg(bx + a), (double)__ldg(row + a), ax);
+                ay = fma(__ldg(by + b), ax, ay);
+            }
+            v = fma(__ldg(bz + c), ay, v);
+        }
+        o[e] = (float)v;
+    }
+}
+
 // Host: the banded rows of bspline._axis_operator's B for (ncp, deg, m):
 // params linspace(0, 1, m), clamped uniform float64 knots
 // (bspline.py:29-38, :98-125), Cox-de Boor with the reference's divisors.
@@ -818,7 +851,8 @@ void host_band(int ncp, int deg, int m, std::vector<double> &b, std::vector<int3
     for (int i = 0; i <= deg; i++) kv[i] = 0.0;
     for (int i = 1; i < ncp - deg; i++) kv[deg + i] = (double)i / (double)(ncp - deg);
     for (int i = 0; i <= deg; i++) kv[ncp + i] = 1.0;
-    b.assign((size_t)m * 4, 0.0);
+    const int bs = band_stride(deg);
+    b.assign((size_t)m * bs, 0.0);
     col0.assign(m, 0);
     const double step = m > 1 ? 1.0 / (double)(m - 1) : 0.0;
     for (int i = 0; i < m; i++) {
@@ -840,7 +874,7 @@ void host_band(int ncp, int deg, int m, std::vector<double> &b, std::vector<int3
             N[j] = saved;
         }
         col0[i] = s - deg;
-        for (int j = 0; j <= deg; j++) b[(size_t)i * 4 + j] = N[j];
+        for (int j = 0; j <= deg; j++) b[(size_t)i * bs + j] = N[j];
     }
 }
 
@@ -891,7 +925,8 @@ static int get_op(afam_store *s, int ncp, int deg, int m, DecodeOp **op) {
         // tensor-core operator: m == 65, ncp <= 72, and the u = 1 row selecting
         // the last control point exactly (what lets the CUDA-core stages supply
         // lattice row/column m-1)
-        if (m == kTcRows + 1 && ncp <= kTcKmax) {
+        o.any = deg > AFAM_FAST_DEGREE;
+        if (!o.any && m == kTcRows + 1 && ncp <= kTcKmax) {
             // (in float32, as the CUDA-core kernels apply it: Cox-de Boor can
             // give 1 - 1e-16 at u = 1, which rounds to 1.0f)
             bool last_ok = c0[m - 1] + deg == ncp - 1 && (float)b[(size_t)(m - 1) * 4 + deg] == 1.0f;
@@ -918,7 +953,7 @@ static int get_op(afam_store *s, int ncp, int deg, int m, DecodeOp **op) {
                 o.tc_kp = kp;
             }
         }
-        {  // register-tiled decode: m == 65, deg + 1 <= ncp <= 65 (lattice steps advance the span by <= 1),
+        if (!o.any) {  // register-tiled decode: m == 65, deg + 1 <= ncp <= 65 (lattice steps advance the span by <= 1),
            // the u = 1 row e_{ncp-1} in float32
             bool ok = m == 65 && ncp <= 65 && ncp >= deg + 1 && c0[m - 1] + deg == ncp - 1 &&
                       (float)b[(size_t)(m - 1) * 4 + deg] == 1.0f;
@@ -957,7 +992,7 @@ extern "C" int afam_decode_grid_ex(afam_store *s, const int32_t *slots, int32_t 
     cudaStream_t st = (cudaStream_t)stream;
     AFAM_CUDA(cudaSetDevice(s->device));
     std::vector<DecodeJob> jobs(nblk);
-    int maxn = 0, ntc = 0, maxkp = 0, maxn_tc = 0, nfx = 0;
+    int maxn = 0, ntc = 0, maxkp = 0, maxn_tc = 0, nfx = 0, nany = 0;
     size_t maxfx = 0;  // largest ncp * pitch among the register-tiled jobs
     {
         std::lock_guard<std::mutex> lk(s->mu);
@@ -976,7 +1011,8 @@ extern "C" int afam_decode_grid_ex(afam_store *s, const int32_t *slots, int32_t 
             jobs[b].tc_b = op->tc_b;
             jobs[b].tc_kp = use_tc ? op->tc_kp : 0;  // float64 slots (device flag) stay on the CUDA-core kernel
             jobs[b].fx = (!jobs[b].tc_kp && op->fx_ok && !fx_disabled()) ? 1 : 0;
-            jobs[b].pad_ = 0;
+            jobs[b].any = op->any ? 1 : 0;
+            nany += jobs[b].any;
             if (jobs[b].fx) {
                 nfx++;
                 maxfx = std::max(maxfx, (size_t)h.ncp * (size_t)((h.ncp + 3) & ~3));
@@ -1020,7 +1056,8 @@ extern "C" int afam_decode_grid_ex(afam_store *s, const int32_t *slots, int32_t 
             decode_fx_kernel<2><<<nblk, 512, smem, st>>>(s->d_desc, d_jobs, out);
         }
     }
-    if (ntc + nfx < nblk) {
+    if (nany > 0) decode_any_kernel<<<dim3(64, nblk), 256, 0, st>>>(s->d_desc, d_jobs, m, out);
+    if (ntc + nfx + nany < nblk) {
         const size_t smem = smem_for(sizeof(float));
         AFAM_CHECK(smem <= 227 * 1024, AFAM_E_VALUE, "decode of ncp=%d onto m=%d needs %zu B of shared memory", maxn,
                    m, smem);

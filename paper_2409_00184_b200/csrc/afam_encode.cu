@@ -274,7 +274,7 @@ static void host_fit_operator(int ncp, int deg, int m, std::vector<double> &F, s
     host_band(ncp, deg, m, band, col0);
     Bd.assign((size_t)m * ncp, 0.0);
     for (int i = 0; i < m; i++)
-        for (int a = 0; a <= deg; a++) Bd[(size_t)i * ncp + col0[i] + a] = band[(size_t)i * 4 + a];
+        for (int a = 0; a <= deg; a++) Bd[(size_t)i * ncp + col0[i] + a] = band[(size_t)i * band_stride(deg) + a];
     F.assign((size_t)ncp * m, 0.0);
     F[0] = 1.0;                                      // c_0 = d_0
     F[(size_t)(ncp - 1) * m + (m - 1)] = 1.0;        // c_{ncp-1} = d_{m-1}

@@ -337,6 +337,88 @@ __device__ __forceinline__ T eval_uncached(const BlockDesc &d, const double (&u6
     }
 }
 
+// ---------------------------------------------------------------------------
+// Any degree (AFAM_FAST_DEGREE < p <= AFAM_MAX_DEGREE; also valid for p <= 3):
+// float64 straight from the stored float32 knots upcast and the pitched
+// control points, with the reference's divisions -- bspline.py:50-70
+// (basis_values), :73-95 (basis_values_and_derivatives: the degree p-1
+// bases on the same span, N'_j = p (L_{j-1}/(t_{i+p}-t_i) -
+// L_j/(t_{i+p+1}-t_{i+1}))), :175-229 (gather + contraction).  No per-span
+// tables: slots of these degrees carry none.
+constexpr int kAnyQ = AFAM_MAX_DEGREE + 1;
+
+static __device__ inline void cox_de_boor_any(const float *__restrict__ kv, int p, int s, double u, double *N) {
+    double left[kAnyQ], right[kAnyQ];
+    N[0] = 1.0;
+    for (int j = 1; j <= p; j++) {
+        left[j] = u - (double)__ldg(kv + s + 1 - j);
+        right[j] = (double)__ldg(kv + s + j) - u;
+        double saved = 0.0;
+        for (int r = 0; r < j; r++) {
+            const double tmp = N[r] / (right[r + 1] + left[j - r]);
+            N[r] = saved + right[r + 1] * tmp;
+            saved = left[j - r] * tmp;
+        }
+        N[j] = saved;
+    }
+}
+
+// Span, p+1 basis values and (with D) their derivatives on one axis.
+static __device__ inline int axis_any(const float *__restrict__ kv, int ncp, int p, double u, double *N, double *D) {
+    const int s = find_span(kv, ncp, p, ncp - p, u);
+    cox_de_boor_any(kv, p, s, u, N);
+    if (D) {
+        double L[kAnyQ];
+        cox_de_boor_any(kv, p - 1, s, u, L);  // N_{s-p+1 .. s, p-1}
+        for (int j = 0; j <= p; j++) {
+            const int i = s - p + j;
+            double term = 0.0;
+            if (j > 0) term = L[j - 1] / ((double)__ldg(kv + i + p) - (double)__ldg(kv + i));
+            if (j < p) term = term - L[j] / ((double)__ldg(kv + i + p + 1) - (double)__ldg(kv + i + 1));
+            D[j] = (double)p * term;
+        }
+    }
+    return s;
+}
+
+// Value (and parameter-space gradient when g != nullptr) at u in [0,1]^3.
+static __device__ __noinline__ double eval_any(const BlockDesc &d, const double (&u)[3], double *g) {
+    const int p = d.deg, Q = p + 1;
+    double N[3][kAnyQ], D[3][kAnyQ];
+    int s[3];
+    for (int a = 0; a < 3; a++) s[a] = axis_any(d.knots + a * d.nk, d.ncp, p, u[a], N[a], g ? D[a] : nullptr);
+    double v = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
+    for (int cz = 0; cz < Q; cz++) {
+        double ry = 0.0, rdx = 0.0, rdy = 0.0;
+        for (int by = 0; by < Q; by++) {
+            const float *row = d.ctrl + ((size_t)(s[2] - p + cz) * d.ncp + (s[1] - p + by)) * d.pitch + (s[0] - p);
+            double rx = 0.0, dx = 0.0;
+            for (int ax = 0; ax < Q; ax++) {
+                const double c = (double)__ldg(row + ax);
+                rx = fma(N[0][ax], c, rx);
+                if (g) dx = fma(D[0][ax], c, dx);
+            }
+            ry = fma(N[1][by], rx, ry);
+            if (g) {
+                rdx = fma(N[1][by], dx, rdx);
+                rdy = fma(D[1][by], rx, rdy);
+            }
+        }
+        v = fma(N[2][cz], ry, v);
+        if (g) {
+            gx = fma(N[2][cz], rdx, gx);
+            gy = fma(N[2][cz], rdy, gy);
+            gz = fma(D[2][cz], ry, gz);
+        }
+    }
+    if (g) {
+        g[0] = gx;
+        g[1] = gy;
+        g[2] = gz;
+    }
+    return v;
+}
+
 __device__ __forceinline__ BlockDesc load_desc(const BlockDesc *__restrict__ p) {
     BlockDesc d;
     const int4 *src = reinterpret_cast<const int4 *>(p);

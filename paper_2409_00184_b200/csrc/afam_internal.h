@@ -24,7 +24,7 @@ namespace afam {
 __host__ __device__ constexpr int tab_stride(int p) {
     return ((2 * p + p * (p + 1) / 2) + 3) / 4 * 4;  // p=1:4 p=2:8 p=3:12
 }
-constexpr int kTabStrideMax = 12;  // tab_stride(AFAM_MAX_DEGREE)
+constexpr int kTabStrideMax = 12;  // tab_stride(AFAM_FAST_DEGREE); higher degrees have no tables
 
 // Device-resident descriptor of one slot (one micro-model).
 struct alignas(16) BlockDesc {
@@ -89,11 +89,13 @@ struct DecodeOp {  // banded collocation matrix of bspline.py:98-125 for (ncp, d
     // deg + 1 <= ncp <= 65 and the u = 1 row selecting the last control
     // point exactly
     bool fx_ok = false;
+    bool any = false;       // degree above AFAM_FAST_DEGREE: decode_any_kernel over b64
 };
 
 // Banded rows of the collocation matrix of bspline.py:98-125 for (ncp, deg,
 // m): params linspace(0, 1, m), fresh float64 clamped uniform knots; row i
-// holds N[col0[i] .. col0[i] + deg] (afam_decode.cu).
+// holds N[col0[i] .. col0[i] + deg] at b[i * band_stride(deg) + j] (afam_decode.cu).
+inline int band_stride(int deg) { return deg + 1 > 4 ? deg + 1 : 4; }
 void host_band(int ncp, int deg, int m, std::vector<double> &b, std::vector<int32_t> &col0);
 
 struct FitOp {  // endpoint-pinned least-squares fit operator (bspline.py:109-159), device

@@ -19,7 +19,14 @@ __device__ __forceinline__ T eval_dispatch(const BlockDesc &d, const double (&u)
     switch (d.deg) {
         case 1: return eval_uncached<1, T, GRAD>(d, u, g);
         case 2: return eval_uncached<2, T, GRAD>(d, u, g);
-        default: return eval_uncached<3, T, GRAD>(d, u, g);
+        case 3: return eval_uncached<3, T, GRAD>(d, u, g);
+        default: {  // degrees above AFAM_FAST_DEGREE: float64 from the knots
+            double gd[3];
+            const double v = eval_any(d, u, GRAD ? gd : nullptr);
+            if constexpr (GRAD)
+                for (int a = 0; a < 3; a++) g[a] = (T)gd[a];
+            return (T)v;
+        }
     }
 }
 
@@ -110,7 +117,7 @@ __global__ void __launch_bounds__(256) eval_points_kernel(const BlockDesc *__res
         u[a] = clamp01(param ? p : __ddiv_rn(__dsub_rn(p, d.lo[a]), d.span[a]));
     }
     double v, g[3] = {0.0, 0.0, 0.0};
-    if (d.flags & AFAM_SLOT_FP64) {
+    if ((d.flags & AFAM_SLOT_FP64) || d.deg > AFAM_FAST_DEGREE) {  // float64 (high degrees: eval_any)
         v = eval_dispatch<double, GRAD>(d, u, g);
     } else {
         float gf[3];

@@ -986,6 +986,28 @@ __device__ __noinline__ int sample_exact(const RenderArgs *GA, const TfTable *tf
     return f64 ? 1 : 0;
 }
 
+// Degrees above AFAM_FAST_DEGREE: float64 evaluation from the knots
+// (afam_eval.cuh eval_any, the reference's Cox-de Boor with its divisions),
+// parameters with the reference's division (model.py:64-68); always a
+// float64 sample.  Compiled only into the render2_kernel instantiations the
+// host selects for frames holding such blocks (HI), so the common kernels
+// carry no trace of its frame.
+__device__ __noinline__ int sample_exact_any(const RenderArgs *GA, const TfTable *tf, RayState *R,
+                                             const BlockDesc *__restrict__ dp, int32_t k) {
+    double pos[3];
+    exact_pos(*GA, *R, k, pos);
+    const BlockDesc d = load_desc(dp);
+    double u[3], gg[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) u[a] = clamp01(__ddiv_rn(__dsub_rn(pos[a], d.lo[a]), d.span[a]));
+    const double v = eval_any(d, u, gg);
+    const float4 tfv = tf_eval(*tf, fminf(fmaxf((float)v, GA->dom_lo), GA->dom_hi));
+    R->tfv = tfv;
+#pragma unroll
+    for (int a = 0; a < 3; a++) R->g[a] = tfv.w > 0.f ? (float)(gg[a] / d.span[a]) : 0.f;
+    return 1;
+}
+
 template <bool DEBUG, bool SMEM_GRID, int FD, int MINB>
 __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__restrict__ descs,
                                                         const int16_t *__restrict__ grid,
@@ -1146,7 +1168,7 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
                 int f64;
                 if (deg == 3) f64 = sample_exact<3>(GA, &tf, &R, dpx, slot, M.k);
                 else if (deg == 2) f64 = sample_exact<2>(GA, &tf, &R, dpx, slot, M.k);
-                else f64 = sample_exact<1>(GA, &tf, &R, dpx, slot, M.k);
+                else f64 = sample_exact<1>(GA, &tf, &R, dpx, slot, M.k);  // (the host routes degrees > 3 to render2_kernel)
                 C.ns64 += f64;
                 ++C.nexact;
                 const float4 tfv = R.tfv;
@@ -1404,7 +1426,7 @@ __device__ __forceinline__ bool sample_fast2(const RenderArgs &A, const TfTable 
     return true;
 }
 
-template <bool DEBUG, bool SMEM_GRID, int P, int MINB, int SR>
+template <bool DEBUG, bool SMEM_GRID, int P, int MINB, int SR, bool HI>
 __global__ void __launch_bounds__(128, MINB) render2_kernel(const BlockDesc *__restrict__ descs,
                                                          const int16_t *__restrict__ grid,
                                                          const int32_t *__restrict__ idx2slot, const RenderArgs A,
@@ -1555,7 +1577,8 @@ __global__ void __launch_bounds__(128, MINB) render2_kernel(const BlockDesc *__r
                 int f64;
                 if (deg == 3) f64 = sample_exact<3>(GA, &tf, &R, dpx, slot, M.k);
                 else if (deg == 2) f64 = sample_exact<2>(GA, &tf, &R, dpx, slot, M.k);
-                else f64 = sample_exact<1>(GA, &tf, &R, dpx, slot, M.k);
+                else if (!HI || deg == 1) f64 = sample_exact<1>(GA, &tf, &R, dpx, slot, M.k);
+                else f64 = sample_exact_any(GA, &tf, &R, dpx, M.k);  // degrees above AFAM_FAST_DEGREE
                 C.ns64 += f64;
                 ++C.nexact;
                 const float4 tfv = R.tfv;
@@ -1828,15 +1851,15 @@ static void launch_render_v(const LaunchArgs &L, const RenderArgs &A) {
                                                                         L.rgba, L.stats, L.nsamp, L.ohash);
 }
 
-template <bool DEBUG, bool SMEM, int P, int MINB, int SR = 0>
+template <bool DEBUG, bool SMEM, int P, int MINB, int SR = 0, bool HI = false>
 static void launch_render2_v(const LaunchArgs &L, const RenderArgs &A) {
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(render2_kernel<DEBUG, SMEM, P, MINB, SR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(render2_kernel<DEBUG, SMEM, P, MINB, SR, HI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              64 * 1024);
         configured = true;
     }
-    render2_kernel<DEBUG, SMEM, P, MINB, SR><<<L.grid, 128, L.smem, L.st>>>(L.descs, L.owner, L.idx, A, L.gargs,
+    render2_kernel<DEBUG, SMEM, P, MINB, SR, HI><<<L.grid, 128, L.smem, L.st>>>(L.descs, L.owner, L.idx, A, L.gargs,
                                                                              L.gtf, L.rgba, L.stats, L.nsamp,
                                                                              L.ohash);
 }
@@ -1864,8 +1887,13 @@ static int render2_minb() {
 // fd: the degree the fast path is compiled for (blocks of other degrees take
 // the exact path); debug and non-shared-grid launches use the default bounds.
 template <bool DEBUG, bool SMEM>
-static void launch_render(const LaunchArgs &L, const RenderArgs &A, int fd) {
+static void launch_render(const LaunchArgs &L, const RenderArgs &A, int fd, bool hi) {
     if (fd == 0) return launch_render_v<DEBUG, SMEM, 0, 4>(L, A);  // DS blocks
+    if (hi) {  // blocks of degrees above AFAM_FAST_DEGREE present
+        if (fd == 1) return launch_render2_v<DEBUG, SMEM, 1, 4, 0, true>(L, A);
+        if (fd == 2) return launch_render2_v<DEBUG, SMEM, 2, 4, 0, true>(L, A);
+        return launch_render2_v<DEBUG, SMEM, 3, 3, 0, true>(L, A);
+    }
     if (!render_v1()) {
         if (fd == 1) return launch_render2_v<DEBUG, SMEM, 1, 4>(L, A);
         if (fd == 2) return launch_render2_v<DEBUG, SMEM, 2, 4>(L, A);
@@ -2025,18 +2053,22 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
     std::vector<int16_t> grid;
     int32_t cells = 1;
     int fd = 3;  // fast-path degree: the most common degree among the blocks
+    bool hi = false;
     {
         std::lock_guard<std::mutex> lk(s->mu);
         int rc = build_owner_grid(s, slots, nblocks, cells, grid);
         if (rc) return rc;
         for (int b = 0; b < nblocks; b++) AFAM_CUDA(wait_slot(s, slots[b], st));
         int cnt[4] = {0, 0, 0, 0}, nds = 0;
+        hi = false;
         for (int b = 0; b < nblocks; b++) {
             if (s->host[slots[b]].ds) {
                 ++nds;
                 continue;
             }
-            cnt[std::min(std::max((int)s->host[slots[b]].deg, 1), 3)]++;
+            const int dg = s->host[slots[b]].deg;
+            if (dg >= 1 && dg <= AFAM_FAST_DEGREE) cnt[dg]++;
+            else hi = true;  // higher degrees: render2_kernel<..., HI> (sample_exact_any)
         }
         AFAM_CHECK(nds == 0 || nds == nblocks, AFAM_E_VALUE,
                    "resident blocks mix spline models and DS blocks (%d of %d DS)", nds, nblocks);
@@ -2109,11 +2141,11 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
         L.nsamp = nsamp;
         L.ohash = ohash;
         if (debug) {
-            if (sg) launch_render<true, true>(L, A, fd);
-            else launch_render<true, false>(L, A, fd);
+            if (sg) launch_render<true, true>(L, A, fd, hi);
+            else launch_render<true, false>(L, A, fd, hi);
         } else {
-            if (sg) launch_render<false, true>(L, A, fd);
-            else launch_render<false, false>(L, A, fd);
+            if (sg) launch_render<false, true>(L, A, fd, hi);
+            else launch_render<false, false>(L, A, fd, hi);
         }
     }
     finish_stats_kernel<<<1, 1, 0, st>>>(stats);

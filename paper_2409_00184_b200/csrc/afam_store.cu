@@ -125,9 +125,11 @@ __global__ void build_tables_kernel(const uint8_t *__restrict__ raw, uint64_t kn
         const float want = k <= deg ? 0.f : (k >= ncp ? 1.f : (float)((double)(k - deg) / (double)nspan));
         if (__float_as_uint(t) != __float_as_uint(want)) atomicAnd(&uniform, 0);
     }
-    for (int i = threadIdx.x; i < 3 * nspan; i += blockDim.x) {
+    // per-span tables for the fast degrees only (higher degrees evaluate from
+    // the knots, afam_eval.cuh eval_any)
+    for (int i = threadIdx.x; i < (deg <= AFAM_FAST_DEGREE ? 3 * nspan : 0); i += blockDim.x) {
         const int a = i / nspan, s = deg + i % nspan;
-        double W[2 * AFAM_MAX_DEGREE];
+        double W[2 * AFAM_FAST_DEGREE];
         for (int k = 0; k < 2 * deg; k++) {
             int idx = s - deg + 1 + k;
             W[k] = (idx >= 0 && idx < nk) ? (double)knot(a, idx) : 0.0;
