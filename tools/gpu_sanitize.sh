@@ -9,3 +9,4 @@ run memcheck decode; run racecheck decode; run synccheck decode
 run memcheck render; run racecheck render
 run memcheck eval; run racecheck eval
 run memcheck replay
+run memcheck highdeg; run racecheck highdeg

@@ -10,6 +10,9 @@ eval    K1 on a bucketed batch (n = 2^17: count / scan / scatter /
         unpermute) and on an unbucketed one
 replay  ModelCache + linear prefetch on the frame thread while the GPU
         marches (cross-stream slot reuse, reader fences)
+highdeg degree-5 blocks (the float64 any-degree path): K2 frames with a
+        300-point transfer function, K3 decode (decode_any_kernel) next to
+        degree-3 blocks, K1 points
 """
 import ctypes as C
 import sys
@@ -92,5 +95,30 @@ def replay():
     print("replay ok")
 
 
+def highdeg():
+    from paper_2409_00184_b200 import bspline
+
+    man, blobs = synth.field_store(levels=2, coarsest=1, micro=9, degree=5, ncp_of=lambda a: 7)
+    models = {a: model.deserialize(b, man.entries[a].ncp, man.entries[a].extent, a.lod) for a, b in blobs.items()}
+    rng = np.random.default_rng(1)
+    cp = np.column_stack([np.sort(rng.uniform(0, 1, 300)), rng.uniform(0, 1, (300, 3))])
+    op = np.column_stack([np.sort(rng.uniform(0, 1, 90)), rng.uniform(0, 0.1, 90)])
+    tf = render.TransferFunction(cp, op)
+    params = render.RenderParams(width=24, height=20, sample_distance=0.01)
+    pov = render.PointOfView([0.2, 0.3, 1.9], [-0.2, -0.3, -1.9], [0, 1, 0], 50.0)
+    vis = render.select_visible(pov, man, params.aspect)
+    render.render(pov, {a: models[a] for a in vis}, tf, params)
+    m5 = models[vis[0]]
+    ds = DeviceStore(2, 9)
+    ds.put_model(0, m5)
+    c3 = rng.normal(size=(9, 9, 9)).astype(np.float32)
+    ds.put_model(1, model.MicroModel(3, np.stack([clamped_knots(9, 3)] * 3).astype(np.float32), c3,
+                                     np.array([[0, 1.0]] * 3), 1))
+    bspline.decode_slots(ds, [0, 1], 17)
+    bspline.evaluate_points_with_gradient(m5.control, 5, rng.uniform(0, 1, (1000, 3)), knots=tuple(m5.knots))
+    torch.cuda.synchronize()
+    print("highdeg ok")
+
+
 if __name__ == "__main__":
-    {"decode": decode, "render": render_frames, "eval": eval_points, "replay": replay}[sys.argv[1]]()
+    {"decode": decode, "render": render_frames, "eval": eval_points, "replay": replay, "highdeg": highdeg}[sys.argv[1]]()
