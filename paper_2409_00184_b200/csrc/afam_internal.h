@@ -57,6 +57,7 @@ struct SlotHost {
     bool pending = false;  // upload possibly still in flight (ready not yet observed)
     int32_t ncp = 0, deg = 0;
     bool ds = false;       // down-sampled raw block (AFAM_SLOT_DS)
+    bool maxabs_known = false;  // afam_store::h_maxabs[slot] set on the host at put time (else after `ready`)
     double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     cudaEvent_t ready = nullptr;  // recorded after the upload kernels
     cudaEvent_t reader = nullptr; // the last kernel reading the slot (a ThreadCtx event): uploads wait on it
@@ -115,6 +116,8 @@ struct afam_store {
     char *arena = nullptr;               // nslots * slot_bytes device bytes
     afam::BlockDesc *d_desc = nullptr;   // nslots descriptors (device)
     float *d_maxabs = nullptr;           // nslots (device)
+    float *h_maxabs = nullptr;           // nslots (pinned host): copied back after each upload, valid once
+                                         // the slot's `ready` event completed (afam_render: float64 kernel?)
     std::vector<afam::SlotHost> host;
     // afam_store_put_file: ring of pinned staging buffers (file -> pinned -> H2D)
     static constexpr int kFileRing = 4;

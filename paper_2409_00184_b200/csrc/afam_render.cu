@@ -1281,13 +1281,8 @@ __device__ __forceinline__ BlockFast fast_block(const BlockFast &sb) {  // sb in
 }
 
 template <int P, int SR>
-__device__ __forceinline__ void fast_cell_update(const BlockFast &sb, float tqx, float tqy, float tqz,
-                                                 FastCell<P, SR> &G) {
+__device__ __forceinline__ void fast_cell_update_k(const BlockFast &b, int kx, int ky, int kz, FastCell<P, SR> &G) {
     constexpr int Q = P + 1;
-    const BlockFast b = fast_block<P>(sb);
-    const int kx = min(max(__float2int_rd(tqx), 0), b.nspan - 1);
-    const int ky = min(max(__float2int_rd(tqy), 0), b.nspan - 1);
-    const int kz = min(max(__float2int_rd(tqz), 0), b.nspan - 1);
     G.cx = (float)kx;
     G.cy = (float)ky;
     G.cz = (float)kz;
@@ -1302,6 +1297,16 @@ __device__ __forceinline__ void fast_cell_update(const BlockFast &sb, float tqx,
             for (int by = 0; by < Q; by++) G.set(cz * Q + by, __ldg(base + cz * b.plane + by));
         G.key = id;
     }
+}
+
+template <int P, int SR>
+__device__ __forceinline__ void fast_cell_update(const BlockFast &sb, float tqx, float tqy, float tqz,
+                                                 FastCell<P, SR> &G) {
+    const BlockFast b = fast_block<P>(sb);
+    const int kx = min(max(__float2int_rd(tqx), 0), b.nspan - 1);
+    const int ky = min(max(__float2int_rd(tqy), 0), b.nspan - 1);
+    const int kz = min(max(__float2int_rd(tqz), 0), b.nspan - 1);
+    fast_cell_update_k<P, SR>(b, kx, ky, kz, G);
 }
 
 // One sample of a clamped-uniform float32 block (render_kernel's
@@ -1426,7 +1431,113 @@ __device__ __forceinline__ bool sample_fast2(const RenderArgs &A, const TfTable 
     return true;
 }
 
-template <bool DEBUG, bool SMEM_GRID, int P, int MINB, int SR, bool HI>
+// ---------------------------------------------------------------------------
+// Float64 fast path (render2_kernel<..., F64>, frames holding ill-conditioned
+// slots: endpoint-pinned fits whose large cancelling
+// coefficients need float64 basis and accumulation): the float32 fast
+// path's schedule -- the owner block's cell rows cached in registers across
+// samples, the span coordinate predicted from the exact block-entry position
+// (tq0 + (k - k0) dtq, now in float64), closed-form uniform bases on interior
+// spans (the float64 Cox-de Boor table on the boundary spans), contraction
+// and gradient in float64 -- instead of the exact path's per-sample float64
+// position, division, span search, table loads and uncached gather.
+struct Pred64 {  // per thread, shared memory: the float64 span prediction of the current owner
+    double tq0[3], dtq[3];
+    const double *tab64;
+};
+__shared__ Pred64 s_pred64[128];
+
+// uniform_basis (afam_eval.cuh) in float64
+template <int P>
+__device__ __forceinline__ void uniform_NE_f64(double x, double ns, double (&N)[P + 1], double (&E)[P]) {
+    const double m = 1.0 - x;
+    if (P == 1) {
+        N[0] = m;
+        N[1] = x;
+        E[0] = ns;
+    } else if (P == 2) {
+        const double x2 = x * x;
+        N[0] = 0.5 * m * m;
+        N[1] = fma(-1.0, x2, x) + 0.5;
+        N[2] = 0.5 * x2;
+        E[0] = ns * m;
+        E[1] = ns * x;
+    } else {
+        const double x2 = x * x, x3 = x2 * x, m2 = m * m, s6 = 1.0 / 6.0;
+        N[0] = s6 * m2 * m;
+        N[1] = fma(0.5, x3, fma(-1.0, x2, 2.0 / 3.0));
+        N[2] = fma(-0.5, x3, fma(0.5, x2, fma(0.5, x, s6)));
+        N[3] = s6 * x3;
+        const double hn = 0.5 * ns;
+        E[0] = hn * m2;
+        E[1] = ns * (fma(-1.0, x2, x) + 0.5);
+        E[2] = hn * x2;
+    }
+}
+
+template <int P, int SR>
+__device__ __forceinline__ bool sample_fast64(const RenderArgs &A, const TfTable &tf, const BlockFast &sb,
+                                              const Pred64 &PD, float dk, ThreadCold &C, FastCell<P, SR> &G,
+                                              March &M) {
+    constexpr int Q = P + 1;
+    const double dkd = (double)dk;
+    double tq[3], f[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) tq[a] = fma(dkd, vld(PD.dtq[a]), vld(PD.tq0[a]));
+    f[0] = tq[0] - (double)G.cx;
+    f[1] = tq[1] - (double)G.cy;
+    f[2] = tq[2] - (double)G.cz;
+    auto in01 = [](double v) { return v >= 0.0 && v < 1.0; };
+    if (!(in01(f[0]) & in01(f[1]) & in01(f[2]))) {
+        const BlockFast b = fast_block<P>(sb);
+        int k[3];
+#pragma unroll
+        for (int a = 0; a < 3; a++) k[a] = min(max((int)floor(tq[a]), 0), b.nspan - 1);
+        fast_cell_update_k<P, SR>(b, k[0], k[1], k[2], G);
+#pragma unroll
+        for (int a = 0; a < 3; a++) f[a] = tq[a] - (double)k[a];
+    }
+    if constexpr (P == 1) {  // the gradient jumps at a knot: the exact path decides there
+#pragma unroll
+        for (int a = 0; a < 3; a++)
+            if (!(fabs(f[a] - 0.5) < 0.5 - 1e-4)) return false;
+    }
+    // basis values now, the derivative weights only for visible samples
+    auto basis = [&](int a, double (&Na)[Q], double (&Ea)[P]) {
+        const int nspan = vld(sb.nspan);
+        if (G.inner & (1u << a)) {
+            uniform_NE_f64<P>(f[a], (double)nspan, Na, Ea);
+        } else {  // boundary span: float64 Cox-de Boor from the span's table entry
+            const int k = (int)(a == 0 ? G.cx : (a == 1 ? G.cy : G.cz));
+            Tab<double> t;
+            load_entry<P>(vld(PD.tab64) + ((size_t)a * nspan + k) * tab_stride(P), t);
+            basis_eval<P, double>(t, clamp01(tq[a] / (double)nspan), Na, Ea);
+        }
+    };
+    double N[3][Q];
+    double E[3][P];
+#pragma unroll
+    for (int a = 0; a < 3; a++) basis(a, N[a], E[a]);
+    float4 c4[16];
+#pragma unroll
+    for (int i = 0; i < Q * Q; i++) c4[i] = G.get(i);
+    double v, g[3];
+    contract_quad<P, double>(c4, N[0], E[0], N[1], E[1], N[2], E[2], v, g);
+    ++C.ns64;
+    const float vc = fminf(fmaxf((float)v, A.dom_lo), A.dom_hi);
+    if (!(vc > A.op_lo) || !(vc < A.op_hi)) return true;
+    int bi;
+    float bf;
+    const float atf = tf_alpha(A, tf, vc, bi, bf);
+    if (!(atf > 0.f)) return true;
+    ++M.nshade;
+    const float4 gi = C.ginv;
+    const float gs[3] = {(float)g[0] * gi.x, (float)g[1] * gi.y, (float)g[2] * gi.z};  // model.py:79
+    composite(A, C.vdir, tf_color(tf, vc, bi, bf, atf), gs, M);
+    return true;
+}
+
+template <bool DEBUG, bool SMEM_GRID, int P, int MINB, int SR, bool HI, bool F64>
 __global__ void __launch_bounds__(128, MINB) render2_kernel(const BlockDesc *__restrict__ descs,
                                                          const int16_t *__restrict__ grid,
                                                          const int32_t *__restrict__ idx2slot, const RenderArgs A,
@@ -1516,6 +1627,7 @@ __global__ void __launch_bounds__(128, MINB) render2_kernel(const BlockDesc *__r
         F.deg = 0;
         BlockFast &b = F.b;
         bool fast = false;
+        bool is64 = false;  // F64: the owner is an ill-conditioned (float64) slot
         __shared__ float4 s_cellrows[SR > 0 ? SR : 1][128];
         FastCell<P, SR> G;
         G.s = &s_cellrows[0][threadIdx.x];
@@ -1549,15 +1661,24 @@ __global__ void __launch_bounds__(128, MINB) render2_kernel(const BlockDesc *__r
                     const int32_t deg = __ldg(&dp->deg);
                     F.deg = deg;
                     const uint32_t flags = __ldg(&dp->flags);
-                    fast = deg == P && (flags & kFlagUniform) && !(flags & AFAM_SLOT_FP64) &&
+                    fast = deg == P && (flags & kFlagUniform) && (F64 || !(flags & AFAM_SLOT_FP64)) &&
                            (deg > 1 || b.nspan <= 128) && k24 && !(A.flags & kRenderForceExact);
+                    if constexpr (F64) is64 = (flags & AFAM_SLOT_FP64) != 0;
                     // span-coordinate prediction from the exact entry position
 #pragma unroll
                     for (int a = 0; a < 3; a++) {
                         const double sc = __ldg(&dp->inv_span[a]) * (double)b.nspan;
                         M.tq0[a] = (float)((p[a] - __ldg(&dp->lo[a])) * sc);
                         M.dtq[a] = (float)(A.sd * R.d[a] * sc);
+                        if constexpr (F64) {
+                            if (is64) {
+                                s_pred64[threadIdx.x].tq0[a] = (p[a] - __ldg(&dp->lo[a])) * sc;
+                                s_pred64[threadIdx.x].dtq[a] = A.sd * R.d[a] * sc;
+                            }
+                        }
                     }
+                    if constexpr (F64)
+                        if (is64) s_pred64[threadIdx.x].tab64 = (const double *)__ldg((const unsigned long long *)&dp->tab64);
                     C.ginv = make_float4(__ldg(&dp->inv_span_f[0]), __ldg(&dp->inv_span_f[1]),
                                          __ldg(&dp->inv_span_f[2]), 0.f);
                     dk = 0.f;
@@ -1566,10 +1687,14 @@ __global__ void __launch_bounds__(128, MINB) render2_kernel(const BlockDesc *__r
             if (DEBUG) M.h = (M.h ^ (uint64_t)(uint32_t)vld(F.cur_own)) * 1099511628211ULL;
             bool ok = false;
             if (fast) {
-                const float tqx = fmaf(dk, M.dtq[0], M.tq0[0]);
-                const float tqy = fmaf(dk, M.dtq[1], M.tq0[1]);
-                const float tqz = fmaf(dk, M.dtq[2], M.tq0[2]);
-                ok = sample_fast2<P, SR>(A, tf, b, tqx, tqy, tqz, C, G, M);
+                if (F64 && is64) {
+                    ok = sample_fast64<P, SR>(A, tf, b, s_pred64[threadIdx.x], dk, C, G, M);
+                } else {
+                    const float tqx = fmaf(dk, M.dtq[0], M.tq0[0]);
+                    const float tqy = fmaf(dk, M.dtq[1], M.tq0[1]);
+                    const float tqz = fmaf(dk, M.dtq[2], M.tq0[2]);
+                    ok = sample_fast2<P, SR>(A, tf, b, tqx, tqy, tqz, C, G, M);
+                }
             }
             if (!ok) {
                 const int32_t slot = vld(F.slot), deg = vld(F.deg);
@@ -1851,15 +1976,15 @@ static void launch_render_v(const LaunchArgs &L, const RenderArgs &A) {
                                                                         L.rgba, L.stats, L.nsamp, L.ohash);
 }
 
-template <bool DEBUG, bool SMEM, int P, int MINB, int SR = 0, bool HI = false>
+template <bool DEBUG, bool SMEM, int P, int MINB, int SR = 0, bool HI = false, bool F64 = false>
 static void launch_render2_v(const LaunchArgs &L, const RenderArgs &A) {
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(render2_kernel<DEBUG, SMEM, P, MINB, SR, HI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             64 * 1024);
+        cudaFuncSetAttribute(render2_kernel<DEBUG, SMEM, P, MINB, SR, HI, F64>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
         configured = true;
     }
-    render2_kernel<DEBUG, SMEM, P, MINB, SR, HI><<<L.grid, 128, L.smem, L.st>>>(L.descs, L.owner, L.idx, A, L.gargs,
+    render2_kernel<DEBUG, SMEM, P, MINB, SR, HI, F64><<<L.grid, 128, L.smem, L.st>>>(L.descs, L.owner, L.idx, A, L.gargs,
                                                                              L.gtf, L.rgba, L.stats, L.nsamp,
                                                                              L.ohash);
 }
@@ -1884,15 +2009,28 @@ static int render2_minb() {
     return v;
 }
 
+// AFAM_RENDER_NO_F64=1: float64 slots on the exact path (A/B of the float64 fast path)
+static bool render_no_f64() {
+    static const bool v = [] {
+        const char *e = getenv("AFAM_RENDER_NO_F64");
+        return e && atoi(e) != 0;
+    }();
+    return v;
+}
+
 // fd: the degree the fast path is compiled for (blocks of other degrees take
 // the exact path); debug and non-shared-grid launches use the default bounds.
 template <bool DEBUG, bool SMEM>
-static void launch_render(const LaunchArgs &L, const RenderArgs &A, int fd, bool hi) {
+static void launch_render(const LaunchArgs &L, const RenderArgs &A, int fd, bool hi, bool f64) {
     if (fd == 0) return launch_render_v<DEBUG, SMEM, 0, 4>(L, A);  // DS blocks
     if (hi) {  // blocks of degrees above AFAM_FAST_DEGREE present
         if (fd == 1) return launch_render2_v<DEBUG, SMEM, 1, 4, 0, true>(L, A);
         if (fd == 2) return launch_render2_v<DEBUG, SMEM, 2, 4, 0, true>(L, A);
         return launch_render2_v<DEBUG, SMEM, 3, 3, 0, true>(L, A);
+    }
+    if (f64 && !render_no_f64()) {  // ill-conditioned (float64) slots present: the float64 fast path
+        if (fd == 2) return launch_render2_v<DEBUG, SMEM, 2, 3, 0, false, true>(L, A);
+        if (fd == 3) return launch_render2_v<DEBUG, SMEM, 3, 2, 0, false, true>(L, A);
     }
     if (!render_v1()) {
         if (fd == 1) return launch_render2_v<DEBUG, SMEM, 1, 4>(L, A);
@@ -2053,12 +2191,19 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
     std::vector<int16_t> grid;
     int32_t cells = 1;
     int fd = 3;  // fast-path degree: the most common degree among the blocks
-    bool hi = false;
+    bool hi = false, any64 = false;
     {
         std::lock_guard<std::mutex> lk(s->mu);
         int rc = build_owner_grid(s, slots, nblocks, cells, grid);
         if (rc) return rc;
-        for (int b = 0; b < nblocks; b++) AFAM_CUDA(wait_slot(s, slots[b], st));
+        for (int b = 0; b < nblocks; b++) {
+            AFAM_CUDA(wait_slot(s, slots[b], st));
+            // float64 slot (max|c| over the limit, afam_store.cu build_tables_kernel)? unknown
+            // while its upload is in flight: then the float64-capable kernel
+            const SlotHost &h = s->host[slots[b]];
+            if (!h.ds && ((h.pending && !h.maxabs_known) || s->h_maxabs[slots[b]] > (float)s->fp64_limit))
+                any64 = true;
+        }
         int cnt[4] = {0, 0, 0, 0}, nds = 0;
         hi = false;
         for (int b = 0; b < nblocks; b++) {
@@ -2141,11 +2286,11 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
         L.nsamp = nsamp;
         L.ohash = ohash;
         if (debug) {
-            if (sg) launch_render<true, true>(L, A, fd, hi);
-            else launch_render<true, false>(L, A, fd, hi);
+            if (sg) launch_render<true, true>(L, A, fd, hi, any64);
+            else launch_render<true, false>(L, A, fd, hi, any64);
         } else {
-            if (sg) launch_render<false, true>(L, A, fd, hi);
-            else launch_render<false, false>(L, A, fd, hi);
+            if (sg) launch_render<false, true>(L, A, fd, hi, any64);
+            else launch_render<false, false>(L, A, fd, hi, any64);
         }
     }
     finish_stats_kernel<<<1, 1, 0, st>>>(stats);

@@ -207,6 +207,7 @@ int afam_store_create(afam_store **out, int device, int32_t slots, int32_t max_n
     AFAM_CUDA(cudaMalloc(&s->d_desc, sizeof(BlockDesc) * slots));
     AFAM_CUDA(cudaMemset(s->d_desc, 0, sizeof(BlockDesc) * slots));
     AFAM_CUDA(cudaMalloc(&s->d_maxabs, sizeof(float) * slots));
+    AFAM_CUDA(cudaHostAlloc((void **)&s->h_maxabs, sizeof(float) * slots, cudaHostAllocDefault));
     s->host.resize(slots);
     for (auto &h : s->host) AFAM_CUDA(cudaEventCreateWithFlags(&h.ready, cudaEventDisableTiming));
     {
@@ -247,6 +248,7 @@ int afam_store_destroy(afam_store *s) {
     cudaFree(s->arena);
     cudaFree(s->d_desc);
     cudaFree(s->d_maxabs);
+    if (s->h_maxabs) cudaFreeHost(s->h_maxabs);
     delete s;
     return AFAM_OK;
 }
@@ -259,8 +261,9 @@ int afam_store_slots(const afam_store *s, int32_t *slots, int32_t *max_ncp) {
 }
 
 // Shared tail of both put paths: raw region already holds the bytes (queued on stream).
+// host_maxabs: max |c| when the caller scanned the control points on the host, else < 0
 static int launch_unpack(afam_store *s, int32_t slot, int deg, int ncp, uint64_t knot_off, int has_t0,
-                         uint64_t ctrl_off, const double extent[6], cudaStream_t st) {
+                         uint64_t ctrl_off, const double extent[6], cudaStream_t st, float host_maxabs) {
     BlockDesc proto{};
     proto.ctrl = s->ctrl_ptr(slot);
     proto.ctrl4 = s->ctrl4_ptr(slot);
@@ -292,6 +295,12 @@ static int launch_unpack(afam_store *s, int32_t slot, int deg, int ncp, uint64_t
                                            (const unsigned int *)(s->d_maxabs + slot), (float)s->fp64_limit);
     AFAM_CUDA(cudaGetLastError());
     SlotHost &h = s->host[slot];
+    // the device's value lands in h_maxabs when the upload completes; a host
+    // scan gives it now.  Either way it only selects afam_render's kernel
+    // (both kernels decode every slot kind correctly), never a result.
+    AFAM_CUDA(cudaMemcpyAsync(s->h_maxabs + slot, s->d_maxabs + slot, sizeof(float), cudaMemcpyDeviceToHost, st));
+    h.maxabs_known = host_maxabs >= 0.f;
+    if (h.maxabs_known) s->h_maxabs[slot] = host_maxabs;
     h.valid = true;
     h.pending = true;
     h.ncp = ncp;
@@ -332,13 +341,19 @@ static int check_put(afam_store *s, int32_t slot, int deg, int ncp, const double
 
 // model.py MicroModel: non-finite control points are a ValueError.  Host
 // scan of the little-endian float32 payload by exponent bits (vectorizes).
-static bool all_finite_le_f32(const uint8_t *p, size_t count) {
-    uint32_t bad = 0;
+// Also returns max |c| (for finite floats the magnitude order is the order of
+// the bit patterns without the sign), the value the device derives in
+// unpack_ctrl_kernel: afam_render picks its kernel from it before the upload
+// has finished.
+static bool all_finite_le_f32(const uint8_t *p, size_t count, float *maxabs = nullptr) {
+    uint32_t bad = 0, mx = 0;
     for (size_t i = 0; i < count; i++) {
         uint32_t u;
         memcpy(&u, p + 4 * i, 4);
         bad |= (uint32_t)((u & 0x7f800000u) == 0x7f800000u);
+        mx = std::max(mx, u & 0x7fffffffu);
     }
+    if (maxabs) memcpy(maxabs, &mx, 4);
     return bad == 0;
 }
 
@@ -353,7 +368,8 @@ int afam_store_put_mfa(afam_store *s, int32_t slot, const uint8_t *bytes, uint64
                "micro-model length mismatch: expected %zu bytes for ncp=%d, degree=%d, found %llu", expected,
                ncp, deg, (unsigned long long)nbytes);
     // model.py MicroModel: non-finite control points are a ValueError
-    AFAM_CHECK(all_finite_le_f32(bytes + 1 + 12ull * (ncp + deg), (size_t)ncp * ncp * ncp), AFAM_E_VALUE,
+    float mx;
+    AFAM_CHECK(all_finite_le_f32(bytes + 1 + 12ull * (ncp + deg), (size_t)ncp * ncp * ncp, &mx), AFAM_E_VALUE,
                "non-finite control points");
     int rc = check_put(s, slot, deg, ncp, extent);
     if (rc) return rc;
@@ -364,7 +380,7 @@ int afam_store_put_mfa(afam_store *s, int32_t slot, const uint8_t *bytes, uint64
     AFAM_CUDA(cudaStreamWaitEvent(st, s->host[slot].ready, 0));
     AFAM_CUDA(wait_readers(s, slot, st));
     AFAM_CUDA(cudaMemcpyAsync(s->raw_ptr(slot), bytes, nbytes, cudaMemcpyHostToDevice, st));
-    return launch_unpack(s, slot, deg, ncp, 1, 0, 1 + 12ull * (ncp + deg), extent, st);
+    return launch_unpack(s, slot, deg, ncp, 1, 0, 1 + 12ull * (ncp + deg), extent, st, mx);
 }
 
 
@@ -395,7 +411,7 @@ int afam_store_put_mfa_device(afam_store *s, int32_t slot, const uint8_t *dbytes
     AFAM_CUDA(cudaStreamWaitEvent(st, s->host[slot].ready, 0));
     AFAM_CUDA(wait_readers(s, slot, st));
     AFAM_CUDA(cudaMemcpyAsync(s->raw_ptr(slot), dbytes, nbytes, cudaMemcpyDeviceToDevice, st));
-    return launch_unpack(s, slot, degree, ncp, 1, 0, 1 + 12ull * (ncp + degree), extent, st);
+    return launch_unpack(s, slot, degree, ncp, 1, 0, 1 + 12ull * (ncp + degree), extent, st, -1.f);
 }
 
 int afam_store_put_file(afam_store *s, int32_t slot, const char *path, int32_t ncp, const double extent[6],
@@ -450,7 +466,8 @@ int afam_store_put_file(afam_store *s, int32_t slot, const char *path, int32_t n
                "micro-model length mismatch: expected %zu bytes for ncp=%d, degree=%d, found %llu", expected, ncp,
                deg, (unsigned long long)nbytes);
     const uint64_t coff = 1 + 12ull * (ncp + deg);
-    AFAM_CHECK(all_finite_le_f32(bytes + coff, (size_t)ncp * ncp * ncp), AFAM_E_VALUE, "non-finite control points");
+    float mx;
+    AFAM_CHECK(all_finite_le_f32(bytes + coff, (size_t)ncp * ncp * ncp, &mx), AFAM_E_VALUE, "non-finite control points");
     rc = check_put(s, slot, deg, ncp, extent);
     if (rc) return rc;
     if (degree) *degree = deg;
@@ -460,7 +477,7 @@ int afam_store_put_file(afam_store *s, int32_t slot, const char *path, int32_t n
     AFAM_CUDA(wait_readers(s, slot, st));
     AFAM_CUDA(cudaMemcpyAsync(s->raw_ptr(slot), bytes, nbytes, cudaMemcpyHostToDevice, st));
     AFAM_CUDA(cudaEventRecord(s->ev_file[b], st));
-    return launch_unpack(s, slot, deg, ncp, 1, 0, coff, extent, st);
+    return launch_unpack(s, slot, deg, ncp, 1, 0, coff, extent, st, mx);
 }
 
 int afam_store_put_ds(afam_store *s, int32_t slot, const uint8_t *bytes, uint64_t nbytes, const double extent[6],
@@ -542,7 +559,9 @@ int afam_store_put(afam_store *s, int32_t slot, int32_t degree, int32_t ncp, con
     AFAM_CUDA(wait_readers(s, slot, st));
     AFAM_CUDA(cudaMemcpyAsync(s->raw_ptr(slot) + koff, knots, kb, cudaMemcpyHostToDevice, st));
     AFAM_CUDA(cudaMemcpyAsync(s->raw_ptr(slot) + coff, ctrl, cb, cudaMemcpyHostToDevice, st));
-    return launch_unpack(s, slot, degree, ncp, koff, 1, coff, extent, st);
+    float mx = -1.f;  // max |c| when finite (a non-finite value leaves it to the device)
+    if (!all_finite_le_f32(reinterpret_cast<const uint8_t *>(ctrl), (size_t)ncp * ncp * ncp, &mx)) mx = -1.f;
+    return launch_unpack(s, slot, degree, ncp, koff, 1, coff, extent, st, mx);
 }
 
 int afam_store_evict(afam_store *s, int32_t slot) {
