@@ -586,8 +586,10 @@ def run_config5(ds, resident_all, man, blobs, rank, world, dev, steps, warmup, e
 
     from paper_2409_00184_b200 import _lib
 
+    from paper_2409_00184_b200 import tiles
+
     m = 65
-    addrs = sorted(resident_all)[rank::world]
+    addrs = tiles.shard_blocks(resident_all, rank, world)  # block i on rank i % N
     slots = np.array([resident_all[a].slot for a in addrs], dtype=np.int32)
     ncps = np.array([resident_all[a].ncp for a in addrs], dtype=np.int64)
     out = torch.empty(len(slots) * m ** 3, dtype=torch.float32, device=dev)

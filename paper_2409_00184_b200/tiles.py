@@ -13,7 +13,7 @@ from __future__ import annotations
 import numpy as np
 
 __all__ = ["part_rows", "assemble", "gather_bands", "render_tiles", "PeerFrame", "render_tiles_fused",
-           "BroadcastLoader", "LockstepDone"]
+           "BroadcastLoader", "LockstepDone", "shard_blocks", "decode_grid_sharded"]
 
 
 def part_rows(height: int, band_rows: int, nparts: int, part: int) -> np.ndarray:
@@ -260,7 +260,10 @@ class BroadcastLoader:
         self.manifest, self.dstore, self.source, self.group = manifest, dstore, source, group
         self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
         self.device = torch.device("cuda", dstore.device) if device is None else torch.device(device)
-        cap = max_bytes if max_bytes is not None else serialized_size(dstore.max_ncp, 3)
+        from . import _lib
+
+        # the largest .mfa image of this store: max_ncp at the largest device degree
+        cap = max_bytes if max_bytes is not None else serialized_size(dstore.max_ncp, _lib.AFAM_MAX_DEGREE)
         self.staging = torch.empty(int(cap), dtype=torch.uint8, device=self.device)
         self.hdr = torch.zeros(3, dtype=torch.int64, device=self.device)
         self.misses = 0
@@ -330,3 +333,49 @@ class BroadcastLoader:
 
     def lockstep(self, done):
         return LockstepDone(done, self.group, self.device)
+
+
+# ---------------------------------------------------------------------------
+# Grid decode over the GPUs of one node (BASELINE config 5):
+# MicroModel.decode_grid (model.py:89-93 -> bspline.py:162-172) of every
+# block, the blocks dealt round-robin over the ranks.  Blocks are
+# independent and the decoded grids stay on their rank, so there is no
+# exchange step and no collective.
+def shard_blocks(addrs, rank: int | None = None, world: int | None = None, group=None) -> list:
+    """This rank's share of a block list: sorted addresses, block i on rank
+    i % world (interleaved, so the NCP mix -- and the work -- balances)."""
+    if rank is None or world is None:
+        import torch.distributed as dist
+
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+    return sorted(addrs)[rank::world]
+
+
+def decode_grid_sharded(blocks: dict, m: int, *, group=None, stream=None, rank: int | None = None,
+                        world: int | None = None):
+    """decode_grid((m, m, m)) of this rank's share of `blocks` ({addr:
+    DeviceBlock}, every block resident in one DeviceStore on this rank's GPU)
+    in one K3 launch.  Returns (addrs, grids): the rank's addresses and a
+    device tensor (n, m, m, m) laid out [b][k][j][i] (x fastest, the decode
+    kernels' layout; grids[b].permute(2, 1, 0) is the reference's [i, j, k])."""
+    import ctypes as C
+
+    import torch
+
+    from . import _lib
+    from .device import stream_handle
+
+    mine = shard_blocks(list(blocks), rank, world, group)
+    if not mine:
+        return mine, None
+    store = blocks[mine[0]].store
+    if any(blocks[a].store is not store for a in mine):
+        raise ValueError("decode_grid_sharded: the rank's blocks must share one DeviceStore")
+    slots = np.ascontiguousarray([blocks[a].slot for a in mine], dtype=np.int32)
+    dev = torch.device("cuda", store.device)
+    out = torch.empty((len(mine), m, m, m), dtype=torch.float32, device=dev)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.lib().afam_decode_grid(store.handle, slots.ctypes.data_as(C.c_void_p), len(mine), int(m),
+                                               C.c_void_p(out.data_ptr()), C.c_void_p(stream_handle(stream, dev))))
+    return mine, out

@@ -100,3 +100,4 @@ def test_degree5_frames_vs_reference(cuda, oracle, name):
     assert st["fp64_samples"] == st["samples"]  # every degree-5 sample on the float64 path
     if p.o_max == 1.0:
         assert st["samples"] == int(z[f"f{name}_samples"])
+

@@ -65,3 +65,37 @@ def _worker(rank, world, port, H, W, br, outdir):
 def test_gather_bands_gloo(world, tmp_path):
     mp.spawn(_worker, args=(world, _free_port(), 50, 6, 8, str(tmp_path)), nprocs=world, join=True)
     assert all((tmp_path / f"r{r}").read_text() == "1" for r in range(world))
+
+
+def _shard_worker(rank, world, port, outdir):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2409_00184_b200 import tiles as t
+    from paper_2409_00184_b200.partition import BlockAddress
+
+    dist.init_process_group("gloo", rank=rank, world_size=world, init_method=f"tcp://127.0.0.1:{port}")
+    # the config-3 skeleton's addresses, in a scrambled order on every rank
+    addrs = [BlockAddress(l, (i, j, k)) for l, b in ((1, 16), (2, 8), (3, 4), (4, 2))
+             for i in range(b) for j in range(b) for k in range(b)]
+    rng = np.random.default_rng(rank)
+    mine = t.shard_blocks([addrs[i] for i in rng.permutation(len(addrs))])  # rank/world from the process group
+    got = [None] * world
+    dist.all_gather_object(got, [(a.lod, *a.ijk) for a in mine])
+    ok = True
+    if rank == 0:
+        flat = [x for part in got for x in part]
+        ok = sorted(flat) == sorted((a.lod, *a.ijk) for a in addrs) and len(set(flat)) == len(flat)
+        ok = ok and max(map(len, got)) - min(map(len, got)) <= 1
+    with open(os.path.join(outdir, f"s{rank}"), "w") as fh:
+        fh.write("1" if ok else "0")
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_shard_blocks_gloo(world, tmp_path):
+    """Grid-decode sharding (config 5): every block on exactly
+    one rank, balanced, the same split whatever order each rank lists them in."""
+    mp.spawn(_shard_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    assert all((tmp_path / f"s{r}").read_text() == "1" for r in range(world))
