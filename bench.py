@@ -499,8 +499,10 @@ def run_e2e(args, man, blobs, povs, tf, params, rank, world, local_rank):
 
     draw.submit = submit
     draw.samples, draw.d2h = 0, 0
+    # config 4: the whole 100-frame orbit is timed (after W warm-up frames
+    # on the same cache, so the first W orbit frames start resident)
     nwarm = args.warmup
-    nsteps = args.e2e_steps or args.steps
+    nsteps = args.e2e_steps or len(povs)
     runtime.replay(povs[:nwarm], man, cache, tf, params, prefetch="linear", keep_frames=False, render_fn=draw)
     c0 = cache.counters()
     draw.samples, draw.d2h = 0, 0
@@ -508,7 +510,7 @@ def run_e2e(args, man, blobs, povs, tf, params, rank, world, local_rank):
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    timings, _, agg = runtime.replay(povs[nwarm:nwarm + nsteps], man, cache, tf, params, prefetch="linear",
+    timings, _, agg = runtime.replay(povs[:nsteps], man, cache, tf, params, prefetch="linear",
                                      keep_frames=False, render_fn=draw)
     torch.cuda.synchronize()
     if world > 1:
@@ -531,7 +533,9 @@ def run_e2e(args, man, blobs, povs, tf, params, rank, world, local_rank):
         extra.update(rank_h2d_bytes=loader.h2d_bytes, rank_recv_bytes=loader.recv_bytes)
     return {**extra, "value": float(tot[0]) / float(tot[1]), "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": draw.d2h / nsteps, "steps": nsteps,
-            "api": "runtime.replay(ModelCache(200), prefetch='linear' on the frame thread while the GPU marches) -> tiles.render_tiles -> Frame bytes on host",
+            "api": "runtime.replay over the 100-frame orbit (ModelCache(200), prefetch='linear' on the frame thread "
+                   "while the GPU marches, the next frame's caching overlapped with the current frame) -> "
+                   "tiles.render_tiles -> Frame bytes on host; wall clock",
             "mean_caching_ms": agg["mean_caching_ms"], "mean_rendering_ms": agg["mean_rendering_ms"],
             "mean_latency_ms": agg["mean_latency_ms"], "miss_rate": agg["miss_rate"],
             "prefetch_models_loaded": agg["prefetch_models_loaded"]}
