@@ -498,6 +498,7 @@ def run_e2e(args, man, blobs, povs, tf, params, rank, world, local_rank):
         return Counted(tiles.submit_tiles(pov, resident, tf_, params_, band_rows=band), tiles.render_tiles)
 
     draw.submit = submit
+    draw.frames_in_flight = 1 if peer is not None else 2  # the fused gather has one frame buffer
     draw.samples, draw.d2h = 0, 0
     # config 4: the whole 100-frame orbit is timed (after W warm-up frames
     # on the same cache, so the first W orbit frames start resident)
@@ -534,7 +535,7 @@ def run_e2e(args, man, blobs, povs, tf, params, rank, world, local_rank):
     return {**extra, "value": float(tot[0]) / float(tot[1]), "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": draw.d2h / nsteps, "steps": nsteps,
             "api": "runtime.replay over the 100-frame orbit (ModelCache(200), prefetch='linear' on the frame thread "
-                   "while the GPU marches, the next frame's caching overlapped with the current frame) -> "
+                   "while the GPU marches, the next frame's caching and launch overlapped with the current frame) -> "
                    "tiles.render_tiles -> Frame bytes on host; wall clock",
             "mean_caching_ms": agg["mean_caching_ms"], "mean_rendering_ms": agg["mean_rendering_ms"],
             "mean_latency_ms": agg["mean_latency_ms"], "miss_rate": agg["miss_rate"],

@@ -308,6 +308,15 @@ int afam_copy_to_host(void *host, const void *dev_ptr, uint64_t bytes);
 /* Device time (ms) of the kernels of the last afam_render on this store
  * (CUDA events recorded on its stream around the launches); waits for them. */
 int afam_render_elapsed(afam_store *s, float *ms);
+/* The calling thread keeps its last 2 afam_render calls in flight-safe
+ * state (frame i+1 may be launched before frame i is collected):
+ * afam_render_seq gives the number of calls the thread has made on the
+ * store's device (the next call's sequence number), afam_render_elapsed_seq
+ * the kernel time of call `seq` (one of the last two; waits for it).
+ * afam_render_elapsed is the last call's.  (runtime.replay's depth-2
+ * pipeline, render.submit) */
+int afam_render_seq(afam_store *s, uint64_t *count);
+int afam_render_elapsed_seq(afam_store *s, uint64_t seq, float *ms);
 
 /* Rows of the full frame rendered by (band_rows, nparts, part). */
 int32_t afam_frame_rows(int32_t height, int32_t band_rows, int32_t nparts, int32_t part);

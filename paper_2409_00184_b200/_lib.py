@@ -121,6 +121,8 @@ SIGNATURES = [
     ("afam_device_free", C.c_int, [C.c_void_p]),
     ("afam_copy_to_host", C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
     ("afam_render_elapsed", C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
+    ("afam_render_seq", C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
+    ("afam_render_elapsed_seq", C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_float)]),
     ("afam_frame_rows", C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
     ("afam_owner_grid", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.c_void_p,
                                   C.c_int32]),

@@ -69,11 +69,15 @@ struct SlotHost {
 // from one store never share these (no lock, no overwritten kernel time).
 // Never destroyed: slots may still name `k1` / `read` as their reader.
 struct ThreadCtx {
-    cudaEvent_t k0 = nullptr, k1 = nullptr;  // bracket the last afam_render's kernels (timing)
-    unsigned char *pack = nullptr;           // pinned staging of afam_render's per-frame upload
-    size_t pack_cap = 0;
-    cudaEvent_t ev_pack = nullptr;           // the last upload out of `pack`
-    cudaEvent_t read = nullptr;              // recorded after afam_eval_points / afam_decode_grid launches
+    // afam_render keeps a ring of kRing frames per thread (a caller may
+    // launch frame i+1 before collecting frame i): call n uses entry n % kRing
+    static constexpr int kRing = 2;
+    cudaEvent_t k0[kRing] = {}, k1[kRing] = {};  // bracket the call's kernels (timing, slot readers)
+    unsigned char *pack[kRing] = {};              // pinned staging of the call's argument upload
+    size_t pack_cap[kRing] = {};
+    cudaEvent_t ev_pack[kRing] = {};              // the last upload out of pack[r]
+    uint64_t nrender = 0;                         // afam_render calls made by this thread on this device
+    cudaEvent_t read = nullptr;                   // recorded after afam_eval_points / afam_decode_grid launches
 };
 ThreadCtx *thread_ctx(int device);  // afam_store.cu
 

@@ -2237,17 +2237,18 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
     ThreadCtx *tc = thread_ctx(s->device);
     AFAM_CHECK(tc, AFAM_E_CUDA, "per-thread render state unavailable");
     ht.mark();
-    if (tc->pack_cap < total) {
-        AFAM_CUDA(cudaEventSynchronize(tc->ev_pack));
-        if (tc->pack) AFAM_CUDA(cudaFreeHost(tc->pack));
-        tc->pack = nullptr;
-        tc->pack_cap = 0;
-        AFAM_CUDA(cudaHostAlloc((void **)&tc->pack, total + (64 << 10), cudaHostAllocDefault));
-        tc->pack_cap = total + (64 << 10);
+    const int ring = (int)(tc->nrender % ThreadCtx::kRing);
+    if (tc->pack_cap[ring] < total) {
+        AFAM_CUDA(cudaEventSynchronize(tc->ev_pack[ring]));
+        if (tc->pack[ring]) AFAM_CUDA(cudaFreeHost(tc->pack[ring]));
+        tc->pack[ring] = nullptr;
+        tc->pack_cap[ring] = 0;
+        AFAM_CUDA(cudaHostAlloc((void **)&tc->pack[ring], total + (64 << 10), cudaHostAllocDefault));
+        tc->pack_cap[ring] = total + (64 << 10);
     } else {
-        AFAM_CUDA(cudaEventSynchronize(tc->ev_pack));
+        AFAM_CUDA(cudaEventSynchronize(tc->ev_pack[ring]));
     }
-    unsigned char *pack = tc->pack;
+    unsigned char *pack = tc->pack[ring];
     unsigned char *d_pack = nullptr;
     AFAM_CUDA(cudaMallocAsync(&d_pack, total, st));
     memset(pack, 0, total);
@@ -2266,9 +2267,9 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
     memcpy(pack + off_grid, grid.data(), gbytes);
     if (nblocks) memcpy(pack + off_idx, slots, (size_t)nblocks * sizeof(int32_t));
     AFAM_CUDA(cudaMemcpyAsync(d_pack, pack, total, cudaMemcpyHostToDevice, st));
-    AFAM_CUDA(cudaEventRecord(tc->ev_pack, st));
+    AFAM_CUDA(cudaEventRecord(tc->ev_pack[ring], st));
     ht.mark();
-    AFAM_CUDA(cudaEventRecord(tc->k0, st));
+    AFAM_CUDA(cudaEventRecord(tc->k0[ring], st));
     init_stats_kernel<<<1, 1, 0, st>>>(stats);
     if (A.rows > 0) {
         LaunchArgs L;
@@ -2294,9 +2295,10 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
         }
     }
     finish_stats_kernel<<<1, 1, 0, st>>>(stats);
-    AFAM_CUDA(cudaEventRecord(tc->k1, st));
+    AFAM_CUDA(cudaEventRecord(tc->k1[ring], st));
     AFAM_CUDA(cudaGetLastError());
-    mark_readers(s, slots, nblocks, tc->k1);  // uploads into these slots now wait for this frame
+    mark_readers(s, slots, nblocks, tc->k1[ring]);  // uploads into these slots now wait for this frame
+    tc->nrender++;
     AFAM_CUDA(cudaFreeAsync(d_pack, st));
     ht.mark();
     ht.report("afam_render: setdevice, args+tf, grid+waits, pack lock, pack+upload, launches");
@@ -2350,7 +2352,28 @@ extern "C" int afam_render_elapsed(afam_store *s, float *ms) {
     AFAM_CUDA(cudaSetDevice(s->device));
     ThreadCtx *tc = thread_ctx(s->device);
     AFAM_CHECK(tc, AFAM_E_CUDA, "per-thread render state unavailable");
-    AFAM_CUDA(cudaEventSynchronize(tc->k1));
-    AFAM_CUDA(cudaEventElapsedTime(ms, tc->k0, tc->k1));
+    AFAM_CHECK(tc->nrender > 0, AFAM_E_VALUE, "no afam_render call on this thread");
+    return afam_render_elapsed_seq(s, tc->nrender - 1, ms);
+}
+
+extern "C" int afam_render_seq(afam_store *s, uint64_t *count) {
+    AFAM_CHECK(s && count, AFAM_E_VALUE, "NULL argument to afam_render_seq");
+    ThreadCtx *tc = thread_ctx(s->device);
+    AFAM_CHECK(tc, AFAM_E_CUDA, "per-thread render state unavailable");
+    *count = tc->nrender;
+    return AFAM_OK;
+}
+
+extern "C" int afam_render_elapsed_seq(afam_store *s, uint64_t seq, float *ms) {
+    AFAM_CHECK(s && ms, AFAM_E_VALUE, "NULL argument to afam_render_elapsed_seq");
+    AFAM_CUDA(cudaSetDevice(s->device));
+    ThreadCtx *tc = thread_ctx(s->device);
+    AFAM_CHECK(tc, AFAM_E_CUDA, "per-thread render state unavailable");
+    AFAM_CHECK(seq < tc->nrender && tc->nrender - seq <= (uint64_t)ThreadCtx::kRing, AFAM_E_VALUE,
+               "afam_render call %llu of this thread is not among its last %d", (unsigned long long)seq,
+               ThreadCtx::kRing);
+    const int r = (int)(seq % ThreadCtx::kRing);
+    AFAM_CUDA(cudaEventSynchronize(tc->k1[r]));
+    AFAM_CUDA(cudaEventElapsedTime(ms, tc->k0[r], tc->k1[r]));
     return AFAM_OK;
 }

@@ -42,9 +42,11 @@ ThreadCtx *thread_ctx(int device) {
     auto it = ctx.find(device);
     if (it != ctx.end()) return it->second;
     ThreadCtx *c = new ThreadCtx();
-    if (cudaEventCreate(&c->k0) != cudaSuccess || cudaEventCreate(&c->k1) != cudaSuccess ||
-        cudaEventCreateWithFlags(&c->ev_pack, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&c->read, cudaEventDisableTiming) != cudaSuccess) {
+    bool ok = cudaEventCreateWithFlags(&c->read, cudaEventDisableTiming) == cudaSuccess;
+    for (int r = 0; r < ThreadCtx::kRing; r++)
+        ok = ok && cudaEventCreate(&c->k0[r]) == cudaSuccess && cudaEventCreate(&c->k1[r]) == cudaSuccess &&
+             cudaEventCreateWithFlags(&c->ev_pack[r], cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) {
         set_error("cannot create the per-thread render events");
         return nullptr;
     }

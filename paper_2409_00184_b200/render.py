@@ -402,15 +402,24 @@ def _missing_message(pov, params, cells, key) -> str:
 _tls = threading.local()
 
 
-def _pinned_stage(nbytes: int):
-    """This thread's pinned host staging buffer of >= 64 + nbytes bytes (grown on demand)."""
+# A thread may have FRAMES_IN_FLIGHT submitted, uncollected frames (libafam
+# keeps the same ring per thread, afam_render_seq): each ring entry has its
+# own pinned staging buffer, device stats buffer and completion event.
+FRAMES_IN_FLIGHT = 2
+
+
+def _pinned_stage(nbytes: int, ring: int = 0):
+    """This thread's pinned host staging buffer `ring` of >= 64 + nbytes bytes (grown on demand)."""
     import torch
 
     need = 64 + nbytes
-    buf = getattr(_tls, "stage", None)
+    stages = getattr(_tls, "stages", None)
+    if stages is None:
+        stages = _tls.stages = [None] * FRAMES_IN_FLIGHT
+    buf = stages[ring]
     if buf is None or buf.numel() < need:
         buf = torch.empty(max(need, 1 << 16), dtype=torch.uint8, pin_memory=True)
-        _tls.stage = buf
+        stages[ring] = buf
     return buf
 
 
@@ -448,37 +457,38 @@ def render_part(pov, blocks: dict, tf, params, *, band_rows: int | None = None, 
                        out_ptr=out_ptr).result()
 
 
-def _thread_stats(dev):
-    """This thread's device stats buffer and completion event (one frame in
-    flight per thread: submit_part's handle is consumed before the next)."""
+def _thread_stats(dev, ring: int = 0):
+    """This thread's device stats buffer and completion event of ring entry `ring`."""
     import torch
 
     key = ("stats", dev.index)
     st = getattr(_tls, "stats", None)
     if st is None or st[0] != key:
-        st = (key, torch.empty(6, dtype=torch.int64, device=dev), torch.cuda.Event())
+        st = (key, [(torch.empty(6, dtype=torch.int64, device=dev), torch.cuda.Event())
+                    for _ in range(FRAMES_IN_FLIGHT)])
         _tls.stats = st
-    return st[1], st[2]
+    return st[1][ring]
 
 
 def _addr_key(a):
     return (a.lod, a.ijk)
 
 
-_inflight: dict = {}  # thread ident -> its uncollected PendingPart (one per thread)
+_inflight: dict = {}  # thread ident -> its uncollected PendingParts, oldest first (<= FRAMES_IN_FLIGHT)
 
 
 class PendingPart:
     """A launched render_part: `done()` polls the GPU (no host wait),
     `result()` waits and returns render_part's (rgba, info, debug).  A thread
-    has at most one uncollected frame: the staging buffer, stats buffer and
-    completion event are per thread."""
+    has at most FRAMES_IN_FLIGHT uncollected frames (ring entries of staging
+    buffer, stats buffer and completion event); a further submit waits for
+    the oldest, whose result() then raises."""
 
     def __init__(self, **kw):
         self.__dict__.update(kw)
         self._res = None
         self._owner = threading.get_ident()
-        _inflight[self._owner] = self
+        _inflight.setdefault(self._owner, []).append(self)
 
     def done(self) -> bool:
         return self._res is not None or self.event.query()
@@ -490,17 +500,18 @@ class PendingPart:
 
         if getattr(self, "_superseded", False):
             raise RuntimeError("this frame's buffers were reused by a later submit on the same thread")
-        if _inflight.get(self._owner) is self:
-            del _inflight[self._owner]
+        mine = _inflight.get(self._owner)
+        if mine is not None and self in mine:
+            mine.remove(self)
 
         with torch.cuda.device(self.dev):
-            self.s_obj.synchronize()
+            self.event.synchronize()  # this frame only (a later frame may be queued behind it)
             st = self.stage[:48].view(torch.int64).numpy().copy()
             out = self.out
             if self.host_out:
                 out = self.stage[64:64 + self.nbytes].view(self.rows, self.W, 4).clone()
         kms = C.c_float()
-        _lib.check(_lib.lib().afam_render_elapsed(self.store.handle, C.byref(kms)))
+        _lib.check(_lib.lib().afam_render_elapsed_seq(self.store.handle, self.seq, C.byref(kms)))
         info = {"samples": int(st[0]), "missing_key": int(st[1]), "fp64_samples": int(st[2]),
                 "shaded_samples": int(st[3]), "exact_samples": int(st[4]),
                 "exact_cells": int(st[5]),
@@ -525,8 +536,11 @@ def submit_part(pov, blocks: dict, tf, params, *, band_rows: int | None = None, 
 
     from .device import as_device_blocks, stream_handle
 
-    prev = _inflight.pop(threading.get_ident(), None)
-    if prev is not None:  # an uncollected frame of this thread: let it finish, then its buffers are reused
+    ring = getattr(_tls, "nsubmit", 0) % FRAMES_IN_FLIGHT
+    _tls.nsubmit = getattr(_tls, "nsubmit", 0) + 1
+    mine = _inflight.setdefault(threading.get_ident(), [])
+    for prev in [p for p in mine if p.ring == ring]:  # uncollected frame FRAMES_IN_FLIGHT submits ago:
+        mine.remove(prev)                               # let it finish, its ring entry is reused
         prev.s_obj.synchronize()
         prev._superseded = True
     try:  # (lod, i, j, k) order as BlockAddress.__lt__, without a Python compare per pair
@@ -546,18 +560,20 @@ def submit_part(pov, blocks: dict, tf, params, *, band_rows: int | None = None, 
     if out_ptr is not None and host_out:
         raise ValueError("out_ptr and host_out are exclusive")
     zero_copy = host_out and out is None
-    stage = _pinned_stage(rows * W * 4 if host_out else 0)
+    stage = _pinned_stage(rows * W * 4 if host_out else 0, ring)
     if out is None and out_ptr is None:
         out = stage[64:64 + rows * W * 4].view(rows, W, 4) if zero_copy else \
             torch.empty((rows, W, 4), dtype=torch.uint8, device=dev)
-    stats, event = _thread_stats(dev)
+    stats, event = _thread_stats(dev, ring)
     nsamp = ohash = None
     if debug:
         nsamp = torch.empty((rows, W), dtype=torch.int32, device=dev)
         ohash = torch.empty((rows, W), dtype=torch.int64, device=dev)
     sl = np.ascontiguousarray(slots, dtype=np.int32)
+    seq = C.c_uint64()
     with torch.cuda.device(dev):
         s_obj = stream if stream is not None else _render_stream(dev)
+        _lib.check(_lib.lib().afam_render_seq(store.handle, C.byref(seq)))  # this call's number (kernel time)
         _lib.check(_lib.lib().afam_render(
             store.handle, C.byref(fr), sl.ctypes.data_as(C.c_void_p), len(sl),
             C.c_void_p(out_ptr if out_ptr is not None else out.data_ptr()),
@@ -570,7 +586,7 @@ def submit_part(pov, blocks: dict, tf, params, *, band_rows: int | None = None, 
             event.record(s_obj)
     return PendingPart(dev=dev, s_obj=s_obj, stage=stage, out=out, host_out=host_out, nbytes=rows * W * 4,
                        rows=rows, W=W, store=store, sl=sl, pov=pov, params=params, raise_missing=raise_missing,
-                       debug=debug, nsamp=nsamp, ohash=ohash, stats=stats, event=event)
+                       debug=debug, nsamp=nsamp, ohash=ohash, stats=stats, event=event, seq=int(seq.value), ring=ring)
 
 
 class PendingFrame:
@@ -603,3 +619,4 @@ def render(pov, blocks: dict, tf, params) -> Frame:
 
 render.submit = submit
 render.last_stats = None
+render.frames_in_flight = FRAMES_IN_FLIGHT  # runtime.replay may launch frame i+1 before collecting frame i

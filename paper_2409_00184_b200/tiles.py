@@ -95,6 +95,7 @@ def submit_tiles(pov, blocks: dict, tf, params, *, group=None, band_rows: int = 
 
 render_tiles.submit = submit_tiles
 render_tiles.last_stats = None
+render_tiles.frames_in_flight = 2  # per-call output buffers: runtime.replay may keep two frames launched
 
 
 class PeerFrame:
@@ -208,6 +209,7 @@ def submit_tiles_fused(pov, blocks: dict, tf, params, peer: PeerFrame, *, group=
 
 render_tiles_fused.submit = submit_tiles_fused
 render_tiles_fused.last_stats = None
+render_tiles_fused.frames_in_flight = 1  # one PeerFrame: a frame is collected before the next is launched
 
 
 # ------------------------------------------------------------ shared misses

@@ -244,3 +244,69 @@ def test_replay_with_submit_prefetches_while_frame_in_flight(manifest):
         assert (loaded > 0) == expect_loads
         for t in timings:
             assert t.input_latency_ms == pytest.approx(t.caching_ms + t.rendering_ms, abs=1e-6)
+
+
+@pytest.mark.parametrize("depth", [1, 2])
+def test_replay_pipeline_keeps_the_reference_operation_order(manifest, depth):
+    """replay's submit schedule (the next frame's caching, and at depth 2 its
+    launch, overlapped with the current frame): the cache sees the
+    reference's operation sequence -- caching i, prefetch i, caching i+1 --
+    exactly as the strict order does (same loads, same hit/miss counters,
+    same residency), at most `depth` frames are launched and uncollected,
+    and frames come back in trajectory order."""
+    from paper_2409_00184_b200.render import PointOfView
+    from paper_2409_00184_b200.runtime import ModelCache, replay
+
+    povs = [PointOfView([0.3 + 0.02 * i, 0.2, 3.2 - 0.15 * i], [0, 0, -1], [0, 1, 0]) for i in range(16)]
+    params = type("P", (), {"aspect": 1.0})()
+
+    def run(overlap, d):
+        log, inflight, peak = [], [], [0]
+
+        class Pending:
+            def __init__(self, i):
+                self.i, self.polls = i, 0
+
+            def done(self):  # each frame "finishes" after 3 polls
+                self.polls += 1
+                return self.polls > 3
+
+            def result(self):
+                inflight.remove(self.i)
+                return ("frame", self.i)
+
+        def draw(pov, resident, tf, params_):
+            raise AssertionError("replay must use submit")
+
+        def submit(pov, resident, tf, params_):
+            i = povs.index(pov)
+            inflight.append(i)
+            peak[0] = max(peak[0], len(inflight))
+            log.append(("submit", i, tuple(sorted(resident))))
+            return Pending(i)
+
+        draw.submit = submit
+        draw.frames_in_flight = d
+
+        def loader(key):
+            log.append(("load", key))
+            return Blob(key)
+
+        cache = ModelCache(40, loader)
+        import os
+
+        os.environ["AFAM_REPLAY_OVERLAP"] = "1" if overlap else "0"
+        try:
+            timings, frames, _ = replay(povs, manifest, cache, None, params, prefetch="linear", render_fn=draw)
+        finally:
+            os.environ.pop("AFAM_REPLAY_OVERLAP", None)
+        return log, frames, cache, peak[0]
+
+    ref_log, ref_frames, ref_cache, _ = run(False, 1)
+    log, frames, cache, peak = run(True, depth)
+    assert frames == ref_frames == [("frame", i) for i in range(len(povs))]
+    assert [e for e in log if e[0] == "load"] == [e for e in ref_log if e[0] == "load"]
+    assert [e for e in log if e[0] == "submit"] == [e for e in ref_log if e[0] == "submit"]
+    assert (cache.hits, cache.misses, cache.evictions) == (ref_cache.hits, ref_cache.misses, ref_cache.evictions)
+    assert cache.resident_addresses() == ref_cache.resident_addresses()
+    assert peak == depth

@@ -28,14 +28,32 @@ def draw(pov, resident, tf_, params_):
     return tiles.render_tiles(pov, resident, tf_, params_, band_rows=8)
 
 
-draw.submit = lambda pov, resident, tf_, params_: tiles.submit_tiles(pov, resident, tf_, params_, band_rows=8)
+class Timed:  # collects each frame's kernel time (CUDA events around the render kernels)
+    def __init__(self, p):
+        self.p = p
+
+    def done(self):
+        return self.p.done()
+
+    def result(self):
+        f = self.p.result()
+        kms.append(tiles.render_tiles.last_stats["kernel_ms"])
+        return f
+
+
+kms = []
+draw.submit = lambda pov, resident, tf_, params_: Timed(tiles.submit_tiles(pov, resident, tf_, params_,
+                                                                          band_rows=8))
+draw.frames_in_flight = 2
 for r in range(rounds):
-    for mode in ("1", "0"):
-        os.environ["AFAM_REPLAY_OVERLAP"] = mode
+    for mode in ("2", "1", "0"):  # depth 2, depth 1 (overlapped caching), the reference's strict order
+        os.environ["AFAM_REPLAY_OVERLAP"] = "0" if mode == "0" else "1"
+        os.environ["AFAM_REPLAY_DEPTH"] = "2" if mode == "2" else "1"
         ds = DeviceStore(201, 65)
         cache = runtime.ModelCache(200, runtime.make_loader(None, man, ds, source=lambda a: blobs[a]))
         runtime.replay(povs[:3], man, cache, tf, params, prefetch="linear", keep_frames=False, render_fn=draw)
         torch.cuda.synchronize()
+        kms.clear()
         t0 = time.perf_counter()
         tim, _, agg = runtime.replay(povs[3:3 + nfr], man, cache, tf, params, prefetch="linear",
                                      keep_frames=False, render_fn=draw)
@@ -44,5 +62,6 @@ for r in range(rounds):
         print(json.dumps({"overlap": mode, "frames": nfr, "ms_per_frame": 1e3 * el / nfr,
                           "caching_ms": sum(t.caching_ms for t in tim) / nfr,
                           "rendering_ms": sum(t.rendering_ms for t in tim) / nfr,
-                          "loaded": sum(t.prefetch_models_loaded for t in tim)}), flush=True)
+                          "loaded": sum(t.prefetch_models_loaded for t in tim),
+                          "kernel_ms": sum(kms) / max(1, len(kms))}), flush=True)
         del cache, ds
