@@ -292,11 +292,25 @@ extern "C" int afam_eval_points(afam_store *s, const int32_t *slots, int32_t slo
             AFAM_CUDA(cudaStreamWaitEvent(st, s->host[slot].ready, 0));
         } else {
             // the caller passes resident slots only; order after every upload still in flight
+            bool any_ds = false;
             for (int32_t k = 0; k < s->nslots; k++) {
                 SlotHost &h = s->host[k];
+                any_ds = any_ds || (h.valid && h.ds);
                 if (!h.valid || !h.pending) continue;
                 if (cudaEventQuery(h.ready) == cudaSuccess) h.pending = false;
                 else AFAM_CUDA(cudaStreamWaitEvent(st, h.ready, 0));
+            }
+            if ((flags & AFAM_EVAL_PARAM) && any_ds) {
+                // parameter-space points need splines: the single-slot rule for
+                // the per-point slots too (read back only when DS slots exist)
+                std::vector<int32_t> hs((size_t)n);
+                AFAM_CUDA(cudaMemcpyAsync(hs.data(), slots, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+                AFAM_CUDA(cudaStreamSynchronize(st));
+                for (int64_t i = 0; i < n; i++) {
+                    const int32_t k = hs[(size_t)i];
+                    AFAM_CHECK(!(k >= 0 && k < s->nslots && s->host[k].valid && s->host[k].ds), AFAM_E_VALUE,
+                               "slot %d holds a DS block: parameter-space evaluation needs a spline", k);
+                }
             }
         }
     }

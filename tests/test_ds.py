@@ -170,3 +170,34 @@ def test_ds_scratch_store_keeps_the_calls_blocks():
             sc.get_ds(blocks[a], downsample.serialize_ds, allp)
     # DS scratch stores are sized by the sample edge, not a spline NCP bucket
     assert device.scratch_store(edge, 0, exact=True).store.max_ncp == edge
+
+
+@pytest.mark.gpu
+def test_ds_slots_reject_parameter_space_points():
+    """Parameter-space evaluation needs a spline (a DS block has no
+    parameter space): the per-point slots path raises like the single-slot
+    one when a batch names a DS slot, and still evaluates spline-only
+    batches of a store that also holds DS blocks."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from helpers import npz
+
+    from paper_2409_00184_b200 import bspline, downsample, model
+    from paper_2409_00184_b200.device import DeviceStore
+
+    z = npz("ds_points.npz")
+    b = downsample.DsBlock(z["b0_samples"], int(z["b0_ghost"]), z["b0_extent"], int(z["b0_lod"]))
+    ds = DeviceStore(2, 65)
+    ds.put_ds(0, downsample.serialize_ds(b), b.extent)
+    c = np.random.default_rng(0).normal(size=(7, 7, 7)).astype(np.float32)
+    m = model.MicroModel(3, np.stack([bspline.clamped_knots(7, 3)] * 3).astype(np.float32), c,
+                         np.array([[0, 1.0]] * 3), 1)
+    ds.put_model(1, m)
+    u = np.random.default_rng(1).uniform(0, 1, size=(64, 3))
+    with pytest.raises(ValueError, match="DS block"):
+        bspline.eval_device(ds, 0, u, gradient=False, param=True)
+    with pytest.raises(ValueError, match="DS block"):
+        bspline.eval_device(ds, np.array([1, 0] * 32, dtype=np.int32), u, gradient=False, param=True)
+    v = bspline.eval_device(ds, np.ones(64, dtype=np.int32), u, gradient=False, param=True)
+    np.testing.assert_allclose(v, bspline.eval_device(ds, 1, u, gradient=False, param=True), rtol=0, atol=0)

@@ -90,7 +90,7 @@ def replay():
     ds = DeviceStore(17, 9)
     cache = runtime.ModelCache(16, runtime.make_loader(None, man, ds, source=lambda a: blobs[a]))
     runtime.replay(povs, man, cache, render.TransferFunction.ml_preset(), params, prefetch="linear",
-                   keep_frames=False)
+                   keep_frames=False)  # render.render: two frames in flight, next caching overlapped
     torch.cuda.synchronize()
     print("replay ok")
 
