@@ -318,32 +318,39 @@ constexpr int kFxXRows = 72;     // X plane rows (the y windows over-read up to 
 constexpr int kFxPad = 16;       // zero floats after each ring slot (x windows over-read the last row)
 
 
-template <int P, int YPT>
+// SMW: the x / y weight windows live in shared memory instead of registers
+// and the plane ring has 3 slots, so two CTAs fit on an SM (<= 128 registers,
+// <= 113 KB of shared memory each): 16 warps instead of 8 to hide the
+// latency-bound plane loop.
+template <int P, int YPT, bool SMW>
 __device__ __forceinline__ void fx_decode_block(const BlockDesc &d, const int32_t *__restrict__ c0g,
                                                 const float *__restrict__ Bg, float *__restrict__ out,
                                                 unsigned char *smem) {
     constexpr int Q = P + 1;
+    constexpr int RING = SMW ? 3 : kFxRing;
     constexpr int M = 65;
     const int n = d.ncp, pitch = d.pitch;
     const int sstride = n * pitch + kFxPad;
     float *ring = reinterpret_cast<float *>(smem);
-    float *xb = ring + kFxRing * sstride;
+    float *xb = ring + RING * sstride;
     float *Bs = xb + 2 * kFxXRows * kFxXPitch;
     int *c0 = reinterpret_cast<int *>(Bs + M * 4);
     float *xcol = reinterpret_cast<float *>(c0 + 68);  // 2 x 72: X[.][64] = control column n-1, contiguous
-    uint64_t *bar = reinterpret_cast<uint64_t *>(xcol + 2 * 72);
+    float4 *wxs = reinterpret_cast<float4 *>(xcol + 2 * 72);  // SMW: [10][16] x weights, (w0..w3)[e] per quad
+    float4 *wys = wxs + (SMW ? 10 * 16 : 0);                  // SMW: [YW][NG] y weights, (wy[0..3])[e] per group
+    uint64_t *bar = reinterpret_cast<uint64_t *>(wys + (SMW ? (YPT + 3) * (16 * 64 / YPT / 16) : 0));
     const int tid = threadIdx.x;
 
     for (int i = tid; i < M * 4; i += blockDim.x) Bs[i] = Bg[i];
     for (int i = tid; i < M; i += blockDim.x) c0[i] = c0g[i];
-    for (int i = tid; i < kFxRing * kFxPad; i += blockDim.x)
+    for (int i = tid; i < RING * kFxPad; i += blockDim.x)
         ring[(i / kFxPad) * sstride + n * pitch + (i % kFxPad)] = 0.f;
     for (int i = tid; i < 2 * (kFxXRows - n) * kFxXPitch; i += blockDim.x) {
         const int b = i / ((kFxXRows - n) * kFxXPitch), o = i % ((kFxXRows - n) * kFxXPitch);
         xb[b * kFxXRows * kFxXPitch + n * kFxXPitch + o] = 0.f;
     }
     if (tid == 0) {
-        for (int r = 0; r < kFxRing; r++) mbar_init(bar + r, 1);
+        for (int r = 0; r < RING; r++) mbar_init(bar + r, 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -351,7 +358,7 @@ __device__ __forceinline__ void fx_decode_block(const BlockDesc &d, const int32_
     const uint32_t plane_bytes = (uint32_t)((size_t)n * pitch * sizeof(float));
     if (tid == 0) {
         fence_proxy_async();
-        for (int z = 0; z < min(n, kFxRing); z++) {
+        for (int z = 0; z < min(n, RING); z++) {
             mbar_arrive_expect_tx(bar + z, plane_bytes);
             tma_load_1d(ring + (size_t)z * sstride, C + (size_t)z * n * pitch, plane_bytes, bar + z);
         }
@@ -363,27 +370,35 @@ __device__ __forceinline__ void fx_decode_block(const BlockDesc &d, const int32_
     constexpr int NT = 16 * 64 / YPT, NG = NT / 16, YW = YPT + 3;
     const int q = tid & 15, g = tid >> 4;
     const int cw = c0[4 * q] & ~3;
-    float wx[4][10];
-#pragma unroll
-    for (int xi = 0; xi < 4; xi++) {
-        const int x = 4 * q + xi, off = c0[x] - cw;
-#pragma unroll
-        for (int e = 0; e < 10; e++) {
-            const int a = e - off;
-            wx[xi][e] = (a >= 0 && a < Q) ? Bs[x * 4 + a] : 0.f;
-        }
-    }
+    auto wx_at = [&](int xi, int e) {
+        const int x = 4 * q + xi, a = e - (c0[x] - cw);
+        return (a >= 0 && a < Q) ? Bs[x * 4 + a] : 0.f;
+    };
     // y stage weights: rows 4g..4g+3 over the 7-row window starting at r0
     const int r0 = c0[YPT * g];
-    float wy[YPT][YW];
+    auto wy_at = [&](int yi, int e) {
+        const int y = YPT * g + yi, b = e - (c0[y] - r0);
+        return (b >= 0 && b < Q) ? Bs[y * 4 + b] : 0.f;
+    };
+    float wx[SMW ? 1 : 4][SMW ? 1 : 10];
+    float wy[SMW ? 1 : YPT][SMW ? 1 : YW];
+    if constexpr (SMW) {
+        if (g == 0)
+            for (int e = 0; e < 10; e++) wxs[e * 16 + q] = make_float4(wx_at(0, e), wx_at(1, e), wx_at(2, e), wx_at(3, e));
+        if (q == 0)
+            for (int e = 0; e < YW; e++)
+                wys[e * NG + g] = make_float4(wy_at(0, e), YPT > 1 ? wy_at(1, e) : 0.f, YPT > 2 ? wy_at(2, e) : 0.f,
+                                              YPT > 3 ? wy_at(3, e) : 0.f);
+        __syncthreads();  // the weight windows before plane 0's x stage reads them
+    } else {
 #pragma unroll
-    for (int yi = 0; yi < YPT; yi++) {
-        const int y = YPT * g + yi, off = c0[y] - r0;
+        for (int xi = 0; xi < 4; xi++)
 #pragma unroll
-        for (int e = 0; e < YW; e++) {
-            const int b = e - off;
-            wy[yi][e] = (b >= 0 && b < Q) ? Bs[y * 4 + b] : 0.f;
-        }
+            for (int e = 0; e < 10; e++) wx[xi][e] = wx_at(xi, e);
+#pragma unroll
+        for (int yi = 0; yi < YPT; yi++)
+#pragma unroll
+            for (int e = 0; e < YW; e++) wy[yi][e] = wy_at(yi, e);
     }
     float yr[4][YPT][4];  // [plane slot][yi][s]: Y of the last 4 planes, columns q + 16 s
     float er[4];        // threads 0..128: the lattice column x = 64 / row y = 64 value of the last 4 planes
@@ -391,8 +406,8 @@ __device__ __forceinline__ void fx_decode_block(const BlockDesc &d, const int32_
 
     // x stage of plane z into X plane z & 1 (ring slot z & 3)
     auto xstage = [&](int z) {
-        mbar_wait(bar + (z & 3), (uint32_t)((z >> 2) & 1));
-        const float *Cp = ring + (z & 3) * sstride;
+        mbar_wait(bar + (z % RING), (uint32_t)((z / RING) & 1));
+        const float *Cp = ring + (z % RING) * sstride;
         float *X = xb + (z & 1) * kFxXRows * kFxXPitch;
                 // ---- x stage: rows g + 16 i two at a time (four independent FFMA2
                 // chains), threads 0..15 also take control row 64; window
@@ -410,14 +425,22 @@ __device__ __forceinline__ void fx_decode_block(const BlockDesc &d, const int32_
                     float2 qa01 = pa01, qa23 = pa01, qb01 = pa01, qb23 = pa01;
 #pragma unroll
                     for (int e = 0; e < 10; e += 2) {
-                        pa01 = __ffma2_rn(make_float2(wx[0][e], wx[1][e]), make_float2(va[e], va[e]), pa01);
-                        pa23 = __ffma2_rn(make_float2(wx[2][e], wx[3][e]), make_float2(va[e], va[e]), pa23);
-                        pb01 = __ffma2_rn(make_float2(wx[0][e], wx[1][e]), make_float2(vb[e], vb[e]), pb01);
-                        pb23 = __ffma2_rn(make_float2(wx[2][e], wx[3][e]), make_float2(vb[e], vb[e]), pb23);
-                        qa01 = __ffma2_rn(make_float2(wx[0][e + 1], wx[1][e + 1]), make_float2(va[e + 1], va[e + 1]), qa01);
-                        qa23 = __ffma2_rn(make_float2(wx[2][e + 1], wx[3][e + 1]), make_float2(va[e + 1], va[e + 1]), qa23);
-                        qb01 = __ffma2_rn(make_float2(wx[0][e + 1], wx[1][e + 1]), make_float2(vb[e + 1], vb[e + 1]), qb01);
-                        qb23 = __ffma2_rn(make_float2(wx[2][e + 1], wx[3][e + 1]), make_float2(vb[e + 1], vb[e + 1]), qb23);
+                        float4 w0, w1;  // (wx[0..3][e]), (wx[0..3][e + 1])
+                        if constexpr (SMW) {
+                            w0 = wxs[e * 16 + q];
+                            w1 = wxs[(e + 1) * 16 + q];
+                        } else {
+                            w0 = make_float4(wx[0][e], wx[1][e], wx[2][e], wx[3][e]);
+                            w1 = make_float4(wx[0][e + 1], wx[1][e + 1], wx[2][e + 1], wx[3][e + 1]);
+                        }
+                        pa01 = __ffma2_rn(make_float2(w0.x, w0.y), make_float2(va[e], va[e]), pa01);
+                        pa23 = __ffma2_rn(make_float2(w0.z, w0.w), make_float2(va[e], va[e]), pa23);
+                        pb01 = __ffma2_rn(make_float2(w0.x, w0.y), make_float2(vb[e], vb[e]), pb01);
+                        pb23 = __ffma2_rn(make_float2(w0.z, w0.w), make_float2(vb[e], vb[e]), pb23);
+                        qa01 = __ffma2_rn(make_float2(w1.x, w1.y), make_float2(va[e + 1], va[e + 1]), qa01);
+                        qa23 = __ffma2_rn(make_float2(w1.z, w1.w), make_float2(va[e + 1], va[e + 1]), qa23);
+                        qb01 = __ffma2_rn(make_float2(w1.x, w1.y), make_float2(vb[e + 1], vb[e + 1]), qb01);
+                        qb23 = __ffma2_rn(make_float2(w1.z, w1.w), make_float2(vb[e + 1], vb[e + 1]), qb23);
                     }
                     pa01 = __fadd2_rn(pa01, qa01);
                     pa23 = __fadd2_rn(pa23, qa23);
@@ -433,8 +456,9 @@ __device__ __forceinline__ void fx_decode_block(const BlockDesc &d, const int32_
                     float2 a01 = make_float2(0.f, 0.f), a23 = make_float2(0.f, 0.f);
 #pragma unroll
                     for (int e = 0; e < 10; e++) {
-                        a01 = __ffma2_rn(make_float2(wx[0][e], wx[1][e]), make_float2(w[e], w[e]), a01);
-                        a23 = __ffma2_rn(make_float2(wx[2][e], wx[3][e]), make_float2(w[e], w[e]), a23);
+                        const float4 we = SMW ? wxs[e * 16 + q] : make_float4(wx[0][e], wx[1][e], wx[2][e], wx[3][e]);
+                        a01 = __ffma2_rn(make_float2(we.x, we.y), make_float2(w[e], w[e]), a01);
+                        a23 = __ffma2_rn(make_float2(we.z, we.w), make_float2(w[e], w[e]), a23);
                     }
                     *reinterpret_cast<float4 *>(X + 64 * kFxXPitch + 4 * q) = make_float4(a01.x, a01.y, a23.x, a23.y);
                 }
@@ -445,10 +469,10 @@ __device__ __forceinline__ void fx_decode_block(const BlockDesc &d, const int32_
     // buffers), so each warp has two independent instruction streams
     xstage(0);
     __syncthreads();
-    if (tid == 0 && kFxRing < n) {  // slot 0 is free: plane 0's x stage is done
+    if (tid == 0 && RING < n) {  // slot 0 is free: plane 0's x stage is done
         fence_proxy_async();
         mbar_arrive_expect_tx(bar, plane_bytes);
-        tma_load_1d(ring, C + (size_t)kFxRing * n * pitch, plane_bytes, bar);
+        tma_load_1d(ring, C + (size_t)RING * n * pitch, plane_bytes, bar);
     }
     for (int z0 = 0; z0 < n; z0 += 4) {
 #pragma unroll
@@ -466,11 +490,21 @@ __device__ __forceinline__ void fx_decode_block(const BlockDesc &d, const int32_
             for (int e = 0; e < YW; e++) {
                 const float *xr = X + (r0 + e) * kFxXPitch + q;
                 const float v[4] = {xr[0], xr[16], xr[32], xr[48]};
+                float we[YPT];
+                if constexpr (SMW) {
+                    const float4 w4 = wys[e * NG + g];
+                    const float wa[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+                    for (int yi = 0; yi < YPT; yi++) we[yi] = wa[yi];
+                } else {
+#pragma unroll
+                    for (int yi = 0; yi < YPT; yi++) we[yi] = wy[yi][e];
+                }
 #pragma unroll
                 for (int yi = 0; yi < YPT; yi++) {
                     float2 lo = make_float2(yr[u][yi][0], yr[u][yi][1]), hi = make_float2(yr[u][yi][2], yr[u][yi][3]);
-                    lo = __ffma2_rn(make_float2(wy[yi][e], wy[yi][e]), make_float2(v[0], v[1]), lo);
-                    hi = __ffma2_rn(make_float2(wy[yi][e], wy[yi][e]), make_float2(v[2], v[3]), hi);
+                    lo = __ffma2_rn(make_float2(we[yi], we[yi]), make_float2(v[0], v[1]), lo);
+                    hi = __ffma2_rn(make_float2(we[yi], we[yi]), make_float2(v[2], v[3]), hi);
                     yr[u][yi][0] = lo.x; yr[u][yi][1] = lo.y; yr[u][yi][2] = hi.x; yr[u][yi][3] = hi.y;
                 }
             }
@@ -518,21 +552,21 @@ __device__ __forceinline__ void fx_decode_block(const BlockDesc &d, const int32_
             }
             __syncthreads();
             // plane zc + 1's slot is free (its x stage is done): fetch plane zc + 1 + kFxRing
-            if (tid == 0 && zc + 1 + kFxRing < n) {
-                const int sl = (zc + 1) & 3;
+            if (tid == 0 && zc + 1 + RING < n) {
+                const int sl = (zc + 1) % RING;
                 fence_proxy_async();
                 mbar_arrive_expect_tx(bar + sl, plane_bytes);
-                tma_load_1d(ring + (size_t)sl * sstride, C + (size_t)(zc + 1 + kFxRing) * n * pitch, plane_bytes,
+                tma_load_1d(ring + (size_t)sl * sstride, C + (size_t)(zc + 1 + RING) * n * pitch, plane_bytes,
                             bar + sl);
             }
         }
     }
 }
 
-template <int YPT>
-__global__ void __launch_bounds__(16 * 64 / YPT, 1) decode_fx_kernel(const BlockDesc *__restrict__ descs,
-                                                                      const DecodeJob *__restrict__ jobs,
-                                                                      float *__restrict__ out) {
+template <int YPT, bool SMW>
+__global__ void __launch_bounds__(16 * 64 / YPT, SMW ? 2 : 1) decode_fx_kernel(const BlockDesc *__restrict__ descs,
+                                                                                const DecodeJob *__restrict__ jobs,
+                                                                                float *__restrict__ out) {
     extern __shared__ __align__(16) unsigned char smem[];
     const DecodeJob jb = jobs[blockIdx.x];
     if (!jb.fx) return;
@@ -540,9 +574,9 @@ __global__ void __launch_bounds__(16 * 64 / YPT, 1) decode_fx_kernel(const Block
     if (d.flags & AFAM_SLOT_FP64) return;  // float64 slots: decode_grid_kernel<double>
     float *o = out + (size_t)blockIdx.x * 65 * 65 * 65;
     switch (d.deg) {
-        case 1: fx_decode_block<1, YPT>(d, jb.col0, jb.b32, o, smem); break;
-        case 2: fx_decode_block<2, YPT>(d, jb.col0, jb.b32, o, smem); break;
-        default: fx_decode_block<3, YPT>(d, jb.col0, jb.b32, o, smem); break;
+        case 1: fx_decode_block<1, YPT, SMW>(d, jb.col0, jb.b32, o, smem); break;
+        case 2: fx_decode_block<2, YPT, SMW>(d, jb.col0, jb.b32, o, smem); break;
+        default: fx_decode_block<3, YPT, SMW>(d, jb.col0, jb.b32, o, smem); break;
     }
 }
 
@@ -913,6 +947,18 @@ static int fx_ypt() {
     return v;
 }
 
+// AFAM_DECODE_FX_SMW=1: the two-CTAs-per-SM variant (measured slower: 2.42 vs
+// 2.13 ms on config 5 -- 16 warps raise issue only from 31% to 34%, the
+// plane loop is bound by the L1/shared-memory pipe, which the weight loads
+// load further)
+static bool fx_smw() {
+    static const bool v = [] {
+        const char *e = getenv("AFAM_DECODE_FX_SMW");
+        return e && atoi(e) != 0;
+    }();
+    return v;
+}
+
 static int get_op(afam_store *s, int ncp, int deg, int m, DecodeOp **op) {
     auto key = std::make_tuple(ncp, deg, m);
     auto it = s->ops.find(key);
@@ -1044,16 +1090,27 @@ extern "C" int afam_decode_grid_ex(afam_store *s, const int32_t *slots, int32_t 
         decode_tc_kernel<<<nblk, kTcThreads, smem, st>>>(s->d_desc, d_jobs, m, out);
     }
     if (nfx > 0) {
+        // the SMW variant (weights in shared memory, 3-slot ring: 2 CTAs per SM) with AFAM_DECODE_FX_SMW=1
+        const bool smw = fx_ypt() == 4 && fx_smw();
+        const int ring = smw ? 3 : kFxRing;
         const size_t smem =
-            ((size_t)kFxRing * (maxfx + kFxPad) + 2 * (size_t)kFxXRows * kFxXPitch + 65 * 4 + 68 + 2 * 72) * 4 +
-            kFxRing * 8;
+            ((size_t)ring * (maxfx + kFxPad) + 2 * (size_t)kFxXRows * kFxXPitch + 65 * 4 + 68 + 2 * 72) * 4 +
+            (smw ? (10 * 16 + 7 * 16) * 16 : 0) + ring * 8;
         AFAM_CHECK(smem <= 227 * 1024, AFAM_E_VALUE, "register-tiled decode needs %zu B of shared memory", smem);
-        if (fx_ypt() == 4) {
-            AFAM_CUDA(cudaFuncSetAttribute(decode_fx_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            decode_fx_kernel<4><<<nblk, 256, smem, st>>>(s->d_desc, d_jobs, out);
+        if (smw) {
+            AFAM_CUDA(cudaFuncSetAttribute(decode_fx_kernel<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem));
+            AFAM_CUDA(cudaFuncSetAttribute(decode_fx_kernel<4, true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                           cudaSharedmemCarveoutMaxShared));  // room for two CTAs per SM
+            decode_fx_kernel<4, true><<<nblk, 256, smem, st>>>(s->d_desc, d_jobs, out);
+        } else if (fx_ypt() == 4) {
+            AFAM_CUDA(cudaFuncSetAttribute(decode_fx_kernel<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem));
+            decode_fx_kernel<4, false><<<nblk, 256, smem, st>>>(s->d_desc, d_jobs, out);
         } else {
-            AFAM_CUDA(cudaFuncSetAttribute(decode_fx_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            decode_fx_kernel<2><<<nblk, 512, smem, st>>>(s->d_desc, d_jobs, out);
+            AFAM_CUDA(cudaFuncSetAttribute(decode_fx_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem));
+            decode_fx_kernel<2, false><<<nblk, 512, smem, st>>>(s->d_desc, d_jobs, out);
         }
     }
     if (nany > 0) decode_any_kernel<<<dim3(64, nblk), 256, 0, st>>>(s->d_desc, d_jobs, m, out);
