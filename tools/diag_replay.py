@@ -46,7 +46,7 @@ draw.submit = lambda pov, resident, tf_, params_: Timed(tiles.submit_tiles(pov, 
                                                                           band_rows=8))
 draw.frames_in_flight = 2
 for r in range(rounds):
-    for mode in ("2", "1", "0"):  # depth 2, depth 1 (overlapped caching), the reference's strict order
+    for mode in os.environ.get("MODES", "2,1,0").split(","):  # depth 2, depth 1 (overlapped caching), strict order
         os.environ["AFAM_REPLAY_OVERLAP"] = "0" if mode == "0" else "1"
         os.environ["AFAM_REPLAY_DEPTH"] = "2" if mode == "2" else "1"
         ds = DeviceStore(201, 65)
