@@ -77,7 +77,10 @@ def test_eval_points_vs_reference_golden(cuda):
         rng_ = max(1.0, float(np.abs(c).max()))
         v, g = bspline.evaluate_points_with_gradient(c, int(degree), u, knots=tuple(z[f"c{ci}_knots32"]))
         assert np.abs(v - z[f"c{ci}_v32"]).max() <= VALUE_TOL * rng_
-        np.testing.assert_allclose(g, z[f"c{ci}_g32"], rtol=0, atol=2e-4 * rng_ * int(ncp))
+        # gradients to the value gate relative to the gradient range (measured worst 9e-7,
+        # tools/diag_gradtol.py)
+        gr = z[f"c{ci}_g32"]
+        np.testing.assert_allclose(g, gr, rtol=0, atol=VALUE_TOL * max(1.0, float(np.abs(gr).max())))
         v0 = bspline.evaluate_points(c, int(degree), u)
         assert np.abs(v0 - z[f"c{ci}_v_default"]).max() <= VALUE_TOL * rng_
     v, g = bspline.evaluate_points_with_gradient(z["nu_coeff"], int(z["nu_degree"]), z["nu_u"],
@@ -97,7 +100,7 @@ def test_world_space_hooks_vs_reference_golden(cuda):
         assert np.abs(mw.values_at(z[f"d{j}_pts"]) - z[f"d{j}_values_at"]).max() <= tol
         g = mw.gradients_at(z[f"d{j}_pts"])
         gr = z[f"d{j}_gradients_at"]
-        assert np.abs(g - gr).max() <= 1e-4 * max(1.0, np.abs(gr).max())
+        assert np.abs(g - gr).max() <= VALUE_TOL * max(1.0, np.abs(gr).max())  # measured worst 1e-6
 
 
 def test_eval_points_ill_conditioned_fp64_path(cuda, oracle):
