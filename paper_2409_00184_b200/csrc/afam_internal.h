@@ -58,6 +58,7 @@ struct SlotHost {
     int32_t ncp = 0, deg = 0;
     bool ds = false;       // down-sampled raw block (AFAM_SLOT_DS)
     bool maxabs_known = false;  // afam_store::h_maxabs[slot] set on the host at put time (else after `ready`)
+    bool uniform = false;       // host-checked: the knots are the clamped uniform ones (kFlagUniform)
     double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     cudaEvent_t ready = nullptr;  // recorded after the upload kernels
     cudaEvent_t reader = nullptr; // the last kernel reading the slot (a ThreadCtx event): uploads wait on it

@@ -1537,7 +1537,11 @@ __device__ __forceinline__ bool sample_fast64(const RenderArgs &A, const TfTable
     return true;
 }
 
-template <bool DEBUG, bool SMEM_GRID, int P, int MINB, int SR, bool HI, bool F64>
+// AF ("all fast"): the host checked that every resident block takes the
+// fast path (degree P, clamped-uniform knots, float32 slot, rays shorter
+// than 2^24 samples, no forced exact path), so the per-sample fast / exact
+// dispatch is compiled out.
+template <bool DEBUG, bool SMEM_GRID, int P, int MINB, int SR, bool HI, bool F64, bool AF>
 __global__ void __launch_bounds__(128, MINB) render2_kernel(const BlockDesc *__restrict__ descs,
                                                          const int16_t *__restrict__ grid,
                                                          const int32_t *__restrict__ idx2slot, const RenderArgs A,
@@ -1686,7 +1690,7 @@ __global__ void __launch_bounds__(128, MINB) render2_kernel(const BlockDesc *__r
             }
             if (DEBUG) M.h = (M.h ^ (uint64_t)(uint32_t)vld(F.cur_own)) * 1099511628211ULL;
             bool ok = false;
-            if (fast) {
+            if (AF || fast) {
                 if (F64 && is64) {
                     ok = sample_fast64<P, SR>(A, tf, b, s_pred64[threadIdx.x], dk, C, G, M);
                 } else {
@@ -1976,15 +1980,15 @@ static void launch_render_v(const LaunchArgs &L, const RenderArgs &A) {
                                                                         L.rgba, L.stats, L.nsamp, L.ohash);
 }
 
-template <bool DEBUG, bool SMEM, int P, int MINB, int SR = 0, bool HI = false, bool F64 = false>
+template <bool DEBUG, bool SMEM, int P, int MINB, int SR = 0, bool HI = false, bool F64 = false, bool AF = false>
 static void launch_render2_v(const LaunchArgs &L, const RenderArgs &A) {
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(render2_kernel<DEBUG, SMEM, P, MINB, SR, HI, F64>,
+        cudaFuncSetAttribute(render2_kernel<DEBUG, SMEM, P, MINB, SR, HI, F64, AF>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
         configured = true;
     }
-    render2_kernel<DEBUG, SMEM, P, MINB, SR, HI, F64><<<L.grid, 128, L.smem, L.st>>>(L.descs, L.owner, L.idx, A, L.gargs,
+    render2_kernel<DEBUG, SMEM, P, MINB, SR, HI, F64, AF><<<L.grid, 128, L.smem, L.st>>>(L.descs, L.owner, L.idx, A, L.gargs,
                                                                              L.gtf, L.rgba, L.stats, L.nsamp,
                                                                              L.ohash);
 }
@@ -2021,8 +2025,12 @@ static bool render_no_f64() {
 // fd: the degree the fast path is compiled for (blocks of other degrees take
 // the exact path); debug and non-shared-grid launches use the default bounds.
 template <bool DEBUG, bool SMEM>
-static void launch_render(const LaunchArgs &L, const RenderArgs &A, int fd, bool hi, bool f64) {
+static void launch_render(const LaunchArgs &L, const RenderArgs &A, int fd, bool hi, bool f64, bool allfast) {
     if (fd == 0) return launch_render_v<DEBUG, SMEM, 0, 4>(L, A);  // DS blocks
+    if (allfast && SMEM && !render_v1() && render2_minb() == 3) {
+        if (fd == 3) return launch_render2_v<DEBUG, SMEM, 3, 3, 0, false, false, true>(L, A);
+        if (fd == 2) return launch_render2_v<DEBUG, SMEM, 2, 4, 0, false, false, true>(L, A);
+    }
     if (hi) {  // blocks of degrees above AFAM_FAST_DEGREE present
         if (fd == 1) return launch_render2_v<DEBUG, SMEM, 1, 4, 0, true>(L, A);
         if (fd == 2) return launch_render2_v<DEBUG, SMEM, 2, 4, 0, true>(L, A);
@@ -2191,7 +2199,7 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
     std::vector<int16_t> grid;
     int32_t cells = 1;
     int fd = 3;  // fast-path degree: the most common degree among the blocks
-    bool hi = false, any64 = false;
+    bool hi = false, any64 = false, allfast = true;
     {
         std::lock_guard<std::mutex> lk(s->mu);
         int rc = build_owner_grid(s, slots, nblocks, cells, grid);
@@ -2201,8 +2209,9 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
             // float64 slot (max|c| over the limit, afam_store.cu build_tables_kernel)? unknown
             // while its upload is in flight: then the float64-capable kernel
             const SlotHost &h = s->host[slots[b]];
-            if (!h.ds && ((h.pending && !h.maxabs_known) || s->h_maxabs[slots[b]] > (float)s->fp64_limit))
-                any64 = true;
+            const bool f64slot = (h.pending && !h.maxabs_known) || s->h_maxabs[slots[b]] > (float)s->fp64_limit;
+            if (!h.ds && f64slot) any64 = true;
+            allfast = allfast && !h.ds && !f64slot && h.uniform;
         }
         int cnt[4] = {0, 0, 0, 0}, nds = 0;
         hi = false;
@@ -2218,6 +2227,11 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
         AFAM_CHECK(nds == 0 || nds == nblocks, AFAM_E_VALUE,
                    "resident blocks mix spline models and DS blocks (%d of %d DS)", nds, nblocks);
         fd = nds ? 0 : (cnt[3] >= cnt[2] && cnt[3] >= cnt[1] ? 3 : (cnt[2] >= cnt[1] ? 2 : 1));
+        // every block on the fast path of degree fd (render2_kernel<..., AF>)?
+        for (int b = 0; b < nblocks && allfast; b++) allfast = s->host[slots[b]].deg == fd;
+        // the float32 sample offset needs rays shorter than 2^24 samples: the
+        // cube's diagonal (2 sqrt 3) over the sample distance
+        allfast = allfast && !hi && fd >= 2 && F->sample_distance > 3.5 / 16777216.0 && !(A.flags & kRenderForceExact);
     }
     ht.mark();
     A.cells = cells;
@@ -2287,11 +2301,11 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
         L.nsamp = nsamp;
         L.ohash = ohash;
         if (debug) {
-            if (sg) launch_render<true, true>(L, A, fd, hi, any64);
-            else launch_render<true, false>(L, A, fd, hi, any64);
+            if (sg) launch_render<true, true>(L, A, fd, hi, any64, allfast);
+            else launch_render<true, false>(L, A, fd, hi, any64, allfast);
         } else {
-            if (sg) launch_render<false, true>(L, A, fd, hi, any64);
-            else launch_render<false, false>(L, A, fd, hi, any64);
+            if (sg) launch_render<false, true>(L, A, fd, hi, any64, allfast);
+            else launch_render<false, false>(L, A, fd, hi, any64, allfast);
         }
     }
     finish_stats_kernel<<<1, 1, 0, st>>>(stats);

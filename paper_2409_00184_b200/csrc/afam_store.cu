@@ -263,9 +263,42 @@ int afam_store_slots(const afam_store *s, int32_t *slots, int32_t *max_ncp) {
 }
 
 // Shared tail of both put paths: raw region already holds the bytes (queued on stream).
+// The device's kFlagUniform test (build_tables_kernel) on the host: every
+// stored knot equals float32((k - deg) / nspan) clamped to [0, 1], bitwise.
+static bool uniform_knot(float t, int k, int ncp, int deg) {
+    const float want = k <= deg ? 0.f : (k >= ncp ? 1.f : (float)((double)(k - deg) / (double)(ncp - deg)));
+    uint32_t x, y;
+    memcpy(&x, &t, 4);
+    memcpy(&y, &want, 4);
+    return x == y;
+}
+
+// .mfa image: knots t1.. per axis after the degree byte (t0 = 0 implicit, FORMAT.md:44-55)
+static bool mfa_uniform(const uint8_t *bytes, int ncp, int deg) {
+    const int stored = ncp + deg;
+    for (int a = 0; a < 3; a++)
+        for (int k = 1; k <= stored; k++) {
+            float t;
+            memcpy(&t, bytes + 1 + 4 * ((size_t)a * stored + (k - 1)), 4);
+            if (!uniform_knot(t, k, ncp, deg)) return false;
+        }
+    return true;
+}
+
+// full knot vectors [3][ncp + deg + 1]
+static bool knots_uniform(const float *knots, int ncp, int deg) {
+    const int nk = ncp + deg + 1;
+    for (int a = 0; a < 3; a++)
+        for (int k = 0; k < nk; k++)
+            if (!uniform_knot(knots[(size_t)a * nk + k], k, ncp, deg)) return false;
+    return true;
+}
+
 // host_maxabs: max |c| when the caller scanned the control points on the host, else < 0
+// host_uniform: the knots are known (on the host) to be the clamped uniform ones
 static int launch_unpack(afam_store *s, int32_t slot, int deg, int ncp, uint64_t knot_off, int has_t0,
-                         uint64_t ctrl_off, const double extent[6], cudaStream_t st, float host_maxabs) {
+                         uint64_t ctrl_off, const double extent[6], cudaStream_t st, float host_maxabs,
+                         bool host_uniform = false) {
     BlockDesc proto{};
     proto.ctrl = s->ctrl_ptr(slot);
     proto.ctrl4 = s->ctrl4_ptr(slot);
@@ -303,6 +336,7 @@ static int launch_unpack(afam_store *s, int32_t slot, int deg, int ncp, uint64_t
     AFAM_CUDA(cudaMemcpyAsync(s->h_maxabs + slot, s->d_maxabs + slot, sizeof(float), cudaMemcpyDeviceToHost, st));
     h.maxabs_known = host_maxabs >= 0.f;
     if (h.maxabs_known) s->h_maxabs[slot] = host_maxabs;
+    h.uniform = host_uniform;
     h.valid = true;
     h.pending = true;
     h.ncp = ncp;
@@ -382,7 +416,8 @@ int afam_store_put_mfa(afam_store *s, int32_t slot, const uint8_t *bytes, uint64
     AFAM_CUDA(cudaStreamWaitEvent(st, s->host[slot].ready, 0));
     AFAM_CUDA(wait_readers(s, slot, st));
     AFAM_CUDA(cudaMemcpyAsync(s->raw_ptr(slot), bytes, nbytes, cudaMemcpyHostToDevice, st));
-    return launch_unpack(s, slot, deg, ncp, 1, 0, 1 + 12ull * (ncp + deg), extent, st, mx);
+    return launch_unpack(s, slot, deg, ncp, 1, 0, 1 + 12ull * (ncp + deg), extent, st, mx,
+                         mfa_uniform(bytes, ncp, deg));
 }
 
 
@@ -479,7 +514,7 @@ int afam_store_put_file(afam_store *s, int32_t slot, const char *path, int32_t n
     AFAM_CUDA(wait_readers(s, slot, st));
     AFAM_CUDA(cudaMemcpyAsync(s->raw_ptr(slot), bytes, nbytes, cudaMemcpyHostToDevice, st));
     AFAM_CUDA(cudaEventRecord(s->ev_file[b], st));
-    return launch_unpack(s, slot, deg, ncp, 1, 0, coff, extent, st, mx);
+    return launch_unpack(s, slot, deg, ncp, 1, 0, coff, extent, st, mx, mfa_uniform(bytes, ncp, deg));
 }
 
 int afam_store_put_ds(afam_store *s, int32_t slot, const uint8_t *bytes, uint64_t nbytes, const double extent[6],
@@ -541,6 +576,7 @@ int afam_store_put_ds(afam_store *s, int32_t slot, const uint8_t *bytes, uint64_
     h.ncp = d.ncp;
     h.deg = g;
     h.ds = true;
+    h.uniform = false;
     for (int a = 0; a < 3; a++) { h.lo[a] = extent[2 * a]; h.hi[a] = extent[2 * a + 1]; }
     AFAM_CUDA(cudaEventRecord(h.ready, st));
     return AFAM_OK;
@@ -563,7 +599,7 @@ int afam_store_put(afam_store *s, int32_t slot, int32_t degree, int32_t ncp, con
     AFAM_CUDA(cudaMemcpyAsync(s->raw_ptr(slot) + coff, ctrl, cb, cudaMemcpyHostToDevice, st));
     float mx = -1.f;  // max |c| when finite (a non-finite value leaves it to the device)
     if (!all_finite_le_f32(reinterpret_cast<const uint8_t *>(ctrl), (size_t)ncp * ncp * ncp, &mx)) mx = -1.f;
-    return launch_unpack(s, slot, degree, ncp, koff, 1, coff, extent, st, mx);
+    return launch_unpack(s, slot, degree, ncp, koff, 1, coff, extent, st, mx, knots_uniform(knots, ncp, degree));
 }
 
 int afam_store_evict(afam_store *s, int32_t slot) {
