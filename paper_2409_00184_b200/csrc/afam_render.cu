@@ -2022,10 +2022,20 @@ static bool render_no_f64() {
     return v;
 }
 
+// CTAs per SM of the all-fast float64 instantiation (AFAM_RENDER_F64_MINB=2|3 A/B)
+static int render_f64_minb() {
+    static const int v = [] {
+        const char *e = getenv("AFAM_RENDER_F64_MINB");
+        return (e && atoi(e) == 2) ? 2 : 3;
+    }();
+    return v;
+}
+
 // fd: the degree the fast path is compiled for (blocks of other degrees take
 // the exact path); debug and non-shared-grid launches use the default bounds.
 template <bool DEBUG, bool SMEM>
-static void launch_render(const LaunchArgs &L, const RenderArgs &A, int fd, bool hi, bool f64, bool allfast) {
+static void launch_render(const LaunchArgs &L, const RenderArgs &A, int fd, bool hi, bool f64, bool allfast,
+                          bool allfast64) {
     if (fd == 0) return launch_render_v<DEBUG, SMEM, 0, 4>(L, A);  // DS blocks
     if (allfast && SMEM && !render_v1() && render2_minb() == 3) {
         if (fd == 3) return launch_render2_v<DEBUG, SMEM, 3, 3, 0, false, false, true>(L, A);
@@ -2035,6 +2045,12 @@ static void launch_render(const LaunchArgs &L, const RenderArgs &A, int fd, bool
         if (fd == 1) return launch_render2_v<DEBUG, SMEM, 1, 4, 0, true>(L, A);
         if (fd == 2) return launch_render2_v<DEBUG, SMEM, 2, 4, 0, true>(L, A);
         return launch_render2_v<DEBUG, SMEM, 3, 3, 0, true>(L, A);
+    }
+    if (f64 && allfast64 && !render_no_f64() && SMEM) {  // ... every block on a fast path (float32 or float64)
+        if (fd == 3) {
+            if (render_f64_minb() == 2) return launch_render2_v<DEBUG, SMEM, 3, 2, 0, false, true, true>(L, A);
+            return launch_render2_v<DEBUG, SMEM, 3, 3, 0, false, true, true>(L, A);
+        }
     }
     if (f64 && !render_no_f64()) {  // ill-conditioned (float64) slots present: the float64 fast path
         if (fd == 2) return launch_render2_v<DEBUG, SMEM, 2, 3, 0, false, true>(L, A);
@@ -2199,7 +2215,7 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
     std::vector<int16_t> grid;
     int32_t cells = 1;
     int fd = 3;  // fast-path degree: the most common degree among the blocks
-    bool hi = false, any64 = false, allfast = true;
+    bool hi = false, any64 = false, allfast = true, allfast64 = true;
     {
         std::lock_guard<std::mutex> lk(s->mu);
         int rc = build_owner_grid(s, slots, nblocks, cells, grid);
@@ -2212,6 +2228,7 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
             const bool f64slot = (h.pending && !h.maxabs_known) || s->h_maxabs[slots[b]] > (float)s->fp64_limit;
             if (!h.ds && f64slot) any64 = true;
             allfast = allfast && !h.ds && !f64slot && h.uniform;
+            allfast64 = allfast64 && !h.ds && h.uniform;
         }
         int cnt[4] = {0, 0, 0, 0}, nds = 0;
         hi = false;
@@ -2228,10 +2245,15 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
                    "resident blocks mix spline models and DS blocks (%d of %d DS)", nds, nblocks);
         fd = nds ? 0 : (cnt[3] >= cnt[2] && cnt[3] >= cnt[1] ? 3 : (cnt[2] >= cnt[1] ? 2 : 1));
         // every block on the fast path of degree fd (render2_kernel<..., AF>)?
-        for (int b = 0; b < nblocks && allfast; b++) allfast = s->host[slots[b]].deg == fd;
+        for (int b = 0; b < nblocks && (allfast || allfast64); b++) {
+            allfast = allfast && s->host[slots[b]].deg == fd;
+            allfast64 = allfast64 && s->host[slots[b]].deg == fd;
+        }
         // the float32 sample offset needs rays shorter than 2^24 samples: the
         // cube's diagonal (2 sqrt 3) over the sample distance
         allfast = allfast && !hi && fd >= 2 && F->sample_distance > 3.5 / 16777216.0 && !(A.flags & kRenderForceExact);
+        allfast64 = allfast64 && !hi && fd >= 2 && F->sample_distance > 3.5 / 16777216.0 &&
+                    !(A.flags & kRenderForceExact);
     }
     ht.mark();
     A.cells = cells;
@@ -2301,11 +2323,11 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
         L.nsamp = nsamp;
         L.ohash = ohash;
         if (debug) {
-            if (sg) launch_render<true, true>(L, A, fd, hi, any64, allfast);
-            else launch_render<true, false>(L, A, fd, hi, any64, allfast);
+            if (sg) launch_render<true, true>(L, A, fd, hi, any64, allfast, allfast64);
+            else launch_render<true, false>(L, A, fd, hi, any64, allfast, allfast64);
         } else {
-            if (sg) launch_render<false, true>(L, A, fd, hi, any64, allfast);
-            else launch_render<false, false>(L, A, fd, hi, any64, allfast);
+            if (sg) launch_render<false, true>(L, A, fd, hi, any64, allfast, allfast64);
+            else launch_render<false, false>(L, A, fd, hi, any64, allfast, allfast64);
         }
     }
     finish_stats_kernel<<<1, 1, 0, st>>>(stats);
