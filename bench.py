@@ -817,8 +817,10 @@ def run_config2(rank, world, dev, steps, warmup, fma_peak, e2e=False):
     # samples at the FP64 peak and the rest at the FP32 peak, over the
     # measured kernel time (shaded fraction applied uniformly to both kinds)
     f64frac = s64 / max(1, samples)
-    flop = samples * FLOP_VALUE_P3 + shaded * (FLOP_PER_SAMPLE_P3 - FLOP_VALUE_P3)
+    flop = samples * FLOP_PER_SAMPLE_P3  # value + gradient per decoded sample
+    flop_exec = samples * FLOP_VALUE_P3 + shaded * (FLOP_PER_SAMPLE_P3 - FLOP_VALUE_P3)
     t_ideal = flop * f64frac / (dfma * 1e12) + flop * (1 - f64frac) / (fma_peak * 1e12)
+    t_ideal_exec = flop_exec * f64frac / (dfma * 1e12) + flop_exec * (1 - f64frac) / (fma_peak * 1e12)
     t_meas = sum(kms) / 1e3
     res = {"metric": C2_METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
            "ms_per_step": float(tot[2]) / steps, "higher_is_better": True, "scaling": "strong",
@@ -834,7 +836,9 @@ def run_config2(rank, world, dev, steps, warmup, fma_peak, e2e=False):
                         "frac": t_ideal / t_meas, "traffic": None, "kernel": "render kernels (K2, float64 path)",
                         "note": f"frac = (float64 samples' algorithmic FLOP at the measured FP64 FMA peak {dfma:.1f} "
                                 f"TFLOP/s + float32 samples' at the FP32 peak {fma_peak:.1f}) / kernel time; "
-                                "FLOP per sample as config 3 (168 value + 216 gradient when shaded)"}}
+                                "384 FLOP per decoded sample (SURVEY.md 8(d), as config 3); frac_executed: the "
+                                "kernel's own count (168 value + 216 gradient when shaded)",
+                        "frac_executed": t_ideal_exec / t_meas}}
     if e2e:
         res["e2e"] = config2_e2e(man, models, povs, tf, params, rank, world, dev, steps)
     return res
