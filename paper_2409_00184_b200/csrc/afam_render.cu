@@ -1441,6 +1441,14 @@ __device__ __forceinline__ bool sample_fast2(const RenderArgs &A, const TfTable 
 // spans (the float64 Cox-de Boor table on the boundary spans), contraction
 // and gradient in float64 -- instead of the exact path's per-sample float64
 // position, division, span search, table loads and uncached gather.
+// -DAFAM_F64_VALUE_FIRST=1: value-first float64 samples in the all-fast kernel
+// (measured: 3.15 vs 3.11 ms on config 2 -- the saved DFMAs of transparent
+// samples are eaten by 228 bytes of spills)
+#ifndef AFAM_F64_VALUE_FIRST
+#define AFAM_F64_VALUE_FIRST 0
+#endif
+constexpr bool F64_VF = AFAM_F64_VALUE_FIRST != 0;
+
 struct Pred64 {  // per thread, shared memory: the float64 span prediction of the current owner
     double tq0[3], dtq[3];
     const double *tab64;
@@ -1475,7 +1483,9 @@ __device__ __forceinline__ void uniform_NE_f64(double x, double ns, double (&N)[
     }
 }
 
-template <int P, int SR>
+// VF: value first, the derivative weights and the gradient contraction only
+// for samples the TF makes visible
+template <int P, int SR, bool VF>
 __device__ __forceinline__ bool sample_fast64(const RenderArgs &A, const TfTable &tf, const BlockFast &sb,
                                               const Pred64 &PD, float dk, ThreadCold &C, FastCell<P, SR> &G,
                                               March &M) {
@@ -1516,13 +1526,36 @@ __device__ __forceinline__ bool sample_fast64(const RenderArgs &A, const TfTable
     };
     double N[3][Q];
     double E[3][P];
-#pragma unroll
-    for (int a = 0; a < 3; a++) basis(a, N[a], E[a]);
-    float4 c4[16];
-#pragma unroll
-    for (int i = 0; i < Q * Q; i++) c4[i] = G.get(i);
     double v, g[3];
-    contract_quad<P, double>(c4, N[0], E[0], N[1], E[1], N[2], E[2], v, g);
+    if constexpr (VF) {
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+            double Ed[P];
+            basis(a, N[a], Ed);
+        }
+        v = 0.0;
+#pragma unroll
+        for (int cz = 0; cz < Q; cz++) {
+            double ay = 0.0;
+#pragma unroll
+            for (int by = 0; by < Q; by++) {
+                const float4 r = G.get(cz * Q + by);
+                double acc = N[0][0] * (double)r.x;
+                acc = fma(N[0][1], (double)r.y, acc);
+                if constexpr (P >= 2) acc = fma(N[0][2], (double)r.z, acc);
+                if constexpr (P >= 3) acc = fma(N[0][3], (double)r.w, acc);
+                ay = fma(N[1][by], acc, ay);
+            }
+            v = fma(N[2][cz], ay, v);
+        }
+    } else {
+#pragma unroll
+        for (int a = 0; a < 3; a++) basis(a, N[a], E[a]);
+        float4 c4[16];
+#pragma unroll
+        for (int i = 0; i < Q * Q; i++) c4[i] = G.get(i);
+        contract_quad<P, double>(c4, N[0], E[0], N[1], E[1], N[2], E[2], v, g);
+    }
     ++C.ns64;
     const float vc = fminf(fmaxf((float)v, A.dom_lo), A.dom_hi);
     if (!(vc > A.op_lo) || !(vc < A.op_hi)) return true;
@@ -1531,6 +1564,15 @@ __device__ __forceinline__ bool sample_fast64(const RenderArgs &A, const TfTable
     const float atf = tf_alpha(A, tf, vc, bi, bf);
     if (!(atf > 0.f)) return true;
     ++M.nshade;
+    if constexpr (VF) {
+#pragma unroll
+        for (int a = 0; a < 3; a++) basis(a, N[a], E[a]);
+        float4 c4[16];
+#pragma unroll
+        for (int i = 0; i < Q * Q; i++) c4[i] = G.get(i);
+        double vv;
+        contract_quad<P, double>(c4, N[0], E[0], N[1], E[1], N[2], E[2], vv, g);
+    }
     const float4 gi = C.ginv;
     const float gs[3] = {(float)g[0] * gi.x, (float)g[1] * gi.y, (float)g[2] * gi.z};  // model.py:79
     composite(A, C.vdir, tf_color(tf, vc, bi, bf, atf), gs, M);
@@ -1692,7 +1734,7 @@ __global__ void __launch_bounds__(128, MINB) render2_kernel(const BlockDesc *__r
             bool ok = false;
             if (AF || fast) {
                 if (F64 && is64) {
-                    ok = sample_fast64<P, SR>(A, tf, b, s_pred64[threadIdx.x], dk, C, G, M);
+                    ok = sample_fast64<P, SR, AF && F64_VF>(A, tf, b, s_pred64[threadIdx.x], dk, C, G, M);
                 } else {
                     const float tqx = fmaf(dk, M.dtq[0], M.tq0[0]);
                     const float tqy = fmaf(dk, M.dtq[1], M.tq0[1]);
