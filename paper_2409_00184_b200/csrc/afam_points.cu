@@ -14,18 +14,25 @@
 
 namespace afam {
 
-template <typename T, bool GRAD>
+// HD: the store holds blocks of degrees above AFAM_FAST_DEGREE (float64 from
+// the knots, eval_any).  A separate instantiation: its call frame alone made
+// the common kernel spill (0 -> 128 bytes, -28% on the 2^24-point batches).
+template <typename T, bool GRAD, bool HD>
 __device__ __forceinline__ T eval_dispatch(const BlockDesc &d, const double (&u)[3], T g[3]) {
     switch (d.deg) {
         case 1: return eval_uncached<1, T, GRAD>(d, u, g);
         case 2: return eval_uncached<2, T, GRAD>(d, u, g);
         case 3: return eval_uncached<3, T, GRAD>(d, u, g);
         default: {  // degrees above AFAM_FAST_DEGREE: float64 from the knots
-            double gd[3];
-            const double v = eval_any(d, u, GRAD ? gd : nullptr);
-            if constexpr (GRAD)
-                for (int a = 0; a < 3; a++) g[a] = (T)gd[a];
-            return (T)v;
+            if constexpr (HD) {
+                double gd[3];
+                const double v = eval_any(d, u, GRAD ? gd : nullptr);
+                if constexpr (GRAD)
+                    for (int a = 0; a < 3; a++) g[a] = (T)gd[a];
+                return (T)v;
+            } else {
+                return eval_uncached<3, T, GRAD>(d, u, g);  // not reached: the host picks HD for such stores
+            }
         }
     }
 }
@@ -80,14 +87,13 @@ __device__ __forceinline__ void eval_ds(const BlockDesc &d, const double *__rest
     }
 }
 
-template <bool GRAD, typename OT>
-__global__ void __launch_bounds__(256) eval_points_kernel(const BlockDesc *__restrict__ descs,
-                                                          const int32_t *__restrict__ slots, int32_t slot,
-                                                          const double *__restrict__ pts, int64_t n,
-                                                          OT *__restrict__ val, OT *__restrict__ grad,
-                                                          uint32_t flags, const int32_t *__restrict__ order,
-                                                          const int32_t *__restrict__ keep, OT *__restrict__ tval,
-                                                          OT *__restrict__ tgrad) {
+template <bool GRAD, typename OT, bool HD>
+__device__ __forceinline__ void eval_points_body(const BlockDesc *__restrict__ descs,
+                                                 const int32_t *__restrict__ slots, int32_t slot,
+                                                 const double *__restrict__ pts, int64_t n, OT *__restrict__ val,
+                                                 OT *__restrict__ grad, uint32_t flags,
+                                                 const int32_t *__restrict__ order, const int32_t *__restrict__ keep,
+                                                 OT *__restrict__ tval, OT *__restrict__ tgrad) {
     const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (j >= n) return;
     // order: the batch bucketed by slot (slot_scatter_kernel), so the lanes
@@ -118,10 +124,10 @@ __global__ void __launch_bounds__(256) eval_points_kernel(const BlockDesc *__res
     }
     double v, g[3] = {0.0, 0.0, 0.0};
     if ((d.flags & AFAM_SLOT_FP64) || d.deg > AFAM_FAST_DEGREE) {  // float64 (high degrees: eval_any)
-        v = eval_dispatch<double, GRAD>(d, u, g);
+        v = eval_dispatch<double, GRAD, HD>(d, u, g);
     } else {
         float gf[3];
-        v = eval_dispatch<float, GRAD>(d, u, gf);
+        v = eval_dispatch<float, GRAD, HD>(d, u, gf);
         if (GRAD)
 #pragma unroll
             for (int a = 0; a < 3; a++) g[a] = gf[a];
@@ -133,18 +139,50 @@ __global__ void __launch_bounds__(256) eval_points_kernel(const BlockDesc *__res
     }
 }
 
-template <typename OT>
-static void launch(const BlockDesc *descs, const int32_t *slots, int32_t slot, const double *pts, int64_t n,
-                   void *val, void *grad, uint32_t flags, const int32_t *order, const int32_t *keep, void *tval,
-                   void *tgrad, cudaStream_t st) {
+// value-only: 64 registers, 4 CTAs of 256 per SM; value + gradient held to
+// 80 registers (3 CTAs per SM: at 86 it dropped to 2 and ran 15% slower)
+template <typename OT, bool HD>
+__global__ void __launch_bounds__(256) eval_points_kernel(const BlockDesc *__restrict__ descs,
+                                                          const int32_t *__restrict__ slots, int32_t slot,
+                                                          const double *__restrict__ pts, int64_t n,
+                                                          OT *__restrict__ val, uint32_t flags,
+                                                          const int32_t *__restrict__ order,
+                                                          const int32_t *__restrict__ keep, OT *__restrict__ tval) {
+    eval_points_body<false, OT, HD>(descs, slots, slot, pts, n, val, nullptr, flags, order, keep, tval, nullptr);
+}
+
+template <typename OT, bool HD>
+__global__ void __launch_bounds__(256, 3) eval_points_grad_kernel(const BlockDesc *__restrict__ descs,
+                                                                  const int32_t *__restrict__ slots, int32_t slot,
+                                                                  const double *__restrict__ pts, int64_t n,
+                                                                  OT *__restrict__ val, OT *__restrict__ grad,
+                                                                  uint32_t flags, const int32_t *__restrict__ order,
+                                                                  const int32_t *__restrict__ keep,
+                                                                  OT *__restrict__ tval, OT *__restrict__ tgrad) {
+    eval_points_body<true, OT, HD>(descs, slots, slot, pts, n, val, grad, flags, order, keep, tval, tgrad);
+}
+
+template <typename OT, bool HD>
+static void launch_hd(const BlockDesc *descs, const int32_t *slots, int32_t slot, const double *pts, int64_t n,
+                      void *val, void *grad, uint32_t flags, const int32_t *order, const int32_t *keep, void *tval,
+                      void *tgrad, cudaStream_t st) {
     const int threads = 256;
     const unsigned blocks = (unsigned)((n + threads - 1) / threads);
     if (grad)
-        eval_points_kernel<true, OT><<<blocks, threads, 0, st>>>(descs, slots, slot, pts, n, (OT *)val, (OT *)grad,
-                                                                 flags, order, keep, (OT *)tval, (OT *)tgrad);
+        eval_points_grad_kernel<OT, HD><<<blocks, threads, 0, st>>>(descs, slots, slot, pts, n, (OT *)val,
+                                                                    (OT *)grad, flags, order, keep, (OT *)tval,
+                                                                    (OT *)tgrad);
     else
-        eval_points_kernel<false, OT><<<blocks, threads, 0, st>>>(descs, slots, slot, pts, n, (OT *)val, nullptr,
-                                                                  flags, order, keep, (OT *)tval, nullptr);
+        eval_points_kernel<OT, HD><<<blocks, threads, 0, st>>>(descs, slots, slot, pts, n, (OT *)val, flags, order,
+                                                               keep, (OT *)tval);
+}
+
+template <typename OT>
+static void launch(const BlockDesc *descs, const int32_t *slots, int32_t slot, const double *pts, int64_t n,
+                   void *val, void *grad, uint32_t flags, const int32_t *order, const int32_t *keep, void *tval,
+                   void *tgrad, cudaStream_t st, bool hd) {
+    if (hd) launch_hd<OT, true>(descs, slots, slot, pts, n, val, grad, flags, order, keep, tval, tgrad, st);
+    else launch_hd<OT, false>(descs, slots, slot, pts, n, val, grad, flags, order, keep, tval, tgrad, st);
 }
 
 // ---- bucketing a per-point slot batch by slot (counting sort, three passes)
@@ -283,9 +321,11 @@ extern "C" int afam_eval_points(afam_store *s, const int32_t *slots, int32_t slo
     AFAM_CHECK(pts && val, AFAM_E_VALUE, "pts/val is NULL");
     cudaStream_t st = (cudaStream_t)stream;
     AFAM_CUDA(cudaSetDevice(s->device));
+    bool hd = false;  // blocks of degrees above AFAM_FAST_DEGREE may be evaluated: the HD kernel
     {
         std::lock_guard<std::mutex> lk(s->mu);
         if (!slots) {
+            hd = s->host[slot].valid && !s->host[slot].ds && s->host[slot].deg > AFAM_FAST_DEGREE;
             AFAM_CHECK(slot >= 0 && slot < s->nslots && s->host[slot].valid, AFAM_E_VALUE, "slot %d is empty", slot);
             AFAM_CHECK(!s->host[slot].ds || !(flags & AFAM_EVAL_PARAM), AFAM_E_VALUE,
                        "slot %d holds a DS block: parameter-space evaluation needs a spline", slot);
@@ -296,6 +336,7 @@ extern "C" int afam_eval_points(afam_store *s, const int32_t *slots, int32_t slo
             for (int32_t k = 0; k < s->nslots; k++) {
                 SlotHost &h = s->host[k];
                 any_ds = any_ds || (h.valid && h.ds);
+                hd = hd || (h.valid && !h.ds && h.deg > AFAM_FAST_DEGREE);
                 if (!h.valid || !h.pending) continue;
                 if (cudaEventQuery(h.ready) == cudaSuccess) h.pending = false;
                 else AFAM_CUDA(cudaStreamWaitEvent(st, h.ready, 0));
@@ -343,9 +384,9 @@ extern "C" int afam_eval_points(afam_store *s, const int32_t *slots, int32_t slo
     void *ev = order ? tmp : nullptr;
     void *eg = order && grad ? (void *)((char *)tmp + (size_t)n * osz) : nullptr;
     if (flags & AFAM_EVAL_OUT_F64)
-        launch<double>(s->d_desc, slots, slot, pts, n, val, grad, flags, order, keep, ev, eg, st);
+        launch<double>(s->d_desc, slots, slot, pts, n, val, grad, flags, order, keep, ev, eg, st, hd);
     else
-        launch<float>(s->d_desc, slots, slot, pts, n, val, grad, flags, order, keep, ev, eg, st);
+        launch<float>(s->d_desc, slots, slot, pts, n, val, grad, flags, order, keep, ev, eg, st, hd);
     AFAM_CUDA(cudaGetLastError());
     if (order) {
         const unsigned g2 = (unsigned)((n + 255) / 256);
