@@ -2079,6 +2079,8 @@ template <bool DEBUG, bool SMEM>
 static void launch_render(const LaunchArgs &L, const RenderArgs &A, int fd, bool hi, bool f64, bool allfast,
                           bool allfast64) {
     if (fd == 0) return launch_render_v<DEBUG, SMEM, 0, 4>(L, A);  // DS blocks
+    if (allfast && SMEM && !render_v1() && render2_minb() == 4 && fd == 3)  // A/B: 4 CTAs/SM (128 registers)
+        return launch_render2_v<DEBUG, SMEM, 3, 4, 0, false, false, true>(L, A);
     if (allfast && SMEM && !render_v1() && render2_minb() == 3) {
         if (fd == 3) return launch_render2_v<DEBUG, SMEM, 3, 3, 0, false, false, true>(L, A);
         if (fd == 2) return launch_render2_v<DEBUG, SMEM, 2, 4, 0, false, false, true>(L, A);
