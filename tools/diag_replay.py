@@ -28,9 +28,9 @@ def draw(pov, resident, tf_, params_):
     return tiles.render_tiles(pov, resident, tf_, params_, band_rows=8)
 
 
-class Timed:  # collects each frame's kernel time (CUDA events around the render kernels)
-    def __init__(self, p):
-        self.p = p
+class Timed:  # collects each frame's kernel time and its stream time (incl. waits for its uploads)
+    def __init__(self, p, ea, eb):
+        self.p, self.ea, self.eb = p, ea, eb
 
     def done(self):
         return self.p.done()
@@ -38,12 +38,23 @@ class Timed:  # collects each frame's kernel time (CUDA events around the render
     def result(self):
         f = self.p.result()
         kms.append(tiles.render_tiles.last_stats["kernel_ms"])
+        spans.append((self.ea, self.eb))
         return f
 
 
-kms = []
-draw.submit = lambda pov, resident, tf_, params_: Timed(tiles.submit_tiles(pov, resident, tf_, params_,
-                                                                          band_rows=8))
+kms, spans = [], []
+
+
+def _submit(pov, resident, tf_, params_):
+    st = render._render_stream(torch.device("cuda", 0))
+    ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ea.record(st)
+    p = tiles.submit_tiles(pov, resident, tf_, params_, band_rows=8)
+    eb.record(st)
+    return Timed(p, ea, eb)
+
+
+draw.submit = _submit
 draw.frames_in_flight = 2
 for r in range(rounds):
     for mode in os.environ.get("MODES", "2,1,0").split(","):  # depth 2, depth 1 (overlapped caching), strict order
@@ -54,6 +65,7 @@ for r in range(rounds):
         runtime.replay(povs[:3], man, cache, tf, params, prefetch="linear", keep_frames=False, render_fn=draw)
         torch.cuda.synchronize()
         kms.clear()
+        spans.clear()
         t0 = time.perf_counter()
         tim, _, agg = runtime.replay(povs[3:3 + nfr], man, cache, tf, params, prefetch="linear",
                                      keep_frames=False, render_fn=draw)
@@ -63,5 +75,10 @@ for r in range(rounds):
                           "caching_ms": sum(t.caching_ms for t in tim) / nfr,
                           "rendering_ms": sum(t.rendering_ms for t in tim) / nfr,
                           "loaded": sum(t.prefetch_models_loaded for t in tim),
-                          "kernel_ms": sum(kms) / max(1, len(kms))}), flush=True)
+                          "kernel_ms": sum(kms) / max(1, len(kms)),
+                          # stream time per frame (pack upload + waits for its uploads + kernels) and the
+                          # GPU gap between a frame's end and the next frame's start on the render stream
+                          "stream_ms": sum(a.elapsed_time(b) for a, b in spans) / max(1, len(spans)),
+                          "gap_ms": sum(spans[j][1].elapsed_time(spans[j + 1][0]) for j in range(len(spans) - 1))
+                          / max(1, len(spans) - 1)}), flush=True)
         del cache, ds
