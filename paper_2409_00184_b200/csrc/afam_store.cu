@@ -381,6 +381,9 @@ static int check_put(afam_store *s, int32_t slot, int deg, int ncp, const double
 // the bit patterns without the sign), the value the device derives in
 // unpack_ctrl_kernel: afam_render picks its kernel from it before the upload
 // has finished.
+// (AVX2 clone where the host has it: 29 vs 78 us for a 65^3 block -- this
+// scan is half the host time of a cache miss on the replay's frame thread)
+__attribute__((target_clones("avx2", "default")))
 static bool all_finite_le_f32(const uint8_t *p, size_t count, float *maxabs = nullptr) {
     uint32_t bad = 0, mx = 0;
     for (size_t i = 0; i < count; i++) {
