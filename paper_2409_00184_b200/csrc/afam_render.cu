@@ -673,6 +673,20 @@ __device__ __forceinline__ T vld(const T &x) {
     return *(const volatile T *)&x;
 }
 
+// render2_kernel's warp tile: kWarpW x (32 / kWarpW) pixels, CTA tile kCtaW x
+// (128 / kCtaW) (-DAFAM_WARP_W / -DAFAM_CTA_W for A/B).  Measured on config 3
+// (ms per frame): 4x8 warps in 8x16 CTAs 1.965, 4x8 in 16x8 1.97, 2x16 in
+// 8x16 1.99, 4x8 in 4x32 2.01, 8x4 in 16x8 2.07, 8x4 in 8x16 2.06, 16x2 in
+// 16x8 2.22.
+#ifndef AFAM_WARP_W
+#define AFAM_WARP_W 4
+#endif
+constexpr int kWarpW = AFAM_WARP_W;
+#ifndef AFAM_CTA_W
+#define AFAM_CTA_W 8
+#endif
+constexpr int kCtaW = AFAM_CTA_W;  // render2_kernel's CTA tile: kCtaW x (128 / kCtaW) pixels
+
 struct FastCold {  // render2_kernel's per-thread rarely-read state
     BlockFast b;                 // the owner block's fields read at cell changes
     int32_t kend;                // alive samples of the ray
@@ -1610,8 +1624,9 @@ __global__ void __launch_bounds__(128, MINB) render2_kernel(const BlockDesc *__r
     // after the march instead of held in registers across it)
     auto pixel = [&](int &j, int &lr, int &i) {
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-        j = blockIdx.x * 16 + (warp & 1) * 8 + (lane & 7);
-        lr = blockIdx.y * 8 + (warp >> 1) * 4 + (lane >> 3);
+        constexpr int W = kWarpW, WPR = kCtaW / kWarpW;  // warp tile W x (32 / W), WPR warps per CTA row
+        j = blockIdx.x * kCtaW + (warp % WPR) * W + (lane % W);
+        lr = blockIdx.y * (128 / kCtaW) + (warp / WPR) * (32 / W) + lane / W;
         const bool in = j < A.width && lr < A.rows;
         i = in ? frame_row(A, lr) : 0;
         return in;
@@ -2030,7 +2045,8 @@ static void launch_render2_v(const LaunchArgs &L, const RenderArgs &A) {
                              cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
         configured = true;
     }
-    render2_kernel<DEBUG, SMEM, P, MINB, SR, HI, F64, AF><<<L.grid, 128, L.smem, L.st>>>(L.descs, L.owner, L.idx, A, L.gargs,
+    const dim3 grid((A.width + kCtaW - 1) / kCtaW, (A.rows + 128 / kCtaW - 1) / (128 / kCtaW));  // its CTA tile
+    render2_kernel<DEBUG, SMEM, P, MINB, SR, HI, F64, AF><<<grid, 128, L.smem, L.st>>>(L.descs, L.owner, L.idx, A, L.gargs,
                                                                              L.gtf, L.rgba, L.stats, L.nsamp,
                                                                              L.ohash);
 }
@@ -2353,7 +2369,7 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
     init_stats_kernel<<<1, 1, 0, st>>>(stats);
     if (A.rows > 0) {
         LaunchArgs L;
-        L.grid = dim3((A.width + 15) / 16, (A.rows + 7) / 8);
+        L.grid = dim3((A.width + 15) / 16, (A.rows + 7) / 8);  // render_kernel's 16 x 8 tile (render2: its own)
         const bool sg = cells <= kSmemGridMaxCells;
         L.smem = kSmemGridOff + (sg ? gbytes : 0);
         L.st = st;
