@@ -382,11 +382,7 @@ def run_ours(args, rank, world, local_rank):
                              exact_geometry_per_sample=exact_c / max(1, samples), gen_s=round(gen_s, 1),
                              upload_s=round(upload_s, 2), fp64_slot_sample=int(nfp64)),
               "roofline": roofline, "clocks": clk.summary(), "gpu_launches": 3 * args.steps,
-              "wall_s_timed_region": t_wall,
-              # host-clock view of the same steps (max over ranks): includes per-step
-              # host work, the L2 flush, the synchronisation and, at N > 1, the
-              # barrier that completes a fused frame on rank 0
-              "value_wall_clock": total_samples / t_wall if t_wall > 0 else None}
+              "wall_s_timed_region": t_wall}
 
     # -- e2e through the public runtime API: ModelCache(200) + linear prefetch, pinned host source
     if not args.no_e2e:

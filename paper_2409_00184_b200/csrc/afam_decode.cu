@@ -312,7 +312,10 @@ __global__ void __launch_bounds__(kDecodeThreads) decode_grid_kernel(const Block
 // Y[64][.] the X row ncp-1: threads 0..128 carry one such value each
 // (threads 0..15 also take the x stage's control row 64).  Control points are read once from HBM (TMA), the
 // output written once; x and y run out of registers and one X plane.
-constexpr int kFxRing = 4;       // TMA plane slots
+#ifndef AFAM_FX_RING
+#define AFAM_FX_RING 4
+#endif
+constexpr int kFxRing = AFAM_FX_RING;  // TMA plane slots (-DAFAM_FX_RING for A/B)
 constexpr int kFxXPitch = 68;    // X plane row pitch (floats)
 constexpr int kFxXRows = 72;     // X plane rows (the y windows over-read up to row ncp + 4, zeros)
 constexpr int kFxPad = 16;       // zero floats after each ring slot (x windows over-read the last row)
