@@ -396,6 +396,7 @@ def run_ours(args, rank, world, local_rank):
         result["workloads"] = {
             "config5": run_config5(ds, resident_all, man, blobs, rank, world, dev, max(3, args.steps // 4),
                                    args.warmup),
+            "k1_points": run_k1(ds, resident_all, dev, max(3, args.steps // 4), args.warmup),
         }
         del resident_all, ds
         torch.cuda.empty_cache()
@@ -688,6 +689,61 @@ def run_config5(ds, resident_all, man, blobs, rank, world, dev, steps, warmup, e
         res["e2e"] = config5_e2e(man, blobs, addrs, rank, world, dev, steps)
     del out
     return res
+
+
+def run_k1(ds, resident_all, dev, steps, warmup):
+    """The K1 decode-gather microbenchmark of SURVEY.md 8(d) on the resident
+    config-3 store: n = 2^24 parameter points u ~ U[0,1)^3 (default_rng(0)),
+    slots uniform over the 4,680 blocks (incoherent gather), value +
+    gradient, float32 out (bspline.evaluate_points_with_gradient /
+    MicroModel.values_at + gradients_at, model.py:64-87).  HBM roofline with
+    the survey's algorithmic bytes per sample (4 q^3 control + 24 point + 4
+    slot + 4 value + 12 gradient)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2409_00184_b200 import _lib
+
+    n = 1 << 24
+    rng = np.random.default_rng(0)
+    slots = np.array([b.slot for b in resident_all.values()], dtype=np.int32)
+    u = torch.from_numpy(rng.uniform(0, 1, size=(n, 3))).to(dev)
+    sl = torch.from_numpy(slots[rng.integers(0, len(slots), size=n)]).to(dev)
+    val = torch.empty(n, dtype=torch.float32, device=dev)
+    grad = torch.empty((n, 3), dtype=torch.float32, device=dev)
+    st = torch.cuda.current_stream(dev)
+    lib = _lib.lib()
+
+    def launch():
+        _lib.check(lib.afam_eval_points(ds.handle, C.c_void_p(sl.data_ptr()), 0, C.c_void_p(u.data_ptr()), n,
+                                        C.c_void_p(val.data_ptr()), C.c_void_p(grad.data_ptr()),
+                                        _lib.AFAM_EVAL_PARAM, C.c_void_p(st.cuda_stream)))
+
+    for _ in range(warmup):
+        launch()
+    torch.cuda.synchronize(dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for e0, e1 in evs:
+        e0.record(st)
+        launch()
+        e1.record(st)
+    torch.cuda.synchronize(dev)
+    ms = float(np.mean([e0.elapsed_time(e1) for e0, e1 in evs]))
+    per = 4 * 64 + 24 + 4 + 4 + 12
+    hbm, src = measured_peaks()
+    achieved = n * per / (ms * 1e-3) / 1e9
+    return {"metric": "decoded samples/s (K1 point decode, 2^24 incoherent points, value + gradient)",
+            "value": n / (ms * 1e-3), "unit": UNIT, "steps": steps, "ms_per_step": ms, "higher_is_better": True,
+            "config": {"workload": "K1: 2^24 u ~ U[0,1)^3 (default_rng(0)), slots uniform over the 4,680 resident "
+                                   "config-3 blocks, AFAM_EVAL_PARAM, value + gradient, float32 out",
+                       "l2": "the batch's control points (2.9 GB of slots) exceed L2"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                         "traffic": None, "kernel": "eval_points_grad_kernel (K1)",
+                         "note": "algorithmic bytes per sample (SURVEY.md 8d) = 4*4^3 control + 24 point + 4 slot + "
+                                 "4 value + 12 gradient; DRAM reads are ~2.2x that (a point's four 64-byte x-quad "
+                                 f"runs at 16-byte alignment touch two 64-byte bursts each, profiles/ncu_points_r02.txt); "
+                                 f"peak = {src}"}}
 
 
 def config5_e2e(man, blobs, addrs, rank, world, dev, steps):
