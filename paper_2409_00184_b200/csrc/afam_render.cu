@@ -673,7 +673,7 @@ __device__ __forceinline__ T vld(const T &x) {
     return *(const volatile T *)&x;
 }
 
-// render2_kernel's warp tile: kWarpW x (32 / kWarpW) pixels, CTA tile kCtaW x
+// K2's warp tile (both kernels): kWarpW x (32 / kWarpW) pixels, CTA tile kCtaW x
 // (128 / kCtaW) (-DAFAM_WARP_W / -DAFAM_CTA_W for A/B).  Measured on config 3
 // (ms per frame): 4x8 warps in 8x16 CTAs 1.965, 4x8 in 16x8 1.97, 2x16 in
 // 8x16 1.99, 4x8 in 4x32 2.01, 8x4 in 16x8 2.07, 8x4 in 8x16 2.06, 16x2 in
@@ -1046,8 +1046,9 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
     RayState R;  // local memory: touched on the exact paths only
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int j = blockIdx.x * 16 + (warp & 1) * 8 + (lane & 7);
-    const int lr = blockIdx.y * 8 + (warp >> 1) * 4 + (lane >> 3);
+    constexpr int WPR = kCtaW / kWarpW;  // the render2_kernel tiles
+    const int j = blockIdx.x * kCtaW + (warp % WPR) * kWarpW + (lane % kWarpW);
+    const int lr = blockIdx.y * (128 / kCtaW) + (warp / WPR) * (32 / kWarpW) + lane / kWarpW;
     const bool inside = j < A.width && lr < A.rows;
     const int i = inside ? frame_row(A, lr) : 0;
 
@@ -2045,8 +2046,7 @@ static void launch_render2_v(const LaunchArgs &L, const RenderArgs &A) {
                              cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
         configured = true;
     }
-    const dim3 grid((A.width + kCtaW - 1) / kCtaW, (A.rows + 128 / kCtaW - 1) / (128 / kCtaW));  // its CTA tile
-    render2_kernel<DEBUG, SMEM, P, MINB, SR, HI, F64, AF><<<grid, 128, L.smem, L.st>>>(L.descs, L.owner, L.idx, A, L.gargs,
+    render2_kernel<DEBUG, SMEM, P, MINB, SR, HI, F64, AF><<<L.grid, 128, L.smem, L.st>>>(L.descs, L.owner, L.idx, A, L.gargs,
                                                                              L.gtf, L.rgba, L.stats, L.nsamp,
                                                                              L.ohash);
 }
@@ -2369,7 +2369,7 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
     init_stats_kernel<<<1, 1, 0, st>>>(stats);
     if (A.rows > 0) {
         LaunchArgs L;
-        L.grid = dim3((A.width + 15) / 16, (A.rows + 7) / 8);  // render_kernel's 16 x 8 tile (render2: its own)
+        L.grid = dim3((A.width + kCtaW - 1) / kCtaW, (A.rows + 128 / kCtaW - 1) / (128 / kCtaW));
         const bool sg = cells <= kSmemGridMaxCells;
         L.smem = kSmemGridOff + (sg ? gbytes : 0);
         L.st = st;
