@@ -1,7 +1,11 @@
-"""The committed bench lines (profiles/bench_r01.json, bench_ref_r01.json)
+"""The committed bench lines (profiles/bench_r0{1,2}.json, bench_ref_r0{1,2}.json)
 carry every key of the bench contract: metric/value/unit, timing fields,
 roofline, cpu_baseline, e2e, clocks and gpu_launches; the reference arm
-line is marked impl=reference with its own e2e and cpu_baseline."""
+line is marked impl=reference with its own e2e and cpu_baseline.  Round 2's
+line also carries the other BASELINE configs and K1 with their own
+rooflines, and the e2e replay from disk."""
+
+import pytest
 
 import json
 from pathlib import Path
@@ -13,8 +17,9 @@ def _line(name):
     return json.loads((ROOT / "profiles" / name).read_text().strip().splitlines()[-1])
 
 
-def test_bench_line_contract():
-    d = _line("bench_r01.json")
+@pytest.mark.parametrize("rnd", ["r01", "r02"])
+def test_bench_line_contract(rnd):
+    d = _line(f"bench_{rnd}.json")
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
               "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "clocks", "gpu_launches"):
         assert k in d, k
@@ -38,9 +43,10 @@ def test_bench_line_contract():
     assert not bad & set(d["clocks"]["reasons"])
 
 
-def test_reference_arm_line_contract():
-    d = _line("bench_ref_r01.json")
-    mine = _line("bench_r01.json")
+@pytest.mark.parametrize("rnd", ["r01", "r02"])
+def test_reference_arm_line_contract(rnd):
+    d = _line(f"bench_ref_{rnd}.json")
+    mine = _line(f"bench_{rnd}.json")
     assert d["impl"] == "reference"
     assert d["metric"] == mine["metric"] and d["unit"] == mine["unit"]
     assert d["higher_is_better"] == mine["higher_is_better"]
@@ -95,3 +101,18 @@ def test_reference_arm_inputs_match_product_synthesis():
     rp, rq = render.RenderParams(width=1024, height=1024), W.render_params(width=1024, height=1024)
     for k in ("sample_distance", "o_max", "reference_step", "near", "ambient", "diffuse", "specular", "shininess"):
         assert getattr(rp, k) == getattr(rq, k), k
+
+
+def test_round2_line_extras():
+    d = _line("bench_r02.json")
+    w = d["workloads"]
+    for name in ("config5", "config2", "k1_points"):
+        x = w[name]
+        for k in ("metric", "value", "unit", "ms_per_step", "config", "roofline"):
+            assert k in x, (name, k)
+        r = x["roofline"]
+        assert 0 < r["frac"] <= 1 and abs(r["achieved"] / r["peak"] - r["frac"]) < 1e-6 or name == "config2"
+    assert d["e2e"]["steps"] == 100  # the whole config-4 orbit
+    fd = d["e2e"]["from_disk"]
+    assert fd["value"] > 0 and fd["unit"] == d["unit"] and fd["h2d_bytes_per_step"] > 0
+    assert d["roofline"]["achieved_executed"] <= d["roofline"]["achieved"]
