@@ -397,6 +397,9 @@ def run_ours(args, rank, world, local_rank):
             "config5": run_config5(ds, resident_all, man, blobs, rank, world, dev, max(3, args.steps // 4),
                                    args.warmup),
             "k1_points": run_k1(ds, resident_all, dev, max(3, args.steps // 4), args.warmup),
+            # the same decode on the tcgen05 kernel (3xTF32 x stage), measured beside the default
+            "config5_tensor_cores": run_config5(ds, resident_all, man, blobs, rank, world, dev, 3, 1,
+                                                path="tensor_cores"),
         }
         del resident_all, ds
         torch.cuda.empty_cache()
@@ -626,7 +629,7 @@ def measure_dfma_peak(dev):
 C5_METRIC = "decoded samples/s (decode_grid 65^3 of all 4,680 blocks, config 5)"
 
 
-def run_config5(ds, resident_all, man, blobs, rank, world, dev, steps, warmup, e2e=False):
+def run_config5(ds, resident_all, man, blobs, rank, world, dev, steps, warmup, e2e=False, path="auto"):
     """BASELINE config 5: decode_grid((65,)*3) of every block of the config-3
     model (model.py:89-93 -> bspline.py:162-172), blocks round-robin over the
     ranks (block i on rank i % N: no exchange, the decoded
@@ -651,9 +654,12 @@ def run_config5(ds, resident_all, man, blobs, rank, world, dev, steps, warmup, e
     st = torch.cuda.current_stream(dev)
     lib = _lib.lib()
 
+    from paper_2409_00184_b200.bspline import DECODE_PATHS
+
     def launch():
-        _lib.check(lib.afam_decode_grid(ds.handle, slots.ctypes.data_as(C.c_void_p), len(slots), m,
-                                        C.c_void_p(out.data_ptr()), C.c_void_p(st.cuda_stream)))
+        _lib.check(lib.afam_decode_grid_ex(ds.handle, slots.ctypes.data_as(C.c_void_p), len(slots), m,
+                                           C.c_void_p(out.data_ptr()), DECODE_PATHS[path], None,
+                                           C.c_void_p(st.cuda_stream)))
 
     for _ in range(warmup):
         launch()
@@ -682,9 +688,12 @@ def run_config5(ds, resident_all, man, blobs, rank, world, dev, steps, warmup, e
                       "parallelism": f"blocks round-robin over {world} rank(s), no collective",
                       "blocks_per_rank": len(slots), "l2": "inputs and outputs exceed L2 (2.9 GB in, 5.1 GB out)"},
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                        "frac": achieved / hbm, "traffic": None, "kernel": "decode_grid_kernel (K3)",
+                        "frac": achieved / hbm, "traffic": None,
+                        "kernel": "decode_tc_kernel (K3, tcgen05 3xTF32 x stage)" if path == "tensor_cores"
+                        else "decode_fx_kernel (K3, register-tiled CUDA cores)",
                         "note": "algorithmic bytes = 4 ncp^3 (control points read) + 4 m^3 (grid written) per "
                                 f"block, this rank's blocks per launch; peak = {src}"}}
+    res["config"]["path"] = path
     if e2e:
         res["e2e"] = config5_e2e(man, blobs, addrs, rank, world, dev, steps)
     del out
