@@ -33,6 +33,8 @@ struct alignas(16) BlockDesc {
     const float *tab32;   // [3][nspan][tab_stride(deg)] float
     const double *tab64;  // [3][nspan][tab_stride(deg)] double
     const float *knots;   // [3][nk] float (full clamped vectors)
+    const float2 *crange; // [nspan^3] per knot cell (kz*nspan+kx)*nspan+ky: [min, max] of its (p+1)^3
+                          // control points widened by max|c| * 2^-14 (degrees <= AFAM_FAST_DEGREE)
     double lo[3];         // extent low corner
     double span[3];       // hi - lo
     double inv_span[3];   // 1 / (hi - lo)
@@ -118,6 +120,7 @@ struct afam_store {
     int32_t nslots = 0, max_ncp = 0;
     double fp64_limit = 4.0;
     size_t raw_bytes = 0, ctrl_floats = 0, ctrl4_elems = 0, knot_floats = 0, tab_elems = 0, slot_bytes = 0;
+    size_t crange_elems = 0;
     char *arena = nullptr;               // nslots * slot_bytes device bytes
     afam::BlockDesc *d_desc = nullptr;   // nslots descriptors (device)
     float *d_maxabs = nullptr;           // nslots (device)
@@ -142,12 +145,14 @@ struct afam_store {
     float *knot_ptr(int32_t slot) const { return (float *)(slot_base(slot) + knot_off()); }
     float *tab32_ptr(int32_t slot) const { return (float *)(slot_base(slot) + tab32_off()); }
     double *tab64_ptr(int32_t slot) const { return (double *)(slot_base(slot) + tab64_off()); }
+    float2 *crange_ptr(int32_t slot) const { return (float2 *)(slot_base(slot) + crange_off()); }
     static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
     size_t raw_off() const { return align256(raw_bytes); }
     size_t ctrl4_off() const { return raw_off() + align256(ctrl_floats * 4); }
     size_t knot_off() const { return ctrl4_off() + align256(ctrl4_elems * 16); }
     size_t tab32_off() const { return knot_off() + align256(knot_floats * 4); }
     size_t tab64_off() const { return tab32_off() + align256(tab_elems * 4); }
+    size_t crange_off() const { return tab64_off() + align256(tab_elems * 8); }
 };
 
 struct afam_manifest {

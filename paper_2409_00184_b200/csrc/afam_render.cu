@@ -460,6 +460,7 @@ constexpr uint32_t kRenderForceExact = 0x100u;
 
 struct BlockFast {
     const float4 *ctrl4;
+    const float2 *rng;  // per-cell value ranges (BlockDesc::crange)
     int32_t ncp, nspan;
     int32_t plane;  // ncp^2: x-quad rows per z plane
     uint32_t nint;  // interior spans (k in [p-1, nspan-p]): max(nspan - 2p + 2, 0)
@@ -1288,6 +1289,7 @@ template <int P>
 __device__ __forceinline__ BlockFast fast_block(const BlockFast &sb) {  // sb in shared memory
     BlockFast b;
     b.ctrl4 = vld(sb.ctrl4);
+    b.rng = vld(sb.rng);
     b.ncp = vld(sb.ncp);
     b.nspan = vld(sb.nspan);
     b.plane = vld(sb.plane);
@@ -1295,14 +1297,35 @@ __device__ __forceinline__ BlockFast fast_block(const BlockFast &sb) {  // sb in
     return b;
 }
 
-template <int P, int SR>
-__device__ __forceinline__ void fast_cell_update_k(const BlockFast &b, int kx, int ky, int kz, FastCell<P, SR> &G) {
+#ifndef AFAM_CELL_SKIP
+#define AFAM_CELL_SKIP 1  // skip the samples of cells the TF makes transparent (BlockDesc::crange)
+#endif
+
+// Bit 3 of FastCell::inner: every value the cell can produce is outside the
+// TF's opacity support, so its samples are transparent without decoding
+// (the per-sample test of sample_fast2 would return on each of them) and
+// its rows are not gathered.
+constexpr uint32_t kCellClear = 8u;
+
+template <int P, int SR, bool SKIP = false>
+__device__ __forceinline__ void fast_cell_update_k(const BlockFast &b, int kx, int ky, int kz, FastCell<P, SR> &G,
+                                                   const RenderArgs *A = nullptr) {
     constexpr int Q = P + 1;
     G.cx = (float)kx;
     G.cy = (float)ky;
     G.cz = (float)kz;
     G.inner = (span_interior<P>(b, kx) ? 1u : 0u) | (span_interior<P>(b, ky) ? 2u : 0u) |
               (span_interior<P>(b, kz) ? 4u : 0u);
+    if constexpr (SKIP && AFAM_CELL_SKIP) {
+        // the clamp of render.py's value to the TF domain is monotone: the
+        // clamped range bounds every clamped sample value
+        const float2 r = __ldg(b.rng + (kz * b.nspan + kx) * b.nspan + ky);
+        const float lo = fminf(fmaxf(r.x, A->dom_lo), A->dom_hi), hi = fminf(fmaxf(r.y, A->dom_lo), A->dom_hi);
+        if (!(hi > A->op_lo) || !(lo < A->op_hi)) {
+            G.inner |= kCellClear;
+            return;  // the rows of G.key stay valid for that key
+        }
+    }
     const int32_t id = (kz * b.ncp + kx) * b.ncp + ky;
     if (id != G.key) {
         const float4 *base = b.ctrl4 + id;
@@ -1316,12 +1339,12 @@ __device__ __forceinline__ void fast_cell_update_k(const BlockFast &b, int kx, i
 
 template <int P, int SR>
 __device__ __forceinline__ void fast_cell_update(const BlockFast &sb, float tqx, float tqy, float tqz,
-                                                 FastCell<P, SR> &G) {
+                                                 FastCell<P, SR> &G, const RenderArgs &A) {
     const BlockFast b = fast_block<P>(sb);
     const int kx = min(max(__float2int_rd(tqx), 0), b.nspan - 1);
     const int ky = min(max(__float2int_rd(tqy), 0), b.nspan - 1);
     const int kz = min(max(__float2int_rd(tqz), 0), b.nspan - 1);
-    fast_cell_update_k<P, SR>(b, kx, ky, kz, G);
+    fast_cell_update_k<P, SR, true>(b, kx, ky, kz, G, &A);
 }
 
 // One sample of a clamped-uniform float32 block (render_kernel's
@@ -1334,7 +1357,7 @@ __device__ __forceinline__ bool sample_fast2(const RenderArgs &A, const TfTable 
     constexpr int Q = P + 1;
     float fx = tqx - G.cx, fy = tqy - G.cy, fz = tqz - G.cz;
     if (!(in_unit(fx) & in_unit(fy) & in_unit(fz))) {
-        fast_cell_update<P, SR>(sb, tqx, tqy, tqz, G);
+        fast_cell_update<P, SR>(sb, tqx, tqy, tqz, G, A);
         fx = tqx - G.cx;
         fy = tqy - G.cy;
         fz = tqz - G.cz;
@@ -1344,6 +1367,7 @@ __device__ __forceinline__ bool sample_fast2(const RenderArgs &A, const TfTable 
             !(fabsf(fz - 0.5f) < 0.5f - 1e-4f))
             return false;
     }
+    if (AFAM_CELL_SKIP && (G.inner & kCellClear)) return true;  // transparent: changes neither C nor A
     float Nx[Q], Ny[Q], Nz[Q];
     {
         float2 Nxy[Q];
@@ -1713,6 +1737,7 @@ __global__ void __launch_bounds__(128, MINB) render2_kernel(const BlockDesc *__r
                     F.slot = slot;
                     const BlockDesc *dp = descs + slot;
                     b.ctrl4 = (const float4 *)__ldg((const unsigned long long *)&dp->ctrl4);
+                    b.rng = (const float2 *)__ldg((const unsigned long long *)&dp->crange);
                     C.tab32 = (const float *)__ldg((const unsigned long long *)&dp->tab32);
                     b.ncp = __ldg(&dp->ncp);
                     b.nspan = __ldg(&dp->nspan);

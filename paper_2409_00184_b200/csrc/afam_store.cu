@@ -101,6 +101,37 @@ __global__ void unpack_quad_kernel(const uint8_t *__restrict__ raw, uint64_t src
     }
 }
 
+// Value range of every knot cell: for cell (kx, ky, kz) the min and max of
+// the (p+1)^3 control points that weight its samples, widened by
+// max|c| * 2^-14.  The basis functions of a cell are non-negative and sum to
+// one, so any value the ray march computes in the cell lies in that range
+// (its float32 rounding is ~1e-6 max|c|, 60x inside the margin); a frame
+// whose transfer function has zero opacity on the whole range skips the
+// cell's samples without decoding them (render2_kernel, sample_fast2).
+__global__ void cell_range_kernel(const float4 *__restrict__ ctrl4, int ncp, int deg,
+                                  const unsigned int *maxabs, float2 *__restrict__ crange) {
+    const int nspan = ncp - deg;
+    const int64_t total = (int64_t)nspan * nspan * nspan;
+    const float eps = __uint_as_float(*maxabs) * 0x1p-14f;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int ky = (int)(i % nspan);
+        const int kx = (int)((i / nspan) % nspan);
+        const int kz = (int)(i / ((int64_t)nspan * nspan));
+        float lo = INFINITY, hi = -INFINITY;
+        for (int cz = 0; cz <= deg; cz++)
+            for (int by = 0; by <= deg; by++) {
+                const float4 r = __ldg(ctrl4 + ((int64_t)(kz + cz) * ncp + kx) * ncp + ky + by);
+                const float v[4] = {r.x, r.y, r.z, r.w};
+                for (int bx = 0; bx <= deg; bx++) {
+                    lo = fminf(lo, v[bx]);
+                    hi = fmaxf(hi, v[bx]);
+                }
+            }
+        crange[i] = make_float2(lo - eps, hi + eps);
+    }
+}
+
 // Knots + per-span basis tables + the slot descriptor.  knot_off: byte
 // offset of the knots; has_t0 = 0 for .mfa images (t0 = 0 implicit,
 // FORMAT.md:44-55), 1 for full vectors.
@@ -195,7 +226,8 @@ int afam_store_create(afam_store **out, int device, int32_t slots, int32_t max_n
     s->ctrl4_elems = (size_t)max_ncp * max_ncp * max_ncp;
     s->knot_floats = 3 * (size_t)(max_ncp + AFAM_MAX_DEGREE + 1);
     s->tab_elems = 3 * (size_t)max_ncp * kTabStrideMax;
-    s->slot_bytes = s->tab64_off() + afam_store::align256(s->tab_elems * 8);
+    s->crange_elems = (size_t)max_ncp * max_ncp * max_ncp;
+    s->slot_bytes = s->crange_off() + afam_store::align256(s->crange_elems * 8);
     cudaError_t e = cudaMalloc(&s->arena, s->slot_bytes * (size_t)slots);
     if (e != cudaSuccess) {
         delete s;
@@ -305,6 +337,7 @@ static int launch_unpack(afam_store *s, int32_t slot, int deg, int ncp, uint64_t
     proto.tab32 = s->tab32_ptr(slot);
     proto.tab64 = s->tab64_ptr(slot);
     proto.knots = s->knot_ptr(slot);
+    proto.crange = deg <= AFAM_FAST_DEGREE ? s->crange_ptr(slot) : nullptr;
     for (int a = 0; a < 3; a++) {
         proto.lo[a] = extent[2 * a];
         proto.span[a] = extent[2 * a + 1] - extent[2 * a];
@@ -325,6 +358,11 @@ static int launch_unpack(afam_store *s, int32_t slot, int deg, int ncp, uint64_t
     const int64_t total4 = (int64_t)ncp * ncp * ncp;
     unpack_quad_kernel<<<(int)std::min<int64_t>((total4 + 255) / 256, 1184), 256, 0, st>>>(
         s->raw_ptr(slot), ctrl_off, ncp, s->ctrl4_ptr(slot));
+    if (deg <= AFAM_FAST_DEGREE) {
+        const int64_t ncell = (int64_t)(ncp - deg) * (ncp - deg) * (ncp - deg);
+        cell_range_kernel<<<(int)std::min<int64_t>((ncell + 255) / 256, 1184), 256, 0, st>>>(
+            s->ctrl4_ptr(slot), ncp, deg, (const unsigned int *)(s->d_maxabs + slot), s->crange_ptr(slot));
+    }
     build_tables_kernel<<<1, 256, 0, st>>>(s->raw_ptr(slot), knot_off, has_t0, ncp, deg, s->knot_ptr(slot),
                                            s->tab32_ptr(slot), s->tab64_ptr(slot), s->d_desc + slot, proto,
                                            (const unsigned int *)(s->d_maxabs + slot), (float)s->fp64_limit);

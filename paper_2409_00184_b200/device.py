@@ -241,7 +241,7 @@ class _ScratchStore:
     """LRU of host models uploaded on demand into one DeviceStore."""
 
     def __init__(self, max_ncp: int, device: int):
-        slot_bytes = 7 * 4 * max_ncp ** 3 + 65536  # raw + pitched + x-quad control points + tables
+        slot_bytes = 9 * 4 * max_ncp ** 3 + 65536  # raw + pitched + x-quad control points + cell ranges + tables
         slots = int(min(1024, max(16, (2 << 30) // slot_bytes)))
         self.store = DeviceStore(slots, max_ncp, device)
         self.lru: OrderedDict = OrderedDict()  # id(model) -> (weakref or None, DeviceBlock)
