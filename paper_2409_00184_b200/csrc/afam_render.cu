@@ -1542,7 +1542,7 @@ __device__ __forceinline__ bool sample_fast64(const RenderArgs &A, const TfTable
         int k[3];
 #pragma unroll
         for (int a = 0; a < 3; a++) k[a] = min(max((int)floor(tq[a]), 0), b.nspan - 1);
-        fast_cell_update_k<P, SR>(b, k[0], k[1], k[2], G);
+        fast_cell_update_k<P, SR, true>(b, k[0], k[1], k[2], G, &A);
 #pragma unroll
         for (int a = 0; a < 3; a++) f[a] = tq[a] - (double)k[a];
     }
@@ -1550,6 +1550,11 @@ __device__ __forceinline__ bool sample_fast64(const RenderArgs &A, const TfTable
 #pragma unroll
         for (int a = 0; a < 3; a++)
             if (!(fabs(f[a] - 0.5) < 0.5 - 1e-4)) return false;
+    }
+    // transparent cell (the float64 value rounds into the cell's widened range)
+    if (AFAM_CELL_SKIP && (G.inner & kCellClear)) {
+        ++C.ns64;
+        return true;
     }
     // basis values now, the derivative weights only for visible samples
     auto basis = [&](int a, double (&Na)[Q], double (&Ea)[P]) {
