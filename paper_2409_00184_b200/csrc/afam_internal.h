@@ -34,7 +34,8 @@ struct alignas(16) BlockDesc {
     const double *tab64;  // [3][nspan][tab_stride(deg)] double
     const float *knots;   // [3][nk] float (full clamped vectors)
     const float2 *crange; // [nspan^3] per knot cell (kz*nspan+kx)*nspan+ky: [min, max] of its (p+1)^3
-                          // control points widened by max|c| * 2^-14 (degrees <= AFAM_FAST_DEGREE)
+                          // control points widened by max|c| * 2^-14 (degrees <= AFAM_FAST_DEGREE),
+                          // then [ns4^3] (ns4 = ceil(nspan/4)) the same over aligned 4x4x4 cell groups
     double lo[3];         // extent low corner
     double span[3];       // hi - lo
     double inv_span[3];   // 1 / (hi - lo)

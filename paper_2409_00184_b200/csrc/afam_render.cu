@@ -1269,6 +1269,8 @@ struct FastCell {
     float4 c[NR > 0 ? NR : 1];
     float4 *s;                    // this thread's shared rows (stride 128)
     float cx, cy, cz;             // the cell's lower corner in span coordinates
+    uint32_t lim;                 // float bits of the cell's width: 1 (a knot cell) or 4 (a transparent
+                                  // 4x4x4 group, AFAM_CELL_GROUP)
     int32_t key;                  // x-quad row index of the (0, 0) row in the owner block; -1: none
     uint32_t inner;               // bit a: axis a on an interior span
     __device__ __forceinline__ float4 get(int i) const { return i < NR ? c[i] : s[(i - NR) * 128]; }
@@ -1281,6 +1283,10 @@ struct FastCell {
 __device__ __forceinline__ bool in_unit(float f) {  // 0 <= f < 1 (also rejects -0.0 and NaN)
     return __float_as_uint(f) < 0x3f800000u;
 }
+__device__ __forceinline__ bool in_lim(float f, uint32_t lim) {  // 0 <= f < lim (lim: float bits)
+    return __float_as_uint(f) < lim;
+}
+constexpr uint32_t kLim1 = 0x3f800000u, kLim4 = 0x40800000u;
 
 // Re-derive the cell of predicted span coordinates tq (render_kernel's
 // axis_span: floor, clamped to the block's spans) and re-gather its rows
@@ -1297,6 +1303,9 @@ __device__ __forceinline__ BlockFast fast_block(const BlockFast &sb) {  // sb in
     return b;
 }
 
+#ifndef AFAM_CELL_GROUP
+#define AFAM_CELL_GROUP 1  // transparent 4x4x4 cell groups passed as one cell (float32 fast path)
+#endif
 #ifndef AFAM_CELL_SKIP
 #define AFAM_CELL_SKIP 1  // skip the samples of cells the TF makes transparent (BlockDesc::crange)
 #endif
@@ -1307,7 +1316,7 @@ __device__ __forceinline__ BlockFast fast_block(const BlockFast &sb) {  // sb in
 // its rows are not gathered.
 constexpr uint32_t kCellClear = 8u;
 
-template <int P, int SR, bool SKIP = false>
+template <int P, int SR, int SKIP = 0>
 __device__ __forceinline__ void fast_cell_update_k(const BlockFast &b, int kx, int ky, int kz, FastCell<P, SR> &G,
                                                    const RenderArgs *A = nullptr) {
     constexpr int Q = P + 1;
@@ -1316,12 +1325,34 @@ __device__ __forceinline__ void fast_cell_update_k(const BlockFast &b, int kx, i
     G.cz = (float)kz;
     G.inner = (span_interior<P>(b, kx) ? 1u : 0u) | (span_interior<P>(b, ky) ? 2u : 0u) |
               (span_interior<P>(b, kz) ? 4u : 0u);
-    if constexpr (SKIP && AFAM_CELL_SKIP) {
+    G.lim = kLim1;
+    if constexpr (SKIP != 0 && AFAM_CELL_SKIP) {
         // the clamp of render.py's value to the TF domain is monotone: the
         // clamped range bounds every clamped sample value
-        const float2 r = __ldg(b.rng + (kz * b.nspan + kx) * b.nspan + ky);
-        const float lo = fminf(fmaxf(r.x, A->dom_lo), A->dom_hi), hi = fminf(fmaxf(r.y, A->dom_lo), A->dom_hi);
-        if (!(hi > A->op_lo) || !(lo < A->op_hi)) {
+        auto clear = [&](float2 r) {
+            const float lo = fminf(fmaxf(r.x, A->dom_lo), A->dom_hi), hi = fminf(fmaxf(r.y, A->dom_lo), A->dom_hi);
+            return !(hi > A->op_lo) || !(lo < A->op_hi);
+        };
+        const int ns = b.nspan;
+        const float2 r = __ldg(b.rng + (kz * ns + kx) * ns + ky);
+        if (SKIP == 2 && AFAM_CELL_GROUP) {
+            // the cell's aligned 4x4x4 group (loaded beside the cell's own
+            // range): when the whole group is transparent the lane treats it
+            // as one cell of width 4 -- any sample whose span coordinates lie
+            // in it falls in one of its cells (the clamp to the block's spans
+            // keeps the group's cells), so it is transparent too
+            const int n4 = (ns + 3) >> 2;
+            const float2 r4 = __ldg(b.rng + ns * ns * ns + ((kz >> 2) * n4 + (kx >> 2)) * n4 + (ky >> 2));
+            if (clear(r4)) {
+                G.cx = (float)(kx & ~3);
+                G.cy = (float)(ky & ~3);
+                G.cz = (float)(kz & ~3);
+                G.lim = kLim4;
+                G.inner |= kCellClear;
+                return;
+            }
+        }
+        if (clear(r)) {
             G.inner |= kCellClear;
             return;  // the rows of G.key stay valid for that key
         }
@@ -1344,7 +1375,7 @@ __device__ __forceinline__ void fast_cell_update(const BlockFast &sb, float tqx,
     const int kx = min(max(__float2int_rd(tqx), 0), b.nspan - 1);
     const int ky = min(max(__float2int_rd(tqy), 0), b.nspan - 1);
     const int kz = min(max(__float2int_rd(tqz), 0), b.nspan - 1);
-    fast_cell_update_k<P, SR, true>(b, kx, ky, kz, G, &A);
+    fast_cell_update_k<P, SR, 2>(b, kx, ky, kz, G, &A);
 }
 
 // One sample of a clamped-uniform float32 block (render_kernel's
@@ -1356,18 +1387,18 @@ __device__ __forceinline__ bool sample_fast2(const RenderArgs &A, const TfTable 
                                              March &M) {
     constexpr int Q = P + 1;
     float fx = tqx - G.cx, fy = tqy - G.cy, fz = tqz - G.cz;
-    if (!(in_unit(fx) & in_unit(fy) & in_unit(fz))) {
+    if (!(in_lim(fx, G.lim) & in_lim(fy, G.lim) & in_lim(fz, G.lim))) {
         fast_cell_update<P, SR>(sb, tqx, tqy, tqz, G, A);
         fx = tqx - G.cx;
         fy = tqy - G.cy;
         fz = tqz - G.cz;
     }
+    if (AFAM_CELL_SKIP && (G.inner & kCellClear)) return true;  // transparent: changes neither C nor A
     if constexpr (P == 1) {
         if (!(fabsf(fx - 0.5f) < 0.5f - 1e-4f) || !(fabsf(fy - 0.5f) < 0.5f - 1e-4f) ||
             !(fabsf(fz - 0.5f) < 0.5f - 1e-4f))
             return false;
     }
-    if (AFAM_CELL_SKIP && (G.inner & kCellClear)) return true;  // transparent: changes neither C nor A
     float Nx[Q], Ny[Q], Nz[Q];
     {
         float2 Nxy[Q];
@@ -1542,7 +1573,7 @@ __device__ __forceinline__ bool sample_fast64(const RenderArgs &A, const TfTable
         int k[3];
 #pragma unroll
         for (int a = 0; a < 3; a++) k[a] = min(max((int)floor(tq[a]), 0), b.nspan - 1);
-        fast_cell_update_k<P, SR, true>(b, k[0], k[1], k[2], G, &A);
+        fast_cell_update_k<P, SR, 1>(b, k[0], k[1], k[2], G, &A);
 #pragma unroll
         for (int a = 0; a < 3; a++) f[a] = tq[a] - (double)k[a];
     }
@@ -1725,6 +1756,7 @@ __global__ void __launch_bounds__(128, MINB) render2_kernel(const BlockDesc *__r
         G.key = -1;
         G.cx = G.cy = G.cz = -1e30f;
         G.inner = 0;
+        G.lim = kLim1;
         float dk = 0.f;  // M.k - (sample at which tq0 was taken), exact below 2^24
         for (;;) {
             if (M.k >= seg_end) {  // rare: exact finest cell, owner change, end of ray

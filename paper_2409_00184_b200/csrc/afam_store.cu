@@ -132,6 +132,27 @@ __global__ void cell_range_kernel(const float4 *__restrict__ ctrl4, int ncp, int
     }
 }
 
+// The second level of the cell ranges: the union of the ranges of each
+// aligned 4x4x4 group of cells (clipped to the block), at crange + nspan^3.
+__global__ void cell_range4_kernel(int nspan, float2 *__restrict__ crange) {
+    const int ns4 = (nspan + 3) / 4;
+    const int64_t total = (int64_t)ns4 * ns4 * ns4;
+    float2 *out = crange + (int64_t)nspan * nspan * nspan;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int Y = (int)(i % ns4), X = (int)((i / ns4) % ns4), Z = (int)(i / ((int64_t)ns4 * ns4));
+        float lo = INFINITY, hi = -INFINITY;
+        for (int kz = 4 * Z; kz < min(4 * Z + 4, nspan); kz++)
+            for (int kx = 4 * X; kx < min(4 * X + 4, nspan); kx++)
+                for (int ky = 4 * Y; ky < min(4 * Y + 4, nspan); ky++) {
+                    const float2 r = crange[((int64_t)kz * nspan + kx) * nspan + ky];
+                    lo = fminf(lo, r.x);
+                    hi = fmaxf(hi, r.y);
+                }
+        out[i] = make_float2(lo, hi);
+    }
+}
+
 // Knots + per-span basis tables + the slot descriptor.  knot_off: byte
 // offset of the knots; has_t0 = 0 for .mfa images (t0 = 0 implicit,
 // FORMAT.md:44-55), 1 for full vectors.
@@ -226,7 +247,8 @@ int afam_store_create(afam_store **out, int device, int32_t slots, int32_t max_n
     s->ctrl4_elems = (size_t)max_ncp * max_ncp * max_ncp;
     s->knot_floats = 3 * (size_t)(max_ncp + AFAM_MAX_DEGREE + 1);
     s->tab_elems = 3 * (size_t)max_ncp * kTabStrideMax;
-    s->crange_elems = (size_t)max_ncp * max_ncp * max_ncp;
+    const size_t ns4 = (size_t)(max_ncp + 3) / 4;
+    s->crange_elems = (size_t)max_ncp * max_ncp * max_ncp + ns4 * ns4 * ns4;
     s->slot_bytes = s->crange_off() + afam_store::align256(s->crange_elems * 8);
     cudaError_t e = cudaMalloc(&s->arena, s->slot_bytes * (size_t)slots);
     if (e != cudaSuccess) {
@@ -362,6 +384,9 @@ static int launch_unpack(afam_store *s, int32_t slot, int deg, int ncp, uint64_t
         const int64_t ncell = (int64_t)(ncp - deg) * (ncp - deg) * (ncp - deg);
         cell_range_kernel<<<(int)std::min<int64_t>((ncell + 255) / 256, 1184), 256, 0, st>>>(
             s->ctrl4_ptr(slot), ncp, deg, (const unsigned int *)(s->d_maxabs + slot), s->crange_ptr(slot));
+        const int64_t ns4 = (ncp - deg + 3) / 4;
+        cell_range4_kernel<<<(int)std::min<int64_t>((ns4 * ns4 * ns4 + 127) / 128, 1184), 128, 0, st>>>(
+            ncp - deg, s->crange_ptr(slot));
     }
     build_tables_kernel<<<1, 256, 0, st>>>(s->raw_ptr(slot), knot_off, has_t0, ncp, deg, s->knot_ptr(slot),
                                            s->tab32_ptr(slot), s->tab64_ptr(slot), s->d_desc + slot, proto,
