@@ -108,49 +108,46 @@ __global__ void unpack_quad_kernel(const uint8_t *__restrict__ raw, uint64_t src
 // (its float32 rounding is ~1e-6 max|c|, 60x inside the margin); a frame
 // whose transfer function has zero opacity on the whole range skips the
 // cell's samples without decoding them (render2_kernel, sample_fast2).
-__global__ void cell_range_kernel(const float4 *__restrict__ ctrl4, int ncp, int deg,
-                                  const unsigned int *maxabs, float2 *__restrict__ crange) {
-    const int nspan = ncp - deg;
-    const int64_t total = (int64_t)nspan * nspan * nspan;
+// One 64-thread CTA per aligned 4x4x4 cell group: the group's (4+p)^3
+// control points staged in shared memory, one cell per thread, then the
+// group's union (the second level, at crange + nspan^3).
+__global__ void __launch_bounds__(64) cell_range_kernel(const float *__restrict__ ctrl, int ncp, int pitch, int deg,
+                                                        const unsigned int *maxabs, float2 *__restrict__ crange) {
+    const int nspan = ncp - deg, ns4 = (nspan + 3) / 4, W = 4 + deg;
+    const int g = blockIdx.x;
+    const int Y = g % ns4, X = (g / ns4) % ns4, Z = g / (ns4 * ns4);
+    __shared__ float s[7 * 7 * 7];  // [z][y][x], W <= 7
+    for (int i = threadIdx.x; i < W * W * W; i += 64) {
+        const int x = i % W, y = (i / W) % W, z = i / (W * W);
+        const int ix = 4 * X + x, iy = 4 * Y + y, iz = 4 * Z + z;
+        s[i] = (ix < ncp && iy < ncp && iz < ncp) ? ctrl[((size_t)iz * ncp + iy) * pitch + ix] : 0.f;
+    }
+    __syncthreads();
     const float eps = __uint_as_float(*maxabs) * 0x1p-14f;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int ky = (int)(i % nspan);
-        const int kx = (int)((i / nspan) % nspan);
-        const int kz = (int)(i / ((int64_t)nspan * nspan));
-        float lo = INFINITY, hi = -INFINITY;
+    const int tx = threadIdx.x & 3, ty = (threadIdx.x >> 2) & 3, tz = threadIdx.x >> 4;
+    const int kx = 4 * X + tx, ky = 4 * Y + ty, kz = 4 * Z + tz;
+    float lo = INFINITY, hi = -INFINITY;
+    if (kx < nspan && ky < nspan && kz < nspan) {
         for (int cz = 0; cz <= deg; cz++)
-            for (int by = 0; by <= deg; by++) {
-                const float4 r = __ldg(ctrl4 + ((int64_t)(kz + cz) * ncp + kx) * ncp + ky + by);
-                const float v[4] = {r.x, r.y, r.z, r.w};
+            for (int by = 0; by <= deg; by++)
                 for (int bx = 0; bx <= deg; bx++) {
-                    lo = fminf(lo, v[bx]);
-                    hi = fmaxf(hi, v[bx]);
+                    const float v = s[((tz + cz) * W + ty + by) * W + tx + bx];
+                    lo = fminf(lo, v);
+                    hi = fmaxf(hi, v);
                 }
-            }
-        crange[i] = make_float2(lo - eps, hi + eps);
+        lo -= eps;
+        hi += eps;
+        crange[((size_t)kz * nspan + kx) * nspan + ky] = make_float2(lo, hi);
     }
-}
-
-// The second level of the cell ranges: the union of the ranges of each
-// aligned 4x4x4 group of cells (clipped to the block), at crange + nspan^3.
-__global__ void cell_range4_kernel(int nspan, float2 *__restrict__ crange) {
-    const int ns4 = (nspan + 3) / 4;
-    const int64_t total = (int64_t)ns4 * ns4 * ns4;
-    float2 *out = crange + (int64_t)nspan * nspan * nspan;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int Y = (int)(i % ns4), X = (int)((i / ns4) % ns4), Z = (int)(i / ((int64_t)ns4 * ns4));
-        float lo = INFINITY, hi = -INFINITY;
-        for (int kz = 4 * Z; kz < min(4 * Z + 4, nspan); kz++)
-            for (int kx = 4 * X; kx < min(4 * X + 4, nspan); kx++)
-                for (int ky = 4 * Y; ky < min(4 * Y + 4, nspan); ky++) {
-                    const float2 r = crange[((int64_t)kz * nspan + kx) * nspan + ky];
-                    lo = fminf(lo, r.x);
-                    hi = fmaxf(hi, r.y);
-                }
-        out[i] = make_float2(lo, hi);
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
     }
+    __shared__ float2 w[2];
+    if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = make_float2(lo, hi);
+    __syncthreads();
+    if (threadIdx.x == 0)
+        crange[(size_t)nspan * nspan * nspan + g] = make_float2(fminf(w[0].x, w[1].x), fmaxf(w[0].y, w[1].y));
 }
 
 // Knots + per-span basis tables + the slot descriptor.  knot_off: byte
@@ -381,12 +378,10 @@ static int launch_unpack(afam_store *s, int32_t slot, int deg, int ncp, uint64_t
     unpack_quad_kernel<<<(int)std::min<int64_t>((total4 + 255) / 256, 1184), 256, 0, st>>>(
         s->raw_ptr(slot), ctrl_off, ncp, s->ctrl4_ptr(slot));
     if (deg <= AFAM_FAST_DEGREE) {
-        const int64_t ncell = (int64_t)(ncp - deg) * (ncp - deg) * (ncp - deg);
-        cell_range_kernel<<<(int)std::min<int64_t>((ncell + 255) / 256, 1184), 256, 0, st>>>(
-            s->ctrl4_ptr(slot), ncp, deg, (const unsigned int *)(s->d_maxabs + slot), s->crange_ptr(slot));
-        const int64_t ns4 = (ncp - deg + 3) / 4;
-        cell_range4_kernel<<<(int)std::min<int64_t>((ns4 * ns4 * ns4 + 127) / 128, 1184), 128, 0, st>>>(
-            ncp - deg, s->crange_ptr(slot));
+        const int ns4 = (ncp - deg + 3) / 4;
+        cell_range_kernel<<<ns4 * ns4 * ns4, 64, 0, st>>>(s->ctrl_ptr(slot), ncp, proto.pitch, deg,
+                                                          (const unsigned int *)(s->d_maxabs + slot),
+                                                          s->crange_ptr(slot));
     }
     build_tables_kernel<<<1, 256, 0, st>>>(s->raw_ptr(slot), knot_off, has_t0, ncp, deg, s->knot_ptr(slot),
                                            s->tab32_ptr(slot), s->tab64_ptr(slot), s->d_desc + slot, proto,
