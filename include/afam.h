@@ -276,6 +276,7 @@ typedef struct {
     uint64_t shaded_samples; /* samples with TF opacity > 0 (gradient + shading evaluated) */
     uint64_t exact_samples;  /* samples decoded from the float64 position (exact span search) */
     uint64_t exact_cells;    /* float64 finest-cell evaluations (ray start, cell crossings, near-face samples) */
+    uint64_t clear_samples;  /* AFAM_RENDER_DEBUG only: samples in transparent cells (counted, not decoded) */
 } afam_render_stats;
 
 /*

@@ -70,7 +70,7 @@ class AfamFrame(C.Structure):
 class AfamRenderStats(C.Structure):
     _fields_ = [("samples", C.c_uint64), ("missing_key", C.c_int64), ("fp64_samples", C.c_uint64),
                 ("shaded_samples", C.c_uint64), ("exact_samples", C.c_uint64),
-                ("exact_cells", C.c_uint64)]
+                ("exact_cells", C.c_uint64), ("clear_samples", C.c_uint64)]
 
 
 # (name, restype, argtypes) for every symbol declared in include/afam.h

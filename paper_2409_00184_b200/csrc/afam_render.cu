@@ -474,6 +474,7 @@ struct alignas(16) ThreadCold {
     float4 ginv;         // 1/span per axis of the owner block (model.py:79)
     const float *tab32;  // owner block's per-span basis tables
     uint32_t ns64, nexact, ncell;
+    uint32_t nclear;  // DEBUG kernels: samples in transparent cells
 };
 
 // render.py:422-428 sample position, float64 in the reference op order, and
@@ -1084,7 +1085,7 @@ __global__ void __launch_bounds__(128, MINB) render_kernel(const BlockDesc *__re
     R.te = te;
 
     C.vdir = make_float4((float)d[0], (float)d[1], (float)d[2], 0.f);
-    C.ns64 = C.nexact = C.ncell = 0;
+    C.ns64 = C.nexact = C.ncell = C.nclear = 0;
     March M;
     M.k = 0;
     M.kend = 0;
@@ -1726,7 +1727,7 @@ __global__ void __launch_bounds__(128, MINB) render2_kernel(const BlockDesc *__r
     R.te = te;
 
     C.vdir = make_float4((float)d[0], (float)d[1], (float)d[2], 0.f);
-    C.ns64 = C.nexact = C.ncell = 0;
+    C.ns64 = C.nexact = C.ncell = C.nclear = 0;
     March M;
     M.k = 0;
     F.kend = 0;
@@ -1820,6 +1821,7 @@ __global__ void __launch_bounds__(128, MINB) render2_kernel(const BlockDesc *__r
                     ok = sample_fast2<P, SR>(A, tf, b, tqx, tqy, tqz, C, G, M);
                 }
             }
+            if (DEBUG && (AF || fast) && ok && (G.inner & kCellClear)) ++C.nclear;
             if (!ok) {
                 const int32_t slot = vld(F.slot), deg = vld(F.deg);
                 const BlockDesc *dpx = descs + slot;
@@ -1867,6 +1869,7 @@ __global__ void __launch_bounds__(128, MINB) render2_kernel(const BlockDesc *__r
     const uint32_t wshade = __reduce_add_sync(0xffffffffu, M.nshade);
     const uint32_t wexact = __reduce_add_sync(0xffffffffu, C.nexact);
     const uint32_t wcell = __reduce_add_sync(0xffffffffu, C.ncell);
+    const uint32_t wclear = DEBUG ? __reduce_add_sync(0xffffffffu, C.nclear) : 0u;
     int64_t wmiss = M.own < 0 && M.k < M.kend ? ((int64_t)M.k << 32) | ((int64_t)i * A.width + j) : INT64_MAX;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -1879,6 +1882,7 @@ __global__ void __launch_bounds__(128, MINB) render2_kernel(const BlockDesc *__r
         if (wshade) atomicAdd((unsigned long long *)&stats->shaded_samples, (unsigned long long)wshade);
         if (wexact) atomicAdd((unsigned long long *)&stats->exact_samples, (unsigned long long)wexact);
         if (wcell) atomicAdd((unsigned long long *)&stats->exact_cells, (unsigned long long)wcell);
+        if (wclear) atomicAdd((unsigned long long *)&stats->clear_samples, (unsigned long long)wclear);
         if (wmiss != INT64_MAX) atomicMin((long long *)&stats->missing_key, (long long)wmiss);
     }
 }
@@ -1890,6 +1894,7 @@ __global__ void init_stats_kernel(afam_render_stats *s) {
     s->shaded_samples = 0;
     s->exact_samples = 0;
     s->exact_cells = 0;
+    s->clear_samples = 0;
 }
 
 __global__ void finish_stats_kernel(afam_render_stats *s) {

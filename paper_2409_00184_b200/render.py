@@ -464,7 +464,7 @@ def _thread_stats(dev, ring: int = 0):
     key = ("stats", dev.index)
     st = getattr(_tls, "stats", None)
     if st is None or st[0] != key:
-        st = (key, [(torch.empty(6, dtype=torch.int64, device=dev), torch.cuda.Event())
+        st = (key, [(torch.empty(7, dtype=torch.int64, device=dev), torch.cuda.Event())
                     for _ in range(FRAMES_IN_FLIGHT)])
         _tls.stats = st
     return st[1][ring]
@@ -514,7 +514,7 @@ class PendingPart:
         _lib.check(_lib.lib().afam_render_elapsed_seq(self.store.handle, self.seq, C.byref(kms)))
         info = {"samples": int(st[0]), "missing_key": int(st[1]), "fp64_samples": int(st[2]),
                 "shaded_samples": int(st[3]), "exact_samples": int(st[4]),
-                "exact_cells": int(st[5]),
+                "exact_cells": int(st[5]), "clear_samples": int(st[6]),
                 "kernel_ms": float(kms.value)}
         if self.raise_missing and info["missing_key"] >= 0:
             cells = C.c_int32()

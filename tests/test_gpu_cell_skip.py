@@ -73,6 +73,11 @@ def test_cell_skip_golden_store(cuda, oracle, tfname):
     got, info = _check(oracle, pov, {a: pm[a] for a in vis}, tf, params)
     if tfname == "none":
         assert not got.any() and info["shaded_samples"] == 0
+        assert info["clear_samples"] == info["samples"]  # every cell transparent
+    elif tfname == "full":
+        assert info["clear_samples"] == 0  # no cell transparent
+    else:
+        assert 0 < info["clear_samples"] < info["samples"]
 
 
 @pytest.mark.parametrize("degree", [1, 2, 3])

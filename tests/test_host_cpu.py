@@ -34,7 +34,7 @@ def test_struct_layouts_match_header():
 
     from paper_2409_00184_b200 import _lib
 
-    assert C.sizeof(_lib.AfamRenderStats) == 48
+    assert C.sizeof(_lib.AfamRenderStats) == 56
     # 12 + 2 doubles, 5 ints (+pad), 8 doubles, 2 ints, 2 doubles, 32*4 + 32*2 doubles, flags (+pad),
     # color_pts / opacity_pts
     expect = 14 * 8 + 5 * 4 + 4 + 8 * 8 + 2 * 4 + 2 * 8 + 32 * 4 * 8 + 32 * 2 * 8 + 8 + 2 * 8
