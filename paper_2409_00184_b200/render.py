@@ -506,7 +506,7 @@ class PendingPart:
 
         with torch.cuda.device(self.dev):
             self.event.synchronize()  # this frame only (a later frame may be queued behind it)
-            st = self.stage[:48].view(torch.int64).numpy().copy()
+            st = self.stage[:56].view(torch.int64).numpy().copy()
             out = self.out
             if self.host_out:
                 out = self.stage[64:64 + self.nbytes].view(self.rows, self.W, 4).clone()
@@ -580,7 +580,7 @@ def submit_part(pov, blocks: dict, tf, params, *, band_rows: int | None = None, 
             C.c_void_p(stats.data_ptr()), None if nsamp is None else C.c_void_p(nsamp.data_ptr()),
             None if ohash is None else C.c_void_p(ohash.data_ptr()), C.c_void_p(int(s_obj.cuda_stream))))
         with torch.cuda.stream(s_obj):
-            stage[:48].view(torch.int64).copy_(stats, non_blocking=True)
+            stage[:56].view(torch.int64).copy_(stats, non_blocking=True)
             if host_out and not zero_copy:
                 stage[64:64 + rows * W * 4].view(rows, W, 4).copy_(out, non_blocking=True)
             event.record(s_obj)
