@@ -90,6 +90,9 @@ struct alignas(16) RenderArgs {
     uint32_t flags;
     float tf_lo, tf_scale;  // TfTable lo / scale, as launch arguments (constant bank, no per-sample load)
     float op_lo, op_hi;     // TF opacity support: the kernel's alpha_tf is exactly 0 unless op_lo < v < op_hi
+    // the support pulled back through the domain clamp: clamp(v) <= op_lo iff
+    // v <= clr_lo, clamp(v) >= op_hi iff v >= clr_hi (transparent-cell test)
+    float clr_lo, clr_hi;
 };
 
 // TransferFunction.color_at / opacity_at (render.py:117-124): every
@@ -1330,10 +1333,7 @@ __device__ __forceinline__ void fast_cell_update_k(const BlockFast &b, int kx, i
     if constexpr (SKIP != 0 && AFAM_CELL_SKIP) {
         // the clamp of render.py's value to the TF domain is monotone: the
         // clamped range bounds every clamped sample value
-        auto clear = [&](float2 r) {
-            const float lo = fminf(fmaxf(r.x, A->dom_lo), A->dom_hi), hi = fminf(fmaxf(r.y, A->dom_lo), A->dom_hi);
-            return !(hi > A->op_lo) || !(lo < A->op_hi);
-        };
+        auto clear = [&](float2 r) { return !(r.y > A->clr_lo) || !(r.x < A->clr_hi); };
         const int ns = b.nspan;
         const float2 r = __ldg(b.rng + (kz * ns + kx) * ns + ky);
         if (SKIP == 2 && AFAM_CELL_GROUP) {
@@ -2337,6 +2337,13 @@ extern "C" int afam_render(afam_store *s, const afam_frame *F, const int32_t *sl
     A.tf_scale = tf.scale;
     A.op_lo = tf.op_lo;
     A.op_hi = tf.op_hi;
+    {
+        const float inf = std::numeric_limits<float>::infinity();
+        // clamp(x) = min(max(x, dom_lo), dom_hi) is monotone: for dom_lo <= op_lo < dom_hi,
+        // clamp(x) <= op_lo iff x <= op_lo; above that range always, below it never
+        A.clr_lo = A.op_lo >= A.dom_hi ? inf : (A.op_lo < A.dom_lo ? -inf : A.op_lo);
+        A.clr_hi = A.op_hi <= A.dom_lo ? -inf : (A.op_hi > A.dom_hi ? inf : A.op_hi);
+    }
     ht.mark();
 
     std::vector<int16_t> grid;
