@@ -1451,9 +1451,10 @@ __device__ __forceinline__ bool sample_fast2(const RenderArgs &A, const TfTable 
     }
     int bi;
     float bf;
-    const float vc = fminf(fmaxf(v, A.dom_lo), A.dom_hi);
     // outside the TF's opacity support alpha_tf is exactly 0: no lookup
-    if (!(vc > A.op_lo) || !(vc < A.op_hi)) return true;
+    // (clr_lo/clr_hi: the support pulled back through the domain clamp)
+    if (!(v > A.clr_lo) || !(v < A.clr_hi)) return true;
+    const float vc = fminf(fmaxf(v, A.dom_lo), A.dom_hi);
     const float atf = tf_alpha(A, tf, vc, bi, bf);
     if (!(atf > 0.f)) return true;  // a_s = 0: the sample changes neither C nor A
     ++M.nshade;
@@ -1633,8 +1634,8 @@ __device__ __forceinline__ bool sample_fast64(const RenderArgs &A, const TfTable
         contract_quad<P, double>(c4, N[0], E[0], N[1], E[1], N[2], E[2], v, g);
     }
     ++C.ns64;
+    if (!((float)v > A.clr_lo) || !((float)v < A.clr_hi)) return true;
     const float vc = fminf(fmaxf((float)v, A.dom_lo), A.dom_hi);
-    if (!(vc > A.op_lo) || !(vc < A.op_hi)) return true;
     int bi;
     float bf;
     const float atf = tf_alpha(A, tf, vc, bi, bf);
